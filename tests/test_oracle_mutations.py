@@ -1,0 +1,58 @@
+"""Mutation check for the oracle pins: plausible transcription mistakes in oracle/spinsim_oracle.cpp (a dropped
+term, a wrong sign, a transposed operand, a misprint left in) must each make tests/test_oracle_pins.py fail.
+Each mutant is compiled to a temporary library and the pins are run against it in a subprocess."""
+import os
+import subprocess
+import sys
+import tempfile
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SRC = os.path.join(ROOT, "oracle", "spinsim_oracle.cpp")
+
+MUTANTS = {
+    # CF4 factor order swapped: exp(−iH̄1δt) exp(−iH̄2δt) (drops to 2nd order, SURVEY [V12])
+    "cf4_order": ("return mul(e2, e1);", "return mul(e1, e2);"),
+    # the misprinted T22 = cosΦ e^{i4q} of Eq. lie_trotter_4 left in
+    "t22_misprint": ("a.a[1][1] = expm1i(th2) - R(2) * s * s * std::exp(I * th2);",
+                     "a.a[1][1] = std::cos(Phi) * std::exp(I * R(4) * q) - R(1);"),
+    # the misprinted T13 phase sign left in
+    "t13_misprint": ("a.a[0][2] = -((s * eq6_m * em_phi) * (s * eq6_m * em_phi));",
+                     "a.a[0][2] = -((s * eq6_p * em_phi) * (s * eq6_p * em_phi));"),
+    # frame rotation direction flipped
+    "frame_sign": ("f[0] = c * fx + s * fy;\n  f[1] = -s * fx + c * fy;", "f[0] = c * fx - s * fy;\n  f[1] = s * fx + c * fy;"),
+    # frame exit forgotten sign: R(+Δt) instead of R(−Δt)
+    "exit_sign": ("std::exp(-I * omega_r * m * (R)g.dt_out)", "std::exp(I * omega_r * m * (R)g.dt_out)"),
+    # residual squaring (a + 2I)a with the 2I dropped
+    "residual_drop_2I": ("b.a[i][i] += R(2);", "b.a[i][i] += R(1);"),
+    # CF4 weights transposed: H̄1 gets w− on f1
+    "weights_swapped": ("a1[j] = (wp * f1[j] + wm * f2[j]) * dt;", "a1[j] = (wm * f1[j] + wp * f2[j]) * dt;"),
+    # accumulate u on the wrong side (postmultiply)
+    "postmultiply": ("U = mul(u, U);", "U = mul(U, u);"),
+    # ω_r sampled at the interval start instead of the midpoint
+    "omega_r_start": ("field_sample<R>(c.field, p, t_k, 0.5 * g.dt_out, f);", "field_sample<R>(c.field, p, t_k, 0.0, f);"),
+    # SU(2) closed form with cos(r) instead of cos(r/2)
+    "su2_halfangle": ("const R c = std::cos(r / R(2));", "const R c = std::cos(r);"),
+    # spin-one Jy sign convention broken inside the analytic map
+    "d1_sign": ("D.a[1][0] = -rt2 * al * std::conj(be);", "D.a[1][0] = rt2 * al * std::conj(be);"),
+}
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", sorted(MUTANTS))
+def test_pins_kill_mutant(name):
+    old, new = MUTANTS[name]
+    src = open(SRC).read()
+    assert src.count(old) == 1, f"mutation anchor for {name} not found exactly once"
+    with tempfile.TemporaryDirectory() as d:
+        cpp = os.path.join(d, "m.cpp")
+        so = os.path.join(d, "libm.so")
+        open(cpp, "w").write(src.replace(old, new))
+        subprocess.check_call(["g++", "-O1", "-std=c++17", "-ffp-contract=off", "-fPIC", "-shared", "-pthread",
+                               cpp, "-o", so])
+        env = dict(os.environ, SPINSIM_ORACLE_LIB=so)
+        r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider",
+                            os.path.join(ROOT, "tests", "test_oracle_pins.py")],
+                           env=env, cwd=ROOT, capture_output=True, text=True, timeout=600)
+        assert r.returncode != 0, f"mutant {name} survived the pins:\n{r.stdout[-2000:]}"
