@@ -1,0 +1,364 @@
+#!/usr/bin/env python
+"""bench.py — fine steps/s of the Spinsim hot path on B200 (BASELINE.json metric), one JSON line on rank 0.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C3|C2|C5|C4] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...           (the driver's launch for N > 1)
+
+A "step" is one pass of the whole hot path (SURVEY §8(a) rows a1–a9: interval kernel + state scan) over one batch.
+Default workload: C3 (BASELINE configs[2]) — 8192 spin-one sweeps × 10 ms, δt = 100 ns, Δt = 1 µs, Lie–Trotter
+τ = 24, rotating frame — the batch-summed FP64 workload the metric is quoted on "at 1/2/4/8 B200".  Multi-GPU
+shards sweeps (no data-path collective); `--scaling weak` (default) keeps 8192 sweeps per rank, `--scaling strong`
+splits 8192 across ranks.  Timing: CUDA events on the launching stream, barrier + synchronize on both sides, max
+over ranks (all_reduce MAX).  Working set (U 11.8 GB + states 3.9 GB per rank) ≫ L2 (126 MB), so no flush is needed.
+
+`--impl reference` times the CPU oracle (oracle/, the "reference arm" of this tier) on the host cores on a bounded
+sample of the same workload; under torchrun only rank 0 runs it.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+UNIT = "fine steps/s"
+# Nominal FP64 peak: 148 SMs × 64 FP64 FMA/clk/SM × 2 flop × 1.965 GHz (max SM clock).
+N_SM, FP64_FMA_PER_CLK_SM, SM_MAX_MHZ = 148, 64, 1965.0
+FP64_PEAK_TFLOPS = N_SM * FP64_FMA_PER_CLK_SM * 2 * SM_MAX_MHZ * 1e6 / 1e12
+
+
+def algorithmic_flops_per_fine_step(spin: str, expo: str, tau: int, method: str = "cf4") -> int:
+    """Matrix arithmetic of one fine step as the algorithm is written, counting real +, −, × as 1:
+    residual squaring (a + 2I)a on 3×3: 3 + 9·(3·6 + 2·2) = 201; residual product a + b + ab: 9·(2 + 3·6 + 3·2)
+    = 234 (3×3) and 4·(2 + 2·6 + 2·2) = 72 (2×2).  Field trig, T − I construction and the frame are not counted
+    (a lower bound)."""
+    n_exp = 2 if method == "cf4" else 1
+    if spin == "one":
+        prod = 234
+        per_exp = 201 * tau if expo == "lie_trotter" else 0
+    else:
+        prod = 72
+        per_exp = 0
+    n_prod = 2 if method == "cf4" else 1
+    return n_exp * per_exp + n_prod * prod
+
+
+def scan_bytes_per_interval(dim: int) -> int:
+    return (2 * dim * dim + 2 * dim) * 8       # read U_k, write ψ_{k+1}
+
+
+def get_workload(name: str, batch: int) -> W.Workload:
+    if name == "C3":
+        return W.c3_batched(batch=batch)
+    if name == "C2":
+        return W.c2_neural(dt_int=100e-9)
+    if name == "C5":
+        return W.c5_matrix("lie_trotter", batch=100)
+    if name == "C4":
+        return W.c4_long()
+    raise ValueError(name)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, power, reasons = [], [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+                power.append(float(f[3]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm), "power_w_median": float(np.median(power))}
+
+
+def dist_setup(n_gpus: int):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != n_gpus and world > 1:
+        raise SystemExit(f"--gpus {n_gpus} but WORLD_SIZE={world}")
+    return rank, world, local
+
+
+def cpu_oracle_sample(w: W.Workload, target_s: float):
+    """Time the oracle (double instantiation, all host cores) on a bounded sample of workload w: sweeps strided
+    across the batch, each over its first k_end intervals, sized from a calibration run to ≈ target_s seconds."""
+    import oracle
+    oracle.build()
+    cores = os.cpu_count() or 1
+
+    def run(n_sweeps, k_end):
+        idx = np.linspace(0, w.batch - 1, n_sweeps).astype(int)
+        t = time.perf_counter()
+        oracle.evaluate(w.spin, w.method, w.expo, w.tau, w.frame, w.field, sweep=w.sweep[idx], t0=w.t0, t1=w.t1,
+                        dt_int=w.dt_int, dt_out=w.dt_out, psi0=w.psi0[idx], long_double=False,
+                        want_unitaries=False, nthreads=cores, k_begin=0, k_end=k_end)
+        return time.perf_counter() - t, n_sweeps * k_end * w.L
+
+    n_sw = min(w.batch, max(1, cores))
+    k_cal = max(1, min(w.K, 64))
+    dt_cal, steps_cal = run(n_sw, k_cal)
+    rate = steps_cal / max(dt_cal, 1e-6)
+    want_steps = rate * target_s
+    k_end = int(min(w.K, max(1, want_steps / (n_sw * w.L))))
+    if k_end == w.K and n_sw < w.batch:
+        n_sw = int(min(w.batch, max(n_sw, want_steps / (w.K * w.L))))
+    return run, n_sw, k_end, cores
+
+
+def run_reference(args, rank, world):
+    """The reference arm of this tier: the CPU oracle, timed as it stands on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    w = get_workload(args.workload, args.batch)
+    run, n_sw, k_end, cores = cpu_oracle_sample(w, target_s=args.ref_step_seconds)
+    for _ in range(args.warmup):
+        run(n_sw, k_end)
+    times, steps = [], 0
+    for _ in range(args.steps):
+        dt, n = run(n_sw, k_end)
+        times.append(dt)
+        steps += n
+    total = sum(times)
+    value = steps / total
+    sample = (f"{n_sw} of {w.batch} sweeps (evenly strided) x first {k_end} of {w.K} intervals x L={w.L} "
+              f"= {n_sw * k_end * w.L} fine steps per step; oracle<double>, std::thread x {cores}")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_of(w, args, world),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_of(w: W.Workload, args, world):
+    return {"workload": w.name, "spin": w.spin, "exponentiator": w.expo, "trotter_cutoff": w.tau,
+            "integration": w.method, "rotating_frame": w.frame, "field": w.field, "time_end": w.t1,
+            "time_step_integration": w.dt_int, "time_step_output": w.dt_out, "K": w.K, "L": w.L,
+            "batch_per_rank": w.batch, "global_batch": w.batch * world if args.scaling == "weak" else args.batch,
+            "parallelism": f"sweep-shard x{world}", "l2": "no flush: per-step working set (U + states) >> 126 MB L2"}
+
+
+def run_ours(args, rank, world, local):
+    import torch
+    import paper_2204_05586_b200 as ss
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    # sweep shard of this rank
+    if args.scaling == "weak":
+        full = get_workload(args.workload, args.batch * world)
+        lo, hi = rank * args.batch, (rank + 1) * args.batch
+    else:
+        full = get_workload(args.workload, args.batch)
+        per = (full.batch + world - 1) // world
+        lo, hi = rank * per, min(full.batch, (rank + 1) * per)
+    w = full.with_(sweep=np.ascontiguousarray(full.sweep[lo:hi]), psi0=np.ascontiguousarray(full.psi0[lo:hi]))
+    B, K, L, D = w.batch, w.K, w.L, w.dim
+    sim = ss.Simulator(w.spin, w.method, w.expo, w.tau, w.frame, args.precision, w.field)
+    sweep = torch.from_numpy(w.sweep).to(dev)
+    psi0 = torch.from_numpy(w.psi0).to(dev)
+    states = torch.empty((B, K + 1, D), dtype=torch.complex128, device=dev)
+    U = torch.empty((B, K, D, D), dtype=torch.complex128, device=dev)
+    scan_ws = torch.empty(int(ss._lib.load().ss_scan_workspace_bytes(D, B, K)), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    # Inputs validated once through the full public call (also a correctness warm-up of ss_evaluate).
+    sim.evaluate(sweep[: min(B, 4)], w.t0, min(w.t1, w.t0 + 20 * w.dt_out), w.dt_int, w.dt_out, psi0[: min(B, 4)])
+
+    def step(ev=None):
+        if ev is not None:
+            ev[0].record(stream)
+        sim.compute_unitaries(sweep, w.t0, w.t1, w.dt_int, w.dt_out, out=U)
+        if ev is not None:
+            ev[1].record(stream)
+        ss.scan_states(U, psi0, out=states, workspace=scan_ws)
+        if ev is not None:
+            ev[2].record(stream)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = ss.kernel_launches()
+    with ClockSampler(local) as clk:
+        start.record(stream)
+        for i in range(args.steps):
+            step(evs[i])
+        end.record(stream)
+        torch.cuda.synchronize()
+    launches = ss.kernel_launches() - launches0
+    barrier()
+    elapsed_ms = start.elapsed_time(end)
+    t_interval = float(np.mean([e[0].elapsed_time(e[1]) for e in evs]))
+    t_scan = float(np.mean([e[1].elapsed_time(e[2]) for e in evs]))
+    if world > 1:
+        t = torch.tensor([elapsed_ms, t_interval, t_scan], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        elapsed_ms, t_interval, t_scan = t.tolist()
+    steps_per_rank = w.fine_steps
+    total_steps = steps_per_rank * world if args.scaling == "weak" else full.fine_steps
+    value = total_steps * args.steps / (elapsed_ms * 1e-3)
+
+    # roofline of the dominant kernel (interval kernel): algorithmic flops per launch / average launch duration
+    flops_launch = algorithmic_flops_per_fine_step(w.spin, w.expo, w.tau, w.method) * steps_per_rank
+    achieved = flops_launch / (t_interval * 1e-3) / 1e12
+    scan_gbs = B * K * scan_bytes_per_interval(D) / (t_scan * 1e-3) / 1e9
+    clocks = clk.summary()
+
+    # e2e through the C ABI with HOST buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        h_sweep = torch.from_numpy(w.sweep).pin_memory().numpy()
+        h_psi0 = torch.from_numpy(w.psi0).pin_memory().numpy()
+        h_states = torch.empty((B, K + 1, D), dtype=torch.complex128).pin_memory().numpy()
+        sim.evaluate_host(h_sweep, w.t0, w.t1, w.dt_int, w.dt_out, h_psi0, out_states=h_states, n_chunks=args.chunks)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            sim.evaluate_host(h_sweep, w.t0, w.t1, w.dt_int, w.dt_out, h_psi0, out_states=h_states,
+                              n_chunks=args.chunks)
+        e2e_s = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            e2e_s = t.item()
+        e2e = {"value": total_steps * args.steps / e2e_s, "unit": UNIT,
+               "h2d_bytes_per_step": int(h_sweep.nbytes + h_psi0.nbytes), "d2h_bytes_per_step": int(h_states.nbytes),
+               "n_chunks": args.chunks}
+
+    measured_peak = None
+    if rank == 0 and not args.no_probe:
+        try:
+            from tools import build_tools
+            measured_peak = build_tools.probe()[0]
+        except Exception as exc:  # probe is context only
+            measured_peak = f"unavailable: {exc}"
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        run, n_sw, k_end, cores = cpu_oracle_sample(w, target_s=args.cpu_seconds)
+        dt, n = run(n_sw, k_end)
+        cpu = {"value": n / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"{n_sw} of {B} sweeps x first {k_end} of {K} intervals x L={L} = {n} fine steps, "
+                         f"oracle<double>, std::thread x {cores}, {dt:.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64" if args.precision == "fp64" else "f32",
+            "data": "synthetic", "config": config_of(w, args, world),
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                         "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+                         "kernel": f"interval_kernel<spin-{w.spin},{w.expo},{w.method},{w.field},{args.precision}>",
+                         "flops_per_launch": flops_launch, "ms_per_launch": t_interval,
+                         "peak_basis": "nominal FP64: 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (DESIGN.md §6)",
+                         "measured_dfma_peak_tflops": measured_peak,
+                         "frac_at_observed_clock": (achieved / (FP64_PEAK_TFLOPS * clocks["sm_mhz"] / SM_MAX_MHZ)
+                                                    if clocks.get("sm_mhz") else None)},
+            "scan": {"bound": "hbm", "achieved": scan_gbs, "unit": "GB/s", "ms_per_launch": t_scan,
+                     "bytes_per_launch": B * K * scan_bytes_per_interval(D)},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
+            "fine_steps_per_step": total_steps,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=["C3", "C2", "C5", "C4"], default="C3")
+    ap.add_argument("--batch", type=int, default=8192, help="sweeps per rank (weak) or in total (strong), C3")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
+    ap.add_argument("--precision", choices=["fp64", "fp32"], default="fp64")
+    ap.add_argument("--chunks", type=int, default=8, help="batch chunks of the pipelined host-buffer (e2e) call")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--ref-step-seconds", type=float, default=8.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-probe", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("note: --warmup < 3 violates the timing rules; using 3", file=sys.stderr)
+        args.warmup = 3
+    rank, world, local = dist_setup(args.gpus)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,173 @@
+/* spinsim_b200.h — C ABI of the B200-native Spinsim hot path (arXiv 2204.05586).
+ *
+ * Integrates the time-dependent Schrödinger equation i dψ/dt = H(t)ψ (Eq. schroedinger) for
+ * spin-half (dim 2) and spin-one (dim 3) systems, H = ωx Jx + ωy Jy + ωz Jz + ωq Q, over a batch of
+ * independent parameter sweeps:
+ *   - one GPU thread owns one coarse interval [t_k, t_k + Δt] and runs L = Δt/δt fine steps
+ *      of the commutator-free 4th-order Magnus method CF4 (Eq. cf4_implementation) inside a
+ *     per-interval rotating frame;
+ *   - exponentials are closed-form SU(2) for spin-half or Lie–Trotter with τ residual squarings for
+ *     spin-one;
+ *   - the interval unitaries U_k are chained into states ψ_{k+1} = U_k ψ_k (Eq. integration_compilation)
+ *     by a decoupled-look-back matrix-product scan on the GPU.
+ *
+ * Conventions (every entry point):
+ *   - Status: 0 = SS_OK, negative = error; ss_last_error() returns a thread-local message naming the offending
+ *     argument.  Argument errors are detected synchronously before any launch; CUDA launch errors are reported as
+ *     SS_ERR_CUDA by the call that detects them.  No entry point falls back to the CPU.
+ *   - Memory: pointers prefixed d_ are CUDA device pointers, h_ are host pointers.  The caller owns every data
+ *     buffer and the workspace; the library owns only the ss_sim handle (and, for ss_evaluate_host, device
+ *     staging buffers cached inside it).  Device entry points never allocate.
+ *   - Layout: row-major; complex numbers are interleaved (re, im) float64 pairs ("complex128"):
+ *       sweep      [batch][P] float64, P = ss_num_sweep_params(field)
+ *       state      [batch][dim] complex128
+ *       states     [batch][K+1][dim] complex128, states[b][0] = state_init[b], states[b][k+1] = U_k states[b][k]
+ *       unitaries  [batch][K][dim][dim] complex128 (lab frame)
+ *     Basis order: spin-half (↑, ↓); spin-one m = +1, 0, −1 (reading R5).
+ *   - Time grid (reading R7): K = (time_end − time_start)/Δt and L = Δt/δt must be integers within 1e-9
+ *     relative (else SS_ERR_INVALID); Δt = time_step_output; δt = Δt / L; t_k = time_start + k·Δt.
+ *   - Streams: `stream` is a cudaStream_t passed as void* (NULL = legacy default stream); all device work is
+ *     stream-ordered and asynchronous unless stated.
+ *   - Precision: `precision` selects only the fine-step arithmetic; all I/O is float64/complex128.
+ */
+#ifndef SPINSIM_B200_H
+#define SPINSIM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  SS_OK = 0,
+  SS_ERR_INVALID = -1,      /* bad argument (names it in ss_last_error) */
+  SS_ERR_UNSUPPORTED = -2,  /* valid but unsupported combination */
+  SS_ERR_CUDA = -3,         /* CUDA runtime / launch error, or no CUDA device */
+  SS_ERR_NONFINITE = -4     /* non-finite sweep parameter or initial state */
+};
+
+enum ss_spin { SS_SPIN_HALF = 1, SS_SPIN_ONE = 2 };                 /* 2j */
+enum ss_integration { SS_CF4 = 0, SS_MIDPOINT = 1, SS_HEUN = 2 };   /* P:323; Euler samplers P:702-704 */
+enum ss_expo { SS_EXP_ANALYTIC = 0, SS_EXP_LIE_TROTTER = 1 };       /* P:359 / P:360-466 */
+enum ss_precision { SS_FP64 = 0, SS_FP32 = 1 };
+/* Built-in field functions replacing the paper's user numba function.  Sweep parameters:
+ *   SS_FIELD_CONSTANT       [ωx, ωy, ωz, ωq]
+ *   SS_FIELD_RABI_LINEAR    [ω0, Ω]            H = ω0 Jz + 2Ω cos(ω0 t) Jx
+ *   SS_FIELD_RABI_CIRCULAR  [ω0, Ω]            H = ω0 Jz + Ω(cos(ω0 t) Jx + sin(ω0 t) Jy)
+ *   SS_FIELD_NEURAL         [ω_bias, ω_rf, Ω, Ω_p, ω_sig, t_p, ω_q]
+ *        H = ω_bias Jz + 2Ω cos(ω_rf t) Jx + Ω_p sinp(ω_sig (t − t_p)) Jz + ω_q Q   (Eq. neural_pulse)
+ *   SS_FIELD_GRADIENT       [x, y]             ω_z = x − 2y                                      */
+enum ss_field {
+  SS_FIELD_CONSTANT = 0,
+  SS_FIELD_RABI_LINEAR = 1,
+  SS_FIELD_RABI_CIRCULAR = 2,
+  SS_FIELD_NEURAL = 3,
+  SS_FIELD_GRADIENT = 4
+};
+
+/* Simulator description (mirrors spinsim.Simulator's constructor arguments). */
+typedef struct {
+  int32_t spin;               /* ss_spin */
+  int32_t integration;        /* ss_integration */
+  int32_t exponentiation;     /* ss_expo; SPIN_HALF requires ANALYTIC; SPIN_ONE accepts both (ANALYTIC iff ω_q ≡ 0) */
+  int32_t trotter_cutoff;     /* τ: n = 2^τ squarings' exponent; 0..60; default 24 */
+  int32_t use_rotating_frame; /* 0/1; default 1 */
+  int32_t precision;          /* ss_precision */
+  int32_t field;              /* ss_field */
+} ss_sim_desc;
+
+typedef struct ss_sim ss_sim;  /* opaque handle, owned by the library */
+
+/* Create / destroy a simulator.  Validates the combination; no CUDA call is made. */
+int ss_create(const ss_sim_desc* desc, ss_sim** out);
+void ss_destroy(ss_sim* sim);
+
+/* Number of sweep parameters P of a built-in field (negative if unknown). */
+int ss_num_sweep_params(int32_t field);
+
+/* State dimension of a simulator: 2 (spin-half) or 3 (spin-one). */
+int ss_dim(const ss_sim* sim);
+
+/* Plan the time grid (reading R7): writes K, L and δt = Δt/L.  Pure host arithmetic. */
+int ss_plan(double time_start, double time_end, double time_step_integration, double time_step_output,
+            int64_t* K, int64_t* L, double* dt_fine);
+
+/* Device workspace needed by ss_evaluate for `batch` sweeps of K intervals; includes room for the interval
+ * unitaries when the caller passes d_unitaries = NULL. */
+size_t ss_workspace_bytes(const ss_sim* sim, int64_t batch, int64_t K, int32_t unitaries_in_workspace);
+
+/* Whole hot path on device buffers: interval kernel (§8(a) rows a1–a8) then the state scan (a9).
+ *   d_sweep       device [batch][P] float64
+ *   d_state_init  device [batch][dim] complex128
+ *   d_states      device [batch][K+1][dim] complex128 (out)
+ *   d_unitaries   device [batch][K][dim][dim] complex128 (out) or NULL (then kept in the workspace)
+ *   d_workspace   device, >= ss_workspace_bytes(sim, batch, K, d_unitaries == NULL), 256-byte aligned
+ * Validates sweep/state finiteness (and ω_q ≡ 0 for ANALYTIC spin-one) with a tiny device check that
+ * synchronises the stream once, unless disabled by ss_set_validation(sim, 0). */
+int ss_evaluate(ss_sim* sim, double time_start, double time_end, double time_step_integration,
+                double time_step_output, int64_t batch, const double* d_sweep, const double* d_state_init,
+                double* d_states, double* d_unitaries, void* d_workspace, size_t workspace_bytes, void* stream);
+
+/* Enable (1, default) / disable (0) the synchronous input validation inside ss_evaluate (disable it to capture
+ * ss_evaluate in a CUDA graph). */
+int ss_set_validation(ss_sim* sim, int32_t enabled);
+
+/* Interval kernel only (rows a1–a8) for global interval indices k ∈ [k_begin, k_begin + k_count) of a grid of K
+ * intervals: writes d_unitaries [batch][k_count][dim][dim].  The time grid uses the global k, so a time partition
+ * reproduces the single-GPU operators bit for bit.  No validation kernel, no synchronisation. */
+int ss_compute_unitaries(ss_sim* sim, double time_start, double time_end, double time_step_integration,
+                         double time_step_output, int64_t k_begin, int64_t k_count, int64_t batch,
+                         const double* d_sweep, double* d_unitaries, void* stream);
+
+/* State scan only (row a9): states[b][0] = state_init[b], states[b][k+1] = U[b][k] states[b][k] for
+ * k < k_count.  Decoupled look-back over tiles; d_workspace >= ss_scan_workspace_bytes(dim, batch, k_count). */
+size_t ss_scan_workspace_bytes(int32_t dim, int64_t batch, int64_t k_count);
+int ss_scan_states(int32_t dim, int64_t batch, int64_t k_count, const double* d_unitaries,
+                   const double* d_state_init, double* d_states, void* d_workspace, size_t workspace_bytes,
+                   void* stream);
+
+/* Time-partition pieces (multi-GPU, one long simulation).  Aggregate of a partition:
+ * d_aggregate[b] = U[b][k_count−1] ⋯ U[b][0]  ([batch][dim][dim] complex128).
+ * d_workspace >= ss_aggregate_workspace_bytes(dim, batch, k_count). */
+size_t ss_aggregate_workspace_bytes(int32_t dim, int64_t batch, int64_t k_count);
+int ss_chain_aggregate(int32_t dim, int64_t batch, int64_t k_count, const double* d_unitaries, double* d_aggregate,
+                       void* d_workspace, size_t workspace_bytes, void* stream);
+
+/* Carry of partition `part`: d_carry[b] = A_{part−1} ⋯ A_0 state_init[b], from the all-gathered aggregates
+ * d_aggregates [n_parts][batch][dim][dim] (applied to the state in this fixed order on every rank, so every rank
+ * computes bit-identical carries).  part = 0 copies state_init. */
+int ss_compose_carry(int32_t dim, int64_t batch, int32_t n_parts, int32_t part, const double* d_aggregates,
+                     const double* d_state_init, double* d_carry, void* stream);
+
+/* Building block for element-wise parity: exp(−i(ax Jx + ay Jy + az Jz + aq Q)) for d_args [n][4] float64,
+ * with the simulator's spin / exponentiation / τ / precision; writes d_out [n][dim][dim] complex128. */
+int ss_exponentiate(const ss_sim* sim, int64_t n, const double* d_args, double* d_out, void* stream);
+
+/* Expected spin projection ⟨J⟩ = (ψ†Jxψ, ψ†Jyψ, ψ†Jzψ) for d_states [n][dim] complex128;
+ * writes d_out [n][3] float64. */
+int ss_spin_projection(int32_t spin, int64_t n, const double* d_states, double* d_out, void* stream);
+
+/* End-to-end call on HOST buffers: copies h_sweep/h_state_init to the device, runs the path and copies the states
+ * (and unitaries if h_unitaries != NULL) back, pipelined over `n_chunks` batch chunks on two internal streams so
+ * device→host copies overlap compute.  Synchronous: returns after the results are in host memory.  Device
+ * buffers are allocated once and cached in `sim`.  Pinned host buffers give full copy bandwidth. */
+int ss_evaluate_host(ss_sim* sim, double time_start, double time_end, double time_step_integration,
+                     double time_step_output, int64_t batch, const double* h_sweep, const double* h_state_init,
+                     double* h_states, double* h_unitaries, int32_t n_chunks);
+
+/* Number of CUDA kernels this library has launched in the process so far (launch accounting for bench.py). */
+int64_t ss_kernel_launches(void);
+
+/* Thread-local description of the last error ("" if none). */
+const char* ss_last_error(void);
+
+/* ABI version (major*100 + minor). */
+int ss_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPINSIM_B200_H */

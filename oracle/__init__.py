@@ -64,6 +64,7 @@ def _load():
     lib.oracle_expm_dense.argtypes = [i, P, d, P]
     lib.oracle_fine_step.argtypes = [i, i, i, i, i, i, i, d, d, d, P, ll, ll, d, P]
     lib.oracle_evaluate.argtypes = [i, i, i, i, i, i, i, d, d, d, d, ll, P, P, P, P, i, ll, ll]
+    lib.oracle_chain.argtypes = [i, ll, ll, P, P, P, P]
     lib.oracle_spin_projection.argtypes = [i, ll, P, P]
     lib.oracle_rms_error.argtypes = [ll, i, P, P]
     lib.oracle_rms_error.restype = d
@@ -185,6 +186,17 @@ def evaluate(spin="half", method="cf4", expo="analytic", tau=24, frame=True, fie
     if rc != 0:
         raise ValueError("oracle_evaluate rejected its arguments")
     return states, U
+
+
+def chain(U, psi0, want_aggregate=False):
+    """Sequential long-double chain ψ_{k+1} = U_k ψ_k.  U [B][K][d][d], psi0 [B][d]."""
+    U = _c128(U)
+    B, K, d, _ = U.shape
+    p0 = _c128(psi0).reshape(B, d)
+    states = np.zeros((B, K + 1, d), np.complex128)
+    agg = np.zeros((B, d, d), np.complex128) if want_aggregate else None
+    _load().oracle_chain(d, B, K, _ptr(U), _ptr(p0), _ptr(states), _ptr(agg) if agg is not None else None)
+    return (states, agg) if want_aggregate else states
 
 
 def spin_projection(spin: str, states) -> np.ndarray:

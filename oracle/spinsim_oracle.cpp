@@ -542,6 +542,38 @@ int oracle_evaluate(int spin, int method, int expo, int tau, int frame, int fiel
   return evaluate<double>(c, g, batch, sweep, np, psi0, states, unitaries, nthreads, k_begin, k_end);
 }
 
+// Sequential chain only (Eq. integration_compilation, as the paper's CPU loop P:640), long double:
+// states[b][0] = psi0[b], states[b][k+1] = U[b][k] states[b][k].  Also returns the product A[b] = U[b][K−1]⋯U[b][0]
+// (if `aggregate` is non-NULL) by plain left-multiplication in index order.
+int oracle_chain(int dim, long long batch, long long K, const double* U, const double* psi0, double* states,
+                 double* aggregate) {
+  typedef long double R;
+  for (long long b = 0; b < batch; ++b) {
+    Cx<R> psi[3];
+    for (int i = 0; i < dim; ++i) psi[i] = Cx<R>(psi0[(b * dim + i) * 2], psi0[(b * dim + i) * 2 + 1]);
+    double* sb = states + b * (K + 1) * dim * 2;
+    for (int i = 0; i < dim; ++i) { sb[2 * i] = (double)psi[i].real(); sb[2 * i + 1] = (double)psi[i].imag(); }
+    Mat<R> A = Mat<R>::eye(dim);
+    for (long long k = 0; k < K; ++k) {
+      Mat<R> Uk = Mat<R>::zero(dim);
+      const double* u = U + ((b * K + k) * dim * dim) * 2;
+      for (int i = 0; i < dim; ++i)
+        for (int j = 0; j < dim; ++j) Uk.a[i][j] = Cx<R>(u[2 * (i * dim + j)], u[2 * (i * dim + j) + 1]);
+      Cx<R> nxt[3];
+      for (int i = 0; i < dim; ++i) {
+        nxt[i] = 0;
+        for (int j = 0; j < dim; ++j) nxt[i] += Uk.a[i][j] * psi[j];
+      }
+      for (int i = 0; i < dim; ++i) psi[i] = nxt[i];
+      double* o = sb + (k + 1) * dim * 2;
+      for (int i = 0; i < dim; ++i) { o[2 * i] = (double)psi[i].real(); o[2 * i + 1] = (double)psi[i].imag(); }
+      if (aggregate) A = mul(Uk, A);
+    }
+    if (aggregate) store(A, aggregate + b * dim * dim * 2);
+  }
+  return 0;
+}
+
 // Expected spin projection ⟨J⟩ = (ψ†Jxψ, ψ†Jyψ, ψ†Jzψ), long double.
 int oracle_spin_projection(int spin, long long n, const double* states, double* out) {
   const int dim = (spin == HALF) ? 2 : 3;

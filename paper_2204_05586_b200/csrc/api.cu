@@ -1,0 +1,454 @@
+// api.cu — the C ABI declared in include/spinsim_b200.h: validation, planning, workspace layout and launches.
+// Host code only; the arithmetic of the method lives in the kernels (interval_*.cu, scan.cu).
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/spinsim_b200.h"
+#include "dispatch.h"
+#include "interval_kernel.cuh"
+#include "kernels.h"
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<int64_t> g_launches{0};
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(SS_ERR_CUDA, "%s: CUDA error %d (%s)", where, (int)e, cudaGetErrorString(e));
+}
+
+inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+int field_params(int field) {
+  switch (field) {
+    case SS_FIELD_CONSTANT: return 4;
+    case SS_FIELD_RABI_LINEAR: return 2;
+    case SS_FIELD_RABI_CIRCULAR: return 2;
+    case SS_FIELD_NEURAL: return 7;
+    case SS_FIELD_GRADIENT: return 2;
+  }
+  return -1;
+}
+
+// Column of the sweep table holding ω_q (must be 0 for the analytic spin-one exponentiator), or −1.
+int qcol_of(int field) {
+  switch (field) {
+    case SS_FIELD_CONSTANT: return 3;
+    case SS_FIELD_NEURAL: return 6;
+  }
+  return -1;
+}
+
+}  // namespace
+
+struct ss_sim {
+  ss_sim_desc d;
+  int dim = 0;
+  int P = 0;
+  int validate = 1;
+  ssb::IntervalLaunchFn interval = nullptr;
+  ssb::ExpoLaunchFn expo = nullptr;
+  // ss_evaluate_host staging (two pipeline slots)
+  cudaStream_t streams[2] = {nullptr, nullptr};
+  int device = -1;
+  struct Slot {
+    void* buf = nullptr;
+    size_t cap = 0;
+  } slots[2];
+};
+
+namespace {
+
+ssb::IntervalLaunchFn pick_interval(const ss_sim_desc& d) {
+  const bool f32 = d.precision == SS_FP32;
+  if (d.spin == SS_SPIN_HALF)
+    return f32 ? ssb::interval_table_half_f32(d.integration, d.field) : ssb::interval_table_half_f64(d.integration, d.field);
+  if (d.exponentiation == SS_EXP_LIE_TROTTER)
+    return f32 ? ssb::interval_table_one_lt_f32(d.integration, d.field)
+               : ssb::interval_table_one_lt_f64(d.integration, d.field);
+  return f32 ? ssb::interval_table_one_an_f32(d.integration, d.field) : ssb::interval_table_one_an_f64(d.integration, d.field);
+}
+
+ssb::ExpoLaunchFn pick_expo(const ss_sim_desc& d) {
+  const bool f32 = d.precision == SS_FP32;
+  if (d.spin == SS_SPIN_HALF) return f32 ? ssb::expo_table_half_f32() : ssb::expo_table_half_f64();
+  if (d.exponentiation == SS_EXP_LIE_TROTTER) return f32 ? ssb::expo_table_one_lt_f32() : ssb::expo_table_one_lt_f64();
+  return f32 ? ssb::expo_table_one_an_f32() : ssb::expo_table_one_an_f64();
+}
+
+int plan_grid(double t0, double t1, double dt_int, double dt_out, int64_t* K, int64_t* L, double* dt) {
+  if (!std::isfinite(t0) || !std::isfinite(t1) || !std::isfinite(dt_int) || !std::isfinite(dt_out))
+    return fail(SS_ERR_NONFINITE, "time arguments must be finite");
+  if (!(t1 > t0)) return fail(SS_ERR_INVALID, "time_end (%g) must exceed time_start (%g)", t1, t0);
+  if (!(dt_int > 0)) return fail(SS_ERR_INVALID, "time_step_integration must be > 0");
+  if (!(dt_out > 0)) return fail(SS_ERR_INVALID, "time_step_output must be > 0");
+  const double kf = (t1 - t0) / dt_out, lf = dt_out / dt_int;
+  if (kf > 9.0e15 || lf > 9.0e15) return fail(SS_ERR_INVALID, "time grid too large");
+  const long long k = std::llround(kf), l = std::llround(lf);
+  if (k < 1 || std::fabs(kf - (double)k) > 1e-9 * kf)
+    return fail(SS_ERR_INVALID, "(time_end - time_start)/time_step_output = %.17g is not an integer", kf);
+  if (l < 1 || std::fabs(lf - (double)l) > 1e-9 * lf)
+    return fail(SS_ERR_INVALID, "time_step_output/time_step_integration = %.17g is not an integer", lf);
+  *K = k;
+  *L = l;
+  *dt = dt_out / (double)l;
+  return SS_OK;
+}
+
+ssb::IntervalParams make_params(const ss_sim* s, double t0, double dt_out, double dt, int64_t L, int64_t k_begin,
+                                int64_t k_count, int64_t batch, const double* sweep, double* U) {
+  ssb::IntervalParams p;
+  p.t0 = t0;
+  p.dt_out = dt_out;
+  p.dt = dt;
+  p.g1dt = ssb::kG1 * dt;      // host IEEE double multiply: fl(g1·δt) (reading R7)
+  p.g2dt = ssb::kG2 * dt;
+  p.half_dt = 0.5 * dt;
+  p.half_dt_out = 0.5 * dt_out;
+  p.L = L;
+  p.k_begin = k_begin;
+  p.k_count = k_count;
+  p.batch = batch;
+  p.n_threads = batch * k_count;
+  p.tau = s->d.trotter_cutoff;
+  p.frame = s->d.use_rotating_frame;
+  p.sweep = sweep;
+  p.unitaries = U;
+  return p;
+}
+
+int check_device_ptr(const void* p, const char* name) {
+  if (!p) return fail(SS_ERR_INVALID, "%s is NULL", name);
+  if ((reinterpret_cast<uintptr_t>(p) & 15) != 0) return fail(SS_ERR_INVALID, "%s must be 16-byte aligned", name);
+  return SS_OK;
+}
+
+int ensure_device() {
+  int n = 0;
+  const cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) return fail(SS_ERR_CUDA, "no CUDA device available (no CPU fallback exists)");
+  return SS_OK;
+}
+
+int launch_interval_checked(ss_sim* s, const ssb::IntervalParams& p, cudaStream_t st) {
+  const cudaError_t e = s->interval(p, st);
+  if (e != cudaSuccess) return cuda_fail(e, "interval kernel launch");
+  g_launches.fetch_add(1);
+  return SS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ss_version(void) { return 100; }
+
+const char* ss_last_error(void) { return g_err.c_str(); }
+
+int64_t ss_kernel_launches(void) { return g_launches.load(); }
+
+int ss_num_sweep_params(int32_t field) { return field_params(field); }
+
+int ss_create(const ss_sim_desc* desc, ss_sim** out) {
+  if (!desc || !out) return fail(SS_ERR_INVALID, "desc and out must be non-NULL");
+  const ss_sim_desc& d = *desc;
+  if (d.spin != SS_SPIN_HALF && d.spin != SS_SPIN_ONE) return fail(SS_ERR_INVALID, "spin must be 1 (half) or 2 (one), got %d", d.spin);
+  if (d.integration < SS_CF4 || d.integration > SS_HEUN) return fail(SS_ERR_INVALID, "integration %d unknown", d.integration);
+  if (d.exponentiation != SS_EXP_ANALYTIC && d.exponentiation != SS_EXP_LIE_TROTTER)
+    return fail(SS_ERR_INVALID, "exponentiation %d unknown", d.exponentiation);
+  if (d.spin == SS_SPIN_HALF && d.exponentiation != SS_EXP_ANALYTIC)
+    return fail(SS_ERR_UNSUPPORTED, "spin-half uses the analytic SU(2) exponentiator (P:359); Lie-Trotter is spin-one only");
+  if (d.trotter_cutoff < 0 || d.trotter_cutoff > 60) return fail(SS_ERR_INVALID, "trotter_cutoff %d outside 0..60", d.trotter_cutoff);
+  if (d.use_rotating_frame != 0 && d.use_rotating_frame != 1) return fail(SS_ERR_INVALID, "use_rotating_frame must be 0 or 1");
+  if (d.precision != SS_FP64 && d.precision != SS_FP32) return fail(SS_ERR_INVALID, "precision %d unknown", d.precision);
+  if (field_params(d.field) < 0) return fail(SS_ERR_INVALID, "field %d unknown", d.field);
+  ss_sim* s = new ss_sim;
+  s->d = d;
+  s->dim = d.spin == SS_SPIN_HALF ? 2 : 3;
+  s->P = field_params(d.field);
+  s->interval = pick_interval(d);
+  s->expo = pick_expo(d);
+  if (!s->interval || !s->expo) {
+    delete s;
+    return fail(SS_ERR_UNSUPPORTED, "no kernel instance for this combination");
+  }
+  *out = s;
+  g_err.clear();
+  return SS_OK;
+}
+
+void ss_destroy(ss_sim* s) {
+  if (!s) return;
+  for (auto& sl : s->slots)
+    if (sl.buf) cudaFree(sl.buf);
+  for (auto& st : s->streams)
+    if (st) cudaStreamDestroy(st);
+  delete s;
+}
+
+int ss_dim(const ss_sim* s) { return s ? s->dim : fail(SS_ERR_INVALID, "sim is NULL"); }
+
+int ss_set_validation(ss_sim* s, int32_t enabled) {
+  if (!s) return fail(SS_ERR_INVALID, "sim is NULL");
+  s->validate = enabled ? 1 : 0;
+  return SS_OK;
+}
+
+int ss_plan(double t0, double t1, double dt_int, double dt_out, int64_t* K, int64_t* L, double* dt) {
+  if (!K || !L || !dt) return fail(SS_ERR_INVALID, "K, L, dt_fine must be non-NULL");
+  return plan_grid(t0, t1, dt_int, dt_out, K, L, dt);
+}
+
+size_t ss_scan_workspace_bytes(int32_t dim, int64_t batch, int64_t k_count) {
+  if ((dim != 2 && dim != 3) || batch < 0 || k_count < 0) return 0;
+  return ssb::scan_workspace_bytes(dim, batch, k_count);
+}
+
+size_t ss_aggregate_workspace_bytes(int32_t dim, int64_t batch, int64_t k_count) {
+  if ((dim != 2 && dim != 3) || batch < 0 || k_count < 0) return 0;
+  return ssb::aggregate_workspace_bytes(dim, batch, k_count);
+}
+
+// Layout: [0, 256) control (validation flag) | scan workspace | U (optional).
+size_t ss_workspace_bytes(const ss_sim* s, int64_t batch, int64_t K, int32_t unitaries_in_workspace) {
+  if (!s || batch < 0 || K < 0) return 0;
+  size_t n = 256 + align256(ssb::scan_workspace_bytes(s->dim, batch, K));
+  if (unitaries_in_workspace) n += align256(sizeof(double) * 2 * s->dim * s->dim * (size_t)batch * (size_t)K);
+  return n;
+}
+
+static int validate_inputs(ss_sim* s, int64_t batch, const double* d_sweep, const double* d_psi0, int* d_flag,
+                           cudaStream_t st) {
+  const int qcol = (s->dim == 3 && s->d.exponentiation == SS_EXP_ANALYTIC) ? qcol_of(s->d.field) : -1;
+  cudaError_t e = cudaMemsetAsync(d_flag, 0, sizeof(int), st);
+  if (e != cudaSuccess) return cuda_fail(e, "validation memset");
+  e = ssb::launch_validate(batch * s->P, d_sweep, s->P, qcol, batch * 2 * s->dim, d_psi0, d_flag, st);
+  if (e != cudaSuccess) return cuda_fail(e, "validation launch");
+  g_launches.fetch_add(1);
+  int h = 0;
+  e = cudaMemcpyAsync(&h, d_flag, sizeof(int), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "validation readback");
+  if (h & 1) return fail(SS_ERR_NONFINITE, "sweep parameters or state_init contain a non-finite value");
+  if (h & 2) return fail(SS_ERR_INVALID, "the analytic spin-one exponentiator requires omega_q == 0 in every sweep (reading R14)");
+  return SS_OK;
+}
+
+int ss_compute_unitaries(ss_sim* s, double t0, double t1, double dt_int, double dt_out, int64_t k_begin,
+                         int64_t k_count, int64_t batch, const double* d_sweep, double* d_U, void* stream) {
+  if (!s) return fail(SS_ERR_INVALID, "sim is NULL");
+  int64_t K, L;
+  double dt;
+  int rc = plan_grid(t0, t1, dt_int, dt_out, &K, &L, &dt);
+  if (rc) return rc;
+  if (batch < 1) return fail(SS_ERR_INVALID, "batch must be >= 1");
+  if (k_begin < 0 || k_count < 1 || k_begin + k_count > K)
+    return fail(SS_ERR_INVALID, "interval range [%lld, %lld) outside [0, K=%lld)", (long long)k_begin,
+                (long long)(k_begin + k_count), (long long)K);
+  if ((rc = check_device_ptr(d_sweep, "d_sweep")) || (rc = check_device_ptr(d_U, "d_unitaries"))) return rc;
+  if ((rc = ensure_device())) return rc;
+  const auto p = make_params(s, t0, dt_out, dt, L, k_begin, k_count, batch, d_sweep, d_U);
+  return launch_interval_checked(s, p, static_cast<cudaStream_t>(stream));
+}
+
+int ss_scan_states(int32_t dim, int64_t batch, int64_t k_count, const double* d_U, const double* d_psi0,
+                   double* d_states, void* d_ws, size_t ws_bytes, void* stream) {
+  if (dim != 2 && dim != 3) return fail(SS_ERR_INVALID, "dim must be 2 or 3");
+  if (batch < 1 || k_count < 1) return fail(SS_ERR_INVALID, "batch and k_count must be >= 1");
+  int rc;
+  if ((rc = check_device_ptr(d_U, "d_unitaries")) || (rc = check_device_ptr(d_psi0, "d_state_init")) ||
+      (rc = check_device_ptr(d_states, "d_states")) || (rc = check_device_ptr(d_ws, "d_workspace")))
+    return rc;
+  const size_t need = ssb::scan_workspace_bytes(dim, batch, k_count);
+  if (ws_bytes < need) return fail(SS_ERR_INVALID, "workspace_bytes %zu < required %zu", ws_bytes, need);
+  if ((rc = ensure_device())) return rc;
+  int n = 0;
+  const cudaError_t e = ssb::launch_scan(dim, batch, k_count, d_U, d_psi0, d_states, d_ws,
+                                         static_cast<cudaStream_t>(stream), &n);
+  g_launches.fetch_add(n);
+  return e == cudaSuccess ? SS_OK : cuda_fail(e, "scan launch");
+}
+
+int ss_chain_aggregate(int32_t dim, int64_t batch, int64_t k_count, const double* d_U, double* d_agg, void* d_ws,
+                       size_t ws_bytes, void* stream) {
+  if (dim != 2 && dim != 3) return fail(SS_ERR_INVALID, "dim must be 2 or 3");
+  if (batch < 1 || k_count < 1) return fail(SS_ERR_INVALID, "batch and k_count must be >= 1");
+  int rc;
+  if ((rc = check_device_ptr(d_U, "d_unitaries")) || (rc = check_device_ptr(d_agg, "d_aggregate")) ||
+      (rc = check_device_ptr(d_ws, "d_workspace")))
+    return rc;
+  const size_t need = ssb::aggregate_workspace_bytes(dim, batch, k_count);
+  if (ws_bytes < need) return fail(SS_ERR_INVALID, "workspace_bytes %zu < required %zu", ws_bytes, need);
+  if ((rc = ensure_device())) return rc;
+  int n = 0;
+  const cudaError_t e = ssb::launch_aggregate(dim, batch, k_count, d_U, d_agg, d_ws, static_cast<cudaStream_t>(stream), &n);
+  g_launches.fetch_add(n);
+  return e == cudaSuccess ? SS_OK : cuda_fail(e, "aggregate launch");
+}
+
+int ss_compose_carry(int32_t dim, int64_t batch, int32_t n_parts, int32_t part, const double* d_aggs,
+                     const double* d_psi0, double* d_carry, void* stream) {
+  if (dim != 2 && dim != 3) return fail(SS_ERR_INVALID, "dim must be 2 or 3");
+  if (batch < 1) return fail(SS_ERR_INVALID, "batch must be >= 1");
+  if (n_parts < 1 || part < 0 || part >= n_parts) return fail(SS_ERR_INVALID, "part %d outside [0, %d)", part, n_parts);
+  int rc;
+  if ((part > 0 && (rc = check_device_ptr(d_aggs, "d_aggregates"))) || (rc = check_device_ptr(d_psi0, "d_state_init")) ||
+      (rc = check_device_ptr(d_carry, "d_carry")))
+    return rc;
+  if ((rc = ensure_device())) return rc;
+  const cudaError_t e = ssb::launch_compose_carry(dim, batch, part, d_aggs, d_psi0, d_carry, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "compose_carry launch");
+  g_launches.fetch_add(1);
+  return SS_OK;
+}
+
+int ss_evaluate(ss_sim* s, double t0, double t1, double dt_int, double dt_out, int64_t batch, const double* d_sweep,
+                const double* d_psi0, double* d_states, double* d_U, void* d_ws, size_t ws_bytes, void* stream) {
+  if (!s) return fail(SS_ERR_INVALID, "sim is NULL");
+  int64_t K, L;
+  double dt;
+  int rc = plan_grid(t0, t1, dt_int, dt_out, &K, &L, &dt);
+  if (rc) return rc;
+  if (batch < 1) return fail(SS_ERR_INVALID, "batch must be >= 1");
+  if ((rc = check_device_ptr(d_sweep, "d_sweep")) || (rc = check_device_ptr(d_psi0, "d_state_init")) ||
+      (rc = check_device_ptr(d_states, "d_states")) || (rc = check_device_ptr(d_ws, "d_workspace")))
+    return rc;
+  if ((reinterpret_cast<uintptr_t>(d_ws) & 255) != 0) return fail(SS_ERR_INVALID, "d_workspace must be 256-byte aligned");
+  const size_t need = ss_workspace_bytes(s, batch, K, d_U == nullptr);
+  if (ws_bytes < need) return fail(SS_ERR_INVALID, "workspace_bytes %zu < required %zu", ws_bytes, need);
+  if ((rc = ensure_device())) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char* w = static_cast<char*>(d_ws);
+  void* scan_ws = w + 256;
+  double* U = d_U ? d_U : reinterpret_cast<double*>(w + 256 + align256(ssb::scan_workspace_bytes(s->dim, batch, K)));
+  if (s->validate && (rc = validate_inputs(s, batch, d_sweep, d_psi0, reinterpret_cast<int*>(w), st))) return rc;
+  const auto p = make_params(s, t0, dt_out, dt, L, 0, K, batch, d_sweep, U);
+  if ((rc = launch_interval_checked(s, p, st))) return rc;
+  return ss_scan_states(s->dim, batch, K, U, d_psi0, d_states, scan_ws, need - 256, stream);
+}
+
+int ss_exponentiate(const ss_sim* s, int64_t n, const double* d_args, double* d_out, void* stream) {
+  if (!s) return fail(SS_ERR_INVALID, "sim is NULL");
+  if (n < 1) return fail(SS_ERR_INVALID, "n must be >= 1");
+  int rc;
+  if ((rc = check_device_ptr(d_args, "d_args")) || (rc = check_device_ptr(d_out, "d_out"))) return rc;
+  if ((rc = ensure_device())) return rc;
+  const cudaError_t e = s->expo(n, d_args, s->d.trotter_cutoff, d_out, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "exponentiate launch");
+  g_launches.fetch_add(1);
+  return SS_OK;
+}
+
+int ss_spin_projection(int32_t spin, int64_t n, const double* d_states, double* d_out, void* stream) {
+  if (spin != SS_SPIN_HALF && spin != SS_SPIN_ONE) return fail(SS_ERR_INVALID, "spin must be 1 or 2");
+  if (n < 1) return fail(SS_ERR_INVALID, "n must be >= 1");
+  int rc;
+  if ((rc = check_device_ptr(d_states, "d_states")) || (rc = check_device_ptr(d_out, "d_out"))) return rc;
+  if ((rc = ensure_device())) return rc;
+  const cudaError_t e = ssb::launch_spin_projection(spin == SS_SPIN_HALF ? 2 : 3, n, d_states, d_out,
+                                                    static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "spin_projection launch");
+  g_launches.fetch_add(1);
+  return SS_OK;
+}
+
+int ss_evaluate_host(ss_sim* s, double t0, double t1, double dt_int, double dt_out, int64_t batch, const double* h_sweep,
+                     const double* h_psi0, double* h_states, double* h_U, int32_t n_chunks) {
+  if (!s) return fail(SS_ERR_INVALID, "sim is NULL");
+  int64_t K, L;
+  double dt;
+  int rc = plan_grid(t0, t1, dt_int, dt_out, &K, &L, &dt);
+  if (rc) return rc;
+  if (batch < 1) return fail(SS_ERR_INVALID, "batch must be >= 1");
+  if (!h_sweep || !h_psi0 || !h_states) return fail(SS_ERR_INVALID, "h_sweep, h_state_init, h_states must be non-NULL");
+  if (n_chunks < 1) n_chunks = 1;
+  if (n_chunks > batch) n_chunks = (int32_t)batch;
+  // host-side input validation (host data: no device round trip needed)
+  const int qcol = (s->dim == 3 && s->d.exponentiation == SS_EXP_ANALYTIC) ? qcol_of(s->d.field) : -1;
+  for (int64_t i = 0; i < batch * s->P; ++i) {
+    if (!std::isfinite(h_sweep[i])) return fail(SS_ERR_NONFINITE, "sweep parameter %lld is not finite", (long long)i);
+    if (qcol >= 0 && i % s->P == qcol && h_sweep[i] != 0.0)
+      return fail(SS_ERR_INVALID, "the analytic spin-one exponentiator requires omega_q == 0 in every sweep (reading R14)");
+  }
+  for (int64_t i = 0; i < batch * 2 * s->dim; ++i)
+    if (!std::isfinite(h_psi0[i])) return fail(SS_ERR_NONFINITE, "state_init value %lld is not finite", (long long)i);
+  if ((rc = ensure_device())) return rc;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  if (s->device != dev) {  // (re)create per-device streams and drop buffers of another device
+    for (auto& st : s->streams) if (st) cudaStreamDestroy(st), st = nullptr;
+    for (auto& sl : s->slots) if (sl.buf) cudaFree(sl.buf), sl.buf = nullptr, sl.cap = 0;
+    for (auto& st : s->streams)
+      if ((e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)) != cudaSuccess) return cuda_fail(e, "stream create");
+    s->device = dev;
+  }
+  const int D = s->dim;
+  const int64_t cb_max = (batch + n_chunks - 1) / n_chunks;
+  const size_t sweep_b = align256(sizeof(double) * s->P * cb_max);
+  const size_t psi0_b = align256(sizeof(double) * 2 * D * cb_max);
+  const size_t states_b = align256(sizeof(double) * 2 * D * (size_t)cb_max * (K + 1));
+  const size_t U_b = align256(sizeof(double) * 2 * D * D * (size_t)cb_max * K);
+  const size_t scan_b = align256(ssb::scan_workspace_bytes(D, cb_max, K));
+  const size_t slot_bytes = sweep_b + psi0_b + states_b + U_b + scan_b;
+  const int nslots = n_chunks > 1 ? 2 : 1;
+  for (int k = 0; k < nslots; ++k) {
+    auto& sl = s->slots[k];
+    if (sl.cap < slot_bytes) {
+      if (sl.buf) cudaFree(sl.buf);
+      sl.buf = nullptr;
+      sl.cap = 0;
+      if ((e = cudaMalloc(&sl.buf, slot_bytes)) != cudaSuccess) return cuda_fail(e, "cudaMalloc (host-API staging)");
+      sl.cap = slot_bytes;
+    }
+  }
+  for (int64_t c = 0, b0 = 0; c < n_chunks; ++c) {
+    const int64_t cb = std::min<int64_t>(cb_max, batch - b0);
+    if (cb <= 0) break;
+    const int k = (int)(c % nslots);
+    cudaStream_t st = s->streams[k];
+    char* base = static_cast<char*>(s->slots[k].buf);
+    double* d_sweep = reinterpret_cast<double*>(base);
+    double* d_psi0 = reinterpret_cast<double*>(base + sweep_b);
+    double* d_states = reinterpret_cast<double*>(base + sweep_b + psi0_b);
+    double* d_U = reinterpret_cast<double*>(base + sweep_b + psi0_b + states_b);
+    void* d_scan = base + sweep_b + psi0_b + states_b + U_b;
+    if ((e = cudaMemcpyAsync(d_sweep, h_sweep + b0 * s->P, sizeof(double) * s->P * cb, cudaMemcpyHostToDevice, st)) ||
+        (e = cudaMemcpyAsync(d_psi0, h_psi0 + b0 * 2 * D, sizeof(double) * 2 * D * cb, cudaMemcpyHostToDevice, st)))
+      return cuda_fail(e, "H2D copy");
+    const auto p = make_params(s, t0, dt_out, dt, L, 0, K, cb, d_sweep, d_U);
+    if ((rc = launch_interval_checked(s, p, st))) return rc;
+    int n = 0;
+    if ((e = ssb::launch_scan(D, cb, K, d_U, d_psi0, d_states, d_scan, st, &n)) != cudaSuccess)
+      return cuda_fail(e, "scan launch");
+    g_launches.fetch_add(n);
+    if ((e = cudaMemcpyAsync(h_states + b0 * 2 * D * (K + 1), d_states, sizeof(double) * 2 * D * cb * (K + 1),
+                             cudaMemcpyDeviceToHost, st)))
+      return cuda_fail(e, "D2H copy (states)");
+    if (h_U && (e = cudaMemcpyAsync(h_U + b0 * 2 * D * D * K, d_U, sizeof(double) * 2 * D * D * cb * K,
+                                    cudaMemcpyDeviceToHost, st)))
+      return cuda_fail(e, "D2H copy (unitaries)");
+    b0 += cb;
+  }
+  for (int k = 0; k < nslots; ++k)
+    if ((e = cudaStreamSynchronize(s->streams[k])) != cudaSuccess) return cuda_fail(e, "stream synchronize");
+  return SS_OK;
+}
+
+}  // extern "C"

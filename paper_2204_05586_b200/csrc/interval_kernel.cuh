@@ -1,0 +1,169 @@
+// interval_kernel.cuh — the per-interval unitary kernel (SURVEY §8(a) rows a1–a8).
+//
+// One thread ↔ one (sweep b, interval k): it enters the rotating frame at ω_r = ω_z(t_k + Δt/2)
+// (P:539-541), runs the L fine steps of CF4 (Eq. cf4_implementation) — two Gauss-point field samples
+// (P:325-329), frame rotation, weights, two exponentials, u = e₂e₁ premultiplied into U_r
+// — holding U_r − I in registers in residual form (reading R9), and finally writes the lab-frame
+// U_k = R_{ω_r}(−Δt) U_r (Eq. exit_rotating_frame).
+//
+// The work per thread is ~6e3 FP64 instructions per fine step for spin-one Lie–Trotter (93 % in the τ residual
+// squarings), all register-resident: the kernel is FP64-pipe bound, so the launch is sized for
+// occupancy with full ILP (18 independent accumulation chains per squaring) rather than for memory.
+#pragma once
+
+#include "spinsim_device.cuh"
+
+namespace ssb {
+
+struct IntervalParams {
+  double t0;          // time_start
+  double dt_out;      // Δt
+  double dt;          // δt = Δt/L
+  double g1dt, g2dt;  // fl(g1·δt), fl(g2·δt)
+  double half_dt;     // fl(0.5·δt)
+  double half_dt_out; // fl(0.5·Δt)
+  int64_t L;
+  int64_t k_begin, k_count, batch;
+  int64_t n_threads;  // batch·k_count
+  int32_t tau;
+  int32_t frame;
+  const double* sweep;  // [batch][P]
+  double* unitaries;    // [batch][k_count][D][D] complex128
+};
+
+constexpr int kIntervalThreads = 128;
+
+template <int F>
+__device__ __forceinline__ void sample_in_frame(const Field<F>& fld, double off, double omega_r, int frame,
+                                                double f[4]) {
+  fld.sample(off, f);
+  if (frame) to_rotating_frame(f, off, omega_r);
+}
+
+template <int SPIN, int EXPO, int METHOD, int FIELD, typename T>
+__global__ void __launch_bounds__(kIntervalThreads)
+interval_kernel(const IntervalParams prm) {
+  constexpr int D = SpinDim<SPIN>::D;
+  constexpr int P = FieldParams<FIELD>::P;
+  const int64_t i = (int64_t)blockIdx.x * kIntervalThreads + threadIdx.x;
+  if (i >= prm.n_threads) return;
+  const int64_t b = i / prm.k_count;
+  const int64_t k = prm.k_begin + (i - b * prm.k_count);
+
+  double p[P];
+#pragma unroll
+  for (int j = 0; j < P; ++j) p[j] = __ldg(prm.sweep + b * P + j);
+
+  // a1: t_k = fl(t0 + fl(k·Δt)) (reading R7); ω_r from the lab field at the interval midpoint.
+  const double t_k = __dadd_rn(prm.t0, __dmul_rn((double)k, prm.dt_out));
+  Field<FIELD> fld;
+  fld.init(p, t_k);
+  double omega_r = 0.0;
+  if (prm.frame) {
+    double f[4];
+    fld.sample(prm.half_dt_out, f);
+    omega_r = f[2];
+  }
+
+  Res<D, T> A;   // U_r − I, U_r initialised to the identity
+  res_zero(A);
+
+#pragma unroll 1
+  for (int64_t l = 0; l < prm.L; ++l) {
+    const double base = __dmul_rn((double)l, prm.dt);
+    Res<D, T> u;
+    if (METHOD == CF4) {
+      // a2/a3: samples at t_k + (l + g1,2)δt, rotated into the frame.
+      double f1[4], f2[4];
+      sample_in_frame(fld, __dadd_rn(base, prm.g1dt), omega_r, prm.frame, f1);
+      sample_in_frame(fld, __dadd_rn(base, prm.g2dt), omega_r, prm.frame, f2);
+      // a4: H̄1 δt = (w+ f1 + w− f2) δt, H̄2 δt = (w− f1 + w+ f2) δt (Eqs. cf4_sample_1/2).
+      T a1[4], a2[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        a1[j] = (T)(fma(kWPlus, f1[j], kWMinus * f2[j]) * prm.dt);
+        a2[j] = (T)(fma(kWMinus, f1[j], kWPlus * f2[j]) * prm.dt);
+      }
+      // a5/a6: exponentials; a7: u = e2·e1 (Eq. cf4_implementation), residual form.
+      Res<D, T> e1, e2;
+      Expo<SPIN, EXPO, T>::run(a1, prm.tau, e1);
+      Expo<SPIN, EXPO, T>::run(a2, prm.tau, e2);
+      res_mul<D, T>(e2, e1, u);
+    } else {
+      double f[4];
+      if (METHOD == MIDPOINT) {                       // one sample at t + δt/2 (reading R13)
+        sample_in_frame(fld, __dadd_rn(base, prm.half_dt), omega_r, prm.frame, f);
+      } else {                                        // HEUN: average of t and t + δt
+        double fa[4], fb[4];
+        sample_in_frame(fld, base, omega_r, prm.frame, fa);
+        sample_in_frame(fld, __dmul_rn((double)(l + 1), prm.dt), omega_r, prm.frame, fb);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) f[j] = 0.5 * (fa[j] + fb[j]);
+      }
+      T a[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) a[j] = (T)(f[j] * prm.dt);
+      Expo<SPIN, EXPO, T>::run(a, prm.tau, u);
+    }
+    // a7: U_r ← u·U_r, residual form: A ← u + A + u·A.
+    Res<D, T> An;
+    res_mul<D, T>(u, A, An);
+    A = An;
+  }
+
+  // a8: U_k = R_{ω_r}(−Δt)(I + A) = diag(e^{−iω_r m Δt})(I + A); written as complex128.
+  double ph_re[D], ph_im[D];
+  {
+    double s, c;
+    if (D == 2) sincos(0.5 * omega_r * prm.dt_out, &s, &c);
+    else sincos(omega_r * prm.dt_out, &s, &c);
+    ph_re[0] = c; ph_im[0] = -s;                      // m = +1 (or +½)
+    ph_re[D - 1] = c; ph_im[D - 1] = s;               // m = −1 (or −½)
+    if (D == 3) { ph_re[1] = 1.0; ph_im[1] = 0.0; }   // m = 0
+  }
+  double2* out = reinterpret_cast<double2*>(prm.unitaries) + i * (D * D);
+#pragma unroll
+  for (int r = 0; r < D; ++r)
+#pragma unroll
+    for (int cc = 0; cc < D; ++cc) {
+      const double mr = (double)A.re[r * D + cc] + (r == cc ? 1.0 : 0.0);
+      const double mi = (double)A.im[r * D + cc];
+      out[r * D + cc] = make_double2(ph_re[r] * mr - ph_im[r] * mi, ph_re[r] * mi + ph_im[r] * mr);
+    }
+}
+
+template <int SPIN, int EXPO, int METHOD, int FIELD, typename T>
+cudaError_t launch_interval(const IntervalParams& prm, cudaStream_t stream) {
+  const int64_t blocks = (prm.n_threads + kIntervalThreads - 1) / kIntervalThreads;
+  if (blocks <= 0) return cudaSuccess;
+  interval_kernel<SPIN, EXPO, METHOD, FIELD, T><<<(unsigned)blocks, kIntervalThreads, 0, stream>>>(prm);
+  return cudaGetLastError();
+}
+
+// Small kernel for element-wise parity of the exponentiators (ss_exponentiate).
+template <int SPIN, int EXPO, typename T>
+__global__ void exponentiate_kernel(int64_t n, const double* args, int tau, double* out) {
+  constexpr int D = SpinDim<SPIN>::D;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  T a[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) a[j] = (T)args[4 * i + j];
+  Res<D, T> e;
+  Expo<SPIN, EXPO, T>::run(a, tau, e);
+  double2* o = reinterpret_cast<double2*>(out) + i * D * D;
+#pragma unroll
+  for (int r = 0; r < D; ++r)
+#pragma unroll
+    for (int c = 0; c < D; ++c)
+      o[r * D + c] = make_double2((double)e.re[r * D + c] + (r == c ? 1.0 : 0.0), (double)e.im[r * D + c]);
+}
+
+template <int SPIN, int EXPO, typename T>
+cudaError_t launch_exponentiate(int64_t n, const double* args, int tau, double* out, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  exponentiate_kernel<SPIN, EXPO, T><<<(unsigned)((n + 127) / 128), 128, 0, stream>>>(n, args, tau, out);
+  return cudaGetLastError();
+}
+
+}  // namespace ssb

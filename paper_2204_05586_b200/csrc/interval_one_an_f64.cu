@@ -1,0 +1,6 @@
+// Interval-kernel instances: spin/expo/precision = one_an_f64.
+#define SS_SPIN ssb::SPIN_ONE
+#define SS_EXPO ssb::EXP_ANALYTIC
+#define SS_T double
+#define SS_NAME one_an_f64
+#include "interval_instances.inc"

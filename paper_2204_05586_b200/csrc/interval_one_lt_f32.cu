@@ -1,0 +1,6 @@
+// Interval-kernel instances: spin/expo/precision = one_lt_f32.
+#define SS_SPIN ssb::SPIN_ONE
+#define SS_EXPO ssb::EXP_LIE_TROTTER
+#define SS_T float
+#define SS_NAME one_lt_f32
+#include "interval_instances.inc"

@@ -1,0 +1,21 @@
+// kernels.h — host-side entry points of the kernels in scan.cu (internal to the library).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stddef.h>
+
+#include "spinsim_device.cuh"
+
+namespace ssb {
+size_t scan_workspace_bytes(int dim, int64_t batch, int64_t k_count);
+size_t aggregate_workspace_bytes(int dim, int64_t batch, int64_t k_count);
+cudaError_t launch_scan(int dim, int64_t batch, int64_t k_count, const double* U, const double* psi0, double* states,
+                        void* ws, cudaStream_t s, int* launches);
+cudaError_t launch_aggregate(int dim, int64_t batch, int64_t k_count, const double* U, double* aggregate, void* ws,
+                             cudaStream_t s, int* launches);
+cudaError_t launch_compose_carry(int dim, int64_t batch, int part, const double* aggs, const double* psi0,
+                                 double* carry, cudaStream_t s);
+cudaError_t launch_spin_projection(int dim, int64_t n, const double* states, double* out, cudaStream_t s);
+cudaError_t launch_validate(int64_t n_sweep, const double* sweep, int P, int qcol, int64_t n_state,
+                            const double* state, int* flag, cudaStream_t s);
+}  // namespace ssb

@@ -1,0 +1,311 @@
+// spinsim_device.cuh — device math of the Spinsim hot path for sm_100a (rows a1–a8 of SURVEY §8(a)).
+//
+// Everything is header-only __device__ __forceinline__ code, templated on the stepper real type T (double for the
+// FP64 path, float for the FP32 mode).  Time, phases, field samples and the frame angle are always FP64
+// (FP32 mode).  No tensor cores: the operands are 2×2 / 3×3 complex matrices held in registers.
+//
+// Residual representation: a matrix M close to the identity is carried as a = M − I; products use
+// (I+a)(I+b) − I = a + b + ab and squares (I+a)² − I = (a + 2I)a, so the accumulated interval unitary never suffers
+// the cancellation of subtracting 1 from near-unity diagonals (reading R9).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ssb {
+
+enum { SPIN_HALF = 1, SPIN_ONE = 2 };
+enum { CF4 = 0, MIDPOINT = 1, HEUN = 2 };
+enum { EXP_ANALYTIC = 0, EXP_LIE_TROTTER = 1 };
+enum { FIELD_CONSTANT = 0, FIELD_RABI_LINEAR = 1, FIELD_RABI_CIRCULAR = 2, FIELD_NEURAL = 3, FIELD_GRADIENT = 4 };
+
+// ---- constants: correctly rounded doubles (reading R7) ------------------------------------------------
+constexpr double kG1 = 0x1.b0cb174df99c7p-3;       // ½(1 − 1/√3)  Gauss–Legendre node
+constexpr double kG2 = 0x1.93cd3a2c8198ep-1;       // ½(1 + 1/√3)
+constexpr double kWPlus = 0x1.13cd3a2c8198ep-1;    // (3 + 2√3)/12 (Eq. cf4_sample_1)
+constexpr double kWMinus = -0x1.3cd3a2c8198e2p-5;  // (3 − 2√3)/12 (negative)
+constexpr double kTwoPi1 = 0x1.921fb54442d18p+2;   // 2π = kTwoPi1 + kTwoPi2 + kTwoPi3 (Cody–Waite, reading R8)
+constexpr double kTwoPi2 = 0x1.1a62633145c07p-52;
+constexpr double kTwoPi3 = -0x1.f1976b7ed8fbcp-108;
+constexpr double kInvTwoPi = 0x1.45f306dc9c883p-3;
+constexpr double kRsqrt2 = 0x1.6a09e667f3bcdp-1;   // 1/√2
+constexpr double kSqrt2 = 0x1.6a09e667f3bcdp+0;
+constexpr double kThird = 0x1.5555555555555p-2;
+
+template <int SPIN> struct SpinDim { static constexpr int D = (SPIN == SPIN_HALF) ? 2 : 3; };
+template <int F> struct FieldParams;
+template <> struct FieldParams<FIELD_CONSTANT> { static constexpr int P = 4; };
+template <> struct FieldParams<FIELD_RABI_LINEAR> { static constexpr int P = 2; };
+template <> struct FieldParams<FIELD_RABI_CIRCULAR> { static constexpr int P = 2; };
+template <> struct FieldParams<FIELD_NEURAL> { static constexpr int P = 7; };
+template <> struct FieldParams<FIELD_GRADIENT> { static constexpr int P = 2; };
+
+// ---- precision-generic scalar helpers ---------------------------------------------------------------------------
+__device__ __forceinline__ double fmaT(double a, double b, double c) { return fma(a, b, c); }
+__device__ __forceinline__ float fmaT(float a, float b, float c) { return fmaf(a, b, c); }
+__device__ __forceinline__ void sincosT(double x, double* s, double* c) { sincos(x, s, c); }
+__device__ __forceinline__ void sincosT(float x, float* s, float* c) { sincosf(x, s, c); }
+__device__ __forceinline__ double sqrtT(double x) { return sqrt(x); }
+__device__ __forceinline__ float sqrtT(float x) { return sqrtf(x); }
+
+// Reduce ω·t (both FP64) to (−π, π] accurately: exact product as hi + lo (FMA), then Cody–Waite with a 3-part 2π.
+// Never a single-double 2π (SURVEY [V15]).  |result error| ≲ 5e-16 for |ω t| ≲ 1e9.
+__device__ __forceinline__ double reduce_phase(double w, double t) {
+  const double hi = __dmul_rn(w, t);
+  const double lo = fma(w, t, -hi);
+  const double n = rint(hi * kInvTwoPi);
+  double r = fma(-n, kTwoPi1, hi);
+  r = fma(-n, kTwoPi2, r);
+  r = fma(-n, kTwoPi3, r);
+  return r + lo;
+}
+
+// ---- built-in field functions (Eq. neural_pulse; MRI example P:668-669) ------------------------
+// A field object is initialised once per interval with its sweep parameters and t_k; sample(off) returns
+// (ωx, ωy, ωz, ωq) at time t_k + off (the (t_k, off) pair is never rounded to one double — reading R8).
+template <int F> struct Field;
+
+template <> struct Field<FIELD_CONSTANT> {
+  double f0, f1, f2, f3;
+  __device__ __forceinline__ void init(const double* p, double) { f0 = p[0]; f1 = p[1]; f2 = p[2]; f3 = p[3]; }
+  __device__ __forceinline__ void sample(double, double f[4]) const { f[0] = f0; f[1] = f1; f[2] = f2; f[3] = f3; }
+};
+
+template <> struct Field<FIELD_RABI_LINEAR> {        // ω0 Jz + 2Ω cos(ω0 t) Jx
+  double w0, two_om, ph0;
+  __device__ __forceinline__ void init(const double* p, double t_k) {
+    w0 = p[0]; two_om = 2.0 * p[1]; ph0 = reduce_phase(p[0], t_k);
+  }
+  __device__ __forceinline__ void sample(double off, double f[4]) const {
+    f[0] = two_om * cos(fma(w0, off, ph0)); f[1] = 0.0; f[2] = w0; f[3] = 0.0;
+  }
+};
+
+template <> struct Field<FIELD_RABI_CIRCULAR> {      // ω0 Jz + Ω(cos(ω0 t) Jx + sin(ω0 t) Jy)
+  double w0, om, ph0;
+  __device__ __forceinline__ void init(const double* p, double t_k) {
+    w0 = p[0]; om = p[1]; ph0 = reduce_phase(p[0], t_k);
+  }
+  __device__ __forceinline__ void sample(double off, double f[4]) const {
+    double s, c;
+    sincos(fma(w0, off, ph0), &s, &c);
+    f[0] = om * c; f[1] = om * s; f[2] = w0; f[3] = 0.0;
+  }
+};
+
+template <> struct Field<FIELD_NEURAL> {
+  // p = [ω_bias, ω_rf, Ω, Ω_p, ω_sig, t_p, ω_q] (reading R16)
+  double wb, wrf, two_om, op, ws, wq, ph0, dtk;
+  __device__ __forceinline__ void init(const double* p, double t_k) {
+    wb = p[0]; wrf = p[1]; two_om = 2.0 * p[2]; op = p[3]; ws = p[4]; wq = p[6];
+    ph0 = reduce_phase(p[1], t_k);
+    dtk = __dsub_rn(t_k, p[5]);                     // t_k − t_p
+  }
+  __device__ __forceinline__ void sample(double off, double f[4]) const {
+    f[0] = two_om * cos(fma(wrf, off, ph0));       // 2Ω cos(ω_rf t)
+    f[1] = 0.0;
+    const double x = ws * (dtk + off);             // ω_sig (t − t_p)
+    const double pulse = (x >= 0.0 && x <= kTwoPi1) ? sin(x) : 0.0;   // sinp (reading R12)
+    f[2] = fma(op, pulse, wb);
+    f[3] = wq;
+  }
+};
+
+template <> struct Field<FIELD_GRADIENT> {          // ω_z = x − 2y
+  double wz;
+  __device__ __forceinline__ void init(const double* p, double) { wz = fma(-2.0, p[1], p[0]); }
+  __device__ __forceinline__ void sample(double, double f[4]) const { f[0] = 0.0; f[1] = 0.0; f[2] = wz; f[3] = 0.0; }
+};
+
+// Rotating frame (reading R6): rotate (ωx, ωy) by θ = ω_r·t_local, shift ωz by −ω_r; ωq unchanged.
+__device__ __forceinline__ void to_rotating_frame(double f[4], double t_local, double omega_r) {
+  double s, c;
+  sincos(omega_r * t_local, &s, &c);
+  const double fx = f[0], fy = f[1];
+  f[0] = fma(c, fx, s * fy);
+  f[1] = fma(c, fy, -s * fx);
+  f[2] = f[2] - omega_r;
+}
+
+// ---- residual matrices ------------------------------------------------------------------------------------------
+template <int D, typename T> struct Res {
+  T re[D * D];
+  T im[D * D];
+};
+
+template <int D, typename T> __device__ __forceinline__ void res_zero(Res<D, T>& a) {
+#pragma unroll
+  for (int e = 0; e < D * D; ++e) { a.re[e] = T(0); a.im[e] = T(0); }
+}
+
+// c = a + b + a·b, i.e. (I+a)(I+b) − I.
+template <int D, typename T>
+__device__ __forceinline__ void res_mul(const Res<D, T>& a, const Res<D, T>& b, Res<D, T>& c) {
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      T r = a.re[i * D + j] + b.re[i * D + j];
+      T m = a.im[i * D + j] + b.im[i * D + j];
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        r = fmaT(a.re[i * D + k], b.re[k * D + j], r);
+        r = fmaT(-a.im[i * D + k], b.im[k * D + j], r);
+        m = fmaT(a.re[i * D + k], b.im[k * D + j], m);
+        m = fmaT(a.im[i * D + k], b.re[k * D + j], m);
+      }
+      c.re[i * D + j] = r;
+      c.im[i * D + j] = m;
+    }
+}
+
+// a ← (a + 2I)·a, i.e. (I+a)² − I.  3 adds + 18 mul + 90 fma for D = 3.
+template <int D, typename T> __device__ __forceinline__ void res_square(Res<D, T>& a) {
+  T d[D];
+#pragma unroll
+  for (int i = 0; i < D; ++i) d[i] = a.re[i * D + i] + T(2);
+  Res<D, T> s;
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      T r = T(0), m = T(0);
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        const T br = (k == i) ? d[i] : a.re[i * D + k];
+        const T bi = a.im[i * D + k];
+        if (k == 0) {
+          r = br * a.re[k * D + j];
+          m = br * a.im[k * D + j];
+        } else {
+          r = fmaT(br, a.re[k * D + j], r);
+          m = fmaT(br, a.im[k * D + j], m);
+        }
+        r = fmaT(-bi, a.im[k * D + j], r);
+        m = fmaT(bi, a.re[k * D + j], m);
+      }
+      s.re[i * D + j] = r;
+      s.im[i * D + j] = m;
+    }
+  a = s;
+}
+
+// ---- exponentiators: residual of exp(−i(ax Jx + ay Jy + az Jz + aq Q)) -----------------------------------------
+
+// Spin-half closed form: exp(−i a·σ/2) = cos(r/2) I − i (sin(r/2)/r) a·σ.  cos(r/2) − 1 = −2 sin²(r/4).
+template <typename T> __device__ __forceinline__ void expo_su2(const T a[4], Res<2, T>& e) {
+  const T r = sqrtT(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]);
+  T sq, cq;
+  sincosT(r * T(0.25), &sq, &cq);
+  const T cm1 = T(-2) * sq * sq;                     // cos(r/2) − 1
+  const T s = (r > T(0)) ? (T(2) * sq * cq) / r : T(0.5);   // sin(r/2)/r (reading R4)
+  const T sx = s * a[0], sy = s * a[1], sz = s * a[2];
+  e.re[0] = cm1;  e.im[0] = -sz;                     // cos − 1 − i s az
+  e.re[1] = -sy;  e.im[1] = -sx;                     // −i s (ax − i ay)
+  e.re[2] = sy;   e.im[2] = -sx;                     // −i s (ax + i ay)
+  e.re[3] = cm1;  e.im[3] = sz;                      // cos − 1 + i s az
+}
+
+// Spin-one Lie–Trotter.  T − I from Eq. lie_trotter_4 with the corrections of reading R1, written with
+// θ1 = z + q/3, θ2 = 2q/3, θ3 = z − q/3 (z = az/n, q = aq/n, n = 2^τ):
+//   T11 − 1 = expm1(−iθ1) − s² e^{−iθ1}      T12 = (−i/√2) sinΦ e^{−iθ3/2} e^{−iφ}   T13 = −s² e^{−iθ2/2} e^{−2iφ}
+//   T21 = (−i/√2) sinΦ e^{−iθ3/2} e^{iφ}     T22 − 1 = expm1(iθ2) − 2s² e^{iθ2}      T23 = (−i/√2) sinΦ e^{iθ1/2} e^{−iφ}
+//   T31 = −s² e^{−iθ2/2} e^{2iφ}             T32 = (−i/√2) sinΦ e^{iθ1/2} e^{iφ}     T33 − 1 = expm1(iθ3) − s² e^{iθ3}
+// with s = sin(Φ/2), e^{iφ} = (ax + i ay)/√(ax²+ay²) (no atan2; := 1 at Φ = 0, reading R3), and the diagonal from
+// half-angle sines (expm1(iθ) = −2 sin²(θ/2) + i sin θ).  Then τ residual squarings.
+template <typename T> __device__ __forceinline__ void trotter_residual(const T a[4], int tau, Res<3, T>& e) {
+  const T inv_n = ldexp(T(1), -tau);
+  const T rxy = sqrtT(a[0] * a[0] + a[1] * a[1]);
+  const T cphi = (rxy > T(0)) ? a[0] / rxy : T(1);
+  const T sphi = (rxy > T(0)) ? a[1] / rxy : T(0);
+  const T Phi = rxy * inv_n;
+  const T z = a[2] * inv_n, q = a[3] * inv_n;
+  const T th1 = z + q * T(kThird), th2 = T(2) * q * T(kThird), th3 = z - q * T(kThird);
+  T s, c, s1, c1, s2, c2, s3, c3;
+  sincosT(Phi * T(0.5), &s, &c);
+  sincosT(th1 * T(0.5), &s1, &c1);
+  sincosT(th2 * T(0.5), &s2, &c2);
+  sincosT(th3 * T(0.5), &s3, &c3);
+  const T ss = s * s;
+  const T sinPhi_r2 = T(2) * s * c * T(kRsqrt2);     // sinΦ/√2
+  // e^{−iφ} = (cphi, −sphi); e^{−2iφ} = (cphi² − sphi², −2 cphi sphi)
+  const T c2phi = cphi * cphi - sphi * sphi, s2phi = T(2) * cphi * sphi;
+  // off-diagonals: (−i)·X·(u + iv) = X·(v − iu)
+  {  // T12 = (−i/√2) sinΦ e^{−iθ3/2} e^{−iφ} : angle −(θ3/2 + φ)
+    const T ur = c3 * cphi - s3 * sphi, ui = -(s3 * cphi + c3 * sphi);   // e^{−iθ3/2} e^{−iφ}
+    e.re[1] = sinPhi_r2 * ui;  e.im[1] = -sinPhi_r2 * ur;
+  }
+  {  // T21 = (−i/√2) sinΦ e^{−iθ3/2} e^{iφ}
+    const T ur = c3 * cphi + s3 * sphi, ui = c3 * sphi - s3 * cphi;
+    e.re[3] = sinPhi_r2 * ui;  e.im[3] = -sinPhi_r2 * ur;
+  }
+  {  // T23 = (−i/√2) sinΦ e^{iθ1/2} e^{−iφ}
+    const T ur = c1 * cphi + s1 * sphi, ui = s1 * cphi - c1 * sphi;
+    e.re[5] = sinPhi_r2 * ui;  e.im[5] = -sinPhi_r2 * ur;
+  }
+  {  // T32 = (−i/√2) sinΦ e^{iθ1/2} e^{iφ}
+    const T ur = c1 * cphi - s1 * sphi, ui = s1 * cphi + c1 * sphi;
+    e.re[7] = sinPhi_r2 * ui;  e.im[7] = -sinPhi_r2 * ur;
+  }
+  {  // T13 = −s² e^{−iθ2/2} e^{−2iφ};  T31 = −s² e^{−iθ2/2} e^{2iφ}
+    e.re[2] = -ss * (c2 * c2phi - s2 * s2phi);
+    e.im[2] = ss * (s2 * c2phi + c2 * s2phi);
+    e.re[6] = -ss * (c2 * c2phi + s2 * s2phi);
+    e.im[6] = -ss * (c2 * s2phi - s2 * c2phi);
+  }
+  {  // diagonal: e^{iθ} = (1 − 2sh², 2 sh ch);  expm1(iθ) = (−2sh², 2 sh ch)
+    const T sin1 = T(2) * s1 * c1, v1 = T(-2) * s1 * s1;   // θ1
+    const T sin2 = T(2) * s2 * c2, v2 = T(-2) * s2 * s2;   // θ2
+    const T sin3 = T(2) * s3 * c3, v3 = T(-2) * s3 * s3;   // θ3
+    // T11 − 1 = expm1(−iθ1) − s² e^{−iθ1}
+    e.re[0] = v1 - ss * (T(1) + v1);    e.im[0] = -sin1 + ss * sin1;
+    // T22 − 1 = expm1(iθ2) − 2s² e^{iθ2}
+    e.re[4] = v2 - T(2) * ss * (T(1) + v2);  e.im[4] = sin2 - T(2) * ss * sin2;
+    // T33 − 1 = expm1(iθ3) − s² e^{iθ3}
+    e.re[8] = v3 - ss * (T(1) + v3);    e.im[8] = sin3 - ss * sin3;
+  }
+#pragma unroll 1
+  for (int it = 0; it < tau; ++it) res_square<3, T>(e);
+}
+
+// Spin-one "analytic" exponential (reading R14): D¹ of the SU(2) closed form, valid iff aq = 0.
+// With α = 1 + δα, β (from expo_su2): D¹ − I = [[δα(δα+2), √2αβ, β²], [−√2αβ*, −2|β|², √2α*β], [β*², −√2α*β*, δα*(δα*+2)]].
+template <typename T> __device__ __forceinline__ void expo_spin1_analytic(const T a[4], Res<3, T>& e) {
+  Res<2, T> u;
+  expo_su2<T>(a, u);
+  const T dar = u.re[0], dai = u.im[0];              // δα = α − 1
+  const T ar = T(1) + dar, ai = dai;                 // α
+  const T br = u.re[1], bi = u.im[1];                // β
+  const T r2 = T(kSqrt2);
+  // δα(δα + 2)
+  e.re[0] = dar * (dar + T(2)) - dai * dai;          e.im[0] = dai * (dar + T(2)) + dar * dai;
+  // √2 α β
+  e.re[1] = r2 * (ar * br - ai * bi);                e.im[1] = r2 * (ar * bi + ai * br);
+  // β²
+  e.re[2] = br * br - bi * bi;                       e.im[2] = T(2) * br * bi;
+  // −√2 α β*
+  e.re[3] = -r2 * (ar * br + ai * bi);               e.im[3] = -r2 * (ai * br - ar * bi);
+  // |α|² − |β|² − 1 = −2|β|²
+  e.re[4] = T(-2) * (br * br + bi * bi);             e.im[4] = T(0);
+  // √2 α* β
+  e.re[5] = r2 * (ar * br + ai * bi);                e.im[5] = r2 * (ar * bi - ai * br);
+  // β*²
+  e.re[6] = br * br - bi * bi;                       e.im[6] = T(-2) * br * bi;
+  // −√2 α* β*
+  e.re[7] = -r2 * (ar * br - ai * bi);               e.im[7] = r2 * (ar * bi + ai * br);
+  // δα*(δα* + 2)
+  e.re[8] = dar * (dar + T(2)) - dai * dai;          e.im[8] = -(dai * (dar + T(2)) + dar * dai);
+}
+
+template <int SPIN, int EXPO, typename T> struct Expo;
+template <int EXPO, typename T> struct Expo<SPIN_HALF, EXPO, T> {
+  __device__ __forceinline__ static void run(const T a[4], int, Res<2, T>& e) { expo_su2<T>(a, e); }
+};
+template <typename T> struct Expo<SPIN_ONE, EXP_LIE_TROTTER, T> {
+  __device__ __forceinline__ static void run(const T a[4], int tau, Res<3, T>& e) { trotter_residual<T>(a, tau, e); }
+};
+template <typename T> struct Expo<SPIN_ONE, EXP_ANALYTIC, T> {
+  __device__ __forceinline__ static void run(const T a[4], int, Res<3, T>& e) { expo_spin1_analytic<T>(a, e); }
+};
+
+}  // namespace ssb

@@ -1,0 +1,125 @@
+"""C-ABI checks that need no GPU: the library builds for sm_100a, loads, exports every symbol include/*.h declares,
+rejects bad arguments synchronously, and fails loudly (no CPU fallback) when no CUDA device is present."""
+import ctypes
+import glob
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2204_05586_b200 import build, _lib
+    build.build()
+    return _lib.load()
+
+
+def header_symbols():
+    syms = set()
+    for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
+        text = open(h).read()
+        text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+        for m in re.finditer(r"^\s*[A-Za-z_][\w\s\*]*?\b(ss_\w+)\s*\(", text, flags=re.M):
+            syms.add(m.group(1))
+    return syms
+
+
+def test_header_declares_the_binding_exports():
+    from paper_2204_05586_b200 import _lib
+    assert header_symbols() == set(_lib.EXPORTS)
+
+
+def test_library_exports_every_header_symbol(lib):
+    so = os.path.join(ROOT, "paper_2204_05586_b200", "libspinsim_b200.so")
+    out = subprocess.run(["nm", "-D", "--defined-only", so], capture_output=True, text=True, check=True).stdout
+    exported = {l.split()[-1] for l in out.splitlines() if l.strip()}
+    missing = header_symbols() - exported
+    assert not missing, missing
+    for s in header_symbols():
+        assert hasattr(lib, s)
+
+
+def test_library_is_sm100a_only(lib):
+    so = os.path.join(ROOT, "paper_2204_05586_b200", "libspinsim_b200.so")
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", so], capture_output=True, text=True).stdout
+    archs = set(re.findall(r"sm_\d+a?", out))
+    assert archs == {"sm_100a"}, archs
+    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", so], capture_output=True, text=True).stdout
+    assert "DFMA" in sass                     # FP64 FMA pipe carries the stepper
+    assert "HMMA" not in sass                 # no legacy tensor-core path
+
+
+def test_version_and_params(lib):
+    assert lib.ss_version() == 100
+    from paper_2204_05586_b200 import num_sweep_params
+    assert [num_sweep_params(f) for f in ("constant", "rabi_linear", "rabi_circular", "neural", "gradient")] == [4, 2, 2, 7, 2]
+    assert lib.ss_num_sweep_params(99) < 0
+
+
+def test_plan(lib):
+    from paper_2204_05586_b200 import plan, SpinsimError
+    assert plan(0.0, 0.1, 100e-9, 1e-6) == (100000, 10, 1e-7)
+    assert plan(0.0, 1.0, 1e-9, 1e-6)[:2] == (1000000, 1000)
+    with pytest.raises(SpinsimError, match="not an integer"):
+        plan(0.0, 0.1, 300e-9, 1e-6)
+    with pytest.raises(SpinsimError, match="exceed"):
+        plan(1.0, 0.5, 1e-7, 1e-6)
+    with pytest.raises(SpinsimError):
+        plan(0.0, float("nan"), 1e-7, 1e-6)
+
+
+def test_create_validation(lib):
+    from paper_2204_05586_b200 import Simulator, SpinsimError
+    from paper_2204_05586_b200._lib import SS_ERR_UNSUPPORTED, SS_ERR_INVALID
+    with pytest.raises(SpinsimError) as e:
+        Simulator(spin="half", exponentiation="lie_trotter")
+    assert e.value.code == SS_ERR_UNSUPPORTED
+    with pytest.raises(SpinsimError) as e:
+        Simulator(spin="one", trotter_cutoff=61)
+    assert e.value.code == SS_ERR_INVALID
+    for spin, expo in (("half", "analytic"), ("one", "lie_trotter"), ("one", "analytic")):
+        for method in ("cf4", "midpoint", "heun"):
+            for field in ("constant", "rabi_linear", "rabi_circular", "neural", "gradient"):
+                for prec in ("fp64", "fp32"):
+                    Simulator(spin, method, expo, 24, True, prec, field)      # every instance exists
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU failure mode")
+def test_no_cpu_fallback(lib):
+    """Without a CUDA device every compute entry point fails with SS_ERR_CUDA — nothing runs on the CPU."""
+    from paper_2204_05586_b200 import Simulator, SpinsimError
+    from paper_2204_05586_b200._lib import SS_ERR_CUDA
+    sim = Simulator("half", field="rabi_circular")
+    sweep = np.array([[1.0, 2.0]])
+    with pytest.raises(SpinsimError) as e:
+        sim.evaluate_host(sweep, 0.0, 1e-5, 1e-7, 1e-6, np.array([[1, 0]], complex))
+    assert e.value.code == SS_ERR_CUDA
+    fake = ctypes.c_void_p(256)
+    rc = lib.ss_compute_unitaries(sim._h, 0.0, 1e-5, 1e-7, 1e-6, 0, 10, 1, fake, fake, None)
+    assert rc == SS_ERR_CUDA
+    with pytest.raises(TypeError):
+        sim.evaluate(torch.zeros((1, 2), dtype=torch.float64), 0.0, 1e-5, 1e-7, 1e-6,
+                     torch.zeros((1, 2), dtype=torch.complex128))
+
+
+def test_argument_errors_are_synchronous(lib):
+    from paper_2204_05586_b200 import Simulator
+    from paper_2204_05586_b200._lib import SS_ERR_INVALID
+    sim = Simulator("one")
+    fake = ctypes.c_void_p(4096)
+    # bad interval range
+    assert lib.ss_compute_unitaries(sim._h, 0.0, 1e-5, 1e-7, 1e-6, 5, 10, 1, fake, fake, None) == SS_ERR_INVALID
+    assert b"outside" in lib.ss_last_error()
+    # misaligned pointer
+    assert lib.ss_compute_unitaries(sim._h, 0.0, 1e-5, 1e-7, 1e-6, 0, 10, 1, ctypes.c_void_p(4097), fake, None) == SS_ERR_INVALID
+    # workspace too small
+    assert lib.ss_scan_states(3, 2, 100, fake, fake, fake, fake, 16, None) == SS_ERR_INVALID
+    assert b"workspace" in lib.ss_last_error()
+    assert lib.ss_compose_carry(3, 1, 2, 2, fake, fake, fake, None) == SS_ERR_INVALID
+    assert lib.ss_workspace_bytes(sim._h, 8192, 10000, 1) > 8192 * 10000 * 144

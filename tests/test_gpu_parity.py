@@ -1,0 +1,244 @@
+"""GPU parity: the CUDA path (through the C ABI) against the long-double oracle on the same seeded inputs.
+
+Bar (BASELINE.json north_star): max |ψ_gpu − ψ_oracle| ≤ 1e-10 in FP64, ≤ 1e-4 in FP32 mode, element by element over
+every (sweep, k, component) — and the same for the interval unitaries U_k.  Full BASELINE sizes are covered in
+test_gpu_fullsize.py on sampled outputs.
+"""
+import numpy as np
+import pytest
+import torch
+
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+TOL64 = 1e-10
+TOL32 = 1e-4
+
+
+@pytest.fixture(scope="module")
+def ss():
+    import paper_2204_05586_b200 as ss
+    assert torch.cuda.is_available()
+    ss.load()
+    return ss
+
+
+def gpu_run(ss, w: W.Workload, precision="fp64", want_unitaries=True):
+    sim = ss.Simulator(w.spin, w.method, w.expo, w.tau, w.frame, precision, w.field)
+    sweep = torch.from_numpy(np.ascontiguousarray(w.sweep)).cuda()
+    psi0 = torch.from_numpy(np.ascontiguousarray(w.psi0)).cuda()
+    res = sim.evaluate(sweep, w.t0, w.t1, w.dt_int, w.dt_out, psi0, want_unitaries=want_unitaries)
+    torch.cuda.synchronize()
+    U = res.time_evolution.cpu().numpy() if want_unitaries else None
+    return res.state.cpu().numpy(), U
+
+
+def oracle_run(orc, w: W.Workload, **kw):
+    return orc.evaluate(w.spin, w.method, w.expo, w.tau, w.frame, w.field, sweep=w.sweep, t0=w.t0, t1=w.t1,
+                        dt_int=w.dt_int, dt_out=w.dt_out, psi0=w.psi0, **kw)
+
+
+def assert_parity(ss, orc, w, tol=TOL64, precision="fp64"):
+    st_g, U_g = gpu_run(ss, w, precision)
+    st_o, U_o = oracle_run(orc, w)
+    eU = np.abs(U_g - U_o).max()
+    eS = np.abs(st_g - st_o).max()
+    assert eU <= tol and eS <= tol, (w.name, precision, eU, eS)
+    return eU, eS
+
+
+# ---- building blocks -------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("spin,expo,scale", [("half", "analytic", 1.0), ("half", "analytic", 1e-6),
+                                             ("one", "lie_trotter", 1.0), ("one", "lie_trotter", 1e-6),
+                                             ("one", "analytic", 1.0)])
+def test_exponentiator_parity(ss, orc, spin, expo, scale):
+    a = W.random_exponent_args(5000, scale, seed=21, quad=(expo != "analytic" or spin == "half"))
+    if spin == "half" or expo == "analytic":
+        a[:, 3] = 0.0
+    a[:3] = 0.0                                       # exact zero args (reading R3/R4)
+    a[3, :2] = 0.0                                    # Φ = 0 with z, q ≠ 0
+    sim = ss.Simulator(spin, "cf4", expo, 24, True, "fp64", "constant")
+    got = sim.exponentiate(torch.from_numpy(a).cuda()).cpu().numpy()
+    ref = orc.exponentiate(spin, a, expo, 24)
+    assert np.abs(got - ref).max() <= 4e-16 * max(1.0, scale) * 8
+    sim32 = ss.Simulator(spin, "cf4", expo, 24, True, "fp32", "constant")
+    got32 = sim32.exponentiate(torch.from_numpy(a).cuda()).cpu().numpy()
+    assert np.abs(got32 - ref).max() <= 2e-6
+
+
+@pytest.mark.parametrize("tau", [0, 1, 7, 24, 40])
+def test_lie_trotter_tau_parity(ss, orc, tau):
+    a = W.random_exponent_args(500, 0.5, seed=22)
+    sim = ss.Simulator("one", "cf4", "lie_trotter", tau, True, "fp64", "constant")
+    got = sim.exponentiate(torch.from_numpy(a).cuda()).cpu().numpy()
+    assert np.abs(got - orc.exponentiate("one", a, "lie_trotter", tau)).max() < 1e-14
+
+
+# ---- configs at oracle-friendly sizes (several scan tiles + ragged tails) ---------------------------------------
+@pytest.mark.parametrize("field", ["rabi_circular", "rabi_linear"])
+def test_c1_rabi_parity(ss, orc, field):
+    assert_parity(ss, orc, W.c1_rabi(field))
+
+
+def test_c2_neural_parity_short(ss, orc):
+    assert_parity(ss, orc, W.c2_neural(duration=3.3e-3))            # K = 3300: 13 tiles of 256, ragged tail
+
+
+@pytest.mark.parametrize("dt_int", [1e-6, 250e-9, 10e-9])
+def test_c2_dt_sweep_parity(ss, orc, dt_int):
+    assert_parity(ss, orc, W.c2_neural(dt_int=dt_int, duration=0.2e-3 if dt_int < 1e-7 else 1e-3))
+
+
+def test_c3_batched_parity_small(ss, orc):
+    w = W.c3_batched(batch=24, duration=0.5e-3)
+    w = w.with_(sweep=W.c3_sweep_params()[::341][:24], psi0=W.random_states(24, 3, seed=23))
+    assert_parity(ss, orc, w)
+
+
+def test_c4_spin_half_parity_short(ss, orc):
+    assert_parity(ss, orc, W.c4_long(duration=2e-3).with_(sweep=W.neural_params(t_p=1e-3, omega_q=0.0)[None, :]))
+
+
+@pytest.mark.parametrize("expo", ["lie_trotter", "analytic"])
+def test_c5_parity_short(ss, orc, expo):
+    w = W.c5_matrix(expo, batch=3)
+    assert_parity(ss, orc, w.with_(t1=2e-3))
+
+
+@pytest.mark.parametrize("spin,expo", [("one", "lie_trotter"), ("one", "analytic"), ("half", "analytic")])
+def test_fp32_mode_parity(ss, orc, spin, expo):
+    w = W.c5_matrix(expo, batch=2).with_(t1=5e-3)
+    if spin == "half":
+        w = w.with_(spin="half", psi0=W.basis_state(2, 2))
+    assert_parity(ss, orc, w, tol=TOL32, precision="fp32")
+
+
+@pytest.mark.parametrize("method", ["midpoint", "heun"])
+@pytest.mark.parametrize("spin", ["half", "one"])
+def test_euler_samplers_parity(ss, orc, method, spin):
+    w = W.c2_neural(duration=0.5e-3).with_(method=method, spin=spin, expo="analytic" if spin == "half" else "lie_trotter",
+                                           psi0=W.random_states(1, 2 if spin == "half" else 3, seed=24))
+    assert_parity(ss, orc, w)
+
+
+@pytest.mark.parametrize("frame", [True, False])
+@pytest.mark.parametrize("field,params", [
+    ("constant", [2.1e5, -1.3e5, 3.7e5, 0.9e5]),
+    ("gradient", [3.0e5, 0.4e5]),
+    ("rabi_circular", [2 * np.pi * 700e3, 2 * np.pi * 1e3]),
+])
+def test_fields_and_frame_parity(ss, orc, field, params, frame):
+    w = W.Workload("f", "one", "cf4", "lie_trotter", 24, frame, field, 0.0, 0.3e-3, 100e-9, 1e-6,
+                   np.array([params], float), W.random_states(1, 3, seed=25))
+    assert_parity(ss, orc, w)
+
+
+# ---- edge cases ------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("K,L", [(1, 1), (1, 7), (2, 1), (255, 2), (256, 1), (257, 1), (513, 1), (1000, 3)])
+def test_grid_edge_cases(ss, orc, K, L):
+    for spin in ("half", "one"):
+        w = W.c2_neural(dt_int=1e-6 / L).with_(t1=K * 1e-6, spin=spin,
+                                               expo="analytic" if spin == "half" else "lie_trotter",
+                                               psi0=W.random_states(2, 2 if spin == "half" else 3, seed=26),
+                                               sweep=np.stack([W.neural_params(t_p=0.1e-3)] * 2))
+        assert_parity(ss, orc, w)
+
+
+def test_time_start_nonzero_and_large(ss, orc):
+    """Large t (RF phase ≈ 4.4e6 rad): the per-interval double-double phase reduction (reading R8)."""
+    w = W.c4_long(duration=0.1).with_(t0=0.9, t1=0.9 + 0.2e-3, dt_int=10e-9,
+                                      sweep=W.neural_params(t_p=0.90005, omega_q=0.0)[None, :])
+    assert_parity(ss, orc, w)
+
+
+def test_validation_errors(ss):
+    from paper_2204_05586_b200._lib import SS_ERR_INVALID, SS_ERR_NONFINITE
+    sim = ss.Simulator("one", "cf4", "analytic", 24, True, "fp64", "neural")
+    sweep = torch.from_numpy(W.neural_params()[None, :]).cuda()          # ω_q ≠ 0
+    psi0 = torch.from_numpy(W.basis_state(3)).cuda()
+    with pytest.raises(ss.SpinsimError) as e:
+        sim.evaluate(sweep, 0.0, 1e-5, 1e-7, 1e-6, psi0)
+    assert e.value.code == SS_ERR_INVALID
+    sim2 = ss.Simulator("one")
+    bad = sweep.clone()
+    bad[0, 2] = float("nan")
+    with pytest.raises(ss.SpinsimError) as e:
+        sim2.evaluate(bad, 0.0, 1e-5, 1e-7, 1e-6, psi0)
+    assert e.value.code == SS_ERR_NONFINITE
+
+
+# ---- scan, aggregate, carry, projection against the oracle's sequential chain ----------------------------------
+def _random_unitaries(B, K, d, seed):
+    rng = np.random.default_rng(seed)
+    z = rng.standard_normal((B, K, d, d)) + 1j * rng.standard_normal((B, K, d, d))
+    q, r = np.linalg.qr(z)
+    return q * (np.diagonal(r, axis1=-2, axis2=-1) / np.abs(np.diagonal(r, axis1=-2, axis2=-1)))[..., None, :]
+
+
+@pytest.mark.parametrize("d", [2, 3])
+@pytest.mark.parametrize("B,K", [(1, 1), (3, 255), (2, 256), (5, 1031), (1, 20000), (300, 7)])
+def test_scan_vs_sequential_chain(ss, orc, d, B, K):
+    U = _random_unitaries(B, K, d, seed=B * 1000 + K)
+    psi0 = W.random_states(B, d, seed=27)
+    ref, agg = orc.chain(U, psi0, want_aggregate=True)
+    Ug = torch.from_numpy(U).cuda()
+    got = ss.scan_states(Ug, torch.from_numpy(psi0).cuda()).cpu().numpy()
+    assert np.abs(got - ref).max() < 1e-12 * max(1.0, np.sqrt(K) / 10)
+    A = ss.chain_aggregate(Ug).cpu().numpy()
+    assert np.abs(A - agg).max() < 1e-12 * max(1.0, np.sqrt(K) / 10)
+
+
+def test_compose_carry(ss, orc):
+    d, B, G = 3, 4, 5
+    A = _random_unitaries(G, B, d, seed=28)           # [G][B][d][d]
+    psi0 = W.random_states(B, d, seed=29)
+    Ag = torch.from_numpy(A).cuda()
+    for part in range(G):
+        got = ss.compose_carry(Ag, torch.from_numpy(psi0).cuda(), part).cpu().numpy()
+        ref = orc.chain(np.transpose(A[:part], (1, 0, 2, 3)), psi0)[:, -1] if part else psi0
+        assert np.abs(got - ref).max() < 1e-14
+
+
+@pytest.mark.parametrize("spin", ["half", "one"])
+def test_spin_projection_parity(ss, orc, spin):
+    d = 2 if spin == "half" else 3
+    psi = W.random_states(1000, d, seed=30)
+    got = ss.spin_projection(spin, torch.from_numpy(psi).cuda()).cpu().numpy()
+    assert np.abs(got - orc.spin_projection(spin, psi)).max() < 1e-15
+
+
+# ---- properties ------------------------------------------------------------------------------------------------
+def test_determinism_bitwise(ss):
+    w = W.c3_batched(batch=64, duration=0.3e-3)
+    a, Ua = gpu_run(ss, w)
+    b, Ub = gpu_run(ss, w)
+    assert np.array_equal(a, b) and np.array_equal(Ua, Ub)
+
+
+def test_host_api_matches_device_api(ss):
+    w = W.c3_batched(batch=10, duration=0.2e-3)
+    st_d, U_d = gpu_run(ss, w)
+    sim = ss.Simulator(w.spin, w.method, w.expo, w.tau, w.frame, "fp64", w.field)
+    for chunks in (1, 3):
+        st_h, U_h = sim.evaluate_host(w.sweep, w.t0, w.t1, w.dt_int, w.dt_out, w.psi0, want_unitaries=True,
+                                      n_chunks=chunks)
+        assert np.array_equal(st_h, st_d) and np.array_equal(U_h, U_d)
+
+
+def test_partition_reproduces_unitaries_bitwise(ss):
+    """The time grid uses the global k, so computing a sub-range reproduces those U_k bit for bit."""
+    w = W.c4_long(duration=1e-3)
+    sim = ss.Simulator(w.spin, w.method, w.expo, w.tau, w.frame, "fp64", w.field)
+    sweep = torch.from_numpy(w.sweep).cuda()
+    full = sim.compute_unitaries(sweep, w.t0, w.t1, w.dt_int, w.dt_out)
+    part = sim.compute_unitaries(sweep, w.t0, w.t1, w.dt_int, w.dt_out, k_begin=333, k_count=100)
+    assert torch.equal(full[:, 333:433], part)
+
+
+def test_unitarity_and_norm(ss):
+    w = W.c2_neural(duration=20e-3).with_(psi0=W.random_states(1, 3, seed=31))
+    st, U = gpu_run(ss, w)
+    UhU = np.conj(np.transpose(U[0], (0, 2, 1))) @ U[0]
+    assert np.abs(UhU - np.eye(3)).max() < 1e-12
+    assert np.abs(np.linalg.norm(st[0], axis=1) - 1).max() < 1e-12
