@@ -39,19 +39,27 @@ FP64_PEAK_TFLOPS = N_SM * FP64_FMA_PER_CLK_SM * 2 * SM_MAX_MHZ * 1e6 / 1e12
 
 
 def algorithmic_flops_per_fine_step(spin: str, expo: str, tau: int, method: str = "cf4") -> int:
-    """Matrix arithmetic of one fine step as the algorithm is written, counting real +, −, × as 1:
-    residual squaring (a + 2I)a on 3×3: 3 + 9·(3·6 + 2·2) = 201; residual product a + b + ab: 9·(2 + 3·6 + 3·2)
-    = 234 (3×3) and 4·(2 + 2·6 + 2·2) = 72 (2×2).  Field trig, T − I construction and the frame are not counted
-    (a lower bound)."""
+    """Matrix arithmetic of one fine step in this implementation's formulation, counting every real
+    +, −, × once (an FMA is 2): Lie–Trotter residual squaring on the complex-symmetric leapfrog factor T₀
+    (6 unique entries) = 99 flop; residual product a + b + ab = 234 (3×3) / 72 (2×2).  Field trig, the T − I
+    construction, the φ phases and the frame are not counted (a lower bound)."""
     n_exp = 2 if method == "cf4" else 1
     if spin == "one":
         prod = 234
-        per_exp = 201 * tau if expo == "lie_trotter" else 0
+        per_exp = 99 * tau if expo == "lie_trotter" else 0
     else:
         prod = 72
         per_exp = 0
-    n_prod = 2 if method == "cf4" else 1
-    return n_exp * per_exp + n_prod * prod
+    return n_exp * (per_exp + prod)
+
+
+def dense_equivalent_flops_per_fine_step(spin: str, expo: str, tau: int, method: str = "cf4") -> int:
+    """SURVEY §8(d)'s per-unit figure: the same step with dense 3×3 squarings as written in P:462, (a + 2I)a =
+    201 flop each (context only)."""
+    n_exp = 2 if method == "cf4" else 1
+    if spin == "one":
+        return n_exp * ((201 * tau if expo == "lie_trotter" else 0) + 234)
+    return n_exp * 72
 
 
 def scan_bytes_per_interval(dim: int) -> int:
@@ -319,6 +327,8 @@ def run_ours(args, rank, world, local):
                          "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
                          "kernel": f"interval_kernel<spin-{w.spin},{w.expo},{w.method},{w.field},{args.precision}>",
                          "flops_per_launch": flops_launch, "ms_per_launch": t_interval,
+                         "dense_equivalent_tflops": dense_equivalent_flops_per_fine_step(w.spin, w.expo, w.tau, w.method)
+                         * steps_per_rank / (t_interval * 1e-3) / 1e12,
                          "peak_basis": "nominal FP64: 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (DESIGN.md §6)",
                          "measured_dfma_peak_tflops": measured_peak,
                          "frac_at_observed_clock": (achieved / (FP64_PEAK_TFLOPS * clocks["sm_mhz"] / SM_MAX_MHZ)

@@ -12,7 +12,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libspinsim_b200.so")
+# SPINSIM_LIB selects an in-tree tuning variant (build.py <variant> ...) for experiments; default is the product build.
+LIB_PATH = os.environ.get("SPINSIM_LIB") or os.path.join(HERE, "libspinsim_b200.so")
 
 SS_OK, SS_ERR_INVALID, SS_ERR_UNSUPPORTED, SS_ERR_CUDA, SS_ERR_NONFINITE = 0, -1, -2, -3, -4
 SPIN = {"half": 1, "one": 2}

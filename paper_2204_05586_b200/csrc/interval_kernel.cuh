@@ -32,6 +32,11 @@ struct IntervalParams {
 };
 
 constexpr int kIntervalThreads = 128;
+// Resident blocks per SM requested from ptxas: 16 warps/SM (128 registers) without spills for every instance.
+#ifndef SS_INTERVAL_MINBLOCKS
+#define SS_INTERVAL_MINBLOCKS 4
+#endif
+template <int SPIN, typename T> constexpr int kIntervalMinBlocks() { return SS_INTERVAL_MINBLOCKS; }
 
 template <int F>
 __device__ __forceinline__ void sample_in_frame(const Field<F>& fld, double off, double omega_r, int frame,
@@ -41,7 +46,7 @@ __device__ __forceinline__ void sample_in_frame(const Field<F>& fld, double off,
 }
 
 template <int SPIN, int EXPO, int METHOD, int FIELD, typename T>
-__global__ void __launch_bounds__(kIntervalThreads)
+__global__ void __launch_bounds__(kIntervalThreads, kIntervalMinBlocks<SPIN, T>())
 interval_kernel(const IntervalParams prm) {
   constexpr int D = SpinDim<SPIN>::D;
   constexpr int P = FieldParams<FIELD>::P;
@@ -84,11 +89,19 @@ interval_kernel(const IntervalParams prm) {
         a1[j] = (T)(fma(kWPlus, f1[j], kWMinus * f2[j]) * prm.dt);
         a2[j] = (T)(fma(kWMinus, f1[j], kWPlus * f2[j]) * prm.dt);
       }
-      // a5/a6: exponentials; a7: u = e2·e1 (Eq. cf4_implementation), residual form.
-      Res<D, T> e1, e2;
-      Expo<SPIN, EXPO, T>::run(a1, prm.tau, e1);
-      Expo<SPIN, EXPO, T>::run(a2, prm.tau, e2);
-      res_mul<D, T>(e2, e1, u);
+      // a5/a6/a7: u·U_r = e2·(e1·U_r) (Eq. cf4_implementation), folded one exponential at a time so only
+      // one exponential is live in registers (occupancy).  Residual form: A ← e + A + e·A.
+      {
+        Res<D, T> e;
+        Expo<SPIN, EXPO, T>::run(a1, prm.tau, e);
+        res_mul<D, T>(e, A, u);
+      }
+      {
+        Res<D, T> e;
+        Expo<SPIN, EXPO, T>::run(a2, prm.tau, e);
+        res_mul<D, T>(e, u, A);
+      }
+      continue;
     } else {
       double f[4];
       if (METHOD == MIDPOINT) {                       // one sample at t + δt/2 (reading R13)

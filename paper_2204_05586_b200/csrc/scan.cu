@@ -16,6 +16,8 @@
 // 96 B (spin-half): the kernel is HBM bound.
 #include <cuda/atomic>
 
+#include <algorithm>
+
 #include "kernels.h"
 
 namespace ssb {
@@ -114,6 +116,8 @@ template <int D> struct ScanLayout {
     total = align256(off_psi + sizeof(double2) * D * (size_t)ntiles);
   }
 };
+
+template <int D> struct Scan2Layout;   // defined after the v2 kernel configuration
 
 struct ScanArgs {
   int64_t batch, k_count, tiles_per_sweep;
@@ -258,6 +262,375 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(const ScanArgs a) {
   for (int e = tid; e < n_items * D; e += kScanThreads) __stcs(gS + e, sPsi[e]);
 }
 
+// ---- state scan v2: persistent CTAs, TMA bulk-copy double buffering, j-major tiles, warp-parallel look-back ----
+//
+// Tile (b, j) covers intervals [j·TILE, (j+1)·TILE) of sweep b; tickets are j-major (ticket = j·batch + b), so the
+// predecessor of a tile is ticket − batch: with many sweeps the predecessor has long finished and the look-back is a
+// single flag read; with one sweep the look-back walks up to 32 predecessors per round in parallel (one lane each)
+// and multiplies their aggregates with a shuffle tree.  Each CTA is persistent: while it computes tile t it has
+// already issued the TMA bulk copy (cp.async.bulk → UBLKCP) of its next tile's operators into the other shared-
+// memory stage, so HBM reads overlap the FP64 work.
+template <int D> struct Scan2Cfg;
+template <> struct Scan2Cfg<2> { static constexpr int NT = 128, C = 8; };
+template <> struct Scan2Cfg<3> { static constexpr int NT = 128, C = 4; };
+template <int D> constexpr int scan2_tile() { return Scan2Cfg<D>::NT * Scan2Cfg<D>::C; }
+template <int D> constexpr size_t scan2_smem() {
+  return sizeof(double2) * (size_t)scan2_tile<D>() * (2 * D * D + D) + 64;
+}
+
+template <int D> struct Scan2Layout {
+  int64_t tiles_per_sweep, ntiles;
+  size_t off_flags, off_agg, off_psi, total;
+  Scan2Layout(int64_t batch, int64_t k_count) {
+    tiles_per_sweep = (k_count + scan2_tile<D>() - 1) / scan2_tile<D>();
+    ntiles = batch * tiles_per_sweep;
+    off_flags = 256;
+    off_agg = align256(off_flags + sizeof(int) * (size_t)ntiles);
+    off_psi = align256(off_agg + sizeof(double2) * D * D * (size_t)ntiles);
+    total = align256(off_psi + sizeof(double2) * D * (size_t)ntiles);
+  }
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src_gmem, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst_smem)),
+      "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+struct Scan2Args {
+  int64_t batch, k_count, tiles_per_sweep, ntiles;
+  const double2* U;
+  const double2* psi0;
+  double2* states;
+  unsigned long long* ticket;
+  int* flags;
+  double2* agg;
+  double2* psi_end;
+};
+
+template <int D> __device__ __forceinline__ CM<D> cm_shfl_down(const CM<D>& m, int delta) {
+  CM<D> r;
+#pragma unroll
+  for (int e = 0; e < D * D; ++e) {
+    r.re[e] = __shfl_down_sync(0xffffffffu, m.re[e], delta);
+    r.im[e] = __shfl_down_sync(0xffffffffu, m.im[e], delta);
+  }
+  return r;
+}
+
+template <int D>
+__global__ void __launch_bounds__(Scan2Cfg<D>::NT, 1) scan2_kernel(const Scan2Args a) {
+  constexpr int NT = Scan2Cfg<D>::NT, C = Scan2Cfg<D>::C, TILE = NT * C, NW = NT / 32;
+  extern __shared__ __align__(128) double2 smem2[];
+  double2* sU[2] = {smem2, smem2 + TILE * D * D};
+  double2* sPsi = smem2 + 2 * TILE * D * D;
+  __shared__ __align__(8) uint64_t sBar[2];
+  __shared__ double2 sWarpTot[NW][D * D];
+  __shared__ double2 sWarpPre[NW][D * D];
+  __shared__ double2 sPsiIn[D];
+  __shared__ long long sNext;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  auto tile_of = [&](long long t, long long& b, long long& j) { j = t / a.batch; b = t - j * a.batch; };
+  auto issue = [&](long long t, int stage) {
+    long long b, j;
+    tile_of(t, b, j);
+    const long long k0 = j * TILE;
+    const int n = (int)min((long long)TILE, a.k_count - k0);
+    const unsigned bytes = (unsigned)(n * D * D * sizeof(double2));
+    mbar_expect_tx(&sBar[stage], bytes);
+    tma_load_1d(sU[stage], a.U + ((size_t)b * a.k_count + k0) * D * D, bytes, &sBar[stage]);
+  };
+
+  if (tid == 0) {
+    mbar_init(&sBar[0], 1);
+    mbar_init(&sBar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const long long t0 = (long long)atomicAdd(a.ticket, 1ull);
+    sNext = t0;
+    if (t0 < a.ntiles) issue(t0, 0);
+  }
+  __syncthreads();
+  long long t = sNext;
+  unsigned phase[2] = {0u, 0u};
+  int stage = 0;
+  while (t < a.ntiles) {
+    // prefetch the next tile into the other stage (its previous contents were consumed last iteration)
+    __syncthreads();
+    if (tid == 0) {
+      const long long nx = (long long)atomicAdd(a.ticket, 1ull);
+      sNext = nx;
+      if (nx < a.ntiles) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(nx, stage ^ 1);
+      }
+    }
+    long long b, j;
+    tile_of(t, b, j);
+    const long long k0 = j * TILE;
+    const int n_items = (int)min((long long)TILE, a.k_count - k0);
+    mbar_wait(&sBar[stage], phase[stage]);
+    phase[stage] ^= 1u;
+    const double2* U = sU[stage];
+
+    // thread aggregate, warp inclusive scan, warp totals
+    CM<D> P;
+    cm_eye(P);
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      const int it = tid * C + c;
+      if (it < n_items) {
+        CM<D> u;
+        cm_load(U + it * D * D, u);
+        P = cm_mul(u, P);
+      }
+    }
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const CM<D> q = cm_shfl_up(P, off);
+      if (lane >= off) P = cm_mul(P, q);
+    }
+    CM<D> E = cm_shfl_up(P, 1);
+    if (lane == 0) cm_eye(E);
+    if (lane == 31) cm_store(sWarpTot[warp], P);
+    __syncthreads();
+
+    if (warp == 0) {
+      // scan of the warp totals (lanes < NW), exclusive prefixes to shared memory, block total in lane NW−1
+      CM<D> T;
+      if (lane < NW) cm_load(sWarpTot[lane], T); else cm_eye(T);
+#pragma unroll
+      for (int off = 1; off < NW; off <<= 1) {
+        const CM<D> q = cm_shfl_up(T, off);
+        if (lane >= off) T = cm_mul(T, q);
+      }
+      CM<D> Wx = cm_shfl_up(T, 1);
+      if (lane == 0) cm_eye(Wx);
+      if (lane < NW) cm_store(sWarpPre[lane], Wx);
+      // block total to every lane
+      CM<D> tot;
+#pragma unroll
+      for (int e = 0; e < D * D; ++e) {
+        tot.re[e] = __shfl_sync(0xffffffffu, T.re[e], NW - 1);
+        tot.im[e] = __shfl_sync(0xffffffffu, T.im[e], NW - 1);
+      }
+      cuda::atomic_ref<int, cuda::thread_scope_device> my_flag(a.flags[t]);
+      double pr[D], pi[D];
+      if (j == 0) {
+#pragma unroll
+        for (int d = 0; d < D; ++d) { const double2 v = a.psi0[b * D + d]; pr[d] = v.x; pi[d] = v.y; }
+      } else {
+        if (lane == 0) {
+          cm_store(a.agg + (size_t)t * D * D, tot);
+          my_flag.store(FLAG_AGG, cuda::memory_order_release);
+        }
+        // warp-parallel look-back: lane ℓ inspects predecessor j − 1 − ℓ − 32r
+        CM<D> M;
+        cm_eye(M);
+        long long jb = j - 1;
+        for (;;) {
+          const long long jq = jb - lane;
+          const long long q = jq * a.batch + b;
+          int fv = FLAG_PREFIX;                       // lanes before tile 0 never matter (tile 0 is PREFIX)
+          if (jq >= 0) {
+            cuda::atomic_ref<int, cuda::thread_scope_device> f(a.flags[q]);
+            while ((fv = f.load(cuda::memory_order_acquire)) == FLAG_EMPTY) __nanosleep(32);
+          }
+          const unsigned pm = __ballot_sync(0xffffffffu, fv == FLAG_PREFIX);
+          const int first = pm ? __ffs(pm) - 1 : 32;
+          if (first > 0) {                            // product of aggregates of lanes < first (nearest first)
+            CM<D> A;
+            if (lane < first) cm_load_cg(a.agg + (size_t)q * D * D, A); else cm_eye(A);
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+              const CM<D> o = cm_shfl_down(A, off);
+              if ((lane & (2 * off - 1)) == 0) A = cm_mul(A, o);
+            }
+            M = cm_mul(M, A);                         // meaningful in lane 0
+          }
+          if (first < 32) {
+            double er[D], ei[D];
+            if (lane == first)
+              for (int d = 0; d < D; ++d) { const double2 v = __ldcg(a.psi_end + q * D + d); er[d] = v.x; ei[d] = v.y; }
+#pragma unroll
+            for (int d = 0; d < D; ++d) {
+              er[d] = __shfl_sync(0xffffffffu, er[d], first);
+              ei[d] = __shfl_sync(0xffffffffu, ei[d], first);
+            }
+            cm_apply(M, er, ei, pr, pi);              // valid in lane 0
+            break;
+          }
+          jb -= 32;
+        }
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          pr[d] = __shfl_sync(0xffffffffu, pr[d], 0);
+          pi[d] = __shfl_sync(0xffffffffu, pi[d], 0);
+        }
+      }
+      if (lane == 0) {
+        double er[D], ei[D];
+        cm_apply(tot, pr, pi, er, ei);
+        for (int d = 0; d < D; ++d) a.psi_end[t * D + d] = make_double2(er[d], ei[d]);
+        my_flag.store(FLAG_PREFIX, cuda::memory_order_release);
+        for (int d = 0; d < D; ++d) sPsiIn[d] = make_double2(pr[d], pi[d]);
+        if (j == 0)
+          for (int d = 0; d < D; ++d) a.states[(size_t)b * (a.k_count + 1) * D + d] = make_double2(pr[d], pi[d]);
+      }
+    }
+    __syncthreads();
+
+    // apply: ψ = (E·W_w)·ψ_in, then the thread's own operators
+    CM<D> Wp;
+    cm_load(sWarpPre[warp], Wp);
+    const CM<D> X = cm_mul(E, Wp);
+    double xr[D], xi[D], yr[D], yi[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) { xr[d] = sPsiIn[d].x; xi[d] = sPsiIn[d].y; }
+    cm_apply(X, xr, xi, yr, yi);
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      const int it = tid * C + c;
+      if (it < n_items) {
+        CM<D> u;
+        cm_load(U + it * D * D, u);
+        cm_apply(u, yr, yi, xr, xi);
+#pragma unroll
+        for (int d = 0; d < D; ++d) { yr[d] = xr[d]; yi[d] = xi[d]; sPsi[it * D + d] = make_double2(xr[d], xi[d]); }
+      }
+    }
+    __syncthreads();
+    double2* gS = a.states + ((size_t)b * (a.k_count + 1) + k0 + 1) * D;
+    for (int e = tid; e < n_items * D; e += NT) __stcs(gS + e, sPsi[e]);
+    t = sNext;
+    stage ^= 1;
+  }
+}
+
+// ---- state chain for large batches: one thread per sweep, TMA-streamed ------------------------------------------
+//
+// With batch ≥ kChainMinBatch the sweeps alone give enough parallelism to saturate HBM, so each thread runs its own
+// sweep's recurrence ψ_{k+1} = U_k ψ_k sequentially (36 FP64 ops per interval, no matrix products, no look-back):
+// lane ℓ bulk-copies (cp.async.bulk → UBLKCP) its next CH operators into its own shared-memory slot while it applies
+// the current CH, so every SM keeps ≥ 64 × CH × 16·dim² bytes of HBM reads in flight.
+constexpr int kChainThreads = 64;
+constexpr int64_t kChainMinBatch = 4096;
+template <int D> struct ChainCfg { static constexpr int CH = 8; };
+template <int D> constexpr size_t chain_smem() { return sizeof(double2) * (size_t)kChainThreads * 2 * ChainCfg<D>::CH * D * D; }
+
+struct ChainArgs {
+  int64_t batch, k_count;
+  const double2* U;
+  const double2* psi0;
+  double2* states;
+};
+
+template <int D>
+__global__ void __launch_bounds__(kChainThreads) chain_kernel(const ChainArgs a) {
+  constexpr int CH = ChainCfg<D>::CH;
+  extern __shared__ __align__(128) double2 smem3[];
+  __shared__ __align__(8) uint64_t sBar[kChainThreads / 32][2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t b = (int64_t)blockIdx.x * kChainThreads + tid;
+  const bool valid = b < a.batch;
+  double2* slot[2] = {smem3 + (size_t)tid * 2 * CH * D * D, smem3 + (size_t)tid * 2 * CH * D * D + CH * D * D};
+  if (lane == 0) {
+    mbar_init(&sBar[warp][0], 32);
+    mbar_init(&sBar[warp][1], 32);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const int64_t nchunks = (a.k_count + CH - 1) / CH;
+  const double2* gU = a.U + (size_t)(valid ? b : 0) * a.k_count * D * D;
+  auto issue = [&](int64_t c, int st) {
+    const int64_t k0 = c * CH;
+    const int n = valid ? (int)min((int64_t)CH, a.k_count - k0) : 0;
+    const unsigned bytes = (unsigned)(n * D * D * sizeof(double2));
+    if (bytes) {
+      mbar_expect_tx(&sBar[warp][st], bytes);
+      tma_load_1d(slot[st], gU + (size_t)k0 * D * D, bytes, &sBar[warp][st]);
+    } else {
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&sBar[warp][st])) : "memory");
+    }
+  };
+  issue(0, 0);
+  double pr[D], pi[D];
+  double2* gS = a.states + (size_t)(valid ? b : 0) * (a.k_count + 1) * D;
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    const double2 v = valid ? a.psi0[b * D + d] : make_double2(0.0, 0.0);
+    pr[d] = v.x; pi[d] = v.y;
+    if (valid) __stcs(gS + d, v);
+  }
+  unsigned phase[2] = {0u, 0u};
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int st = (int)(c & 1);
+    if (c + 1 < nchunks) {
+      __syncwarp();
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(c + 1, st ^ 1);
+    }
+    mbar_wait(&sBar[warp][st], phase[st]);
+    phase[st] ^= 1u;
+    if (valid) {
+      const int n = (int)min((int64_t)CH, a.k_count - c * CH);
+      const double2* u = slot[st];
+      double2* o = gS + (size_t)(c * CH + 1) * D;
+      for (int i = 0; i < n; ++i) {
+        double yr[D], yi[D];
+#pragma unroll
+        for (int r = 0; r < D; ++r) {
+          double sr = 0.0, si = 0.0;
+#pragma unroll
+          for (int k = 0; k < D; ++k) {
+            const double2 m = u[(i * D + r) * D + k];
+            sr = fma(m.x, pr[k], sr);
+            sr = fma(-m.y, pi[k], sr);
+            si = fma(m.x, pi[k], si);
+            si = fma(m.y, pr[k], si);
+          }
+          yr[r] = sr; yi[r] = si;
+        }
+#pragma unroll
+        for (int d = 0; d < D; ++d) { pr[d] = yr[d]; pi[d] = yi[d]; __stcs(o + i * D + d, make_double2(yr[d], yi[d])); }
+      }
+    }
+  }
+}
+
+template <int D>
+static cudaError_t run_chain(int64_t batch, int64_t k_count, const double* U, const double* psi0, double* states,
+                             cudaStream_t s, int* launches) {
+  constexpr size_t smem = chain_smem<D>();
+  static bool attr = false;
+  if (!attr) {
+    const cudaError_t e = cudaFuncSetAttribute(chain_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  ChainArgs a{batch, k_count, reinterpret_cast<const double2*>(U), reinterpret_cast<const double2*>(psi0),
+              reinterpret_cast<double2*>(states)};
+  chain_kernel<D><<<(unsigned)((batch + kChainThreads - 1) / kChainThreads), kChainThreads, smem, s>>>(a);
+  ++*launches;
+  return cudaGetLastError();
+}
+
 // Per-sweep product of the tile aggregates, in order: A[b] = T_{n−1} ⋯ T_0.
 template <int D>
 __global__ void combine_tiles_kernel(int64_t batch, int64_t tiles_per_sweep, const double2* tiles, double2* out) {
@@ -335,12 +708,12 @@ __global__ void validate_kernel(int64_t n_sweep, const double* sweep, int P, int
 template <int D> size_t scan_ws_bytes(int64_t batch, int64_t k_count) { return ScanLayout<D>(batch, k_count).total; }
 
 size_t scan_workspace_bytes(int dim, int64_t batch, int64_t k_count) {
-  return dim == 2 ? scan_ws_bytes<2>(batch, k_count) : scan_ws_bytes<3>(batch, k_count);
+  return dim == 2 ? Scan2Layout<2>(batch, k_count).total : Scan2Layout<3>(batch, k_count).total;
 }
 
 size_t aggregate_workspace_bytes(int dim, int64_t batch, int64_t k_count) {
-  // same tiling; per-tile totals live in the agg region
-  return scan_workspace_bytes(dim, batch, k_count);
+  // v1 tiling; per-tile totals live in the agg region
+  return dim == 2 ? scan_ws_bytes<2>(batch, k_count) : scan_ws_bytes<3>(batch, k_count);
 }
 
 template <int D, bool SCAN>
@@ -381,10 +754,50 @@ static cudaError_t run_scan(int64_t batch, int64_t k_count, const double* U, con
   return cudaGetLastError();
 }
 
+template <int D>
+static cudaError_t run_scan2(int64_t batch, int64_t k_count, const double* U, const double* psi0, double* states,
+                             void* ws, cudaStream_t s, int* launches) {
+  Scan2Layout<D> L(batch, k_count);
+  char* w = static_cast<char*>(ws);
+  Scan2Args a;
+  a.batch = batch;
+  a.k_count = k_count;
+  a.tiles_per_sweep = L.tiles_per_sweep;
+  a.ntiles = L.ntiles;
+  a.U = reinterpret_cast<const double2*>(U);
+  a.psi0 = reinterpret_cast<const double2*>(psi0);
+  a.states = reinterpret_cast<double2*>(states);
+  a.ticket = reinterpret_cast<unsigned long long*>(w);
+  a.flags = reinterpret_cast<int*>(w + L.off_flags);
+  a.agg = reinterpret_cast<double2*>(w + L.off_agg);
+  a.psi_end = reinterpret_cast<double2*>(w + L.off_psi);
+  cudaError_t e = cudaMemsetAsync(w, 0, L.off_agg, s);   // ticket + flags
+  if (e != cudaSuccess) return e;
+  constexpr size_t smem = scan2_smem<D>();
+  static int grid = 0;
+  if (grid == 0) {
+    e = cudaFuncSetAttribute(scan2_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scan2_kernel<D>, Scan2Cfg<D>::NT, smem);
+    if (e != cudaSuccess) return e;
+    grid = sms * (per_sm > 0 ? per_sm : 1);   // persistent: every CTA resident (look-back forward progress)
+  }
+  const int g = (int)std::min<int64_t>(grid, L.ntiles);
+  scan2_kernel<D><<<g, Scan2Cfg<D>::NT, smem, s>>>(a);
+  ++*launches;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_scan(int dim, int64_t batch, int64_t k_count, const double* U, const double* psi0, double* states,
                         void* ws, cudaStream_t s, int* launches) {
-  return dim == 2 ? run_scan<2, true>(batch, k_count, U, psi0, states, nullptr, ws, s, launches)
-                  : run_scan<3, true>(batch, k_count, U, psi0, states, nullptr, ws, s, launches);
+  if (batch >= kChainMinBatch)   // enough sweeps to saturate HBM with one sequential chain per thread
+    return dim == 2 ? run_chain<2>(batch, k_count, U, psi0, states, s, launches)
+                    : run_chain<3>(batch, k_count, U, psi0, states, s, launches);
+  return dim == 2 ? run_scan2<2>(batch, k_count, U, psi0, states, ws, s, launches)
+                  : run_scan2<3>(batch, k_count, U, psi0, states, ws, s, launches);
 }
 
 cudaError_t launch_aggregate(int dim, int64_t batch, int64_t k_count, const double* U, double* aggregate, void* ws,

@@ -48,6 +48,15 @@ __device__ __forceinline__ void sincosT(float x, float* s, float* c) { sincosf(x
 __device__ __forceinline__ double sqrtT(double x) { return sqrt(x); }
 __device__ __forceinline__ float sqrtT(float x) { return sqrtf(x); }
 
+// sin/cos of a small angle (|x| ≤ 2^-6) by its Taylor polynomial through x^9 / x^8 (truncation < 1e-25 relative):
+// the Lie–Trotter arguments are Φ/2, θ/2 divided by n = 2^τ, so this path is the common one; larger arguments go to
+// the library sincos.
+template <typename T> __device__ __forceinline__ void sincos_small(T x, T* s, T* c) {
+  const T x2 = x * x;
+  *s = fmaT(x * x2, fmaT(x2, fmaT(x2, fmaT(x2, T(1.0 / 362880.0), T(-1.0 / 5040.0)), T(1.0 / 120.0)), T(-1.0 / 6.0)), x);
+  *c = fmaT(x2, fmaT(x2, fmaT(x2, fmaT(x2, T(1.0 / 40320.0), T(-1.0 / 720.0)), T(1.0 / 24.0)), T(-0.5)), T(1));
+}
+
 // Reduce ω·t (both FP64) to (−π, π] accurately: exact product as hi + lo (FMA), then Cody–Waite with a 3-part 2π.
 // Never a single-double 2π (SURVEY [V15]).  |result error| ≲ 5e-16 for |ω t| ≲ 1e9.
 __device__ __forceinline__ double reduce_phase(double w, double t) {
@@ -206,13 +215,62 @@ template <typename T> __device__ __forceinline__ void expo_su2(const T a[4], Res
   e.re[3] = cm1;  e.im[3] = sz;                      // cos − 1 + i s az
 }
 
-// Spin-one Lie–Trotter.  T − I from Eq. lie_trotter_4 with the corrections of reading R1, written with
-// θ1 = z + q/3, θ2 = 2q/3, θ3 = z − q/3 (z = az/n, q = aq/n, n = 2^τ):
-//   T11 − 1 = expm1(−iθ1) − s² e^{−iθ1}      T12 = (−i/√2) sinΦ e^{−iθ3/2} e^{−iφ}   T13 = −s² e^{−iθ2/2} e^{−2iφ}
-//   T21 = (−i/√2) sinΦ e^{−iθ3/2} e^{iφ}     T22 − 1 = expm1(iθ2) − 2s² e^{iθ2}      T23 = (−i/√2) sinΦ e^{iθ1/2} e^{−iφ}
-//   T31 = −s² e^{−iθ2/2} e^{2iφ}             T32 = (−i/√2) sinΦ e^{iθ1/2} e^{iφ}     T33 − 1 = expm1(iθ3) − s² e^{iθ3}
-// with s = sin(Φ/2), e^{iφ} = (ax + i ay)/√(ax²+ay²) (no atan2; := 1 at Φ = 0, reading R3), and the diagonal from
-// half-angle sines (expm1(iθ) = −2 sin²(θ/2) + i sin θ).  Then τ residual squarings.
+// Spin-one Lie–Trotter.  The leapfrog factor T = e^{−iD/2} e^{−iΦJφ} e^{−iD/2} with
+// Jφ = e^{−iφJz} Jx e^{iφJz} and D diagonal factors as T = R_φ T₀ R_φ†, R_φ = e^{−iφJz} = diag(e^{−iφ}, 1, e^{iφ}),
+// T₀ = e^{−iD/2} e^{−iΦJx} e^{−iD/2}.  T₀ is complex SYMMETRIC (diagonal·symmetric·diagonal), so is every power
+// T₀^{2^k}, and T^n = R_φ T₀^n R_φ† exactly.  The τ residual squarings therefore run on the 6 unique
+// entries of T₀ − I (63 FP64 instructions per squaring instead of 111 for a dense 3×3 complex square), and the
+// phases e^{−iφ(m−n)} are applied once at the end.  Same algorithm, same result up to rounding.
+//
+// T₀ − I from Eq. lie_trotter_4 at φ = 0 with the corrections of reading R1, θ1 = z + q/3, θ2 = 2q/3, θ3 = z − q/3
+// (z = az/n, q = aq/n, n = 2^τ, s = sin(Φ/2)):
+//   T11 − 1 = expm1(−iθ1) − s² e^{−iθ1}   T12 = T21 = (−i/√2) sinΦ e^{−iθ3/2}   T13 = T31 = −s² e^{−iθ2/2}
+//   T22 − 1 = expm1(iθ2) − 2s² e^{iθ2}    T23 = T32 = (−i/√2) sinΦ e^{iθ1/2}    T33 − 1 = expm1(iθ3) − s² e^{iθ3}
+// with the diagonal from half-angle sines (expm1(iθ) = −2 sin²(θ/2) + i sin θ), and e^{iφ} =
+// (ax + i ay)/√(ax² + ay²) (no atan2; := 1 at Φ = 0, reading R3).
+template <typename T> struct Sym3 {   // unique entries of a complex symmetric 3×3 residual
+  T r00, i00, r01, i01, r02, i02, r11, i11, r12, i12, r22, i22;
+};
+
+// s = (a + 2I)a for symmetric a (so s is symmetric):
+//   s00 = (a00+2)a00 + a01² + a02²   s01 = a01(a00 + a11 + 2) + a02 a12   s02 = a02(a00 + a22 + 2) + a01 a12
+//   s11 = (a11+2)a11 + a01² + a12²   s12 = a12(a11 + a22 + 2) + a01 a02   s22 = (a22+2)a22 + a02² + a12²
+template <typename T> __device__ __forceinline__ void sym_square(Sym3<T>& a) {
+  // complex squares of the off-diagonal entries
+  const T q01r = fmaT(a.r01, a.r01, -a.i01 * a.i01), q01i = fmaT(a.r01, a.i01, a.r01 * a.i01);
+  const T q02r = fmaT(a.r02, a.r02, -a.i02 * a.i02), q02i = fmaT(a.r02, a.i02, a.r02 * a.i02);
+  const T q12r = fmaT(a.r12, a.r12, -a.i12 * a.i12), q12i = fmaT(a.r12, a.i12, a.r12 * a.i12);
+  const T d0 = a.r00 + T(2), d1 = a.r11 + T(2), d2 = a.r22 + T(2);
+  Sym3<T> s;
+  // diagonal
+  s.r00 = fmaT(d0, a.r00, fmaT(-a.i00, a.i00, q01r + q02r));
+  s.i00 = fmaT(d0, a.i00, fmaT(a.i00, a.r00, q01i + q02i));
+  s.r11 = fmaT(d1, a.r11, fmaT(-a.i11, a.i11, q01r + q12r));
+  s.i11 = fmaT(d1, a.i11, fmaT(a.i11, a.r11, q01i + q12i));
+  s.r22 = fmaT(d2, a.r22, fmaT(-a.i22, a.i22, q02r + q12r));
+  s.i22 = fmaT(d2, a.i22, fmaT(a.i22, a.r22, q02i + q12i));
+  // off-diagonal: x·c + y·w with c = a_ii + a_jj + 2
+  {
+    const T cr = d0 + a.r11, ci = a.i00 + a.i11;
+    const T pr = fmaT(a.r02, a.r12, -a.i02 * a.i12), pi = fmaT(a.r02, a.i12, a.i02 * a.r12);
+    s.r01 = fmaT(a.r01, cr, fmaT(-a.i01, ci, pr));
+    s.i01 = fmaT(a.r01, ci, fmaT(a.i01, cr, pi));
+  }
+  {
+    const T cr = d0 + a.r22, ci = a.i00 + a.i22;
+    const T pr = fmaT(a.r01, a.r12, -a.i01 * a.i12), pi = fmaT(a.r01, a.i12, a.i01 * a.r12);
+    s.r02 = fmaT(a.r02, cr, fmaT(-a.i02, ci, pr));
+    s.i02 = fmaT(a.r02, ci, fmaT(a.i02, cr, pi));
+  }
+  {
+    const T cr = d1 + a.r22, ci = a.i11 + a.i22;
+    const T pr = fmaT(a.r01, a.r02, -a.i01 * a.i02), pi = fmaT(a.r01, a.i02, a.i01 * a.r02);
+    s.r12 = fmaT(a.r12, cr, fmaT(-a.i12, ci, pr));
+    s.i12 = fmaT(a.r12, ci, fmaT(a.i12, cr, pi));
+  }
+  a = s;
+}
+
 template <typename T> __device__ __forceinline__ void trotter_residual(const T a[4], int tau, Res<3, T>& e) {
   const T inv_n = ldexp(T(1), -tau);
   const T rxy = sqrtT(a[0] * a[0] + a[1] * a[1]);
@@ -222,50 +280,51 @@ template <typename T> __device__ __forceinline__ void trotter_residual(const T a
   const T z = a[2] * inv_n, q = a[3] * inv_n;
   const T th1 = z + q * T(kThird), th2 = T(2) * q * T(kThird), th3 = z - q * T(kThird);
   T s, c, s1, c1, s2, c2, s3, c3;
-  sincosT(Phi * T(0.5), &s, &c);
-  sincosT(th1 * T(0.5), &s1, &c1);
-  sincosT(th2 * T(0.5), &s2, &c2);
-  sincosT(th3 * T(0.5), &s3, &c3);
+  const T big = fmax(fmax(Phi, fabs(th1)), fmax(fabs(th2), fabs(th3)));
+  if (big <= T(0.03125)) {                           // half-angles ≤ 2^-6: polynomial
+    sincos_small<T>(Phi * T(0.5), &s, &c);
+    sincos_small<T>(th1 * T(0.5), &s1, &c1);
+    sincos_small<T>(th2 * T(0.5), &s2, &c2);
+    sincos_small<T>(th3 * T(0.5), &s3, &c3);
+  } else {
+    sincosT(Phi * T(0.5), &s, &c);
+    sincosT(th1 * T(0.5), &s1, &c1);
+    sincosT(th2 * T(0.5), &s2, &c2);
+    sincosT(th3 * T(0.5), &s3, &c3);
+  }
   const T ss = s * s;
   const T sinPhi_r2 = T(2) * s * c * T(kRsqrt2);     // sinΦ/√2
-  // e^{−iφ} = (cphi, −sphi); e^{−2iφ} = (cphi² − sphi², −2 cphi sphi)
+  Sym3<T> m;
+  // T12 = (−i/√2) sinΦ e^{−iθ3/2} = (−i) X (c3 − i s3) = X(−s3 − i c3)
+  m.r01 = -sinPhi_r2 * s3;  m.i01 = -sinPhi_r2 * c3;
+  // T23 = (−i/√2) sinΦ e^{iθ1/2} = (−i) X (c1 + i s1) = X(s1 − i c1)
+  m.r12 = sinPhi_r2 * s1;   m.i12 = -sinPhi_r2 * c1;
+  // T13 = −s² e^{−iθ2/2}
+  m.r02 = -ss * c2;         m.i02 = ss * s2;
+  {  // diagonal: e^{iθ} = (1 − 2sh², 2 sh ch); expm1(iθ) = (−2sh², 2 sh ch)
+    const T sin1 = T(2) * s1 * c1, v1 = T(-2) * s1 * s1;
+    const T sin2 = T(2) * s2 * c2, v2 = T(-2) * s2 * s2;
+    const T sin3 = T(2) * s3 * c3, v3 = T(-2) * s3 * s3;
+    m.r00 = v1 - ss * (T(1) + v1);             m.i00 = -sin1 + ss * sin1;          // expm1(−iθ1) − s² e^{−iθ1}
+    m.r11 = v2 - T(2) * ss * (T(1) + v2);      m.i11 = sin2 - T(2) * ss * sin2;    // expm1(iθ2) − 2s² e^{iθ2}
+    m.r22 = v3 - ss * (T(1) + v3);             m.i22 = sin3 - ss * sin3;           // expm1(iθ3) − s² e^{iθ3}
+  }
+#pragma unroll 2
+  for (int it = 0; it < tau; ++it) sym_square<T>(m);
+  // e = R_φ (T₀^n − I) R_φ†: entry (m, n) gains e^{−iφ(m−n)} (m = +1, 0, −1 ↔ rows 0, 1, 2)
   const T c2phi = cphi * cphi - sphi * sphi, s2phi = T(2) * cphi * sphi;
-  // off-diagonals: (−i)·X·(u + iv) = X·(v − iu)
-  {  // T12 = (−i/√2) sinΦ e^{−iθ3/2} e^{−iφ} : angle −(θ3/2 + φ)
-    const T ur = c3 * cphi - s3 * sphi, ui = -(s3 * cphi + c3 * sphi);   // e^{−iθ3/2} e^{−iφ}
-    e.re[1] = sinPhi_r2 * ui;  e.im[1] = -sinPhi_r2 * ur;
-  }
-  {  // T21 = (−i/√2) sinΦ e^{−iθ3/2} e^{iφ}
-    const T ur = c3 * cphi + s3 * sphi, ui = c3 * sphi - s3 * cphi;
-    e.re[3] = sinPhi_r2 * ui;  e.im[3] = -sinPhi_r2 * ur;
-  }
-  {  // T23 = (−i/√2) sinΦ e^{iθ1/2} e^{−iφ}
-    const T ur = c1 * cphi + s1 * sphi, ui = s1 * cphi - c1 * sphi;
-    e.re[5] = sinPhi_r2 * ui;  e.im[5] = -sinPhi_r2 * ur;
-  }
-  {  // T32 = (−i/√2) sinΦ e^{iθ1/2} e^{iφ}
-    const T ur = c1 * cphi - s1 * sphi, ui = s1 * cphi + c1 * sphi;
-    e.re[7] = sinPhi_r2 * ui;  e.im[7] = -sinPhi_r2 * ur;
-  }
-  {  // T13 = −s² e^{−iθ2/2} e^{−2iφ};  T31 = −s² e^{−iθ2/2} e^{2iφ}
-    e.re[2] = -ss * (c2 * c2phi - s2 * s2phi);
-    e.im[2] = ss * (s2 * c2phi + c2 * s2phi);
-    e.re[6] = -ss * (c2 * c2phi + s2 * s2phi);
-    e.im[6] = -ss * (c2 * s2phi - s2 * c2phi);
-  }
-  {  // diagonal: e^{iθ} = (1 − 2sh², 2 sh ch);  expm1(iθ) = (−2sh², 2 sh ch)
-    const T sin1 = T(2) * s1 * c1, v1 = T(-2) * s1 * s1;   // θ1
-    const T sin2 = T(2) * s2 * c2, v2 = T(-2) * s2 * s2;   // θ2
-    const T sin3 = T(2) * s3 * c3, v3 = T(-2) * s3 * s3;   // θ3
-    // T11 − 1 = expm1(−iθ1) − s² e^{−iθ1}
-    e.re[0] = v1 - ss * (T(1) + v1);    e.im[0] = -sin1 + ss * sin1;
-    // T22 − 1 = expm1(iθ2) − 2s² e^{iθ2}
-    e.re[4] = v2 - T(2) * ss * (T(1) + v2);  e.im[4] = sin2 - T(2) * ss * sin2;
-    // T33 − 1 = expm1(iθ3) − s² e^{iθ3}
-    e.re[8] = v3 - ss * (T(1) + v3);    e.im[8] = sin3 - ss * sin3;
-  }
-#pragma unroll 1
-  for (int it = 0; it < tau; ++it) res_square<3, T>(e);
+  e.re[0] = m.r00;  e.im[0] = m.i00;
+  e.re[4] = m.r11;  e.im[4] = m.i11;
+  e.re[8] = m.r22;  e.im[8] = m.i22;
+  // × e^{−iφ} = (cphi, −sphi)
+  e.re[1] = m.r01 * cphi + m.i01 * sphi;   e.im[1] = m.i01 * cphi - m.r01 * sphi;
+  e.re[5] = m.r12 * cphi + m.i12 * sphi;   e.im[5] = m.i12 * cphi - m.r12 * sphi;
+  // × e^{+iφ}
+  e.re[3] = m.r01 * cphi - m.i01 * sphi;   e.im[3] = m.i01 * cphi + m.r01 * sphi;
+  e.re[7] = m.r12 * cphi - m.i12 * sphi;   e.im[7] = m.i12 * cphi + m.r12 * sphi;
+  // × e^{∓2iφ}
+  e.re[2] = m.r02 * c2phi + m.i02 * s2phi; e.im[2] = m.i02 * c2phi - m.r02 * s2phi;
+  e.re[6] = m.r02 * c2phi - m.i02 * s2phi; e.im[6] = m.i02 * c2phi + m.r02 * s2phi;
 }
 
 // Spin-one "analytic" exponential (reading R14): D¹ of the SU(2) closed form, valid iff aq = 0.
