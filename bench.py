@@ -36,6 +36,8 @@ UNIT = "fine steps/s"
 # Nominal FP64 peak: 148 SMs × 64 FP64 FMA/clk/SM × 2 flop × 1.965 GHz (max SM clock).
 N_SM, FP64_FMA_PER_CLK_SM, SM_MAX_MHZ = 148, 64, 1965.0
 FP64_PEAK_TFLOPS = N_SM * FP64_FMA_PER_CLK_SM * 2 * SM_MAX_MHZ * 1e6 / 1e12
+# FP32 mode: 128 FP32 FMA/clk/SM (2:1 FP32:FP64 on B200, confirmed by ncu's roofline note), same clock.
+FP32_PEAK_TFLOPS = 2 * FP64_PEAK_TFLOPS
 
 
 def algorithmic_flops_per_fine_step(spin: str, expo: str, tau: int, method: str = "cf4") -> int:
@@ -212,6 +214,8 @@ def run_ours(args, rank, world, local):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
+    if args.workload == "C4":
+        return run_time_partition(args, rank, world, local, dev)
     # sweep shard of this rank
     if args.scaling == "weak":
         full = get_workload(args.workload, args.batch * world)
@@ -279,6 +283,7 @@ def run_ours(args, rank, world, local):
     achieved = flops_launch / (t_interval * 1e-3) / 1e12
     scan_gbs = B * K * scan_bytes_per_interval(D) / (t_scan * 1e-3) / 1e9
     clocks = clk.summary()
+    peak = FP64_PEAK_TFLOPS if args.precision == "fp64" else FP32_PEAK_TFLOPS
 
     # e2e through the C ABI with HOST buffers (pinned), copies inside the timed region
     e2e = None
@@ -323,20 +328,103 @@ def run_ours(args, rank, world, local):
             "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
             "scaling": args.scaling, "vs_baseline": None, "dtype": "f64" if args.precision == "fp64" else "f32",
             "data": "synthetic", "config": config_of(w, args, world),
-            "roofline": {"bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                         "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": None,
                          "kernel": f"interval_kernel<spin-{w.spin},{w.expo},{w.method},{w.field},{args.precision}>",
                          "flops_per_launch": flops_launch, "ms_per_launch": t_interval,
                          "dense_equivalent_tflops": dense_equivalent_flops_per_fine_step(w.spin, w.expo, w.tau, w.method)
                          * steps_per_rank / (t_interval * 1e-3) / 1e12,
-                         "peak_basis": "nominal FP64: 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (DESIGN.md §6)",
+                         "peak_basis": ("nominal FP64: 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (DESIGN.md §6)"
+                                        if args.precision == "fp64" else
+                                        "nominal FP32: 148 SM x 128 FFMA/clk x 2 x 1.965 GHz (DESIGN.md §6)"),
                          "measured_dfma_peak_tflops": measured_peak,
-                         "frac_at_observed_clock": (achieved / (FP64_PEAK_TFLOPS * clocks["sm_mhz"] / SM_MAX_MHZ)
+                         "frac_at_observed_clock": (achieved / (peak * clocks["sm_mhz"] / SM_MAX_MHZ)
                                                     if clocks.get("sm_mhz") else None)},
             "scan": {"bound": "hbm", "achieved": scan_gbs, "unit": "GB/s", "ms_per_launch": t_scan,
                      "bytes_per_launch": B * K * scan_bytes_per_interval(D)},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
             "fine_steps_per_step": total_steps,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def run_time_partition(args, rank, world, local, dev):
+    """C4: one long spin-half simulation (1 s at δt = 1 ns, K = 1e6) time-partitioned over the ranks: each rank
+    computes its intervals (global k), reduces them to its aggregate, the aggregates are all-gathered over NCCL
+    (the only exchange, 64 B per rank), each rank composes its carry and scans its own intervals (strong scaling)."""
+    import torch
+    import paper_2204_05586_b200 as ss
+    from paper_2204_05586_b200.distributed import gather_aggregates, partition_bounds
+
+    w = get_workload("C4", 1)
+    K, L, D = w.K, w.L, w.dim
+    kb, kc = partition_bounds(K, world, rank)
+    sim = ss.Simulator(w.spin, w.method, w.expo, w.tau, w.frame, args.precision, w.field)
+    sweep = torch.from_numpy(w.sweep).to(dev)
+    psi0 = torch.from_numpy(w.psi0).to(dev)
+    U = torch.empty((1, kc, D, D), dtype=torch.complex128, device=dev)
+    states = torch.empty((1, kc + 1, D), dtype=torch.complex128, device=dev)
+    lib = ss._lib.load()
+    scan_ws = torch.empty(int(lib.ss_scan_workspace_bytes(D, 1, kc)), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    sim.evaluate(sweep, w.t0, w.t0 + 20 * w.dt_out, w.dt_int, w.dt_out, psi0)     # validation + warm-up
+
+    def step(ev=None):
+        if ev is not None:
+            ev[0].record(stream)
+        sim.compute_unitaries(sweep, w.t0, w.t1, w.dt_int, w.dt_out, k_begin=kb, k_count=kc, out=U)
+        if ev is not None:
+            ev[1].record(stream)
+        A = ss.chain_aggregate(U)
+        A_all = gather_aggregates(A) if world > 1 else A[None]
+        carry = ss.compose_carry(A_all, psi0, rank)
+        ss.scan_states(U, carry, out=states, workspace=scan_ws)
+        if ev is not None:
+            ev[2].record(stream)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = ss.kernel_launches()
+    with ClockSampler(local) as clk:
+        start.record(stream)
+        for i in range(args.steps):
+            step(evs[i])
+        end.record(stream)
+        torch.cuda.synchronize()
+    launches = ss.kernel_launches() - launches0
+    barrier()
+    elapsed_ms = start.elapsed_time(end)
+    t_interval = float(np.mean([e[0].elapsed_time(e[1]) for e in evs]))
+    t_rest = float(np.mean([e[1].elapsed_time(e[2]) for e in evs]))
+    if world > 1:
+        t = torch.tensor([elapsed_ms, t_interval, t_rest], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        elapsed_ms, t_interval, t_rest = t.tolist()
+    value = w.fine_steps * args.steps / (elapsed_ms * 1e-3)
+    clocks = clk.summary()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64" if args.precision == "fp64" else "f32",
+            "data": "synthetic",
+            "config": {"workload": "C4", "spin": "half", "field": w.field, "time_end": w.t1,
+                       "time_step_integration": w.dt_int, "time_step_output": w.dt_out, "K": K, "L": L,
+                       "parallelism": f"time-partition x{world} (NCCL all_gather of carry aggregates)",
+                       "k_per_rank": kc},
+            "interval_ms_per_launch": t_interval, "exchange_and_scan_ms": t_rest,
+            "gpu_launches": int(launches), "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -271,11 +271,13 @@ template <typename T> __device__ __forceinline__ void sym_square(Sym3<T>& a) {
   a = s;
 }
 
-template <typename T> __device__ __forceinline__ void trotter_residual(const T a[4], int tau, Res<3, T>& e) {
+// T₀ − I and the phase of φ (cos φ, sin φ) for exponent arguments a (divided by n = 2^τ inside).
+template <typename T>
+__device__ __forceinline__ void trotter_init(const T a[4], int tau, Sym3<T>& m, T& cphi, T& sphi) {
   const T inv_n = ldexp(T(1), -tau);
   const T rxy = sqrtT(a[0] * a[0] + a[1] * a[1]);
-  const T cphi = (rxy > T(0)) ? a[0] / rxy : T(1);
-  const T sphi = (rxy > T(0)) ? a[1] / rxy : T(0);
+  cphi = (rxy > T(0)) ? a[0] / rxy : T(1);
+  sphi = (rxy > T(0)) ? a[1] / rxy : T(0);
   const T Phi = rxy * inv_n;
   const T z = a[2] * inv_n, q = a[3] * inv_n;
   const T th1 = z + q * T(kThird), th2 = T(2) * q * T(kThird), th3 = z - q * T(kThird);
@@ -294,7 +296,6 @@ template <typename T> __device__ __forceinline__ void trotter_residual(const T a
   }
   const T ss = s * s;
   const T sinPhi_r2 = T(2) * s * c * T(kRsqrt2);     // sinΦ/√2
-  Sym3<T> m;
   // T12 = (−i/√2) sinΦ e^{−iθ3/2} = (−i) X (c3 − i s3) = X(−s3 − i c3)
   m.r01 = -sinPhi_r2 * s3;  m.i01 = -sinPhi_r2 * c3;
   // T23 = (−i/√2) sinΦ e^{iθ1/2} = (−i) X (c1 + i s1) = X(s1 − i c1)
@@ -309,9 +310,11 @@ template <typename T> __device__ __forceinline__ void trotter_residual(const T a
     m.r11 = v2 - T(2) * ss * (T(1) + v2);      m.i11 = sin2 - T(2) * ss * sin2;    // expm1(iθ2) − 2s² e^{iθ2}
     m.r22 = v3 - ss * (T(1) + v3);             m.i22 = sin3 - ss * sin3;           // expm1(iθ3) − s² e^{iθ3}
   }
-#pragma unroll 2
-  for (int it = 0; it < tau; ++it) sym_square<T>(m);
-  // e = R_φ (T₀^n − I) R_φ†: entry (m, n) gains e^{−iφ(m−n)} (m = +1, 0, −1 ↔ rows 0, 1, 2)
+}
+
+// e = R_φ (T₀^n − I) R_φ†: entry (m, n) gains e^{−iφ(m−n)} (m = +1, 0, −1 ↔ rows 0, 1, 2).
+template <typename T>
+__device__ __forceinline__ void trotter_expand(const Sym3<T>& m, T cphi, T sphi, Res<3, T>& e) {
   const T c2phi = cphi * cphi - sphi * sphi, s2phi = T(2) * cphi * sphi;
   e.re[0] = m.r00;  e.im[0] = m.i00;
   e.re[4] = m.r11;  e.im[4] = m.i11;
@@ -325,6 +328,15 @@ template <typename T> __device__ __forceinline__ void trotter_residual(const T a
   // × e^{∓2iφ}
   e.re[2] = m.r02 * c2phi + m.i02 * s2phi; e.im[2] = m.i02 * c2phi - m.r02 * s2phi;
   e.re[6] = m.r02 * c2phi - m.i02 * s2phi; e.im[6] = m.i02 * c2phi + m.r02 * s2phi;
+}
+
+template <typename T> __device__ __forceinline__ void trotter_residual(const T a[4], int tau, Res<3, T>& e) {
+  Sym3<T> m;
+  T cphi, sphi;
+  trotter_init<T>(a, tau, m, cphi, sphi);
+#pragma unroll 2
+  for (int it = 0; it < tau; ++it) sym_square<T>(m);
+  trotter_expand<T>(m, cphi, sphi, e);
 }
 
 // Spin-one "analytic" exponential (reading R14): D¹ of the SU(2) closed form, valid iff aq = 0.
