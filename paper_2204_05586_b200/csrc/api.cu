@@ -128,6 +128,15 @@ ssb::IntervalParams make_params(const ss_sim* s, double t0, double dt_out, doubl
   p.n_threads = batch * k_count;
   p.tau = s->d.trotter_cutoff;
   p.frame = s->d.use_rotating_frame;
+  // Sub-interval split: when batch·K intervals fill fewer than ~2 waves of resident threads
+  // (148 SMs × 512), let S = 2, 4, … adjacent lanes share an interval.  S divides L (no ragged lanes in a warp) and
+  // S ≤ 32.  C3-sized batches keep S = 1.
+  {
+    const int64_t target = (int64_t)2 * 148 * 512;
+    int S = 1;
+    while (S < 32 && L % (2 * S) == 0 && p.n_threads * S < target) S *= 2;
+    p.split = S;
+  }
   p.sweep = sweep;
   p.unitaries = U;
   return p;

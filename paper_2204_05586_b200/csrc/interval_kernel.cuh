@@ -27,6 +27,7 @@ struct IntervalParams {
   int64_t n_threads;  // batch·k_count
   int32_t tau;
   int32_t frame;
+  int32_t split;        // S: lanes per interval (power of two ≤ 32); lane p runs fine steps [p·L/S, (p+1)·L/S)
   const double* sweep;  // [batch][P]
   double* unitaries;    // [batch][k_count][D][D] complex128
 };
@@ -53,10 +54,15 @@ __global__ void __launch_bounds__(kIntervalThreads, kIntervalMinBlocks<SPIN, T>(
 interval_kernel(const IntervalParams prm) {
   constexpr int D = SpinDim<SPIN>::D;
   constexpr int P = FieldParams<FIELD>::P;
-  const int64_t i = (int64_t)blockIdx.x * kIntervalThreads + threadIdx.x;
-  if (i >= prm.n_threads) return;
-  const int64_t b = i / prm.k_count;
-  const int64_t k = prm.k_begin + (i - b * prm.k_count);
+  const int64_t gt = (int64_t)blockIdx.x * kIntervalThreads + threadIdx.x;
+  const int S = prm.split;
+  const int64_t i = gt / S;                          // interval index (sweep-major)
+  const int part = (int)(gt - i * S);
+  const bool active = i < prm.n_threads;
+  if (S == 1 && !active) return;                     // with S > 1 every lane must reach the shuffles below
+  const int64_t ic = active ? i : 0;
+  const int64_t b = ic / prm.k_count;
+  const int64_t k = prm.k_begin + (ic - b * prm.k_count);
 
   double p[P];
 #pragma unroll
@@ -76,8 +82,9 @@ interval_kernel(const IntervalParams prm) {
   Res<D, T> A;   // U_r − I, U_r initialised to the identity
   res_zero(A);
 
+  const int64_t l_begin = (prm.L * part) / S, l_end = active ? (prm.L * (part + 1)) / S : l_begin;
 #pragma unroll 1
-  for (int64_t l = 0; l < prm.L; ++l) {
+  for (int64_t l = l_begin; l < l_end; ++l) {
     const double base = __dmul_rn((double)l, prm.dt);
     Res<D, T> u;
     if (METHOD == CF4) {
@@ -147,6 +154,25 @@ interval_kernel(const IntervalParams prm) {
     A = An;
   }
 
+  // Sub-interval split: lane p holds the partial product of its fine steps; combine later·earlier in a shuffle tree
+  // (U_r = P_{S−1} ⋯ P_0, same samples, only the association of the product differs).
+  if (S > 1) {
+    for (int off = 1; off < S; off <<= 1) {
+      Res<D, T> B;
+#pragma unroll
+      for (int e = 0; e < D * D; ++e) {
+        B.re[e] = __shfl_down_sync(0xffffffffu, A.re[e], off);
+        B.im[e] = __shfl_down_sync(0xffffffffu, A.im[e], off);
+      }
+      if ((part & (2 * off - 1)) == 0) {
+        Res<D, T> C;
+        res_mul<D, T>(B, A, C);
+        A = C;
+      }
+    }
+    if (part != 0 || !active) return;
+  }
+
   // a8: U_k = R_{ω_r}(−Δt)(I + A) = diag(e^{−iω_r m Δt})(I + A); written as complex128.
   double ph_re[D], ph_im[D];
   {
@@ -170,7 +196,7 @@ interval_kernel(const IntervalParams prm) {
 
 template <int SPIN, int EXPO, int METHOD, int FIELD, typename T>
 cudaError_t launch_interval(const IntervalParams& prm, cudaStream_t stream) {
-  const int64_t blocks = (prm.n_threads + kIntervalThreads - 1) / kIntervalThreads;
+  const int64_t blocks = (prm.n_threads * prm.split + kIntervalThreads - 1) / kIntervalThreads;
   if (blocks <= 0) return cudaSuccess;
   interval_kernel<SPIN, EXPO, METHOD, FIELD, T><<<(unsigned)blocks, kIntervalThreads, 0, stream>>>(prm);
   return cudaGetLastError();

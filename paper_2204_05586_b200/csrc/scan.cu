@@ -274,8 +274,12 @@ template <int D> struct Scan2Cfg;
 template <> struct Scan2Cfg<2> { static constexpr int NT = 128, C = 8; };
 template <> struct Scan2Cfg<3> { static constexpr int NT = 128, C = 4; };
 template <int D> constexpr int scan2_tile() { return Scan2Cfg<D>::NT * Scan2Cfg<D>::C; }
+// Per-thread shared-memory slots (a thread's C operators / C states), strides padded to an odd number of 16-byte
+// words so the warp's LDS.128/STS.128 at equal offsets of 32 slots are bank-conflict free.
+template <int D> __host__ __device__ constexpr int scan2_u_stride() { return (Scan2Cfg<D>::C * D * D) | 1; }
+template <int D> __host__ __device__ constexpr int scan2_s_stride() { return (Scan2Cfg<D>::C * D) | 1; }
 template <int D> constexpr size_t scan2_smem() {
-  return sizeof(double2) * (size_t)scan2_tile<D>() * (2 * D * D + D) + 64;
+  return sizeof(double2) * (size_t)Scan2Cfg<D>::NT * (2 * scan2_u_stride<D>() + scan2_s_stride<D>()) + 64;
 }
 
 template <int D> struct Scan2Layout {
@@ -337,9 +341,10 @@ template <int D> __device__ __forceinline__ CM<D> cm_shfl_down(const CM<D>& m, i
 template <int D>
 __global__ void __launch_bounds__(Scan2Cfg<D>::NT, 1) scan2_kernel(const Scan2Args a) {
   constexpr int NT = Scan2Cfg<D>::NT, C = Scan2Cfg<D>::C, TILE = NT * C, NW = NT / 32;
+  constexpr int SU = scan2_u_stride<D>(), SS = scan2_s_stride<D>();
   extern __shared__ __align__(128) double2 smem2[];
-  double2* sU[2] = {smem2, smem2 + TILE * D * D};
-  double2* sPsi = smem2 + 2 * TILE * D * D;
+  double2* sU[2] = {smem2, smem2 + NT * SU};                // [stage][thread][SU]
+  double2* sPsi = smem2 + 2 * NT * SU;                      // [thread][SS]
   __shared__ __align__(8) uint64_t sBar[2];
   __shared__ double2 sWarpTot[NW][D * D];
   __shared__ double2 sWarpPre[NW][D * D];
@@ -348,38 +353,42 @@ __global__ void __launch_bounds__(Scan2Cfg<D>::NT, 1) scan2_kernel(const Scan2Ar
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   auto tile_of = [&](long long t, long long& b, long long& j) { j = t / a.batch; b = t - j * a.batch; };
+  // every thread bulk-copies its own C consecutive operators of tile t into its padded slot of `stage`
   auto issue = [&](long long t, int stage) {
     long long b, j;
     tile_of(t, b, j);
-    const long long k0 = j * TILE;
-    const int n = (int)min((long long)TILE, a.k_count - k0);
-    const unsigned bytes = (unsigned)(n * D * D * sizeof(double2));
-    mbar_expect_tx(&sBar[stage], bytes);
-    tma_load_1d(sU[stage], a.U + ((size_t)b * a.k_count + k0) * D * D, bytes, &sBar[stage]);
+    const long long k0 = j * TILE + (long long)tid * C;
+    const int n = (int)max(0LL, min((long long)C, a.k_count - k0));
+    if (n > 0) {
+      const unsigned bytes = (unsigned)(n * D * D * sizeof(double2));
+      mbar_expect_tx(&sBar[stage], bytes);
+      tma_load_1d(sU[stage] + tid * SU, a.U + ((size_t)b * a.k_count + k0) * D * D, bytes, &sBar[stage]);
+    } else {
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&sBar[stage])) : "memory");
+    }
   };
 
   if (tid == 0) {
-    mbar_init(&sBar[0], 1);
-    mbar_init(&sBar[1], 1);
+    mbar_init(&sBar[0], NT);
+    mbar_init(&sBar[1], NT);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    const long long t0 = (long long)atomicAdd(a.ticket, 1ull);
-    sNext = t0;
-    if (t0 < a.ntiles) issue(t0, 0);
+    sNext = (long long)atomicAdd(a.ticket, 1ull);
   }
   __syncthreads();
   long long t = sNext;
+  if (t < a.ntiles) issue(t, 0);
   unsigned phase[2] = {0u, 0u};
   int stage = 0;
   while (t < a.ntiles) {
-    // prefetch the next tile into the other stage (its previous contents were consumed last iteration)
+    // Take the next ticket only now (one tile ahead, like every other CTA), so the tiles in flight at any moment
+    // form a contiguous ticket range; then prefetch it into the other stage (consumed last iteration).
     __syncthreads();
-    if (tid == 0) {
-      const long long nx = (long long)atomicAdd(a.ticket, 1ull);
-      sNext = nx;
-      if (nx < a.ntiles) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue(nx, stage ^ 1);
-      }
+    if (tid == 0) sNext = (long long)atomicAdd(a.ticket, 1ull);
+    __syncthreads();
+    const long long nx = sNext;
+    if (nx < a.ntiles) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(nx, stage ^ 1);
     }
     long long b, j;
     tile_of(t, b, j);
@@ -387,7 +396,7 @@ __global__ void __launch_bounds__(Scan2Cfg<D>::NT, 1) scan2_kernel(const Scan2Ar
     const int n_items = (int)min((long long)TILE, a.k_count - k0);
     mbar_wait(&sBar[stage], phase[stage]);
     phase[stage] ^= 1u;
-    const double2* U = sU[stage];
+    const double2* U = sU[stage] + tid * SU;                // this thread's C operators
 
     // thread aggregate, warp inclusive scan, warp totals
     CM<D> P;
@@ -397,7 +406,7 @@ __global__ void __launch_bounds__(Scan2Cfg<D>::NT, 1) scan2_kernel(const Scan2Ar
       const int it = tid * C + c;
       if (it < n_items) {
         CM<D> u;
-        cm_load(U + it * D * D, u);
+        cm_load(U + c * D * D, u);
         P = cm_mul(u, P);
       }
     }
@@ -509,16 +518,16 @@ __global__ void __launch_bounds__(Scan2Cfg<D>::NT, 1) scan2_kernel(const Scan2Ar
       const int it = tid * C + c;
       if (it < n_items) {
         CM<D> u;
-        cm_load(U + it * D * D, u);
+        cm_load(U + c * D * D, u);
         cm_apply(u, yr, yi, xr, xi);
 #pragma unroll
-        for (int d = 0; d < D; ++d) { yr[d] = xr[d]; yi[d] = xi[d]; sPsi[it * D + d] = make_double2(xr[d], xi[d]); }
+        for (int d = 0; d < D; ++d) { yr[d] = xr[d]; yi[d] = xi[d]; sPsi[tid * SS + c * D + d] = make_double2(xr[d], xi[d]); }
       }
     }
     __syncthreads();
     double2* gS = a.states + ((size_t)b * (a.k_count + 1) + k0 + 1) * D;
-    for (int e = tid; e < n_items * D; e += NT) __stcs(gS + e, sPsi[e]);
-    t = sNext;
+    for (int e = tid; e < n_items * D; e += NT) __stcs(gS + e, sPsi[(e / (C * D)) * SS + e % (C * D)]);
+    t = nx;
     stage ^= 1;
   }
 }
@@ -532,7 +541,10 @@ __global__ void __launch_bounds__(Scan2Cfg<D>::NT, 1) scan2_kernel(const Scan2Ar
 constexpr int kChainThreads = 64;
 constexpr int64_t kChainMinBatch = 4096;
 template <int D> struct ChainCfg { static constexpr int CH = 8; };
-template <int D> constexpr size_t chain_smem() { return sizeof(double2) * (size_t)kChainThreads * 2 * ChainCfg<D>::CH * D * D; }
+// Per-lane slot: 2 stages of CH operators, stride padded to an odd number of 16-byte words so the 32 lanes' LDS.128
+// at the same offset hit distinct banks (an unpadded stride is a multiple of 128 B: a 32-way conflict).
+template <int D> __host__ __device__ constexpr int chain_slot_stride() { return (2 * ChainCfg<D>::CH * D * D) | 1; }
+template <int D> constexpr size_t chain_smem() { return sizeof(double2) * (size_t)kChainThreads * chain_slot_stride<D>(); }
 
 struct ChainArgs {
   int64_t batch, k_count;
@@ -549,7 +561,7 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(const ChainArgs a)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t b = (int64_t)blockIdx.x * kChainThreads + tid;
   const bool valid = b < a.batch;
-  double2* slot[2] = {smem3 + (size_t)tid * 2 * CH * D * D, smem3 + (size_t)tid * 2 * CH * D * D + CH * D * D};
+  double2* slot[2] = {smem3 + (size_t)tid * chain_slot_stride<D>(), smem3 + (size_t)tid * chain_slot_stride<D>() + CH * D * D};
   if (lane == 0) {
     mbar_init(&sBar[warp][0], 32);
     mbar_init(&sBar[warp][1], 32);
