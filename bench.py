@@ -64,6 +64,16 @@ def dense_equivalent_flops_per_fine_step(spin: str, expo: str, tau: int, method:
     return n_exp * 72
 
 
+def ncu_traffic(kernel: str, workload: str, full_size: bool):
+    """DRAM bytes per launch of this kernel on this workload from the committed ncu capture (profiles/), or None."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+    except (OSError, ValueError):
+        return None
+    e = d.get(f"{kernel}@{workload}") if full_size else None
+    return e["bytes"] if e else None
+
+
 def scan_bytes_per_interval(dim: int) -> int:
     return (2 * dim * dim + 2 * dim) * 8       # read U_k, write ψ_{k+1}
 
@@ -284,6 +294,7 @@ def run_ours(args, rank, world, local):
     scan_gbs = B * K * scan_bytes_per_interval(D) / (t_scan * 1e-3) / 1e9
     clocks = clk.summary()
     peak = FP64_PEAK_TFLOPS if args.precision == "fp64" else FP32_PEAK_TFLOPS
+    kernel_name = f"interval_kernel<spin-{w.spin},{w.expo},{w.method},{w.field},{args.precision}>"
 
     # e2e through the C ABI with HOST buffers (pinned), copies inside the timed region
     e2e = None
@@ -329,8 +340,8 @@ def run_ours(args, rank, world, local):
             "scaling": args.scaling, "vs_baseline": None, "dtype": "f64" if args.precision == "fp64" else "f32",
             "data": "synthetic", "config": config_of(w, args, world),
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": None,
-                         "kernel": f"interval_kernel<spin-{w.spin},{w.expo},{w.method},{w.field},{args.precision}>",
+                         "frac": achieved / peak, "traffic": ncu_traffic(kernel_name, w.name, B == 8192),
+                         "kernel": kernel_name,
                          "flops_per_launch": flops_launch, "ms_per_launch": t_interval,
                          "dense_equivalent_tflops": dense_equivalent_flops_per_fine_step(w.spin, w.expo, w.tau, w.method)
                          * steps_per_rank / (t_interval * 1e-3) / 1e12,
