@@ -79,6 +79,12 @@ interval_kernel(const IntervalParams prm) {
     omega_r = f[2];
   }
 
+  FrameCF4 frame2;
+  if (METHOD == CF4) {
+    fld.init_cf4(prm.g1dt, prm.g2dt, prm.dt);
+    frame2.init(omega_r, prm.g1dt, prm.g2dt, prm.dt);
+  }
+
   Res<D, T> A;   // U_r − I, U_r initialised to the identity
   res_zero(A);
 
@@ -90,8 +96,11 @@ interval_kernel(const IntervalParams prm) {
     if (METHOD == CF4) {
       // a2/a3: samples at t_k + (l + g1,2)δt, rotated into the frame.
       double f1[4], f2[4];
-      sample_in_frame(fld, __dadd_rn(base, prm.g1dt), omega_r, prm.frame, f1);
-      sample_in_frame(fld, __dadd_rn(base, prm.g2dt), omega_r, prm.frame, f2);
+      // spin-half steps are trig-bound: advance the phases by rotation between anchors; spin-one steps are squaring-
+      // bound, so every step is an anchor there (no loop-carried phase state, fewer registers).
+      const bool anchor = (SPIN == SPIN_ONE) || ((l - l_begin) % kAnchor) == 0;
+      fld.sample_cf4(base, anchor, __dadd_rn(base, prm.g1dt), __dadd_rn(base, prm.g2dt), f1, f2);
+      if (prm.frame) frame2.apply(base, anchor, f1, f2);
       // a4: H̄1 δt = (w+ f1 + w− f2) δt, H̄2 δt = (w− f1 + w+ f2) δt (Eqs. cf4_sample_1/2).
       T a1[4], a2[4];
 #pragma unroll

@@ -47,6 +47,8 @@ __device__ __forceinline__ void sincosT(double x, double* s, double* c) { sincos
 __device__ __forceinline__ void sincosT(float x, float* s, float* c) { sincosf(x, s, c); }
 __device__ __forceinline__ double sqrtT(double x) { return sqrt(x); }
 __device__ __forceinline__ float sqrtT(float x) { return sqrtf(x); }
+__device__ __forceinline__ double rsqrtT(double x) { return rsqrt(x); }
+__device__ __forceinline__ float rsqrtT(float x) { return rsqrtf(x); }
 
 // sin/cos of a small angle (|x| ≤ 2^-6) by its Taylor polynomial through x^9 / x^8 (truncation < 1e-25 relative):
 // the Lie–Trotter arguments are Φ/2, θ/2 divided by n = 2^τ, so this path is the common one; larger arguments go to
@@ -74,24 +76,65 @@ __device__ __forceinline__ double reduce_phase(double w, double t) {
 // (ωx, ωy, ωz, ωq) at time t_k + off (the (t_k, off) pair is never rounded to one double — reading R8).
 template <int F> struct Field;
 
+// e^{i(ph0 + w·base_l)} along the fine steps of one interval: an exact sincos on anchor steps (every kAnchor-th step
+// of a lane, and its first), otherwise advanced by the per-interval rotation e^{iwδt} (error ≲ kAnchor·2 ulp of a
+// unit vector; the grid's base_l = fl(l·δt) differs from l·δt by < 1 ulp, i.e. ≲ 1e-15 rad at |w δt| ≤ 5).
+constexpr int kAnchor = 8;
+struct PhaseStepper {
+  double w, ph0, cd, sd, c, s;
+  __device__ __forceinline__ void init(double w_, double ph0_, double dt) {
+    w = w_; ph0 = ph0_;
+    sincos(w * dt, &sd, &cd);
+  }
+  __device__ __forceinline__ void next(double base, bool anchor) {
+    if (anchor) {
+      sincos(fma(w, base, ph0), &s, &c);
+    } else {
+      const double cn = fma(c, cd, -s * sd);
+      s = fma(s, cd, c * sd);
+      c = cn;
+    }
+  }
+};
+
+// CF4 pair sampling: sample_cf4(base, off1, off2, ...) returns the fields at the two Gauss points of the step that
+// starts at t_k + base (off1,2 = fl(base + fl(g1,2·δt))).  Fields with an RF phase evaluate one sincos at the step
+// base and reach both Gauss points by rotating with per-interval constants e^{iω g1,2 δt} (init_cf4) — the same
+// angle up to ~1e-15 rad at half the trigonometric work.
 template <> struct Field<FIELD_CONSTANT> {
   double f0, f1, f2, f3;
   __device__ __forceinline__ void init(const double* p, double) { f0 = p[0]; f1 = p[1]; f2 = p[2]; f3 = p[3]; }
   __device__ __forceinline__ void sample(double, double f[4]) const { f[0] = f0; f[1] = f1; f[2] = f2; f[3] = f3; }
+  __device__ __forceinline__ void init_cf4(double, double, double) {}
+  __device__ __forceinline__ void sample_cf4(double, bool, double o1, double o2, double g1[4], double g2[4]) {
+    sample(o1, g1); sample(o2, g2);
+  }
 };
 
 template <> struct Field<FIELD_RABI_LINEAR> {        // ω0 Jz + 2Ω cos(ω0 t) Jx
-  double w0, two_om, ph0;
+  double w0, two_om, ph0, c1, s1, c2, s2;
+  PhaseStepper ps;
   __device__ __forceinline__ void init(const double* p, double t_k) {
     w0 = p[0]; two_om = 2.0 * p[1]; ph0 = reduce_phase(p[0], t_k);
   }
   __device__ __forceinline__ void sample(double off, double f[4]) const {
     f[0] = two_om * cos(fma(w0, off, ph0)); f[1] = 0.0; f[2] = w0; f[3] = 0.0;
   }
+  __device__ __forceinline__ void init_cf4(double g1dt, double g2dt, double dt) {
+    sincos(w0 * g1dt, &s1, &c1); sincos(w0 * g2dt, &s2, &c2);
+    ps.init(w0, ph0, dt);
+  }
+  __device__ __forceinline__ void sample_cf4(double base, bool anchor, double, double, double g1[4], double g2[4]) {
+    ps.next(base, anchor);
+    const double sb = ps.s, cb = ps.c;
+    g1[0] = two_om * fma(cb, c1, -sb * s1); g1[1] = 0.0; g1[2] = w0; g1[3] = 0.0;
+    g2[0] = two_om * fma(cb, c2, -sb * s2); g2[1] = 0.0; g2[2] = w0; g2[3] = 0.0;
+  }
 };
 
 template <> struct Field<FIELD_RABI_CIRCULAR> {      // ω0 Jz + Ω(cos(ω0 t) Jx + sin(ω0 t) Jy)
-  double w0, om, ph0;
+  double w0, om, ph0, c1, s1, c2, s2;
+  PhaseStepper ps;
   __device__ __forceinline__ void init(const double* p, double t_k) {
     w0 = p[0]; om = p[1]; ph0 = reduce_phase(p[0], t_k);
   }
@@ -100,23 +143,47 @@ template <> struct Field<FIELD_RABI_CIRCULAR> {      // ω0 Jz + Ω(cos(ω0 t) J
     sincos(fma(w0, off, ph0), &s, &c);
     f[0] = om * c; f[1] = om * s; f[2] = w0; f[3] = 0.0;
   }
+  __device__ __forceinline__ void init_cf4(double g1dt, double g2dt, double dt) {
+    sincos(w0 * g1dt, &s1, &c1); sincos(w0 * g2dt, &s2, &c2);
+    ps.init(w0, ph0, dt);
+  }
+  __device__ __forceinline__ void sample_cf4(double base, bool anchor, double, double, double g1[4], double g2[4]) {
+    ps.next(base, anchor);
+    const double sb = ps.s, cb = ps.c;
+    g1[0] = om * fma(cb, c1, -sb * s1); g1[1] = om * fma(sb, c1, cb * s1); g1[2] = w0; g1[3] = 0.0;
+    g2[0] = om * fma(cb, c2, -sb * s2); g2[1] = om * fma(sb, c2, cb * s2); g2[2] = w0; g2[3] = 0.0;
+  }
 };
 
 template <> struct Field<FIELD_NEURAL> {
   // p = [ω_bias, ω_rf, Ω, Ω_p, ω_sig, t_p, ω_q] (reading R16)
-  double wb, wrf, two_om, op, ws, wq, ph0, dtk;
+  double wb, wrf, two_om, op, ws, wq, ph0, dtk, c1, s1, c2, s2;
   __device__ __forceinline__ void init(const double* p, double t_k) {
     wb = p[0]; wrf = p[1]; two_om = 2.0 * p[2]; op = p[3]; ws = p[4]; wq = p[6];
     ph0 = reduce_phase(p[1], t_k);
     dtk = __dsub_rn(t_k, p[5]);                     // t_k − t_p
   }
+  __device__ __forceinline__ double pulse_z(double off) const {
+    const double x = ws * (dtk + off);             // ω_sig (t − t_p)
+    const double pulse = (x >= 0.0 && x <= kTwoPi1) ? sin(x) : 0.0;   // sinp (reading R12)
+    return fma(op, pulse, wb);
+  }
   __device__ __forceinline__ void sample(double off, double f[4]) const {
     f[0] = two_om * cos(fma(wrf, off, ph0));       // 2Ω cos(ω_rf t)
     f[1] = 0.0;
-    const double x = ws * (dtk + off);             // ω_sig (t − t_p)
-    const double pulse = (x >= 0.0 && x <= kTwoPi1) ? sin(x) : 0.0;   // sinp (reading R12)
-    f[2] = fma(op, pulse, wb);
+    f[2] = pulse_z(off);
     f[3] = wq;
+  }
+  PhaseStepper ps;
+  __device__ __forceinline__ void init_cf4(double g1dt, double g2dt, double dt) {
+    sincos(wrf * g1dt, &s1, &c1); sincos(wrf * g2dt, &s2, &c2);
+    ps.init(wrf, ph0, dt);
+  }
+  __device__ __forceinline__ void sample_cf4(double base, bool anchor, double o1, double o2, double g1[4], double g2[4]) {
+    ps.next(base, anchor);                         // e^{i ω_rf (t_k + base)}, reduced
+    const double sb = ps.s, cb = ps.c;
+    g1[0] = two_om * fma(cb, c1, -sb * s1); g1[1] = 0.0; g1[2] = pulse_z(o1); g1[3] = wq;
+    g2[0] = two_om * fma(cb, c2, -sb * s2); g2[1] = 0.0; g2[2] = pulse_z(o2); g2[3] = wq;
   }
 };
 
@@ -124,6 +191,10 @@ template <> struct Field<FIELD_GRADIENT> {          // ω_z = x − 2y
   double wz;
   __device__ __forceinline__ void init(const double* p, double) { wz = fma(-2.0, p[1], p[0]); }
   __device__ __forceinline__ void sample(double, double f[4]) const { f[0] = 0.0; f[1] = 0.0; f[2] = wz; f[3] = 0.0; }
+  __device__ __forceinline__ void init_cf4(double, double, double) {}
+  __device__ __forceinline__ void sample_cf4(double, bool, double o1, double o2, double g1[4], double g2[4]) {
+    sample(o1, g1); sample(o2, g2);
+  }
 };
 
 // Rotating frame (reading R6): rotate (ωx, ωy) by θ = ω_r·t_local, shift ωz by −ω_r; ωq unchanged.
@@ -135,6 +206,29 @@ __device__ __forceinline__ void to_rotating_frame(double f[4], double t_local, d
   f[1] = fma(c, fy, -s * fx);
   f[2] = f[2] - omega_r;
 }
+
+// Frame rotation for the two CF4 samples of one step: θ1,2 = ω_r·base + ω_r·g1,2δt, one sincos per step plus the
+// per-interval rotations (cb1, sb1), (cb2, sb2) of ω_r·g1,2δt.
+struct FrameCF4 {
+  double wr, c1, s1, c2, s2;
+  PhaseStepper ps;
+  __device__ __forceinline__ void init(double omega_r, double g1dt, double g2dt, double dt) {
+    wr = omega_r;
+    sincos(omega_r * g1dt, &s1, &c1);
+    sincos(omega_r * g2dt, &s2, &c2);
+    ps.init(omega_r, 0.0, dt);
+  }
+  __device__ __forceinline__ void apply(double base, bool anchor, double f1[4], double f2[4]) {
+    ps.next(base, anchor);
+    const double sb = ps.s, cb = ps.c;
+    const double ca = fma(cb, c1, -sb * s1), sa = fma(sb, c1, cb * s1);
+    const double cc = fma(cb, c2, -sb * s2), sc = fma(sb, c2, cb * s2);
+    double fx = f1[0], fy = f1[1];
+    f1[0] = fma(ca, fx, sa * fy); f1[1] = fma(ca, fy, -sa * fx); f1[2] -= wr;
+    fx = f2[0]; fy = f2[1];
+    f2[0] = fma(cc, fx, sc * fy); f2[1] = fma(cc, fy, -sc * fx); f2[2] -= wr;
+  }
+};
 
 // ---- residual matrices ------------------------------------------------------------------------------------------
 template <int D, typename T> struct Res {
@@ -203,11 +297,23 @@ template <int D, typename T> __device__ __forceinline__ void res_square(Res<D, T
 
 // Spin-half closed form: exp(−i a·σ/2) = cos(r/2) I − i (sin(r/2)/r) a·σ.  cos(r/2) − 1 = −2 sin²(r/4).
 template <typename T> __device__ __forceinline__ void expo_su2(const T a[4], Res<2, T>& e) {
-  const T r = sqrtT(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]);
-  T sq, cq;
-  sincosT(r * T(0.25), &sq, &cq);
-  const T cm1 = T(-2) * sq * sq;                     // cos(r/2) − 1
-  const T s = (r > T(0)) ? (T(2) * sq * cq) / r : T(0.5);   // sin(r/2)/r (reading R4)
+  const T r2 = a[0] * a[0] + a[1] * a[1] + a[2] * a[2];
+  T cm1, s;
+  if (r2 <= T(0.00390625)) {
+    // r ≤ 2^-4 (every fine step of the configs): both functions are even, so series in r² need no sqrt, sincos
+    // or division.  cos(r/2) − 1 = −r²/8 + r⁴/384 − r⁶/46080 + r⁸/10321920 − r¹⁰/3715891200,
+    // sin(r/2)/r = 1/2 − r²/48 + r⁴/3840 − r⁶/645120 + r⁸/185794560 (truncation < 1e-19 relative).
+    cm1 = r2 * fmaT(r2, fmaT(r2, fmaT(r2, fmaT(r2, T(-1.0 / 3715891200.0), T(1.0 / 10321920.0)),
+                                        T(-1.0 / 46080.0)), T(1.0 / 384.0)), T(-0.125));
+    s = fmaT(r2, fmaT(r2, fmaT(r2, fmaT(r2, T(1.0 / 185794560.0), T(-1.0 / 645120.0)), T(1.0 / 3840.0)),
+                      T(-1.0 / 48.0)), T(0.5));
+  } else {
+    const T r = sqrtT(r2);
+    T sq, cq;
+    sincosT(r * T(0.25), &sq, &cq);
+    cm1 = T(-2) * sq * sq;                           // cos(r/2) − 1 without cancellation
+    s = (T(2) * sq * cq) / r;                        // sin(r/2)/r  (r = 0 takes the series branch: ½, reading R4)
+  }
   const T sx = s * a[0], sy = s * a[1], sz = s * a[2];
   e.re[0] = cm1;  e.im[0] = -sz;                     // cos − 1 − i s az
   e.re[1] = -sy;  e.im[1] = -sx;                     // −i s (ax − i ay)
@@ -275,9 +381,16 @@ template <typename T> __device__ __forceinline__ void sym_square(Sym3<T>& a) {
 template <typename T>
 __device__ __forceinline__ void trotter_init(const T a[4], int tau, Sym3<T>& m, T& cphi, T& sphi) {
   const T inv_n = ldexp(T(1), -tau);
-  const T rxy = sqrtT(a[0] * a[0] + a[1] * a[1]);
-  cphi = (rxy > T(0)) ? a[0] / rxy : T(1);
-  sphi = (rxy > T(0)) ? a[1] / rxy : T(0);
+  const T r2 = a[0] * a[0] + a[1] * a[1];
+  T rxy = T(0);
+  cphi = T(1);
+  sphi = T(0);
+  if (r2 > T(0)) {                                   // e^{iφ} = (ax + i ay)/√(ax² + ay²) via one reciprocal sqrt
+    const T ir = rsqrtT(r2);
+    rxy = r2 * ir;
+    cphi = a[0] * ir;
+    sphi = a[1] * ir;
+  }
   const T Phi = rxy * inv_n;
   const T z = a[2] * inv_n, q = a[3] * inv_n;
   const T th1 = z + q * T(kThird), th2 = T(2) * q * T(kThird), th3 = z - q * T(kThird);
