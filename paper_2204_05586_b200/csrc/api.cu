@@ -64,8 +64,10 @@ struct ss_sim {
   int validate = 1;
   ssb::IntervalLaunchFn interval = nullptr;
   ssb::ExpoLaunchFn expo = nullptr;
-  // ss_evaluate_host staging (two pipeline slots)
+  // ss_evaluate_host pipeline: streams[0] computes, streams[1] copies; two staging slots; events order them
   cudaStream_t streams[2] = {nullptr, nullptr};
+  cudaEvent_t computed[2] = {nullptr, nullptr};   // slot's kernels done → its D2H may start
+  cudaEvent_t drained[2] = {nullptr, nullptr};    // slot's D2H done → its buffers may be reused
   int device = -1;
   struct Slot {
     void* buf = nullptr;
@@ -208,6 +210,10 @@ void ss_destroy(ss_sim* s) {
     if (sl.buf) cudaFree(sl.buf);
   for (auto& st : s->streams)
     if (st) cudaStreamDestroy(st);
+  for (int k = 0; k < 2; ++k) {
+    if (s->computed[k]) cudaEventDestroy(s->computed[k]);
+    if (s->drained[k]) cudaEventDestroy(s->drained[k]);
+  }
   delete s;
 }
 
@@ -401,11 +407,19 @@ int ss_evaluate_host(ss_sim* s, double t0, double t1, double dt_int, double dt_o
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
-  if (s->device != dev) {  // (re)create per-device streams and drop buffers of another device
+  if (s->device != dev) {  // (re)create per-device streams/events and drop buffers of another device
     for (auto& st : s->streams) if (st) cudaStreamDestroy(st), st = nullptr;
     for (auto& sl : s->slots) if (sl.buf) cudaFree(sl.buf), sl.buf = nullptr, sl.cap = 0;
+    for (int k = 0; k < 2; ++k) {
+      if (s->computed[k]) cudaEventDestroy(s->computed[k]), s->computed[k] = nullptr;
+      if (s->drained[k]) cudaEventDestroy(s->drained[k]), s->drained[k] = nullptr;
+    }
     for (auto& st : s->streams)
       if ((e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)) != cudaSuccess) return cuda_fail(e, "stream create");
+    for (int k = 0; k < 2; ++k)
+      if ((e = cudaEventCreateWithFlags(&s->computed[k], cudaEventDisableTiming)) != cudaSuccess ||
+          (e = cudaEventCreateWithFlags(&s->drained[k], cudaEventDisableTiming)) != cudaSuccess)
+        return cuda_fail(e, "event create");
     s->device = dev;
   }
   const int D = s->dim;
@@ -427,35 +441,42 @@ int ss_evaluate_host(ss_sim* s, double t0, double t1, double dt_int, double dt_o
       sl.cap = slot_bytes;
     }
   }
+  // Chunk c: [compute stream] wait drained[slot] (its D2H two chunks ago) → H2D inputs → kernels → record
+  // computed[slot];  [copy stream] wait computed[slot] → D2H → record drained[slot].  Compute stays serial over
+  // chunks (each chunk fills the GPU), so the D2H of chunk c overlaps the kernels of chunk c+1.
+  cudaStream_t cs = s->streams[0], xs = s->streams[1];
   for (int64_t c = 0, b0 = 0; c < n_chunks; ++c) {
     const int64_t cb = std::min<int64_t>(cb_max, batch - b0);
     if (cb <= 0) break;
     const int k = (int)(c % nslots);
-    cudaStream_t st = s->streams[k];
     char* base = static_cast<char*>(s->slots[k].buf);
     double* d_sweep = reinterpret_cast<double*>(base);
     double* d_psi0 = reinterpret_cast<double*>(base + sweep_b);
     double* d_states = reinterpret_cast<double*>(base + sweep_b + psi0_b);
     double* d_U = reinterpret_cast<double*>(base + sweep_b + psi0_b + states_b);
     void* d_scan = base + sweep_b + psi0_b + states_b + U_b;
-    if ((e = cudaMemcpyAsync(d_sweep, h_sweep + b0 * s->P, sizeof(double) * s->P * cb, cudaMemcpyHostToDevice, st)) ||
-        (e = cudaMemcpyAsync(d_psi0, h_psi0 + b0 * 2 * D, sizeof(double) * 2 * D * cb, cudaMemcpyHostToDevice, st)))
+    if (c >= nslots && (e = cudaStreamWaitEvent(cs, s->drained[k], 0)) != cudaSuccess) return cuda_fail(e, "event wait");
+    if ((e = cudaMemcpyAsync(d_sweep, h_sweep + b0 * s->P, sizeof(double) * s->P * cb, cudaMemcpyHostToDevice, cs)) ||
+        (e = cudaMemcpyAsync(d_psi0, h_psi0 + b0 * 2 * D, sizeof(double) * 2 * D * cb, cudaMemcpyHostToDevice, cs)))
       return cuda_fail(e, "H2D copy");
     const auto p = make_params(s, t0, dt_out, dt, L, 0, K, cb, d_sweep, d_U);
-    if ((rc = launch_interval_checked(s, p, st))) return rc;
+    if ((rc = launch_interval_checked(s, p, cs))) return rc;
     int n = 0;
-    if ((e = ssb::launch_scan(D, cb, K, d_U, d_psi0, d_states, d_scan, st, &n)) != cudaSuccess)
+    if ((e = ssb::launch_scan(D, cb, K, d_U, d_psi0, d_states, d_scan, cs, &n)) != cudaSuccess)
       return cuda_fail(e, "scan launch");
     g_launches.fetch_add(n);
+    if ((e = cudaEventRecord(s->computed[k], cs)) || (e = cudaStreamWaitEvent(xs, s->computed[k], 0)))
+      return cuda_fail(e, "event record/wait");
     if ((e = cudaMemcpyAsync(h_states + b0 * 2 * D * (K + 1), d_states, sizeof(double) * 2 * D * cb * (K + 1),
-                             cudaMemcpyDeviceToHost, st)))
+                             cudaMemcpyDeviceToHost, xs)))
       return cuda_fail(e, "D2H copy (states)");
     if (h_U && (e = cudaMemcpyAsync(h_U + b0 * 2 * D * D * K, d_U, sizeof(double) * 2 * D * D * cb * K,
-                                    cudaMemcpyDeviceToHost, st)))
+                                    cudaMemcpyDeviceToHost, xs)))
       return cuda_fail(e, "D2H copy (unitaries)");
+    if ((e = cudaEventRecord(s->drained[k], xs))) return cuda_fail(e, "event record");
     b0 += cb;
   }
-  for (int k = 0; k < nslots; ++k)
+  for (int k = 0; k < 2; ++k)
     if ((e = cudaStreamSynchronize(s->streams[k])) != cudaSuccess) return cuda_fail(e, "stream synchronize");
   return SS_OK;
 }
