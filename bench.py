@@ -41,18 +41,21 @@ FP32_PEAK_TFLOPS = 2 * FP64_PEAK_TFLOPS
 
 
 def algorithmic_flops_per_fine_step(spin: str, expo: str, tau: int, method: str = "cf4") -> int:
-    """Matrix arithmetic of one fine step in this implementation's formulation, counting every real
-    +, −, × once (an FMA is 2): Lie–Trotter residual squaring on the complex-symmetric leapfrog factor T₀
-    (6 unique entries) = 99 flop; residual product a + b + ab = 234 (3×3) / 72 (2×2).  Field trig, the T − I
-    construction, the φ phases and the frame are not counted (a lower bound)."""
+    """Arithmetic of one fine step in this implementation's formulation, counting every real +, −, ×
+    once (an FMA is 2).
+
+    spin-one Lie–Trotter: residual squaring on the complex-symmetric leapfrog factor T₀ (6 unique entries) = 99 flop
+    × τ per exponential, residual product a + b + ab = 234 (3×3) per exponential; field, frame, T − I construction
+    and phases are not counted (a lower bound: ncu counts 5 706 executed FP64 flop per step at τ = 24 vs 5 220 here,
+    profiles/r01/r01_flops_c3.csv).
+    spin-half: per CF4 step 2 × (SU(2) series 26 + residual product 2×2 72) + CF4 weights 32 + two field samples 16 +
+    frame rotation 26 + phase steppers 12 + grid 2 = 284 (ncu: 283 executed, profiles/r01/r01_flops_c4.csv)."""
     n_exp = 2 if method == "cf4" else 1
     if spin == "one":
         prod = 234
         per_exp = 99 * tau if expo == "lie_trotter" else 0
-    else:
-        prod = 72
-        per_exp = 0
-    return n_exp * (per_exp + prod)
+        return n_exp * (per_exp + prod)
+    return 284 if method == "cf4" else 142
 
 
 def dense_equivalent_flops_per_fine_step(spin: str, expo: str, tau: int, method: str = "cf4") -> int:
@@ -424,6 +427,8 @@ def run_time_partition(args, rank, world, local, dev):
         elapsed_ms, t_interval, t_rest = t.tolist()
     value = w.fine_steps * args.steps / (elapsed_ms * 1e-3)
     clocks = clk.summary()
+    flops_launch = algorithmic_flops_per_fine_step(w.spin, w.expo, w.tau, w.method) * kc * L
+    achieved = flops_launch / (t_interval * 1e-3) / 1e12
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -434,6 +439,11 @@ def run_time_partition(args, rank, world, local, dev):
                        "time_step_integration": w.dt_int, "time_step_output": w.dt_out, "K": K, "L": L,
                        "parallelism": f"time-partition x{world} (NCCL all_gather of carry aggregates)",
                        "k_per_rank": kc},
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                         "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+                         "kernel": f"interval_kernel<spin-half,analytic,cf4,neural,{args.precision}>",
+                         "flops_per_launch": flops_launch, "ms_per_launch": t_interval,
+                         "peak_basis": "nominal FP64: 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (DESIGN.md §6)"},
             "interval_ms_per_launch": t_interval, "exchange_and_scan_ms": t_rest,
             "gpu_launches": int(launches), "clocks": clocks,
         }
