@@ -128,6 +128,14 @@ int ss_scan_states(int32_t dim, int64_t batch, int64_t k_count, const double* d_
                    const double* d_state_init, double* d_states, void* d_workspace, size_t workspace_bytes,
                    void* stream);
 
+/* Row a9 with the expected spin projection ⟨J⟩ = (ψ†Jxψ, ψ†Jyψ, ψ†Jzψ) (the paper's lazily computed
+ * observable) fused into the state write-out.  d_spin: device [batch][k_count+1][3]
+ * float64 (8-byte aligned).  d_states may be NULL to write only ⟨J⟩ (24 B instead of 16·dim B per interval); at least
+ * one of the two must be non-NULL.  Workspace as ss_scan_states. */
+int ss_scan_states_spin(int32_t dim, int64_t batch, int64_t k_count, const double* d_unitaries,
+                        const double* d_state_init, double* d_states, double* d_spin, void* d_workspace,
+                        size_t workspace_bytes, void* stream);
+
 /* Time-partition pieces (multi-GPU, one long simulation).  Aggregate of a partition:
  * d_aggregate[b] = U[b][k_count−1] ⋯ U[b][0]  ([batch][dim][dim] complex128).
  * d_workspace >= ss_aggregate_workspace_bytes(dim, batch, k_count). */

@@ -23,7 +23,8 @@ import torch
 from . import _lib
 from ._lib import EXPONENTIATION, FIELD, INTEGRATION, PRECISION, SPIN, SpinsimError, check
 
-__all__ = ["Simulator", "Results", "SpinsimError", "plan", "num_sweep_params", "scan_states", "chain_aggregate",
+__all__ = ["Simulator", "Results", "SpinsimError", "plan", "num_sweep_params", "scan_states", "scan_states_spin",
+           "chain_aggregate",
            "compose_carry", "spin_projection", "kernel_launches", "load"]
 
 
@@ -201,6 +202,24 @@ def scan_states(unitaries: torch.Tensor, state_init: torch.Tensor, out=None, wor
                              _dev_ptr(state_init, "state_init", torch.complex128), _dev_ptr(states, "states"),
                              _dev_ptr(workspace, "workspace"), workspace.numel(), _stream_ptr(stream)), "ss_scan_states")
     return states
+
+
+def scan_states_spin(unitaries: torch.Tensor, state_init: torch.Tensor, want_states: bool = True, workspace=None,
+                     stream=None):
+    """Row a9 with ⟨J⟩ fused into the write-out: returns (states [B][K+1][dim] or None, spin [B][K+1][3])."""
+    B, K, dim, _ = unitaries.shape
+    lib = _lib.load()
+    need = int(lib.ss_scan_workspace_bytes(dim, B, K))
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(need, dtype=torch.uint8, device=unitaries.device)
+    states = torch.empty((B, K + 1, dim), dtype=torch.complex128, device=unitaries.device) if want_states else None
+    spin = torch.empty((B, K + 1, 3), dtype=torch.float64, device=unitaries.device)
+    check(lib.ss_scan_states_spin(dim, B, K, _dev_ptr(unitaries, "unitaries", torch.complex128),
+                                  _dev_ptr(state_init, "state_init", torch.complex128),
+                                  _dev_ptr(states, "states") if states is not None else None, _dev_ptr(spin, "spin"),
+                                  _dev_ptr(workspace, "workspace"), workspace.numel(), _stream_ptr(stream)),
+          "ss_scan_states_spin")
+    return states, spin
 
 
 def chain_aggregate(unitaries: torch.Tensor, stream=None) -> torch.Tensor:

@@ -25,7 +25,7 @@ FIELD = {"constant": 0, "rabi_linear": 1, "rabi_circular": 2, "neural": 3, "grad
 # Every symbol include/spinsim_b200.h declares (tests/test_abi.py checks the header and the .so against this).
 EXPORTS = [
     "ss_create", "ss_destroy", "ss_num_sweep_params", "ss_dim", "ss_plan", "ss_workspace_bytes", "ss_evaluate",
-    "ss_set_validation", "ss_compute_unitaries", "ss_scan_workspace_bytes", "ss_scan_states",
+    "ss_set_validation", "ss_compute_unitaries", "ss_scan_workspace_bytes", "ss_scan_states", "ss_scan_states_spin",
     "ss_aggregate_workspace_bytes", "ss_chain_aggregate", "ss_compose_carry", "ss_exponentiate",
     "ss_spin_projection", "ss_evaluate_host", "ss_kernel_launches", "ss_last_error", "ss_version",
 ]
@@ -68,6 +68,7 @@ def load() -> ctypes.CDLL:
         "ss_compute_unitaries": (ctypes.c_int, [P, d, d, d, d, i64, i64, i64, P, P, P]),
         "ss_scan_workspace_bytes": (sz, [i32, i64, i64]),
         "ss_scan_states": (ctypes.c_int, [i32, i64, i64, P, P, P, P, sz, P]),
+        "ss_scan_states_spin": (ctypes.c_int, [i32, i64, i64, P, P, P, P, P, sz, P]),
         "ss_aggregate_workspace_bytes": (sz, [i32, i64, i64]),
         "ss_chain_aggregate": (ctypes.c_int, [i32, i64, i64, P, P, P, sz, P]),
         "ss_compose_carry": (ctypes.c_int, [i32, i64, i32, i32, P, P, P, P]),

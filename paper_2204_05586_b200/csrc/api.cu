@@ -300,6 +300,27 @@ int ss_scan_states(int32_t dim, int64_t batch, int64_t k_count, const double* d_
   return e == cudaSuccess ? SS_OK : cuda_fail(e, "scan launch");
 }
 
+int ss_scan_states_spin(int32_t dim, int64_t batch, int64_t k_count, const double* d_U, const double* d_psi0,
+                        double* d_states, double* d_spin, void* d_ws, size_t ws_bytes, void* stream) {
+  if (dim != 2 && dim != 3) return fail(SS_ERR_INVALID, "dim must be 2 or 3");
+  if (batch < 1 || k_count < 1) return fail(SS_ERR_INVALID, "batch and k_count must be >= 1");
+  int rc;
+  if ((rc = check_device_ptr(d_U, "d_unitaries")) || (rc = check_device_ptr(d_psi0, "d_state_init")) ||
+      (rc = check_device_ptr(d_ws, "d_workspace")))
+    return rc;
+  if (!d_states && !d_spin) return fail(SS_ERR_INVALID, "at least one of d_states, d_spin must be non-NULL");
+  if (d_states && (rc = check_device_ptr(d_states, "d_states"))) return rc;
+  if (d_spin && (reinterpret_cast<uintptr_t>(d_spin) & 7) != 0) return fail(SS_ERR_INVALID, "d_spin must be 8-byte aligned");
+  const size_t need = ssb::scan_workspace_bytes(dim, batch, k_count);
+  if (ws_bytes < need) return fail(SS_ERR_INVALID, "workspace_bytes %zu < required %zu", ws_bytes, need);
+  if ((rc = ensure_device())) return rc;
+  int n = 0;
+  const cudaError_t e = ssb::launch_scan(dim, batch, k_count, d_U, d_psi0, d_states, d_ws,
+                                         static_cast<cudaStream_t>(stream), &n, d_spin);
+  g_launches.fetch_add(n);
+  return e == cudaSuccess ? SS_OK : cuda_fail(e, "scan launch");
+}
+
 int ss_chain_aggregate(int32_t dim, int64_t batch, int64_t k_count, const double* d_U, double* d_agg, void* d_ws,
                        size_t ws_bytes, void* stream) {
   if (dim != 2 && dim != 3) return fail(SS_ERR_INVALID, "dim must be 2 or 3");

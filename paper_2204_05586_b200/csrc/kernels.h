@@ -10,7 +10,7 @@ namespace ssb {
 size_t scan_workspace_bytes(int dim, int64_t batch, int64_t k_count);
 size_t aggregate_workspace_bytes(int dim, int64_t batch, int64_t k_count);
 cudaError_t launch_scan(int dim, int64_t batch, int64_t k_count, const double* U, const double* psi0, double* states,
-                        void* ws, cudaStream_t s, int* launches);
+                        void* ws, cudaStream_t s, int* launches, double* spin = nullptr);
 cudaError_t launch_aggregate(int dim, int64_t batch, int64_t k_count, const double* U, double* aggregate, void* ws,
                              cudaStream_t s, int* launches);
 cudaError_t launch_compose_carry(int dim, int64_t batch, int part, const double* aggs, const double* psi0,

@@ -100,6 +100,21 @@ template <int D> __device__ __forceinline__ CM<D> cm_shfl_up(const CM<D>& m, int
   return r;
 }
 
+// ⟨J⟩ = (Re ψ†Jxψ, Re ψ†Jyψ, ψ†Jzψ) (P:241-243), closed forms of the textbook matrices (reading R5).
+template <int D> __device__ __forceinline__ void spin_of(const double pr[D], const double pi[D], double j[3]) {
+  if (D == 2) {
+    // Jx = σx/2: Re(ψ0*ψ1); Jy = σy/2: Im(ψ0*ψ1); Jz = (|ψ0|² − |ψ1|²)/2
+    j[0] = pr[0] * pr[1] + pi[0] * pi[1];
+    j[1] = pr[0] * pi[1] - pi[0] * pr[1];
+    j[2] = 0.5 * ((pr[0] * pr[0] + pi[0] * pi[0]) - (pr[1] * pr[1] + pi[1] * pi[1]));
+  } else {
+    // Jx = (1/√2)·tridiag(1): √2 Re(ψ0*ψ1 + ψ1*ψ2); Jy: √2 Im(ψ0*ψ1 + ψ1*ψ2); Jz = |ψ0|² − |ψ2|²
+    j[0] = kSqrt2 * (pr[0] * pr[1] + pi[0] * pi[1] + pr[1] * pr[D - 1] + pi[1] * pi[D - 1]);
+    j[1] = kSqrt2 * (pr[0] * pi[1] - pi[0] * pr[1] + pr[1] * pi[D - 1] - pi[1] * pr[D - 1]);
+    j[2] = (pr[0] * pr[0] + pi[0] * pi[0]) - (pr[D - 1] * pr[D - 1] + pi[D - 1] * pi[D - 1]);
+  }
+}
+
 // Workspace layout (all offsets 256-byte aligned): [ticket u64][flags int32 × ntiles][agg dim² c128 × ntiles]
 // [psi_end dim c128 × ntiles].
 static inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -278,8 +293,10 @@ template <int D> constexpr int scan2_tile() { return Scan2Cfg<D>::NT * Scan2Cfg<
 // words so the warp's LDS.128/STS.128 at equal offsets of 32 slots are bank-conflict free.
 template <int D> __host__ __device__ constexpr int scan2_u_stride() { return (Scan2Cfg<D>::C * D * D) | 1; }
 template <int D> __host__ __device__ constexpr int scan2_s_stride() { return (Scan2Cfg<D>::C * D) | 1; }
+template <int D> __host__ __device__ constexpr int scan2_j_stride() { return (Scan2Cfg<D>::C * 3) | 1; }  // doubles
 template <int D> constexpr size_t scan2_smem() {
-  return sizeof(double2) * (size_t)Scan2Cfg<D>::NT * (2 * scan2_u_stride<D>() + scan2_s_stride<D>()) + 64;
+  return sizeof(double2) * (size_t)Scan2Cfg<D>::NT * (2 * scan2_u_stride<D>() + scan2_s_stride<D>()) +
+         sizeof(double) * (size_t)Scan2Cfg<D>::NT * scan2_j_stride<D>() + 64;
 }
 
 template <int D> struct Scan2Layout {
@@ -321,7 +338,8 @@ struct Scan2Args {
   int64_t batch, k_count, tiles_per_sweep, ntiles;
   const double2* U;
   const double2* psi0;
-  double2* states;
+  double2* states;   // or NULL
+  double* spin;      // [batch][K+1][3] or NULL
   unsigned long long* ticket;
   int* flags;
   double2* agg;
@@ -345,6 +363,8 @@ __global__ void __launch_bounds__(Scan2Cfg<D>::NT, 1) scan2_kernel(const Scan2Ar
   extern __shared__ __align__(128) double2 smem2[];
   double2* sU[2] = {smem2, smem2 + NT * SU};                // [stage][thread][SU]
   double2* sPsi = smem2 + 2 * NT * SU;                      // [thread][SS]
+  constexpr int SJ = scan2_j_stride<D>();
+  double* sJ = reinterpret_cast<double*>(sPsi + NT * SS);   // [thread][SJ]
   __shared__ __align__(8) uint64_t sBar[2];
   __shared__ double2 sWarpTot[NW][D * D];
   __shared__ double2 sWarpPre[NW][D * D];
@@ -499,8 +519,15 @@ __global__ void __launch_bounds__(Scan2Cfg<D>::NT, 1) scan2_kernel(const Scan2Ar
         for (int d = 0; d < D; ++d) a.psi_end[t * D + d] = make_double2(er[d], ei[d]);
         my_flag.store(FLAG_PREFIX, cuda::memory_order_release);
         for (int d = 0; d < D; ++d) sPsiIn[d] = make_double2(pr[d], pi[d]);
-        if (j == 0)
-          for (int d = 0; d < D; ++d) a.states[(size_t)b * (a.k_count + 1) * D + d] = make_double2(pr[d], pi[d]);
+        if (j == 0) {
+          if (a.states)
+            for (int d = 0; d < D; ++d) a.states[(size_t)b * (a.k_count + 1) * D + d] = make_double2(pr[d], pi[d]);
+          if (a.spin) {
+            double jj3[3];
+            spin_of<D>(pr, pi, jj3);
+            for (int q = 0; q < 3; ++q) a.spin[(size_t)b * (a.k_count + 1) * 3 + q] = jj3[q];
+          }
+        }
       }
     }
     __syncthreads();
@@ -522,11 +549,21 @@ __global__ void __launch_bounds__(Scan2Cfg<D>::NT, 1) scan2_kernel(const Scan2Ar
         cm_apply(u, yr, yi, xr, xi);
 #pragma unroll
         for (int d = 0; d < D; ++d) { yr[d] = xr[d]; yi[d] = xi[d]; sPsi[tid * SS + c * D + d] = make_double2(xr[d], xi[d]); }
+        if (a.spin) {
+          double jj3[3];
+          spin_of<D>(xr, xi, jj3);
+          for (int q = 0; q < 3; ++q) sJ[tid * SJ + c * 3 + q] = jj3[q];
+        }
       }
     }
     __syncthreads();
     double2* gS = a.states + ((size_t)b * (a.k_count + 1) + k0 + 1) * D;
-    for (int e = tid; e < n_items * D; e += NT) __stcs(gS + e, sPsi[(e / (C * D)) * SS + e % (C * D)]);
+    if (a.states)
+      for (int e = tid; e < n_items * D; e += NT) __stcs(gS + e, sPsi[(e / (C * D)) * SS + e % (C * D)]);
+    if (a.spin) {
+      double* gJ = a.spin + ((size_t)b * (a.k_count + 1) + k0 + 1) * 3;
+      for (int e = tid; e < n_items * 3; e += NT) __stcs(gJ + e, sJ[(e / (C * 3)) * SJ + e % (C * 3)]);
+    }
     t = nx;
     stage ^= 1;
   }
@@ -550,7 +587,8 @@ struct ChainArgs {
   int64_t batch, k_count;
   const double2* U;
   const double2* psi0;
-  double2* states;
+  double2* states;   // [batch][K+1][D] or NULL
+  double* spin;      // [batch][K+1][3] or NULL (⟨J⟩ fused into the write-out)
 };
 
 template <int D>
@@ -583,12 +621,18 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(const ChainArgs a)
   };
   issue(0, 0);
   double pr[D], pi[D];
-  double2* gS = a.states + (size_t)(valid ? b : 0) * (a.k_count + 1) * D;
+  double2* gS = a.states ? a.states + (size_t)(valid ? b : 0) * (a.k_count + 1) * D : nullptr;
+  double* gJ = a.spin ? a.spin + (size_t)(valid ? b : 0) * (a.k_count + 1) * 3 : nullptr;
 #pragma unroll
   for (int d = 0; d < D; ++d) {
     const double2 v = valid ? a.psi0[b * D + d] : make_double2(0.0, 0.0);
     pr[d] = v.x; pi[d] = v.y;
-    if (valid) __stcs(gS + d, v);
+    if (valid && gS) __stcs(gS + d, v);
+  }
+  if (valid && gJ) {
+    double j[3];
+    spin_of<D>(pr, pi, j);
+    for (int q = 0; q < 3; ++q) __stcs(gJ + q, j[q]);
   }
   unsigned phase[2] = {0u, 0u};
   for (int64_t c = 0; c < nchunks; ++c) {
@@ -603,7 +647,7 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(const ChainArgs a)
     if (valid) {
       const int n = (int)min((int64_t)CH, a.k_count - c * CH);
       const double2* u = slot[st];
-      double2* o = gS + (size_t)(c * CH + 1) * D;
+      const size_t kout = (size_t)(c * CH + 1);
       for (int i = 0; i < n; ++i) {
         double yr[D], yi[D];
 #pragma unroll
@@ -620,7 +664,15 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(const ChainArgs a)
           yr[r] = sr; yi[r] = si;
         }
 #pragma unroll
-        for (int d = 0; d < D; ++d) { pr[d] = yr[d]; pi[d] = yi[d]; __stcs(o + i * D + d, make_double2(yr[d], yi[d])); }
+        for (int d = 0; d < D; ++d) { pr[d] = yr[d]; pi[d] = yi[d]; }
+        if (gS)
+#pragma unroll
+          for (int d = 0; d < D; ++d) __stcs(gS + (kout + i) * D + d, make_double2(yr[d], yi[d]));
+        if (gJ) {
+          double j[3];
+          spin_of<D>(pr, pi, j);
+          for (int q = 0; q < 3; ++q) __stcs(gJ + (kout + i) * 3 + q, j[q]);
+        }
       }
     }
   }
@@ -628,7 +680,7 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(const ChainArgs a)
 
 template <int D>
 static cudaError_t run_chain(int64_t batch, int64_t k_count, const double* U, const double* psi0, double* states,
-                             cudaStream_t s, int* launches) {
+                             double* spin, cudaStream_t s, int* launches) {
   constexpr size_t smem = chain_smem<D>();
   static bool attr = false;
   if (!attr) {
@@ -637,7 +689,7 @@ static cudaError_t run_chain(int64_t batch, int64_t k_count, const double* U, co
     attr = true;
   }
   ChainArgs a{batch, k_count, reinterpret_cast<const double2*>(U), reinterpret_cast<const double2*>(psi0),
-              reinterpret_cast<double2*>(states)};
+              reinterpret_cast<double2*>(states), spin};
   chain_kernel<D><<<(unsigned)((batch + kChainThreads - 1) / kChainThreads), kChainThreads, smem, s>>>(a);
   ++*launches;
   return cudaGetLastError();
@@ -674,32 +726,17 @@ __global__ void compose_carry_kernel(int64_t batch, int part, const double2* agg
   for (int d = 0; d < D; ++d) carry[b * D + d] = make_double2(xr[d], xi[d]);
 }
 
-// ⟨J⟩ = (Re ψ†Jxψ, Re ψ†Jyψ, ψ†Jzψ) (P:241-243), closed forms of the textbook matrices (reading R5).
 template <int D>
 __global__ void spin_projection_kernel(int64_t n, const double2* states, double* out) {
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
-  double2 p[D];
+  double pr[D], pi[D], j[3];
 #pragma unroll
-  for (int d = 0; d < D; ++d) p[d] = states[s * D + d];
-  double jx, jy, jz;
-  if (D == 2) {
-    // Jx = σx/2: Re(ψ0*ψ1); Jy = σy/2: Im(ψ0*ψ1); Jz = (|ψ0|² − |ψ1|²)/2
-    const double cr = p[0].x * p[1].x + p[0].y * p[1].y, ci = p[0].x * p[1].y - p[0].y * p[1].x;
-    jx = cr;
-    jy = ci;
-    jz = 0.5 * ((p[0].x * p[0].x + p[0].y * p[0].y) - (p[1].x * p[1].x + p[1].y * p[1].y));
-  } else {
-    // Jx = (1/√2)·tridiag(1): √2 Re(ψ0*ψ1 + ψ1*ψ2); Jy: √2 Im(ψ0*ψ1 + ψ1*ψ2); Jz = |ψ0|² − |ψ2|²
-    const double ar = p[0].x * p[1].x + p[0].y * p[1].y + p[1].x * p[2].x + p[1].y * p[2].y;
-    const double ai = p[0].x * p[1].y - p[0].y * p[1].x + p[1].x * p[2].y - p[1].y * p[2].x;
-    jx = kSqrt2 * ar;
-    jy = kSqrt2 * ai;
-    jz = (p[0].x * p[0].x + p[0].y * p[0].y) - (p[2].x * p[2].x + p[2].y * p[2].y);
-  }
-  out[3 * s + 0] = jx;
-  out[3 * s + 1] = jy;
-  out[3 * s + 2] = jz;
+  for (int d = 0; d < D; ++d) { const double2 v = states[s * D + d]; pr[d] = v.x; pi[d] = v.y; }
+  spin_of<D>(pr, pi, j);
+  out[3 * s + 0] = j[0];
+  out[3 * s + 1] = j[1];
+  out[3 * s + 2] = j[2];
 }
 
 // Input validation: bit 1 = non-finite sweep/state value, bit 2 = ω_q ≠ 0 in column qcol (analytic spin-one).
@@ -768,7 +805,7 @@ static cudaError_t run_scan(int64_t batch, int64_t k_count, const double* U, con
 
 template <int D>
 static cudaError_t run_scan2(int64_t batch, int64_t k_count, const double* U, const double* psi0, double* states,
-                             void* ws, cudaStream_t s, int* launches) {
+                             double* spin, void* ws, cudaStream_t s, int* launches) {
   Scan2Layout<D> L(batch, k_count);
   char* w = static_cast<char*>(ws);
   Scan2Args a;
@@ -779,6 +816,7 @@ static cudaError_t run_scan2(int64_t batch, int64_t k_count, const double* U, co
   a.U = reinterpret_cast<const double2*>(U);
   a.psi0 = reinterpret_cast<const double2*>(psi0);
   a.states = reinterpret_cast<double2*>(states);
+  a.spin = spin;
   a.ticket = reinterpret_cast<unsigned long long*>(w);
   a.flags = reinterpret_cast<int*>(w + L.off_flags);
   a.agg = reinterpret_cast<double2*>(w + L.off_agg);
@@ -804,12 +842,12 @@ static cudaError_t run_scan2(int64_t batch, int64_t k_count, const double* U, co
 }
 
 cudaError_t launch_scan(int dim, int64_t batch, int64_t k_count, const double* U, const double* psi0, double* states,
-                        void* ws, cudaStream_t s, int* launches) {
+                        void* ws, cudaStream_t s, int* launches, double* spin) {
   if (batch >= kChainMinBatch)   // enough sweeps to saturate HBM with one sequential chain per thread
-    return dim == 2 ? run_chain<2>(batch, k_count, U, psi0, states, s, launches)
-                    : run_chain<3>(batch, k_count, U, psi0, states, s, launches);
-  return dim == 2 ? run_scan2<2>(batch, k_count, U, psi0, states, ws, s, launches)
-                  : run_scan2<3>(batch, k_count, U, psi0, states, ws, s, launches);
+    return dim == 2 ? run_chain<2>(batch, k_count, U, psi0, states, spin, s, launches)
+                    : run_chain<3>(batch, k_count, U, psi0, states, spin, s, launches);
+  return dim == 2 ? run_scan2<2>(batch, k_count, U, psi0, states, spin, ws, s, launches)
+                  : run_scan2<3>(batch, k_count, U, psi0, states, spin, ws, s, launches);
 }
 
 cudaError_t launch_aggregate(int dim, int64_t batch, int64_t k_count, const double* U, double* aggregate, void* ws,

@@ -243,3 +243,20 @@ def test_unitarity_and_norm(ss):
     UhU = np.conj(np.transpose(U[0], (0, 2, 1))) @ U[0]
     assert np.abs(UhU - np.eye(3)).max() < 1e-12
     assert np.abs(np.linalg.norm(st[0], axis=1) - 1).max() < 1e-12
+
+
+@pytest.mark.parametrize("d", [2, 3])
+@pytest.mark.parametrize("B,K", [(3, 1031), (4100, 9)])        # tiled scan and per-sweep chain kernel
+@pytest.mark.parametrize("want_states", [True, False])
+def test_scan_with_fused_spin_projection(ss, orc, d, B, K, want_states):
+    """⟨J⟩ fused into the state write-out (SURVEY §8(f) NEXT #1) equals the oracle's projection of its own chain."""
+    U = _random_unitaries(B, K, d, seed=B + K + d)
+    psi0 = W.random_states(B, d, seed=32)
+    ref_states = orc.chain(U, psi0)
+    ref_spin = orc.spin_projection("half" if d == 2 else "one", ref_states)
+    st, spin = ss.scan_states_spin(torch.from_numpy(U).cuda(), torch.from_numpy(psi0).cuda(), want_states=want_states)
+    assert np.abs(spin.cpu().numpy() - ref_spin).max() < 1e-12
+    if want_states:
+        assert np.abs(st.cpu().numpy() - ref_states).max() < 1e-12
+    else:
+        assert st is None
