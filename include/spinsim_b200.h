@@ -64,7 +64,8 @@ enum ss_field {
   SS_FIELD_RABI_LINEAR = 1,
   SS_FIELD_RABI_CIRCULAR = 2,
   SS_FIELD_NEURAL = 3,
-  SS_FIELD_GRADIENT = 4
+  SS_FIELD_GRADIENT = 4,
+  SS_FIELD_USER = 5         /* set by ss_create_user; not accepted by ss_create */
 };
 
 /* Simulator description (mirrors spinsim.Simulator's constructor arguments). */
@@ -83,6 +84,22 @@ typedef struct ss_sim ss_sim;  /* opaque handle, owned by the library */
 /* Create / destroy a simulator.  Validates the combination; no CUDA call is made. */
 int ss_create(const ss_sim_desc* desc, ss_sim** out);
 void ss_destroy(ss_sim* sim);
+
+/* Create a simulator whose field function is user code compiled at run time (the paper's
+ * user-supplied field functions).  `field_source` is CUDA C++ that defines
+ *     __device__ void user_field(double t_k, double off, const double* p, double f[4])
+ * writing f = (ωx, ωy, ωz, ωq) in rad/s at time t_k + off (t_k = interval start, off = offset inside the interval,
+ * kept apart so phases of fast drives can be formed accurately; f is zeroed before the call) for the sweep parameters
+ * p[0 .. n_params).  NVRTC compiles it with the library's own interval kernel for sm_100a (first call per simulator:
+ * ~1 s); the rest of the description (spin, integration, exponentiation, τ, frame, precision) is honoured as for
+ * built-in fields.  desc->field is ignored.  Compile errors return SS_ERR_INVALID with the NVRTC log in
+ * ss_last_error().  Needs a CUDA device (SS_ERR_CUDA otherwise).  The analytic spin-one exponentiator is rejected
+ * (ω_q ≡ 0 cannot be verified for user code). */
+int ss_create_user(const ss_sim_desc* desc, const char* field_source, int32_t n_params, ss_sim** out);
+
+/* Compile-only check of a user field (no device needed): SS_OK, or SS_ERR_INVALID with the NVRTC log in
+ * ss_last_error(). */
+int ss_compile_user_field(const ss_sim_desc* desc, const char* field_source, int32_t n_params);
 
 /* Number of sweep parameters P of a built-in field (negative if unknown). */
 int ss_num_sweep_params(int32_t field);

@@ -91,19 +91,33 @@ class Simulator:
     for every (spin, exponentiator, integration method, field, precision); construction only picks them."""
 
     def __init__(self, spin="one", integration="cf4", exponentiation=None, trotter_cutoff=24,
-                 use_rotating_frame=True, precision="fp64", field="neural"):
+                 use_rotating_frame=True, precision="fp64", field="neural", field_source=None, n_params=None):
+        """field="user": `field_source` is CUDA C++ defining
+        ``__device__ void user_field(double t_k, double off, const double* p, double f[4])`` (compiled at run time
+        by NVRTC into the library's interval kernel; the paper's user field functions) and `n_params`
+        the number of sweep parameters it reads."""
         if exponentiation is None:
             exponentiation = "analytic" if spin == "half" else "lie_trotter"
         self.spin, self.integration, self.exponentiation = spin, integration, exponentiation
         self.trotter_cutoff, self.use_rotating_frame = int(trotter_cutoff), bool(use_rotating_frame)
         self.precision, self.field = precision, field
         self.dim = 2 if spin == "half" else 3
-        self.n_params = num_sweep_params(field)
-        desc = _lib.ss_sim_desc(SPIN[spin], INTEGRATION[integration], EXPONENTIATION[exponentiation],
-                                int(trotter_cutoff), int(bool(use_rotating_frame)), PRECISION[precision], FIELD[field])
         h = ctypes.c_void_p()
         lib = _lib.load()
-        check(lib.ss_create(ctypes.byref(desc), ctypes.byref(h)), "ss_create")
+        if field == "user":
+            if field_source is None or n_params is None:
+                raise ValueError('field="user" needs field_source and n_params')
+            self.n_params = int(n_params)
+            desc = _lib.ss_sim_desc(SPIN[spin], INTEGRATION[integration], EXPONENTIATION[exponentiation],
+                                    int(trotter_cutoff), int(bool(use_rotating_frame)), PRECISION[precision], 0)
+            check(lib.ss_create_user(ctypes.byref(desc), field_source.encode(), self.n_params, ctypes.byref(h)),
+                  "ss_create_user")
+        else:
+            self.n_params = num_sweep_params(field)
+            desc = _lib.ss_sim_desc(SPIN[spin], INTEGRATION[integration], EXPONENTIATION[exponentiation],
+                                    int(trotter_cutoff), int(bool(use_rotating_frame)), PRECISION[precision],
+                                    FIELD[field])
+            check(lib.ss_create(ctypes.byref(desc), ctypes.byref(h)), "ss_create")
         self._h = h
         self._lib = lib
 

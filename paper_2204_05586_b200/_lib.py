@@ -24,7 +24,7 @@ FIELD = {"constant": 0, "rabi_linear": 1, "rabi_circular": 2, "neural": 3, "grad
 
 # Every symbol include/spinsim_b200.h declares (tests/test_abi.py checks the header and the .so against this).
 EXPORTS = [
-    "ss_create", "ss_destroy", "ss_num_sweep_params", "ss_dim", "ss_plan", "ss_workspace_bytes", "ss_evaluate",
+    "ss_create", "ss_create_user", "ss_compile_user_field", "ss_destroy", "ss_num_sweep_params", "ss_dim", "ss_plan", "ss_workspace_bytes", "ss_evaluate",
     "ss_set_validation", "ss_compute_unitaries", "ss_scan_workspace_bytes", "ss_scan_states", "ss_scan_states_spin",
     "ss_aggregate_workspace_bytes", "ss_chain_aggregate", "ss_compose_carry", "ss_exponentiate",
     "ss_spin_projection", "ss_evaluate_host", "ss_kernel_launches", "ss_last_error", "ss_version",
@@ -58,6 +58,8 @@ def load() -> ctypes.CDLL:
     i32, i64, d, P, sz = ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p, ctypes.c_size_t
     sig = {
         "ss_create": (ctypes.c_int, [ctypes.POINTER(ss_sim_desc), ctypes.POINTER(P)]),
+        "ss_create_user": (ctypes.c_int, [ctypes.POINTER(ss_sim_desc), ctypes.c_char_p, i32, ctypes.POINTER(P)]),
+        "ss_compile_user_field": (ctypes.c_int, [ctypes.POINTER(ss_sim_desc), ctypes.c_char_p, i32]),
         "ss_destroy": (None, [P]),
         "ss_num_sweep_params": (ctypes.c_int, [i32]),
         "ss_dim": (ctypes.c_int, [P]),

@@ -13,6 +13,7 @@
 #include "dispatch.h"
 #include "interval_kernel.cuh"
 #include "kernels.h"
+#include "user_field.h"
 
 namespace {
 
@@ -64,6 +65,8 @@ struct ss_sim {
   int validate = 1;
   ssb::IntervalLaunchFn interval = nullptr;
   ssb::ExpoLaunchFn expo = nullptr;
+  bool user = false;               // run-time compiled user field (ss_create_user)
+  ssb::UserKernel user_kernel;
   // ss_evaluate_host pipeline: streams[0] computes, streams[1] copies; two staging slots; events order them
   cudaStream_t streams[2] = {nullptr, nullptr};
   cudaEvent_t computed[2] = {nullptr, nullptr};   // slot's kernels done → its D2H may start
@@ -158,7 +161,7 @@ int ensure_device() {
 }
 
 int launch_interval_checked(ss_sim* s, const ssb::IntervalParams& p, cudaStream_t st) {
-  const cudaError_t e = s->interval(p, st);
+  const cudaError_t e = s->user ? ssb::launch_user(s->user_kernel, p, st) : s->interval(p, st);
   if (e != cudaSuccess) return cuda_fail(e, "interval kernel launch");
   g_launches.fetch_add(1);
   return SS_OK;
@@ -204,8 +207,47 @@ int ss_create(const ss_sim_desc* desc, ss_sim** out) {
   return SS_OK;
 }
 
+int ss_create_user(const ss_sim_desc* desc, const char* field_source, int32_t n_params, ss_sim** out) {
+  if (!desc || !out || !field_source) return fail(SS_ERR_INVALID, "desc, field_source and out must be non-NULL");
+  if (n_params < 0 || n_params > 64) return fail(SS_ERR_INVALID, "n_params %d outside 0..64", n_params);
+  ss_sim_desc d = *desc;
+  d.field = SS_FIELD_CONSTANT;      // validated like a built-in description; the field itself is the user's
+  int rc = ss_create(&d, out);
+  if (rc) return rc;
+  ss_sim* s = *out;
+  if (s->dim == 3 && d.exponentiation == SS_EXP_ANALYTIC) {
+    ss_destroy(s);
+    *out = nullptr;
+    return fail(SS_ERR_UNSUPPORTED, "the analytic spin-one exponentiator needs omega_q == 0, which cannot be checked "
+                                    "for a user field; use the Lie-Trotter exponentiator");
+  }
+  if ((rc = ensure_device())) { ss_destroy(s); *out = nullptr; return rc; }
+  std::string err;
+  if (ssb::build_user_kernel(d.spin, d.exponentiation, d.integration, d.precision == SS_FP32, field_source, n_params,
+                             &s->user_kernel, &err) != 0) {
+    ss_destroy(s);
+    *out = nullptr;
+    return fail(SS_ERR_INVALID, "%s", err.c_str());
+  }
+  s->user = true;
+  s->P = n_params;
+  s->d.field = SS_FIELD_USER;
+  return SS_OK;
+}
+
+int ss_compile_user_field(const ss_sim_desc* desc, const char* field_source, int32_t n_params) {
+  if (!desc || !field_source) return fail(SS_ERR_INVALID, "desc and field_source must be non-NULL");
+  if (n_params < 0 || n_params > 64) return fail(SS_ERR_INVALID, "n_params %d outside 0..64", n_params);
+  std::string err;
+  if (ssb::build_user_kernel(desc->spin, desc->exponentiation, desc->integration, desc->precision == SS_FP32,
+                             field_source, n_params, nullptr, &err) != 0)
+    return fail(SS_ERR_INVALID, "%s", err.c_str());
+  return SS_OK;
+}
+
 void ss_destroy(ss_sim* s) {
   if (!s) return;
+  if (s->user) ssb::destroy_user_kernel(&s->user_kernel);
   for (auto& sl : s->slots)
     if (sl.buf) cudaFree(sl.buf);
   for (auto& st : s->streams)

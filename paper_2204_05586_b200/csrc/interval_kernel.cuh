@@ -50,8 +50,7 @@ __device__ __forceinline__ void sample_in_frame(const Field<F>& fld, double off,
 }
 
 template <int SPIN, int EXPO, int METHOD, int FIELD, typename T>
-__global__ void __launch_bounds__(kIntervalThreads, kIntervalMinBlocks<SPIN, T>())
-interval_kernel(const IntervalParams prm) {
+__device__ __forceinline__ void interval_body(const IntervalParams& prm) {
   constexpr int D = SpinDim<SPIN>::D;
   constexpr int P = FieldParams<FIELD>::P;
   const int64_t gt = (int64_t)blockIdx.x * kIntervalThreads + threadIdx.x;
@@ -204,6 +203,13 @@ interval_kernel(const IntervalParams prm) {
 }
 
 template <int SPIN, int EXPO, int METHOD, int FIELD, typename T>
+__global__ void __launch_bounds__(kIntervalThreads, kIntervalMinBlocks<SPIN, T>())
+interval_kernel(const IntervalParams prm) {
+  interval_body<SPIN, EXPO, METHOD, FIELD, T>(prm);
+}
+
+#ifndef __CUDACC_RTC__
+template <int SPIN, int EXPO, int METHOD, int FIELD, typename T>
 cudaError_t launch_interval(const IntervalParams& prm, cudaStream_t stream) {
   const int64_t blocks = (prm.n_threads * prm.split + kIntervalThreads - 1) / kIntervalThreads;
   if (blocks <= 0) return cudaSuccess;
@@ -236,5 +242,6 @@ cudaError_t launch_exponentiate(int64_t n, const double* args, int tau, double* 
   exponentiate_kernel<SPIN, EXPO, T><<<(unsigned)((n + 127) / 128), 128, 0, stream>>>(n, args, tau, out);
   return cudaGetLastError();
 }
+#endif  // !__CUDACC_RTC__
 
 }  // namespace ssb

@@ -9,15 +9,23 @@
 // the cancellation of subtracting 1 from near-unity diagonals (reading R9).
 #pragma once
 
+#ifndef __CUDACC_RTC__
 #include <cuda_runtime.h>
 #include <stdint.h>
+#else   // NVRTC compile of a user field (user_field.cu): no system headers
+typedef long long int64_t;
+typedef int int32_t;
+typedef unsigned int uint32_t;
+typedef unsigned long long uint64_t;
+#endif
 
 namespace ssb {
 
 enum { SPIN_HALF = 1, SPIN_ONE = 2 };
 enum { CF4 = 0, MIDPOINT = 1, HEUN = 2 };
 enum { EXP_ANALYTIC = 0, EXP_LIE_TROTTER = 1 };
-enum { FIELD_CONSTANT = 0, FIELD_RABI_LINEAR = 1, FIELD_RABI_CIRCULAR = 2, FIELD_NEURAL = 3, FIELD_GRADIENT = 4 };
+enum { FIELD_CONSTANT = 0, FIELD_RABI_LINEAR = 1, FIELD_RABI_CIRCULAR = 2, FIELD_NEURAL = 3, FIELD_GRADIENT = 4,
+       FIELD_USER = 5 };
 
 // ---- constants: correctly rounded doubles (reading R7) ------------------------------------------------
 constexpr double kG1 = 0x1.b0cb174df99c7p-3;       // ½(1 − 1/√3)  Gauss–Legendre node

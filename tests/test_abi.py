@@ -123,3 +123,15 @@ def test_argument_errors_are_synchronous(lib):
     assert b"workspace" in lib.ss_last_error()
     assert lib.ss_compose_carry(3, 1, 2, 2, fake, fake, fake, None) == SS_ERR_INVALID
     assert lib.ss_workspace_bytes(sim._h, 8192, 10000, 1) > 8192 * 10000 * 144
+
+
+def test_user_field_compiles_without_gpu(lib):
+    """NVRTC compile of a user field together with the library's interval kernel (NEXT #5) needs no GPU."""
+    from paper_2204_05586_b200 import _lib
+    src = b"__device__ void user_field(double t_k, double off, const double* p, double f[4]) { f[2] = p[0]; }"
+    for spin, expo, prec in ((1, 0, 0), (2, 1, 0), (2, 1, 1)):
+        d = _lib.ss_sim_desc(spin, 0, expo, 24, 1, prec, 0)
+        assert lib.ss_compile_user_field(ctypes.byref(d), src, 1) == 0, lib.ss_last_error()
+    d = _lib.ss_sim_desc(1, 0, 0, 24, 1, 0, 0)
+    assert lib.ss_compile_user_field(ctypes.byref(d), b"__device__ void user_field( {", 1) == _lib.SS_ERR_INVALID
+    assert b"compilation failed" in lib.ss_last_error()
