@@ -107,6 +107,32 @@ __device__ __forceinline__ void interval_body(const IntervalParams& prm) {
         a1[j] = (T)(fma(kWPlus, f1[j], kWMinus * f2[j]) * prm.dt);
         a2[j] = (T)(fma(kWMinus, f1[j], kWPlus * f2[j]) * prm.dt);
       }
+      if constexpr (SPIN == SPIN_ONE && EXPO == EXP_LIE_TROTTER && sizeof(T) == 4) {
+        // FP32 mode: both exponentials' symmetric squarings in lockstep, packed one per float2 lane (FFMA2)
+        Sym3<float> m1, m2;
+        float c1, s1, c2, s2;
+        trotter_init<float>(a1, prm.tau, m1, c1, s1);
+        trotter_init<float>(a2, prm.tau, m2, c2, s2);
+        Sym3<float2> m;
+        m.r00 = make_float2(m1.r00, m2.r00); m.i00 = make_float2(m1.i00, m2.i00);
+        m.r01 = make_float2(m1.r01, m2.r01); m.i01 = make_float2(m1.i01, m2.i01);
+        m.r02 = make_float2(m1.r02, m2.r02); m.i02 = make_float2(m1.i02, m2.i02);
+        m.r11 = make_float2(m1.r11, m2.r11); m.i11 = make_float2(m1.i11, m2.i11);
+        m.r12 = make_float2(m1.r12, m2.r12); m.i12 = make_float2(m1.i12, m2.i12);
+        m.r22 = make_float2(m1.r22, m2.r22); m.i22 = make_float2(m1.i22, m2.i22);
+#pragma unroll 2
+        for (int it = 0; it < prm.tau; ++it) sym_square<float2>(m);
+        m1.r00 = m.r00.x; m1.i00 = m.i00.x; m1.r01 = m.r01.x; m1.i01 = m.i01.x; m1.r02 = m.r02.x; m1.i02 = m.i02.x;
+        m1.r11 = m.r11.x; m1.i11 = m.i11.x; m1.r12 = m.r12.x; m1.i12 = m.i12.x; m1.r22 = m.r22.x; m1.i22 = m.i22.x;
+        m2.r00 = m.r00.y; m2.i00 = m.i00.y; m2.r01 = m.r01.y; m2.i01 = m.i01.y; m2.r02 = m.r02.y; m2.i02 = m.i02.y;
+        m2.r11 = m.r11.y; m2.i11 = m.i11.y; m2.r12 = m.r12.y; m2.i12 = m.i12.y; m2.r22 = m.r22.y; m2.i22 = m.i22.y;
+        Res<D, T> e;
+        trotter_expand<T>(m1, c1, s1, e);
+        res_mul<D, T>(e, A, u);
+        trotter_expand<T>(m2, c2, s2, e);
+        res_mul<D, T>(e, u, A);
+        continue;
+      }
 #if SS_DUAL_EXP
       if constexpr (SPIN == SPIN_ONE && EXPO == EXP_LIE_TROTTER) {
         // both CF4 exponentials' squaring chains interleaved in one loop (2 independent dependency chains)

@@ -51,6 +51,14 @@ template <> struct FieldParams<FIELD_GRADIENT> { static constexpr int P = 2; };
 // ---- precision-generic scalar helpers ---------------------------------------------------------------------------
 __device__ __forceinline__ double fmaT(double a, double b, double c) { return fma(a, b, c); }
 __device__ __forceinline__ float fmaT(float a, float b, float c) { return fmaf(a, b, c); }
+// float2 = two independent FP32 lanes (the FP32 mode runs both CF4 exponentials of a step in lockstep, one per lane):
+// Blackwell's packed FFMA2 / FMUL2 / FADD2, with negations folded into the operands by ptxas.
+__device__ __forceinline__ float2 fmaT(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 operator*(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 operator+(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 operator-(float2 a) { return make_float2(-a.x, -a.y); }
+template <typename T> __device__ __forceinline__ T splat(double v) { return T(v); }
+template <> __device__ __forceinline__ float2 splat<float2>(double v) { return make_float2((float)v, (float)v); }
 __device__ __forceinline__ void sincosT(double x, double* s, double* c) { sincos(x, s, c); }
 __device__ __forceinline__ void sincosT(float x, float* s, float* c) { sincosf(x, s, c); }
 __device__ __forceinline__ double sqrtT(double x) { return sqrt(x); }
@@ -354,7 +362,8 @@ template <typename T> __device__ __forceinline__ void sym_square(Sym3<T>& a) {
   const T q01r = fmaT(a.r01, a.r01, -a.i01 * a.i01), q01i = fmaT(a.r01, a.i01, a.r01 * a.i01);
   const T q02r = fmaT(a.r02, a.r02, -a.i02 * a.i02), q02i = fmaT(a.r02, a.i02, a.r02 * a.i02);
   const T q12r = fmaT(a.r12, a.r12, -a.i12 * a.i12), q12i = fmaT(a.r12, a.i12, a.r12 * a.i12);
-  const T d0 = a.r00 + T(2), d1 = a.r11 + T(2), d2 = a.r22 + T(2);
+  const T two = splat<T>(2.0);
+  const T d0 = a.r00 + two, d1 = a.r11 + two, d2 = a.r22 + two;
   Sym3<T> s;
   // diagonal
   s.r00 = fmaT(d0, a.r00, fmaT(-a.i00, a.i00, q01r + q02r));
