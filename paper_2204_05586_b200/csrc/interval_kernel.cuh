@@ -34,9 +34,6 @@ struct IntervalParams {
 
 constexpr int kIntervalThreads = 128;
 // Resident blocks per SM requested from ptxas: 16 warps/SM (128 registers) without spills for every instance.
-#ifndef SS_DUAL_EXP
-#define SS_DUAL_EXP 0
-#endif
 #ifndef SS_INTERVAL_MINBLOCKS
 #define SS_INTERVAL_MINBLOCKS 4
 #endif
@@ -133,26 +130,6 @@ __device__ __forceinline__ void interval_body(const IntervalParams& prm) {
         res_mul<D, T>(e, u, A);
         continue;
       }
-#if SS_DUAL_EXP
-      if constexpr (SPIN == SPIN_ONE && EXPO == EXP_LIE_TROTTER) {
-        // both CF4 exponentials' squaring chains interleaved in one loop (2 independent dependency chains)
-        Sym3<T> m1, m2;
-        T c1, s1, c2, s2;
-        trotter_init<T>(a1, prm.tau, m1, c1, s1);
-        trotter_init<T>(a2, prm.tau, m2, c2, s2);
-#pragma unroll 1
-        for (int it = 0; it < prm.tau; ++it) {
-          sym_square<T>(m1);
-          sym_square<T>(m2);
-        }
-        Res<D, T> e;
-        trotter_expand<T>(m1, c1, s1, e);
-        res_mul<D, T>(e, A, u);
-        trotter_expand<T>(m2, c2, s2, e);
-        res_mul<D, T>(e, u, A);
-        continue;
-      }
-#endif
       // a5/a6/a7: u·U_r = e2·(e1·U_r) (Eq. cf4_implementation), folded one exponential at a time so only
       // one exponential is live in registers (occupancy).  Residual form: A ← e + A + e·A.
       {

@@ -260,3 +260,30 @@ def test_scan_with_fused_spin_projection(ss, orc, d, B, K, want_states):
         assert np.abs(st.cpu().numpy() - ref_states).max() < 1e-12
     else:
         assert st is None
+
+
+def test_cuda_graph_capture_replay(ss):
+    """ss_evaluate (validation off) is stream-ordered and capturable: a CUDA graph replay reproduces the direct call
+    bit for bit (the way a sweep loop would amortise launch overhead)."""
+    w = W.c2_neural(duration=2e-3)
+    sim = ss.Simulator(w.spin, w.method, w.expo, w.tau, w.frame, "fp64", w.field)
+    sweep = torch.from_numpy(w.sweep).cuda()
+    psi0 = torch.from_numpy(w.psi0).cuda()
+    ref = sim.evaluate(sweep, w.t0, w.t1, w.dt_int, w.dt_out, psi0)       # also warms up first-call attributes
+    sim.set_validation(False)
+    K = w.K
+    states = torch.empty((1, K + 1, 3), dtype=torch.complex128, device="cuda")
+    U = torch.empty((1, K, 3, 3), dtype=torch.complex128, device="cuda")
+    ws = torch.empty(sim.workspace_bytes(1, K, False), dtype=torch.uint8, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        sim.evaluate(sweep, w.t0, w.t1, w.dt_int, w.dt_out, psi0, workspace=ws, out_states=states, out_unitaries=U)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        sim.evaluate(sweep, w.t0, w.t1, w.dt_int, w.dt_out, psi0, workspace=ws, out_states=states, out_unitaries=U)
+    states.zero_()
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(states, ref.state) and torch.equal(U, ref.time_evolution)
