@@ -149,6 +149,51 @@ class ClockSampler:
                 "samples": len(sm), "power_w_median": float(np.median(power))}
 
 
+BAD_REASONS = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+
+
+def clocks_ok(c: dict) -> bool:
+    """Timing rule: no hardware/thermal slowdown, and SM clock not stuck well below max without a reason."""
+    if set(c.get("reasons", [])) & BAD_REASONS:
+        return False
+    if c.get("sm_mhz") and c.get("sm_max_mhz") and c["sm_mhz"] < 0.8 * c["sm_max_mhz"] and not c.get("reasons"):
+        return False
+    return True
+
+
+def timed_loop(step, steps, stream, local, barrier):
+    """K timed steps bracketed by barrier + synchronize, CUDA events on the launching stream, nvidia-smi clocks
+    sampled during the region; re-measured once if the clock record breaks the timing rules."""
+    import torch
+    import paper_2204_05586_b200 as ss
+    for attempt in range(2):
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        launches0 = ss.kernel_launches()
+        with ClockSampler(local) as clk:
+            start.record(stream)
+            for i in range(steps):
+                step(evs[i])
+            end.record(stream)
+            torch.cuda.synchronize()
+        launches = ss.kernel_launches() - launches0
+        barrier()
+        clocks = clk.summary()
+        if attempt:
+            clocks["remeasured"] = True
+        bad = 0.0 if clocks_ok(clocks) else 1.0
+        if torch.distributed.is_available() and torch.distributed.is_initialized():
+            flag = torch.tensor([bad], device="cuda")          # collective decision: every rank re-measures or none
+            torch.distributed.all_reduce(flag, op=torch.distributed.ReduceOp.MAX)
+            bad = flag.item()
+        if not bad:
+            break
+    return start.elapsed_time(end), evs, launches, clocks
+
+
 def dist_setup(n_gpus: int):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -269,18 +314,7 @@ def run_ours(args, rank, world, local):
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    launches0 = ss.kernel_launches()
-    with ClockSampler(local) as clk:
-        start.record(stream)
-        for i in range(args.steps):
-            step(evs[i])
-        end.record(stream)
-        torch.cuda.synchronize()
-    launches = ss.kernel_launches() - launches0
-    barrier()
-    elapsed_ms = start.elapsed_time(end)
+    elapsed_ms, evs, launches, clocks = timed_loop(step, args.steps, stream, local, barrier)
     t_interval = float(np.mean([e[0].elapsed_time(e[1]) for e in evs]))
     t_scan = float(np.mean([e[1].elapsed_time(e[2]) for e in evs]))
     if world > 1:
@@ -295,7 +329,6 @@ def run_ours(args, rank, world, local):
     flops_launch = algorithmic_flops_per_fine_step(w.spin, w.expo, w.tau, w.method) * steps_per_rank
     achieved = flops_launch / (t_interval * 1e-3) / 1e12
     scan_gbs = B * K * scan_bytes_per_interval(D) / (t_scan * 1e-3) / 1e9
-    clocks = clk.summary()
     peak = FP64_PEAK_TFLOPS if args.precision == "fp64" else FP32_PEAK_TFLOPS
     kernel_name = f"interval_kernel<spin-{w.spin},{w.expo},{w.method},{w.field},{args.precision}>"
 
@@ -407,18 +440,7 @@ def run_time_partition(args, rank, world, local, dev):
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    launches0 = ss.kernel_launches()
-    with ClockSampler(local) as clk:
-        start.record(stream)
-        for i in range(args.steps):
-            step(evs[i])
-        end.record(stream)
-        torch.cuda.synchronize()
-    launches = ss.kernel_launches() - launches0
-    barrier()
-    elapsed_ms = start.elapsed_time(end)
+    elapsed_ms, evs, launches, clocks = timed_loop(step, args.steps, stream, local, barrier)
     t_interval = float(np.mean([e[0].elapsed_time(e[1]) for e in evs]))
     t_rest = float(np.mean([e[1].elapsed_time(e[2]) for e in evs]))
     if world > 1:
@@ -426,7 +448,6 @@ def run_time_partition(args, rank, world, local, dev):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         elapsed_ms, t_interval, t_rest = t.tolist()
     value = w.fine_steps * args.steps / (elapsed_ms * 1e-3)
-    clocks = clk.summary()
     flops_launch = algorithmic_flops_per_fine_step(w.spin, w.expo, w.tau, w.method) * kc * L
     achieved = flops_launch / (t_interval * 1e-3) / 1e12
     if rank == 0:

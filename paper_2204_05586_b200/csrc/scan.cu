@@ -285,9 +285,12 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(const ScanArgs a) {
 // and multiplies their aggregates with a shuffle tree.  Each CTA is persistent: while it computes tile t it has
 // already issued the TMA bulk copy (cp.async.bulk → UBLKCP) of its next tile's operators into the other shared-
 // memory stage, so HBM reads overlap the FP64 work.
+#ifndef SS_SCAN2_NT
+#define SS_SCAN2_NT 128
+#endif
 template <int D> struct Scan2Cfg;
-template <> struct Scan2Cfg<2> { static constexpr int NT = 128, C = 8; };
-template <> struct Scan2Cfg<3> { static constexpr int NT = 128, C = 4; };
+template <> struct Scan2Cfg<2> { static constexpr int NT = SS_SCAN2_NT, C = 1024 / SS_SCAN2_NT; };
+template <> struct Scan2Cfg<3> { static constexpr int NT = SS_SCAN2_NT, C = 512 / SS_SCAN2_NT; };
 template <int D> constexpr int scan2_tile() { return Scan2Cfg<D>::NT * Scan2Cfg<D>::C; }
 // Per-thread shared-memory slots (a thread's C operators / C states), strides padded to an odd number of 16-byte
 // words so the warp's LDS.128/STS.128 at equal offsets of 32 slots are bank-conflict free.
@@ -575,7 +578,10 @@ __global__ void __launch_bounds__(Scan2Cfg<D>::NT, 1) scan2_kernel(const Scan2Ar
 // sweep's recurrence ψ_{k+1} = U_k ψ_k sequentially (36 FP64 ops per interval, no matrix products, no look-back):
 // lane ℓ bulk-copies (cp.async.bulk → UBLKCP) its next CH operators into its own shared-memory slot while it applies
 // the current CH, so every SM keeps ≥ 64 × CH × 16·dim² bytes of HBM reads in flight.
-constexpr int kChainThreads = 64;
+#ifndef SS_CHAIN_THREADS
+#define SS_CHAIN_THREADS 64
+#endif
+constexpr int kChainThreads = SS_CHAIN_THREADS;
 constexpr int64_t kChainMinBatch = 4096;
 template <int D> struct ChainCfg { static constexpr int CH = 8; };
 // Per-lane slot: 2 stages of CH operators, stride padded to an odd number of 16-byte words so the 32 lanes' LDS.128
