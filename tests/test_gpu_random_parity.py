@@ -1,0 +1,75 @@
+"""Randomised parity sweep: 48 seeded random configurations (spin, integration method, exponentiator, τ, frame,
+field, precision, grid, batch, start time, sweep values) of small size, GPU vs the long-double oracle element by
+element.  Complements the structured cases in test_gpu_parity.py."""
+import numpy as np
+import pytest
+import torch
+
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+FIELDS = ["constant", "rabi_linear", "rabi_circular", "neural", "gradient"]
+
+
+def random_config(seed):
+    rng = np.random.default_rng(1000 + seed)
+    spin = str(rng.choice(["half", "one"]))
+    expo = "analytic" if spin == "half" else str(rng.choice(["lie_trotter", "lie_trotter", "analytic"]))
+    field = str(rng.choice(FIELDS))
+    method = str(rng.choice(["cf4", "cf4", "midpoint", "heun"]))
+    frame = bool(rng.integers(0, 2))
+    tau = int(rng.choice([0, 3, 12, 24, 30]))
+    L = int(rng.choice([1, 2, 3, 5, 8, 16]))
+    K = int(rng.integers(1, 300))
+    B = int(rng.integers(1, 4))
+    dt_out = float(rng.choice([0.5e-6, 1e-6, 2e-6]))
+    t0 = float(rng.choice([0.0, 1e-3, 0.37]))
+    two_pi = 2 * np.pi
+    rows = []
+    for _ in range(B):
+        if field == "constant":
+            p = rng.uniform(-1, 1, 4) * two_pi * 2e5
+        elif field in ("rabi_linear", "rabi_circular"):
+            p = np.array([rng.uniform(0.3, 1.0) * two_pi * 7e5, rng.uniform(0.2, 2.0) * two_pi * 1e3])
+        elif field == "neural":
+            wb = rng.uniform(0.5, 1.0) * two_pi * 7e5
+            p = W.neural_params(omega_bias=wb, omega_rf=wb + rng.uniform(-1, 1) * two_pi * 2e3,
+                                omega_dress=rng.uniform(0.5, 5) * two_pi * 1e3, omega_pulse=two_pi * 70 * rng.uniform(1, 50),
+                                omega_sig=two_pi * rng.uniform(1e3, 2e4), t_p=t0 + rng.uniform(0, K * dt_out),
+                                omega_q=two_pi * 72 * rng.uniform(0, 5))
+        else:
+            p = rng.uniform(-1, 1, 2) * two_pi * 3e5
+        rows.append(p)
+    sweep = np.stack(rows)
+    if expo == "analytic" and spin == "one":          # ω_q must vanish (reading R14)
+        if field == "constant":
+            sweep[:, 3] = 0.0
+        if field == "neural":
+            sweep[:, 6] = 0.0
+    psi0 = W.random_states(B, 2 if spin == "half" else 3, seed=seed)
+    # FP32 mode's 1e-4 bar is stated for the rotating-frame configuration it is built for: without the
+    # frame each fine step rotates by |ω_z δt| ~ rad and FP32 rounding accumulates as ε₃₂·Σ|a|.
+    prec = "fp32" if (rng.random() < 0.15 and frame) else "fp64"
+    return W.Workload(f"rand{seed}", spin, method, expo, tau, frame, field, t0, t0 + K * dt_out,
+                      dt_out / L, dt_out, sweep, psi0), prec
+
+
+@pytest.fixture(scope="module")
+def ss():
+    import paper_2204_05586_b200 as ss
+    ss.load()
+    return ss
+
+
+@pytest.mark.parametrize("seed", range(48))
+def test_random_config_parity(ss, orc, seed):
+    w, prec = random_config(seed)
+    sim = ss.Simulator(w.spin, w.method, w.expo, w.tau, w.frame, prec, w.field)
+    res = sim.evaluate(torch.from_numpy(w.sweep).cuda(), w.t0, w.t1, w.dt_int, w.dt_out, torch.from_numpy(w.psi0).cuda())
+    st_o, U_o = orc.evaluate(w.spin, w.method, w.expo, w.tau, w.frame, w.field, sweep=w.sweep, t0=w.t0, t1=w.t1,
+                             dt_int=w.dt_int, dt_out=w.dt_out, psi0=w.psi0)
+    tol = 1e-4 if prec == "fp32" else 1e-10
+    eU = np.abs(res.time_evolution.cpu().numpy() - U_o).max()
+    eS = np.abs(res.state.cpu().numpy() - st_o).max()
+    assert eU <= tol and eS <= tol, (w, prec, eU, eS)
