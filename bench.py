@@ -45,17 +45,16 @@ def algorithmic_flops_per_fine_step(spin: str, expo: str, tau: int, method: str 
     once (an FMA is 2).
 
     spin-one Lie–Trotter: residual squaring on the complex-symmetric leapfrog factor T₀ (6 unique entries) = 99 flop
-    × τ per exponential, residual product a + b + ab = 234 (3×3) per exponential; field, frame, T − I construction
-    and phases are not counted (a lower bound: ncu counts 5 706 executed FP64 flop per step at τ = 24 vs 5 220 here,
-    profiles/r01/r01_flops_c3.csv).
-    spin-half: per CF4 step 2 × (SU(2) series 26 + residual product 2×2 72) + CF4 weights 32 + two field samples 16 +
-    frame rotation 26 + phase steppers 12 + grid 2 = 284 (ncu: 283 executed, profiles/r01/r01_flops_c4.csv)."""
+    × τ per exponential, residual product b + a(I + b) = 219 (3×3) per exponential; field, frame, T − I construction
+    and phases are not counted (a lower bound; ncu's executed count is in profiles/r01/).
+    spin-half: per CF4 step 2 × (SU(2) series 26 + residual product 2×2 66) + CF4 weights 32 + two field samples 16 +
+    frame rotation 26 + phase steppers 12 + grid 2 = 272."""
     n_exp = 2 if method == "cf4" else 1
     if spin == "one":
-        prod = 234
+        prod = 219
         per_exp = 99 * tau if expo == "lie_trotter" else 0
         return n_exp * (per_exp + prod)
-    return 284 if method == "cf4" else 142
+    return 272 if method == "cf4" else 136
 
 
 def dense_equivalent_flops_per_fine_step(spin: str, expo: str, tau: int, method: str = "cf4") -> int:

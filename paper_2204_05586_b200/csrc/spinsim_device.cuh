@@ -257,21 +257,26 @@ template <int D, typename T> __device__ __forceinline__ void res_zero(Res<D, T>&
   for (int e = 0; e < D * D; ++e) { a.re[e] = T(0); a.im[e] = T(0); }
 }
 
-// c = a + b + a·b, i.e. (I+a)(I+b) − I.
+// c = a + b + a·b, i.e. (I+a)(I+b) − I, evaluated as b + a·(I + b): the accumulation starts from b_ij and the
+// identity only touches the D diagonal real parts of I + b (D adds + 4D³ FMAs instead of 2D² adds + 4D³ FMAs).
 template <int D, typename T>
 __device__ __forceinline__ void res_mul(const Res<D, T>& a, const Res<D, T>& b, Res<D, T>& c) {
+  T bd[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) bd[k] = b.re[k * D + k] + T(1);
 #pragma unroll
   for (int i = 0; i < D; ++i)
 #pragma unroll
     for (int j = 0; j < D; ++j) {
-      T r = a.re[i * D + j] + b.re[i * D + j];
-      T m = a.im[i * D + j] + b.im[i * D + j];
+      T r = b.re[i * D + j];
+      T m = b.im[i * D + j];
 #pragma unroll
       for (int k = 0; k < D; ++k) {
-        r = fmaT(a.re[i * D + k], b.re[k * D + j], r);
+        const T br = (k == j) ? bd[k] : b.re[k * D + j];
+        r = fmaT(a.re[i * D + k], br, r);
         r = fmaT(-a.im[i * D + k], b.im[k * D + j], r);
         m = fmaT(a.re[i * D + k], b.im[k * D + j], m);
-        m = fmaT(a.im[i * D + k], b.re[k * D + j], m);
+        m = fmaT(a.im[i * D + k], br, m);
       }
       c.re[i * D + j] = r;
       c.im[i * D + j] = m;
