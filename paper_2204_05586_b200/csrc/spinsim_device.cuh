@@ -75,6 +75,12 @@ template <typename T> __device__ __forceinline__ void sincos_small(T x, T* s, T*
   *c = fmaT(x2, fmaT(x2, fmaT(x2, fmaT(x2, T(1.0 / 40320.0), T(-1.0 / 720.0)), T(1.0 / 24.0)), T(-0.5)), T(1));
 }
 
+template <typename T> __device__ __forceinline__ void sincos_tiny(T x, T* s, T* c) {
+  const T x2 = x * x;
+  *s = fmaT(x * x2, T(-1.0 / 6.0), x);
+  *c = fmaT(x2, T(-0.5), T(1));
+}
+
 // Reduce ω·t (both FP64) to (−π, π] accurately: exact product as hi + lo (FMA), then Cody–Waite with a 3-part 2π.
 // Never a single-double 2π (SURVEY [V15]).  |result error| ≲ 5e-16 for |ω t| ≲ 1e9.
 __device__ __forceinline__ double reduce_phase(double w, double t) {
@@ -418,7 +424,14 @@ __device__ __forceinline__ void trotter_init(const T a[4], int tau, Sym3<T>& m, 
   const T th1 = z + q * T(kThird), th2 = T(2) * q * T(kThird), th3 = z - q * T(kThird);
   T s, c, s1, c1, s2, c2, s3, c3;
   const T big = fmax(fmax(Phi, fabs(th1)), fmax(fabs(th2), fabs(th3)));
-  if (big <= T(0.03125)) {                           // half-angles ≤ 2^-6: polynomial
+  if (big <= T(1.9073486328125e-06)) {
+    // half-angles ≤ 2^-20 (every physical step at τ = 24: |a| ≲ 16 rad ⇒ |x| ≤ 2^-21): sin x = x − x³/6 and
+    // cos x = 1 − x²/2 are exact to < 1e-25 relative (cos enters only through sin 2x = 2 sin x cos x).
+    sincos_tiny<T>(Phi * T(0.5), &s, &c);
+    sincos_tiny<T>(th1 * T(0.5), &s1, &c1);
+    sincos_tiny<T>(th2 * T(0.5), &s2, &c2);
+    sincos_tiny<T>(th3 * T(0.5), &s3, &c3);
+  } else if (big <= T(0.03125)) {                    // half-angles ≤ 2^-6: polynomial
     sincos_small<T>(Phi * T(0.5), &s, &c);
     sincos_small<T>(th1 * T(0.5), &s1, &c1);
     sincos_small<T>(th2 * T(0.5), &s2, &c2);
