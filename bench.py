@@ -185,9 +185,8 @@ def timed_loop(step, steps, stream, local, barrier):
             clocks["remeasured"] = True
         bad = 0.0 if clocks_ok(clocks) else 1.0
         if torch.distributed.is_available() and torch.distributed.is_initialized():
-            flag = torch.tensor([bad], device="cuda")          # collective decision: every rank re-measures or none
-            torch.distributed.all_reduce(flag, op=torch.distributed.ReduceOp.MAX)
-            bad = flag.item()
+            # collective decision: every rank re-measures or none
+            bad = reduce_max([bad], "cuda", torch.distributed.get_world_size())[0]
         if not bad:
             break
     return start.elapsed_time(end), evs, launches, clocks
@@ -262,15 +261,30 @@ def config_of(w: W.Workload, args, world):
             "parallelism": f"sweep-shard x{world}", "l2": "no flush: per-step working set (U + states) >> 126 MB L2"}
 
 
+def reduce_max(vals, dev, world):
+    """MAX over ranks (NCCL: on the device; gloo: on the host)."""
+    import torch
+    if world == 1:
+        return list(vals)
+    t = torch.tensor(vals, dtype=torch.float64,
+                     device=dev if torch.distributed.get_backend() == "nccl" else "cpu")
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return t.tolist()
+
+
 def run_ours(args, rank, world, local):
     import torch
     import paper_2204_05586_b200 as ss
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    gpu = 0 if args.share_gpu else local
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     if args.workload == "C4":
         return run_time_partition(args, rank, world, local, dev)
     # sweep shard of this rank
@@ -316,10 +330,7 @@ def run_ours(args, rank, world, local):
     elapsed_ms, evs, launches, clocks = timed_loop(step, args.steps, stream, local, barrier)
     t_interval = float(np.mean([e[0].elapsed_time(e[1]) for e in evs]))
     t_scan = float(np.mean([e[1].elapsed_time(e[2]) for e in evs]))
-    if world > 1:
-        t = torch.tensor([elapsed_ms, t_interval, t_scan], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        elapsed_ms, t_interval, t_scan = t.tolist()
+    elapsed_ms, t_interval, t_scan = reduce_max([elapsed_ms, t_interval, t_scan], dev, world)
     steps_per_rank = w.fine_steps
     total_steps = steps_per_rank * world if args.scaling == "weak" else full.fine_steps
     value = total_steps * args.steps / (elapsed_ms * 1e-3)
@@ -344,10 +355,7 @@ def run_ours(args, rank, world, local):
             sim.evaluate_host(h_sweep, w.t0, w.t1, w.dt_int, w.dt_out, h_psi0, out_states=h_states,
                               n_chunks=args.chunks)
         e2e_s = time.perf_counter() - t0
-        if world > 1:
-            t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            e2e_s = t.item()
+        e2e_s = reduce_max([e2e_s], dev, world)[0]
         e2e = {"value": total_steps * args.steps / e2e_s, "unit": UNIT,
                "h2d_bytes_per_step": int(h_sweep.nbytes + h_psi0.nbytes), "d2h_bytes_per_step": int(h_states.nbytes),
                "n_chunks": args.chunks}
@@ -442,10 +450,7 @@ def run_time_partition(args, rank, world, local, dev):
     elapsed_ms, evs, launches, clocks = timed_loop(step, args.steps, stream, local, barrier)
     t_interval = float(np.mean([e[0].elapsed_time(e[1]) for e in evs]))
     t_rest = float(np.mean([e[1].elapsed_time(e[2]) for e in evs]))
-    if world > 1:
-        t = torch.tensor([elapsed_ms, t_interval, t_rest], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        elapsed_ms, t_interval, t_rest = t.tolist()
+    elapsed_ms, t_interval, t_rest = reduce_max([elapsed_ms, t_interval, t_rest], dev, world)
     value = w.fine_steps * args.steps / (elapsed_ms * 1e-3)
     flops_launch = algorithmic_flops_per_fine_step(w.spin, w.expo, w.tau, w.method) * kc * L
     achieved = flops_launch / (t_interval * 1e-3) / 1e12
@@ -488,6 +493,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-probe", action="store_true")
+    ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
+                    help="gloo only to exercise the multi-rank code path where NCCL cannot run (e.g. ranks sharing a GPU)")
+    ap.add_argument("--share-gpu", action="store_true", help="map every rank to cuda:0 (code-path test, not timing)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("note: --warmup < 3 violates the timing rules; using 3", file=sys.stderr)

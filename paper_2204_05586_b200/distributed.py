@@ -41,10 +41,11 @@ def gather_aggregates(local: torch.Tensor, group=None) -> torch.Tensor:
     if dist.get_backend(group) == "nccl":
         out = torch.empty(world * flat.numel(), dtype=flat.dtype, device=flat.device)
         dist.all_gather_into_tensor(out, flat, group=group)
-    else:
-        parts = [torch.empty_like(flat) for _ in range(world)]
-        dist.all_gather(parts, flat, group=group)
-        out = torch.cat(parts)
+    else:                                   # gloo (CPU tests, several ranks sharing one GPU): stage through host
+        host = flat.cpu()
+        parts = [torch.empty_like(host) for _ in range(world)]
+        dist.all_gather(parts, host, group=group)
+        out = torch.cat(parts).to(flat.device)
     return torch.view_as_complex(out.reshape(world, *local.shape, 2))
 
 
