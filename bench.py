@@ -487,7 +487,7 @@ def main():
     ap.add_argument("--batch", type=int, default=8192, help="sweeps per rank (weak) or in total (strong), C3")
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
     ap.add_argument("--precision", choices=["fp64", "fp32"], default="fp64")
-    ap.add_argument("--chunks", type=int, default=16, help="batch chunks of the pipelined host-buffer (e2e) call")
+    ap.add_argument("--chunks", type=int, default=10, help="batch chunks of the pipelined host-buffer (e2e) call")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-step-seconds", type=float, default=8.0)
     ap.add_argument("--no-e2e", action="store_true")

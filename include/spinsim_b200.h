@@ -175,8 +175,8 @@ int ss_exponentiate(const ss_sim* sim, int64_t n, const double* d_args, double* 
 int ss_spin_projection(int32_t spin, int64_t n, const double* d_states, double* d_out, void* stream);
 
 /* End-to-end call on HOST buffers: copies h_sweep/h_state_init to the device, runs the path and copies the states
- * (and unitaries if h_unitaries != NULL) back, pipelined over `n_chunks` batch chunks on two internal streams so
- * device→host copies overlap compute.  Synchronous: returns after the results are in host memory.  Device
+ * (and unitaries if h_unitaries != NULL) back, pipelined over `n_chunks` batch chunks of geometrically shrinking
+ * size (B/2, B/4, …) on an internal compute stream and copy stream so device→host copies overlap compute.  Synchronous: returns after the results are in host memory.  Device
  * buffers are allocated once and cached in `sim`.  Pinned host buffers give full copy bandwidth. */
 int ss_evaluate_host(ss_sim* sim, double time_start, double time_end, double time_step_integration,
                      double time_step_output, int64_t batch, const double* h_sweep, const double* h_state_init,

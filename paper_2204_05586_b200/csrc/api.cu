@@ -486,7 +486,20 @@ int ss_evaluate_host(ss_sim* s, double t0, double t1, double dt_int, double dt_o
     s->device = dev;
   }
   const int D = s->dim;
-  const int64_t cb_max = (batch + n_chunks - 1) / n_chunks;
+  // Geometric chunks (B/2, B/4, …, the last two equal): early chunks are big (full-speed chain scan, long compute
+  // that hides the previous chunk's D2H), the final chunk — whose D2H cannot be hidden — is small.
+  std::vector<int64_t> sizes;
+  {
+    int64_t left = batch;
+    for (int c = 0; c < n_chunks; ++c) {
+      const int64_t cb = (c == n_chunks - 1) ? left : std::max<int64_t>(1, (left + 1) / 2);
+      if (cb <= 0) break;
+      sizes.push_back(cb);
+      left -= cb;
+    }
+    n_chunks = (int32_t)sizes.size();
+  }
+  const int64_t cb_max = sizes[0];
   const size_t sweep_b = align256(sizeof(double) * s->P * cb_max);
   const size_t psi0_b = align256(sizeof(double) * 2 * D * cb_max);
   const size_t states_b = align256(sizeof(double) * 2 * D * (size_t)cb_max * (K + 1));
@@ -509,7 +522,7 @@ int ss_evaluate_host(ss_sim* s, double t0, double t1, double dt_int, double dt_o
   // chunks (each chunk fills the GPU), so the D2H of chunk c overlaps the kernels of chunk c+1.
   cudaStream_t cs = s->streams[0], xs = s->streams[1];
   for (int64_t c = 0, b0 = 0; c < n_chunks; ++c) {
-    const int64_t cb = std::min<int64_t>(cb_max, batch - b0);
+    const int64_t cb = sizes[c];
     if (cb <= 0) break;
     const int k = (int)(c % nslots);
     char* base = static_cast<char*>(s->slots[k].buf);
