@@ -491,9 +491,8 @@ int ss_evaluate_host(ss_sim* s, double t0, double t1, double dt_int, double dt_o
   std::vector<int64_t> sizes;
   {
     int64_t left = batch;
-    for (int c = 0; c < n_chunks; ++c) {
+    for (int c = 0; c < n_chunks && left > 0; ++c) {
       const int64_t cb = (c == n_chunks - 1) ? left : std::max<int64_t>(1, (left + 1) / 2);
-      if (cb <= 0) break;
       sizes.push_back(cb);
       left -= cb;
     }

@@ -218,10 +218,10 @@ def test_determinism_bitwise(ss):
 
 
 def test_host_api_matches_device_api(ss):
-    w = W.c3_batched(batch=10, duration=0.2e-3)
+    w = W.c3_batched(batch=5, duration=0.2e-3)
     st_d, U_d = gpu_run(ss, w)
     sim = ss.Simulator(w.spin, w.method, w.expo, w.tau, w.frame, "fp64", w.field)
-    for chunks in (1, 3):
+    for chunks in (1, 3, 7, 10):                      # geometric chunking incl. more chunks than halvings
         st_h, U_h = sim.evaluate_host(w.sweep, w.t0, w.t1, w.dt_int, w.dt_out, w.psi0, want_unitaries=True,
                                       n_chunks=chunks)
         assert np.array_equal(st_h, st_d) and np.array_equal(U_h, U_d)
