@@ -90,7 +90,7 @@ void ss_destroy(ss_sim* sim);
  *     __device__ void user_field(double t_k, double off, const double* p, double f[4])
  * writing f = (ωx, ωy, ωz, ωq) in rad/s at time t_k + off (t_k = interval start, off = offset inside the interval,
  * kept apart so phases of fast drives can be formed accurately; f is zeroed before the call) for the sweep parameters
- * p[0 .. n_params).  NVRTC compiles it with the library's own interval kernel for sm_100a (first call per simulator:
+ * p[0 .. n_params), 1 ≤ n_params ≤ 64.  NVRTC compiles it with the library's own interval kernel for sm_100a (first call per simulator:
  * ~1 s); the rest of the description (spin, integration, exponentiation, τ, frame, precision) is honoured as for
  * built-in fields.  desc->field is ignored.  Compile errors return SS_ERR_INVALID with the NVRTC log in
  * ss_last_error().  Needs a CUDA device (SS_ERR_CUDA otherwise).  The analytic spin-one exponentiator is rejected

@@ -209,7 +209,7 @@ int ss_create(const ss_sim_desc* desc, ss_sim** out) {
 
 int ss_create_user(const ss_sim_desc* desc, const char* field_source, int32_t n_params, ss_sim** out) {
   if (!desc || !out || !field_source) return fail(SS_ERR_INVALID, "desc, field_source and out must be non-NULL");
-  if (n_params < 0 || n_params > 64) return fail(SS_ERR_INVALID, "n_params %d outside 0..64", n_params);
+  if (n_params < 1 || n_params > 64) return fail(SS_ERR_INVALID, "n_params %d outside 1..64", n_params);
   ss_sim_desc d = *desc;
   d.field = SS_FIELD_CONSTANT;      // validated like a built-in description; the field itself is the user's
   int rc = ss_create(&d, out);
@@ -237,7 +237,7 @@ int ss_create_user(const ss_sim_desc* desc, const char* field_source, int32_t n_
 
 int ss_compile_user_field(const ss_sim_desc* desc, const char* field_source, int32_t n_params) {
   if (!desc || !field_source) return fail(SS_ERR_INVALID, "desc and field_source must be non-NULL");
-  if (n_params < 0 || n_params > 64) return fail(SS_ERR_INVALID, "n_params %d outside 0..64", n_params);
+  if (n_params < 1 || n_params > 64) return fail(SS_ERR_INVALID, "n_params %d outside 1..64", n_params);
   std::string err;
   if (ssb::build_user_kernel(desc->spin, desc->exponentiation, desc->integration, desc->precision == SS_FP32,
                              field_source, n_params, nullptr, &err) != 0)
