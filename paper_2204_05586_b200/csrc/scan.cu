@@ -289,8 +289,14 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(const ScanArgs a) {
 #define SS_SCAN2_NT 128
 #endif
 template <int D> struct Scan2Cfg;
-template <> struct Scan2Cfg<2> { static constexpr int NT = SS_SCAN2_NT, C = 1024 / SS_SCAN2_NT; };
-template <> struct Scan2Cfg<3> { static constexpr int NT = SS_SCAN2_NT, C = 512 / SS_SCAN2_NT; };
+#ifndef SS_SCAN2_TILE3
+#define SS_SCAN2_TILE3 512
+#endif
+#ifndef SS_SCAN2_TILE2
+#define SS_SCAN2_TILE2 1024
+#endif
+template <> struct Scan2Cfg<2> { static constexpr int NT = SS_SCAN2_NT, C = SS_SCAN2_TILE2 / SS_SCAN2_NT; };
+template <> struct Scan2Cfg<3> { static constexpr int NT = SS_SCAN2_NT, C = SS_SCAN2_TILE3 / SS_SCAN2_NT; };
 template <int D> constexpr int scan2_tile() { return Scan2Cfg<D>::NT * Scan2Cfg<D>::C; }
 // Per-thread shared-memory slots (a thread's C operators / C states), strides padded to an odd number of 16-byte
 // words so the warp's LDS.128/STS.128 at equal offsets of 32 slots are bank-conflict free.
@@ -360,7 +366,7 @@ template <int D> __device__ __forceinline__ CM<D> cm_shfl_down(const CM<D>& m, i
 }
 
 template <int D>
-__global__ void __launch_bounds__(Scan2Cfg<D>::NT, 1) scan2_kernel(const Scan2Args a) {
+__global__ void __launch_bounds__(Scan2Cfg<D>::NT) scan2_kernel(const Scan2Args a) {
   constexpr int NT = Scan2Cfg<D>::NT, C = Scan2Cfg<D>::C, TILE = NT * C, NW = NT / 32;
   constexpr int SU = scan2_u_stride<D>(), SS = scan2_s_stride<D>();
   extern __shared__ __align__(128) double2 smem2[];
