@@ -17,6 +17,9 @@
 #include <cuda/atomic>
 
 #include <algorithm>
+#include <cstring>
+
+#include <cuda.h>
 
 #include "kernels.h"
 
@@ -578,6 +581,374 @@ __global__ void __launch_bounds__(Scan2Cfg<D>::NT) scan2_kernel(const Scan2Args 
   }
 }
 
+// ---- state scan v3 (small batches / long sweeps): thread-contiguous tiles, one look-back per tile -------------------
+//
+// Thread i of a tile owns the IPT = nst·C consecutive intervals [i·IPT, (i+1)·IPT) (nst stages of C; the tile is
+// NT·IPT intervals, up to 4096 spin-one / 8192 spin-half).  Viewing one sweep's U as rows of IPT intervals, stage s of
+// a tile is the box {C intervals of column s} × {NT rows}: ONE 4-D tensor-TMA load (padded by one out-of-bounds 16-B
+// element per row so the per-thread slots land at an odd 16-B pitch — conflict-free).  Pass A streams the tile from
+// HBM through an NSTAGE-deep full/empty mbarrier ring and folds each thread's operators into its running product P_i
+// in registers — no block-level work per stage.  One warp Kogge–Stone + warp-total combine turns the P_i into
+// exclusive prefixes X_i and the tile aggregate G; G is published and the decoupled look-back (warp 0, 32
+// predecessors per round, j-major tickets) yields ψ_in.  Pass B re-streams the tile (L2-resident: 148 CTAs × ≤ 0.6 MB)
+// and each thread propagates y = X_i ψ_in through its intervals; the states of a stage are staged in shared memory
+// and leave as ONE tensor-TMA store.  The last tile of a sweep (when K is not a multiple of the tile) falls back to
+// per-thread bulk copies.  The tile size nst adapts so that small problems still fill the GPU.
+#ifndef SS_SCAN3_MAXST
+#define SS_SCAN3_MAXST 16   // stages per pass in the largest tile
+#endif
+template <int D> struct Scan3Cfg {
+  static constexpr int NT = 128, NW = NT / 32, C = (D == 2) ? 4 : 2, NSTAGE = 5, MAXST = SS_SCAN3_MAXST;
+  static constexpr int SU = C * D * D + 1;   // slot pitch in double2: odd → conflict-free per-thread reads
+  static constexpr int SS = C * D + 1;       // state staging pitch in double2
+};
+template <int D> constexpr size_t scan3_smem() {
+  return sizeof(double2) * (size_t)Scan3Cfg<D>::NT * (Scan3Cfg<D>::NSTAGE * Scan3Cfg<D>::SU + 2 * Scan3Cfg<D>::SS);
+}
+template <int D> struct Scan3Layout {
+  int64_t tile, tiles_per_sweep, ntiles;
+  size_t off_flags, off_agg, off_psi, total;
+  Scan3Layout(int64_t batch, int64_t k_count, int nst) {
+    tile = (int64_t)Scan3Cfg<D>::NT * Scan3Cfg<D>::C * nst;
+    tiles_per_sweep = (k_count + tile - 1) / tile;
+    ntiles = batch * tiles_per_sweep;
+    off_flags = 256;
+    off_agg = align256(off_flags + sizeof(int) * (size_t)ntiles);
+    off_psi = align256(off_agg + sizeof(double2) * D * D * (size_t)ntiles);
+    total = align256(off_psi + sizeof(double2) * D * (size_t)ntiles);
+  }
+};
+struct Scan3Args {
+  Scan2Args s;
+  int nst;
+  int tensor_u, tensor_s;   // tensor maps valid (some full tile exists / states requested)
+};
+
+__device__ __forceinline__ void bulk_store(void* dst_gmem, const void* src_smem, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst_gmem), "r"(smem_u32(src_smem)),
+               "r"(bytes)
+               : "memory");
+}
+#ifndef SS_SCAN3_HINTS
+#define SS_SCAN3_HINTS 1   // L2 eviction hints: pass A evict_last (re-read by pass B), pass B + state stores evict_first
+#endif
+__device__ __forceinline__ void tma_load_4d(void* dst_smem, const CUtensorMap* tm, int c0, int c1, int c2, int c3,
+                                            uint64_t* bar, uint64_t policy) {
+#if SS_SCAN3_HINTS
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6], %7;"
+      ::"r"(smem_u32(dst_smem)), "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+#else
+  (void)policy;
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
+      ::"r"(smem_u32(dst_smem)), "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+#endif
+}
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* tm, const void* src_smem, int c0, int c1, int c2, int c3,
+                                             uint64_t policy) {
+#if SS_SCAN3_HINTS
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2, %3, %4}], [%5], %6;"
+               ::"l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(src_smem)), "l"(policy)
+               : "memory");
+#else
+  (void)policy;
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];"
+               ::"l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(src_smem))
+               : "memory");
+#endif
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <int D>
+__global__ void __launch_bounds__(Scan3Cfg<D>::NT, 1)
+    scan3_kernel(const __grid_constant__ Scan3Args A3, const __grid_constant__ CUtensorMap tmU,
+                 const __grid_constant__ CUtensorMap tmS) {
+  constexpr int NT = Scan3Cfg<D>::NT, NW = Scan3Cfg<D>::NW, C = Scan3Cfg<D>::C, NSTAGE = Scan3Cfg<D>::NSTAGE;
+  constexpr int SU = Scan3Cfg<D>::SU, SS = Scan3Cfg<D>::SS;
+  const Scan2Args& a = A3.s;
+  const int nst = A3.nst, IPT = nst * C, LPT = 2 * nst;   // stages per pass, intervals per thread, loads per tile
+  const long long TILE = (long long)NT * IPT;
+  extern __shared__ __align__(128) double2 smem5[];
+  double2* const sStage = smem5 + NSTAGE * NT * SU;         // [2][NT][SS] state staging
+  __shared__ __align__(8) uint64_t sFull[NSTAGE];
+  __shared__ __align__(8) uint64_t sEmpty[NSTAGE];
+  __shared__ double2 sWarpTot[NW][D * D];
+  __shared__ double2 sPsiIn[D];
+  __shared__ double2 sPsiEnd[D];
+  __shared__ double2 sTot[D * D];
+  __shared__ double2 sM[D * D];
+  __shared__ double2 sWarpAgg[NW][D * D];
+  __shared__ unsigned sBal[NW];
+  __shared__ long long sNext;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  auto buf = [&](long long n) { return smem5 + (int)(n % NSTAGE) * NT * SU; };
+
+  // The CTA's load sequence: per tile LPT loads, pass A stages 0..nst−1 then pass B stages 0..nst−1.  Only the current
+  // tile and the next have known tickets, so the issue cursor `ic` (relative to the current tile's first load) stays
+  // below 2·LPT.  Ring slots and mbarrier parities advance incrementally: no 64-bit division on the per-stage path.
+  long long tcur = 0, tnext = 0, n_iss = 0;
+  long long jc = 0, bc = 0, jn = 0, bn = 0;
+  bool fc = false, fn = false;                               // current / next tile is full (tensor path)
+  int ic = 0, cc = 0, ix = 0, cx = 0;
+  unsigned iph = 0, cph = 0;
+  uint64_t pol_keep = 0, pol_stream = 0;
+#if SS_SCAN3_HINTS
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
+#endif
+  auto issue = [&](int r_rel) {
+    const bool sel = r_rel >= LPT;
+    const int r = sel ? r_rel - LPT : r_rel;
+    const bool passB = r >= nst;
+    const int s = passB ? r - nst : r;
+    const long long j = sel ? jn : jc, b = sel ? bn : bc;
+    const int x = ix;
+    if (sel ? fn : fc) {                                     // full tile: one tensor load by thread 0
+      if (tid == 0) {
+        if (n_iss >= NSTAGE) mbar_wait(&sEmpty[x], iph ^ 1u);
+        mbar_expect_tx(&sFull[x], (unsigned)(NT * SU * sizeof(double2)));
+        tma_load_4d(smem5 + x * NT * SU, &tmU, 0, s, (int)(j * NT), (int)b, &sFull[x], passB ? pol_stream : pol_keep);
+      } else {
+        mbar_arrive(&sFull[x]);
+      }
+    } else {                                                 // last tile of a sweep: per-thread bulk copies
+      const long long k0 = j * TILE + (long long)tid * IPT + (long long)s * C;
+      const int nit = (int)max(0LL, min((long long)C, a.k_count - k0));
+      if (nit > 0) {
+        const unsigned bytes = (unsigned)(nit * D * D * sizeof(double2));
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&sFull[x], bytes);
+        tma_load_1d(smem5 + (x * NT + tid) * SU, a.U + ((size_t)b * a.k_count + k0) * D * D, bytes, &sFull[x]);
+      } else {
+        mbar_arrive(&sFull[x]);
+      }
+    }
+    ++n_iss;
+    if (++ix == NSTAGE) { ix = 0; iph ^= 1u; }
+  };
+  auto top_up = [&]() {                                      // keep NSTAGE − 1 loads ahead of the consumer
+    int lim = cc + NSTAGE - 1;
+    const int known = (tnext < a.ntiles ? 2 : 1) * LPT;
+    if (lim > known) lim = known;
+    for (; ic < lim; ++ic) issue(ic);
+  };
+  auto consume = [&]() -> const double2* {
+    mbar_wait(&sFull[cx], cph);
+    return smem5 + (cx * NT + tid) * SU;
+  };
+  auto release = [&]() {                                     // this thread is done reading the current slot
+    mbar_arrive(&sEmpty[cx]);
+    if (++cx == NSTAGE) { cx = 0; cph ^= 1u; }
+    ++cc;
+  };
+
+  if (tid == 0) {
+    for (int i = 0; i < NSTAGE; ++i) {
+      mbar_init(&sFull[i], NT);
+      mbar_init(&sEmpty[i], NT);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (A3.tensor_u) asm volatile("prefetch.tensormap [%0];" ::"l"(&tmU) : "memory");
+    if (A3.tensor_s) asm volatile("prefetch.tensormap [%0];" ::"l"(&tmS) : "memory");
+    sNext = (long long)atomicAdd(a.ticket, 1ull);
+  }
+  __syncthreads();
+  tcur = sNext;
+  tnext = a.ntiles;
+  jc = tcur / a.batch;
+  bc = tcur - jc * a.batch;
+  fc = (jc + 1) * TILE <= a.k_count;
+  long long m = 0;                                           // pass-B stages done (staging buffer parity)
+  while (tcur < a.ntiles) {
+    __syncthreads();                                         // everyone has read sNext
+    if (tid == 0) sNext = (long long)atomicAdd(a.ticket, 1ull);
+    __syncthreads();
+    tnext = sNext;
+    jn = tnext / a.batch;
+    bn = tnext - jn * a.batch;
+    fn = (jn + 1) * TILE <= a.k_count;
+    top_up();
+    const long long j = jc, b = bc;
+    const long long kt = j * TILE + (long long)tid * IPT;     // this thread's first interval
+    const bool full = fc;
+    // ---- pass A: P_i = U_{last} ⋯ U_{first} over this thread's intervals (HBM stream)
+    CM<D> P;
+    cm_eye(P);
+    for (int s = 0; s < nst; ++s) {
+      const double2* U = consume();
+      const long long k0 = kt + (long long)s * C;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        if (k0 + c < a.k_count) {
+          CM<D> u;
+          cm_load(U + c * D * D, u);
+          P = cm_mul(u, P);
+        }
+      }
+      release();
+      top_up();
+    }
+    // ---- block exclusive scan of the P_i: X_i = (P_{i-1} ⋯ P_0); tile aggregate G
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const CM<D> o = cm_shfl_up(P, off);
+      if (lane >= off) P = cm_mul(P, o);
+    }
+    CM<D> X = cm_shfl_up(P, 1);
+    if (lane == 0) cm_eye(X);
+    if (lane == 31) cm_store(sWarpTot[warp], P);
+    __syncthreads();
+    {
+      CM<D> W, T;
+      cm_eye(W);
+      for (int w = 0; w < warp; ++w) { cm_load(sWarpTot[w], T); W = cm_mul(T, W); }
+      X = cm_mul(X, W);
+    }
+    // ---- publish AGG, then a block-wide decoupled look-back: 128 predecessors per round (one round covers a wave)
+    if (tid == 0) {
+      CM<D> tot, T;
+      cm_eye(tot);
+      for (int w = 0; w < NW; ++w) { cm_load(sWarpTot[w], T); tot = cm_mul(T, tot); }
+      cm_store(sTot, tot);
+      if (j > 0) {
+        cm_store(a.agg + (size_t)tcur * D * D, tot);
+        cuda::atomic_ref<int, cuda::thread_scope_device>(a.flags[tcur]).store(FLAG_AGG, cuda::memory_order_release);
+        cm_store(sM, [] { CM<D> e; cm_eye(e); return e; }());
+      } else {
+        for (int d = 0; d < D; ++d) sPsiIn[d] = a.psi0[b * D + d];
+      }
+    }
+    if (j > 0) {
+      for (long long jb = j - 1;; jb -= NT) {
+        const long long jq = jb - tid;
+        const long long tq = jq * a.batch + b;
+        int fv = FLAG_PREFIX;                                  // jq < 0 is never reached: tile 0 publishes PREFIX
+        if (jq >= 0) {
+          cuda::atomic_ref<int, cuda::thread_scope_device> f(a.flags[tq]);
+          while ((fv = f.load(cuda::memory_order_acquire)) == FLAG_EMPTY) __nanosleep(32);
+        }
+        const unsigned pm = __ballot_sync(0xffffffffu, fv == FLAG_PREFIX);
+        if (lane == 0) sBal[warp] = pm;
+        __syncthreads();
+        int first = NT;
+        for (int w = NW - 1; w >= 0; --w)
+          if (sBal[w]) first = w * 32 + __ffs(sBal[w]) - 1;
+        if (first > 0) {                                       // product of the AGGs before the first PREFIX
+          CM<D> Ag;
+          if (tid < first) cm_load_cg(a.agg + (size_t)tq * D * D, Ag); else cm_eye(Ag);
+#pragma unroll
+          for (int off = 1; off < 32; off <<= 1) {
+            const CM<D> o = cm_shfl_down(Ag, off);
+            if ((lane & (2 * off - 1)) == 0) Ag = cm_mul(Ag, o);
+          }
+          if (lane == 0) cm_store(sWarpAgg[warp], Ag);
+        }
+        if (tid == first) for (int d = 0; d < D; ++d) sPsiEnd[d] = __ldcg(a.psi_end + tq * D + d);
+        __syncthreads();
+        if (tid == 0) {
+          CM<D> M, T;
+          cm_load(sM, M);
+          if (first > 0)
+            for (int w = 0; w < NW; ++w) { cm_load(sWarpAgg[w], T); M = cm_mul(M, T); }
+          if (first < NT) {
+            double er[D], ei[D], pr[D], pi[D];
+            for (int d = 0; d < D; ++d) { er[d] = sPsiEnd[d].x; ei[d] = sPsiEnd[d].y; }
+            cm_apply(M, er, ei, pr, pi);
+            for (int d = 0; d < D; ++d) sPsiIn[d] = make_double2(pr[d], pi[d]);
+          } else {
+            cm_store(sM, M);
+          }
+        }
+        if (first < NT) break;
+      }
+    }
+    if (tid == 0) {                                            // publish PREFIX: ψ at the end of this tile
+      CM<D> tot;
+      cm_load(sTot, tot);
+      double pr[D], pi[D], er[D], ei[D];
+      for (int d = 0; d < D; ++d) { pr[d] = sPsiIn[d].x; pi[d] = sPsiIn[d].y; }
+      cm_apply(tot, pr, pi, er, ei);
+      for (int d = 0; d < D; ++d) a.psi_end[tcur * D + d] = make_double2(er[d], ei[d]);
+      cuda::atomic_ref<int, cuda::thread_scope_device>(a.flags[tcur]).store(FLAG_PREFIX, cuda::memory_order_release);
+      if (j == 0) {
+        if (a.states)
+          for (int d = 0; d < D; ++d) a.states[(size_t)b * (a.k_count + 1) * D + d] = make_double2(pr[d], pi[d]);
+        if (a.spin) {
+          double jj3[3];
+          spin_of<D>(pr, pi, jj3);
+          for (int c = 0; c < 3; ++c) a.spin[(size_t)b * (a.k_count + 1) * 3 + c] = jj3[c];
+        }
+      }
+    }
+    __syncthreads();
+    // ---- pass B: y = X_i ψ_in through this thread's intervals (L2 re-stream); states leave by TMA stores
+    double yr[D], yi[D];
+    {
+      double xr[D], xi[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) { xr[d] = sPsiIn[d].x; xi[d] = sPsiIn[d].y; }
+      cm_apply(X, xr, xi, yr, yi);
+    }
+    for (int s = 0; s < nst; ++s, ++m) {
+      const double2* U = consume();
+      double2* const st = sStage + ((int)(m & 1) * NT + tid) * SS;
+      const long long k0 = kt + (long long)s * C;
+      const int nit = (int)max(0LL, min((long long)C, a.k_count - k0));
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        if (c < nit) {
+          CM<D> u;
+          cm_load(U + c * D * D, u);
+          double zr[D], zi[D];
+          cm_apply(u, yr, yi, zr, zi);
+#pragma unroll
+          for (int d = 0; d < D; ++d) { yr[d] = zr[d]; yi[d] = zi[d]; st[c * D + d] = make_double2(zr[d], zi[d]); }
+          if (a.spin) {
+            double jj3[3];
+            spin_of<D>(zr, zi, jj3);
+            double* gJ = a.spin + ((size_t)b * (a.k_count + 1) + k0 + c + 1) * 3;
+            for (int e = 0; e < 3; ++e) __stcs(gJ + e, jj3[e]);
+          }
+        }
+      }
+      release();
+      if (a.states) {                                        // per warp: its 32 rows leave as one TMA store
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // staging writes → TMA store
+        bulk_wait_read0();                                   // the store that read the other staging buffer is done
+        __syncwarp();
+        if (full) {
+          if (lane == 0) {
+            tma_store_4d(&tmS, sStage + ((int)(m & 1) * NT + warp * 32) * SS, 0, s, (int)(j * NT) + warp * 32, (int)b,
+                         pol_stream);
+            bulk_commit();
+          }
+        } else if (nit > 0) {
+          bulk_store(a.states + ((size_t)b * (a.k_count + 1) + k0 + 1) * D, st, (unsigned)(nit * D * sizeof(double2)));
+          bulk_commit();
+        }
+      }
+      top_up();
+    }
+    tcur = tnext;
+    jc = jn;
+    bc = bn;
+    fc = fn;
+    ic -= LPT;
+    cc -= LPT;
+  }
+  bulk_wait_all();
+}
+
 // ---- state chain for large batches: one thread per sweep, TMA-streamed ------------------------------------------
 //
 // With batch ≥ kChainMinBatch the sweeps alone give enough parallelism to saturate HBM, so each thread runs its own
@@ -769,7 +1140,8 @@ __global__ void validate_kernel(int64_t n_sweep, const double* sweep, int P, int
 template <int D> size_t scan_ws_bytes(int64_t batch, int64_t k_count) { return ScanLayout<D>(batch, k_count).total; }
 
 size_t scan_workspace_bytes(int dim, int64_t batch, int64_t k_count) {
-  return dim == 2 ? Scan2Layout<2>(batch, k_count).total : Scan2Layout<3>(batch, k_count).total;
+  return dim == 2 ? std::max(Scan2Layout<2>(batch, k_count).total, Scan3Layout<2>(batch, k_count, 1).total)
+                  : std::max(Scan2Layout<3>(batch, k_count).total, Scan3Layout<3>(batch, k_count, 1).total);
 }
 
 size_t aggregate_workspace_bytes(int dim, int64_t batch, int64_t k_count) {
@@ -853,8 +1225,116 @@ static cudaError_t run_scan2(int64_t batch, int64_t k_count, const double* U, co
   return cudaGetLastError();
 }
 
+template <int D> static int scan3_nst(int64_t batch, int64_t k_count, int grid) {
+  int nst = Scan3Cfg<D>::MAXST;   // largest tile that still leaves ≥ 4 tiles per CTA
+  while (nst > 1 && Scan3Layout<D>(batch, k_count, nst).ntiles < 4LL * grid) nst >>= 1;
+  return nst;
+}
+
+using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// 4-D view of a [B][rows·IPT + …][w] complex128 array (w = D² for U, D for states) for scan3's stage boxes:
+// dim0 = the C·w·2 doubles of one stage of one row, dim1 = stage s, dim2 = row (IPT intervals), dim3 = sweep.  The box
+// is one double2 wider than dim0: the out-of-bounds element is zero-filled on loads and dropped on stores, and gives the
+// shared-memory rows an odd 16-B pitch.
+static cudaError_t encode_stage_map(CUtensorMap* tm, const void* base, int w, int C, int nst, int64_t rows,
+                                    int64_t sweep_stride_items, int64_t batch, int box_rows) {
+  static EncodeTiled encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult qr;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&encode, cudaEnableDefault, &qr);
+    if (e != cudaSuccess || qr != cudaDriverEntryPointSuccess || !encode) return cudaErrorSymbolNotFound;
+  }
+  const cuuint64_t item = (cuuint64_t)w * sizeof(double2);
+  const cuuint64_t dims[4] = {(cuuint64_t)C * w * 2, (cuuint64_t)nst, (cuuint64_t)rows, (cuuint64_t)batch};
+  const cuuint64_t strides[3] = {C * item, (cuuint64_t)nst * C * item, (cuuint64_t)sweep_stride_items * item};
+  const cuuint32_t box[4] = {(cuuint32_t)(C * w * 2 + 2), 1u, (cuuint32_t)box_rows, 1u};
+  const cuuint32_t estr[4] = {1u, 1u, 1u, 1u};
+  const CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<void*>(base), dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+// persistent grid of scan3: every CTA resident (look-back forward progress); 0 on error
+template <int D> static int scan3_grid() {
+  static int grid = 0;
+  if (grid == 0) {
+    if (cudaFuncSetAttribute(scan3_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan3_smem<D>()) !=
+        cudaSuccess)
+      return 0;
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scan3_kernel<D>, Scan3Cfg<D>::NT, scan3_smem<D>()) !=
+        cudaSuccess)
+      return 0;
+    grid = sms * (per_sm > 0 ? per_sm : 1);
+  }
+  return grid;
+}
+
+template <int D>
+static cudaError_t run_scan3(int64_t batch, int64_t k_count, const double* U, const double* psi0, double* states,
+                             double* spin, void* ws, cudaStream_t s, int* launches) {
+  using Cfg = Scan3Cfg<D>;
+  constexpr size_t smem = scan3_smem<D>();
+  const int grid = scan3_grid<D>();
+  if (grid == 0) return cudaErrorInvalidConfiguration;
+  cudaError_t e;
+  const int nst = scan3_nst<D>(batch, k_count, grid);
+  Scan3Layout<D> L(batch, k_count, nst);
+  char* w = static_cast<char*>(ws);
+  Scan3Args A3;
+  Scan2Args& a = A3.s;
+  A3.nst = nst;
+  a.batch = batch;
+  a.k_count = k_count;
+  a.tiles_per_sweep = L.tiles_per_sweep;
+  a.ntiles = L.ntiles;
+  a.U = reinterpret_cast<const double2*>(U);
+  a.psi0 = reinterpret_cast<const double2*>(psi0);
+  a.states = reinterpret_cast<double2*>(states);
+  a.spin = spin;
+  a.ticket = reinterpret_cast<unsigned long long*>(w);
+  a.flags = reinterpret_cast<int*>(w + L.off_flags);
+  a.agg = reinterpret_cast<double2*>(w + L.off_agg);
+  a.psi_end = reinterpret_cast<double2*>(w + L.off_psi);
+  CUtensorMap tmU, tmS;
+  std::memset(&tmU, 0, sizeof tmU);
+  std::memset(&tmS, 0, sizeof tmS);
+  const int64_t ipt = (int64_t)nst * Cfg::C, rows = k_count / ipt;
+  A3.tensor_u = k_count >= L.tile;             // some tile is full
+  A3.tensor_s = A3.tensor_u && states != nullptr;
+  if (A3.tensor_u) {
+    e = encode_stage_map(&tmU, U, D * D, Cfg::C, nst, rows, k_count, batch, Cfg::NT);
+    if (e != cudaSuccess) return e;
+  }
+  if (A3.tensor_s) {   // states[b][k + 1] for interval k: base at state 1, sweep stride K + 1
+    e = encode_stage_map(&tmS, states + 2 * D, D, Cfg::C, nst, rows, k_count + 1, batch, 32);   // per-warp boxes
+    if (e != cudaSuccess) return e;
+  }
+  e = cudaMemsetAsync(w, 0, L.off_agg, s);   // ticket + flags
+  if (e != cudaSuccess) return e;
+  const int g = (int)std::min<int64_t>(grid, L.ntiles);
+  scan3_kernel<D><<<g, Cfg::NT, smem, s>>>(A3, tmU, tmS);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+#ifndef SS_SCAN_VERSION
+#define SS_SCAN_VERSION 3
+#endif
+
 cudaError_t launch_scan(int dim, int64_t batch, int64_t k_count, const double* U, const double* psi0, double* states,
                         void* ws, cudaStream_t s, int* launches, double* spin) {
+  // scan3 amortises its look-back over big tiles; below ~4 stages per tile (small problems) scan2's single pass wins
+  if (SS_SCAN_VERSION == 3 && batch < kChainMinBatch &&
+      (dim == 2 ? scan3_nst<2>(batch, k_count, scan3_grid<2>()) : scan3_nst<3>(batch, k_count, scan3_grid<3>())) >= 4)
+    return dim == 2 ? run_scan3<2>(batch, k_count, U, psi0, states, spin, ws, s, launches)
+                    : run_scan3<3>(batch, k_count, U, psi0, states, spin, ws, s, launches);
   if (batch >= kChainMinBatch)   // enough sweeps to saturate HBM with one sequential chain per thread
     return dim == 2 ? run_chain<2>(batch, k_count, U, psi0, states, spin, s, launches)
                     : run_chain<3>(batch, k_count, U, psi0, states, spin, s, launches);

@@ -190,6 +190,44 @@ def test_scan_vs_sequential_chain(ss, orc, d, B, K):
     assert np.abs(A - agg).max() < 1e-12 * max(1.0, np.sqrt(K) / 10)
 
 
+def _fast_unitaries(B, K, d, seed):
+    """Random unitaries without a batched QR (large K): SU(2) from a unit quaternion; for d = 3 the spin-1
+    representation of it times random diagonal phases (still unitary, entries all non-trivial)."""
+    rng = np.random.default_rng(seed)
+    q = rng.standard_normal((B, K, 4))
+    q /= np.linalg.norm(q, axis=-1, keepdims=True)
+    a, b = q[..., 0] + 1j * q[..., 1], q[..., 2] + 1j * q[..., 3]
+    if d == 2:
+        return np.stack([np.stack([a, -np.conj(b)], -1), np.stack([b, np.conj(a)], -1)], -2)
+    s2 = np.sqrt(2.0)
+    u = np.stack([np.stack([a * a, -s2 * a * np.conj(b), np.conj(b) ** 2], -1),
+                  np.stack([s2 * a * b, np.abs(a) ** 2 - np.abs(b) ** 2, -s2 * np.conj(a) * np.conj(b)], -1),
+                  np.stack([b * b, s2 * np.conj(a) * b, np.conj(a) ** 2], -1)], -2)
+    return u * np.exp(1j * rng.uniform(0, 2 * np.pi, (B, K, 1, 3)))
+
+
+@pytest.mark.parametrize("d,B,K,spin", [(2, 1, 8192 * 600, False),      # tiles of 8192, all full (tensor TMA only)
+                                        (2, 1, 1300001, True),          # nst = 4, ragged last tile
+                                        (2, 7, 300000, False),          # several sweeps, j-major look-back
+                                        (3, 1, 4096 * 592, True),       # tiles of 4096, all full
+                                        (3, 3, 700001, False)])         # nst = 8, ragged, several sweeps
+def test_scan_large_single_sweep_path(ss, orc, d, B, K, spin):
+    """Sizes that select the super-tile scan (scan3: tensor-TMA stage boxes, one look-back per tile) against the
+    oracle's sequential long-double chain, element by element; with the fused ⟨J⟩ where `spin`."""
+    U = _fast_unitaries(B, K, d, seed=K + B)
+    psi0 = W.random_states(B, d, seed=33)
+    ref = orc.chain(U, psi0)
+    tol = 1e-12 * np.sqrt(K) / 10
+    Ug, pg = torch.from_numpy(U).cuda(), torch.from_numpy(psi0).cuda()
+    if spin:
+        st, J = ss.scan_states_spin(Ug, pg, want_states=True)
+        refJ = orc.spin_projection("half" if d == 2 else "one", ref)
+        assert np.abs(J.cpu().numpy() - refJ).max() < 2 * tol
+    else:
+        st = ss.scan_states(Ug, pg)
+    assert np.abs(st.cpu().numpy() - ref).max() < tol
+
+
 def test_compose_carry(ss, orc):
     d, B, G = 3, 4, 5
     A = _random_unitaries(G, B, d, seed=28)           # [G][B][d][d]

@@ -1,5 +1,5 @@
 """Scan-stress variant of C4: one spin-half sweep, 1 s at δt = 1 ns with Δt = 10 ns → K = 1e8
-intervals, L = 10.  Times the interval kernel and the single-sweep decoupled-look-back scan (scan2) separately and
+intervals, L = 10.  Times the interval kernel and the single-sweep decoupled-look-back scan (scan3) separately and
 reports the scan's HBM bandwidth (96 B per interval: read U_k 64 B + write ψ 32 B).
 
     python tools/scan_stress.py > profiles/r01/scan_stress.txt
