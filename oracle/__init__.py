@@ -25,8 +25,10 @@ _OVERRIDE = os.environ.get("SPINSIM_ORACLE_LIB")
 
 SPIN = {"half": 1, "one": 2}
 METHOD = {"cf4": 0, "midpoint": 1, "heun": 2}
-EXPO = {"analytic": 0, "lie_trotter": 1}
-FIELD = {"constant": 0, "rabi_linear": 1, "rabi_circular": 2, "neural": 3, "gradient": 4}
+EXPO = {"analytic": 0, "lie_trotter": 1, "lie_trotter_su3": 2}
+FIELD = {"constant": 0, "rabi_linear": 1, "rabi_circular": 2, "neural": 3, "gradient": 4,
+         "su3_constant": 6, "su3_drive": 7}
+SU3_FIELDS = ("su3_constant", "su3_drive")     # fields with U1, U2, V1, V2 components (8 coefficients)
 
 _lib = None
 
@@ -59,7 +61,8 @@ def _load():
     lib.oracle_grid.argtypes = [d, d, d, ll, ll, P]
     lib.oracle_field_sample.argtypes = [i, P, d, d, i, P]
     lib.oracle_rotating_frame.argtypes = [P, d, d, P]
-    lib.oracle_exponentiate.argtypes = [i, i, i, i, ll, P, P]
+    lib.oracle_exponentiate.argtypes = [i, i, i, i, ll, i, P, P]
+    lib.oracle_trotter_residual_su3.argtypes = [P, i, P]
     lib.oracle_trotter_residual.argtypes = [d, d, d, d, P]
     lib.oracle_expm_dense.argtypes = [i, P, d, P]
     lib.oracle_fine_step.argtypes = [i, i, i, i, i, i, i, d, d, d, P, ll, ll, d, P]
@@ -113,29 +116,46 @@ def grid(t0, dt_out, dt_int, k, l):
 
 
 def field_sample(field: str, params, t_k: float, off: float, long_double: bool = True) -> np.ndarray:
+    """(ωx, ωy, ωz, ωq) — plus (ωu1, ωu2, ωv1, ωv2) for the su(3) fields — at t_k + off."""
     p = _f64(params)
-    out = np.zeros(4)
+    out = np.zeros(8)
     rc = _load().oracle_field_sample(FIELD[field], _ptr(p), t_k, off, int(long_double), _ptr(out))
     if rc != 0:
         raise ValueError(field)
-    return out
+    return out if field in SU3_FIELDS else out[:4]
 
 
 def rotating_frame(f, t_local: float, omega_r: float) -> np.ndarray:
+    """Field coefficients in the rotating frame; f has 4 or 8 entries (returned with the same length)."""
     f = _f64(f)
-    out = np.zeros(4)
-    _load().oracle_rotating_frame(_ptr(f), t_local, omega_r, _ptr(out))
-    return out
+    n = f.shape[0]
+    f8 = np.zeros(8)
+    f8[:n] = f
+    out = np.zeros(8)
+    _load().oracle_rotating_frame(_ptr(f8), t_local, omega_r, _ptr(out))
+    return out[:n]
 
 
 def exponentiate(spin: str, args, expo: str = "analytic", tau: int = 24, long_double: bool = True) -> np.ndarray:
-    """exp(−i(ax Jx + ay Jy + az Jz + aq Q)) for args [n][4]; returns [n][dim][dim] complex128."""
-    a = _f64(args).reshape(-1, 4)
+    """exp(−i(ax Jx + ay Jy + az Jz + aq Q [+ au1 U1 + au2 U2 + av1 V1 + av2 V2])) for args [n][4] (or [n][8] for
+    the su(3) exponentiator); returns [n][dim][dim] complex128."""
+    a = _f64(args)
+    na = 8 if (a.ndim >= 1 and a.shape[-1] == 8) else 4
+    a = np.ascontiguousarray(a.reshape(-1, na))
     d = dim_of(spin)
     out = np.zeros((a.shape[0], d, d), dtype=np.complex128)
-    rc = _load().oracle_exponentiate(SPIN[spin], EXPO[expo], tau, int(long_double), a.shape[0], _ptr(a), _ptr(out))
+    rc = _load().oracle_exponentiate(SPIN[spin], EXPO[expo], tau, int(long_double), a.shape[0], na, _ptr(a),
+                                     _ptr(out))
     if rc != 0:
         raise ValueError("invalid exponentiator configuration")
+    return out
+
+
+def trotter_residual_su3(args, tau: int) -> np.ndarray:
+    """T − I of the general spin-one leapfrog factor for args [8] divided by n = 2^tau (reading R20)."""
+    a = _f64(args).reshape(8)
+    out = np.zeros((3, 3), dtype=np.complex128)
+    _load().oracle_trotter_residual_su3(_ptr(a), tau, _ptr(out))
     return out
 
 

@@ -34,8 +34,14 @@ namespace oracle {
 // ------------------------------------------------------------------------------------------------
 enum Spin { HALF = 1, ONE = 2 };                            // 2j
 enum Method { CF4 = 0, MIDPOINT = 1, HEUN = 2 };
-enum Expo { ANALYTIC = 0, LIE_TROTTER = 1 };
-enum Field { CONSTANT = 0, RABI_LINEAR = 1, RABI_CIRCULAR = 2, NEURAL = 3, GRADIENT = 4 };
+enum Expo { ANALYTIC = 0, LIE_TROTTER = 1, LIE_TROTTER_SU3 = 2 };   // P:359; general su(3): P:478-479
+enum Field { CONSTANT = 0, RABI_LINEAR = 1, RABI_CIRCULAR = 2, NEURAL = 3, GRADIENT = 4,
+             SU3_CONSTANT = 6, SU3_DRIVE = 7 };                     // 6, 7: general spin-one
+
+// Field samples carry NF = 8 coefficients (ωx, ωy, ωz, ωq, ωu1, ωu2, ωv1, ωv2) of
+// H = ωx Jx + ωy Jy + ωz Jz + ωq Q + ωu1 U1 + ωu2 U2 + ωv1 V1 + ωv2 V2; the last four are zero for
+// every field of the 4-operator family and are used only by the su(3) exponentiator.
+constexpr int NF = 8;
 
 template <class R> using Cx = std::complex<R>;
 
@@ -91,9 +97,9 @@ template <class R> R sinp(R x) {                  // "a single cycle of a sine w
   return (x >= R(0) && x <= two_pi) ? std::sin(x) : R(0);
 }
 
-template <class R> void field_sample(int field, const double* p, double t_k, double off, R f[4]) {
+template <class R> void field_sample(int field, const double* p, double t_k, double off, R f[NF]) {
   const R t = (R)t_k + (R)off;
-  f[0] = f[1] = f[2] = f[3] = R(0);
+  for (int j = 0; j < NF; ++j) f[j] = R(0);
   switch (field) {
     case CONSTANT:         // p = [ωx, ωy, ωz, ωq]
       f[0] = p[0]; f[1] = p[1]; f[2] = p[2]; f[3] = p[3];
@@ -119,6 +125,20 @@ template <class R> void field_sample(int field, const double* p, double t_k, dou
     case GRADIENT:         // MRI example: ω_z = x − 2y, p = [x, y]
       f[2] = (R)p[0] - R(2) * (R)p[1];
       break;
+    case SU3_CONSTANT:     // p = all 8 coefficients, constant in time
+      for (int j = 0; j < NF; ++j) f[j] = p[j];
+      break;
+    case SU3_DRIVE: {      // reading R20: bias + quadratic shift + a circular drive of frequency ω_d coupling the
+      // upper and lower pairs with different strengths (Ω_x Jφ + Ω_v Vφ) and a two-photon drive (Ω_u Uφ) at 2ω_d
+      // ("different coupling between the lower and upper pairs of states, or with two-photon coupling").
+      // p = [ω0, ω_q, Ω_x, Ω_v, Ω_u, ω_d]
+      const R ph = (R)p[5] * t;
+      f[0] = (R)p[2] * std::cos(ph);          f[1] = (R)p[2] * std::sin(ph);
+      f[2] = p[0];                            f[3] = p[1];
+      f[4] = (R)p[4] * std::cos(R(2) * ph);   f[5] = (R)p[4] * std::sin(R(2) * ph);
+      f[6] = (R)p[3] * std::cos(ph);          f[7] = (R)p[3] * std::sin(ph);
+      break;
+    }
   }
 }
 
@@ -129,6 +149,8 @@ inline int field_num_params(int field) {
     case RABI_CIRCULAR: return 2;
     case NEURAL: return 7;
     case GRADIENT: return 2;
+    case SU3_CONSTANT: return 8;
+    case SU3_DRIVE: return 6;
   }
   return -1;
 }
@@ -139,7 +161,10 @@ inline int field_num_params(int field) {
 // exp(iθJz) Jy exp(−iθJz) = cosθ Jy + sinθ Jx, the transverse coefficients rotate as below
 // (pinned by explicit matrix conjugation in the tests).  t_local = 0 at the interval start (reading R6).
 // ------------------------------------------------------------------------------------------------
-template <class R> void to_rotating_frame(R f[4], R t_local, R omega_r) {
+//
+// General spin-one (reading R19/R20): conjugation multiplies matrix entry (i, j) by e^{iθ(m_i − m_j)}, so the
+// Δm = ±1 quadrupole pair (V1, V2) rotates like (Jx, Jy) and the Δm = ±2 pair (U1, U2) by the angle 2θ.
+template <class R> void to_rotating_frame(R f[NF], R t_local, R omega_r) {
   const R th = omega_r * t_local;
   const R c = std::cos(th), s = std::sin(th);
   const R fx = f[0], fy = f[1];
@@ -147,6 +172,13 @@ template <class R> void to_rotating_frame(R f[4], R t_local, R omega_r) {
   f[1] = -s * fx + c * fy;
   f[2] = f[2] - omega_r;
   // f[3] (ωq) unchanged: [Jz, Q] = 0
+  const R c2 = std::cos(R(2) * th), s2 = std::sin(R(2) * th);
+  const R u1 = f[4], u2 = f[5];
+  f[4] = c2 * u1 + s2 * u2;
+  f[5] = -s2 * u1 + c2 * u2;
+  const R v1 = f[6], v2 = f[7];
+  f[6] = c * v1 + s * v2;
+  f[7] = -s * v1 + c * v2;
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -245,9 +277,80 @@ template <class R> Mat<R> expm_spin1_analytic(R ax, R ay, R az) {
   return D;
 }
 
-template <class R> Mat<R> exponentiate(int spin, int expo, int tau, const R a[4]) {
+// ------------------------------------------------------------------------------------------------
+// General spin-one exponentiator (the paper ships it but does not describe it — readings
+// R19, R20 in DESIGN.md).  H = Σ a_j A_j over the su(3) basis
+//   Jx, Jy, Jz (reading R5), Q = diag(1,−2,1)/3, U1 = Jx² − Jy², U2 = JxJy + JyJx (Δm = ±2 quadrupoles),
+//   V1 = JxJz + JzJx, V2 = JyJz + JzJy (Δm = ±1 quadrupoles)   (reading R19),
+// i.e. the Hermitian matrix with
+//   diagonal (az + aq/3, −2aq/3, −az + aq/3),
+//   H01 = (ax − i ay + av1 − i av2)/√2,  H12 = (ax − i ay − av1 + i av2)/√2,  H02 = au1 − i au2.
+// Lie–Trotter in the paper's form: U = T^n, n = 2^τ, with the symmetric (leapfrog) factor
+//   T = e^{−iD/2} e^{−iX/2} e^{−iY} e^{−iX/2} e^{−iD/2}     (all arguments divided by n),
+// D = diagonal part, X = the (0,1)/(1,2) part, Y = the (0,2) part.  X and Y each have a closed-form exponential
+// (X³ = r² X with r² = |H01|² + |H12|²; Y³ = |H02|² Y):  e^{−iX} = I − i (sin r / r) X + ((cos r − 1)/r²) X².
+// With au = av = 0, Y = 0 and X = Φ Jφ, so T is exactly the paper's factor of Eq. lie_trotter_4.
+// T − I is assembled from the factors' residuals (cos − 1 = −2 sin²(·/2), expm1 diagonals) by the
+// residual product (I + x)(I + y) − I = x + y + xy; then τ residual squarings s = (a + 2I)a.
+// ------------------------------------------------------------------------------------------------
+template <class R> Mat<R> res_prod(const Mat<R>& x, const Mat<R>& y) {   // (I + x)(I + y) − I
+  Mat<R> z = mul(x, y);
+  for (int i = 0; i < 3; ++i) for (int j = 0; j < 3; ++j) z.a[i][j] += x.a[i][j] + y.a[i][j];
+  return z;
+}
+
+// residual of exp(−iX) for a Hermitian X with X³ = r² X (r² given)
+template <class R> Mat<R> rodrigues_residual(const Mat<R>& X, R r2) {
+  const R r = std::sqrt(r2);
+  const R sinc = (r == R(0)) ? R(1) : std::sin(r) / r;                               // sin r / r
+  const R sh = std::sin(r / R(2));
+  const R cosm1 = (r == R(0)) ? R(-0.5) : -R(2) * sh * sh / r2;                     // (cos r − 1)/r²
+  const Mat<R> X2 = mul(X, X);
+  const Cx<R> I(0, 1);
+  Mat<R> a = Mat<R>::zero(3);
+  for (int i = 0; i < 3; ++i) for (int j = 0; j < 3; ++j) a.a[i][j] = -I * sinc * X.a[i][j] + cosm1 * X2.a[i][j];
+  return a;
+}
+
+template <class R> Mat<R> trotter_factor_residual_su3(const R a[NF], R n) {
+  const Cx<R> I(0, 1);
+  const R rt2 = std::sqrt(R(2));
+  const R z = a[2] / n, q = a[3] / n;
+  const R d[3] = {z + q / R(3), -R(2) * q / R(3), -z + q / R(3)};
+  const Cx<R> h01 = Cx<R>(a[0] + a[6], -(a[1] + a[7])) / (rt2 * n);
+  const Cx<R> h12 = Cx<R>(a[0] - a[6], -(a[1] - a[7])) / (rt2 * n);
+  const Cx<R> h02 = Cx<R>(a[4], -a[5]) / n;
+  Mat<R> eD = Mat<R>::zero(3);                       // e^{−iD/2} − I
+  for (int i = 0; i < 3; ++i) eD.a[i][i] = expm1i(-d[i] / R(2));
+  Mat<R> Xh = Mat<R>::zero(3);                       // X/2
+  Xh.a[0][1] = h01 / R(2); Xh.a[1][0] = std::conj(h01) / R(2);
+  Xh.a[1][2] = h12 / R(2); Xh.a[2][1] = std::conj(h12) / R(2);
+  Mat<R> Y = Mat<R>::zero(3);
+  Y.a[0][2] = h02; Y.a[2][0] = std::conj(h02);
+  const Mat<R> eX = rodrigues_residual(Xh, (std::norm(h01) + std::norm(h12)) / R(4));
+  const Mat<R> eY = rodrigues_residual(Y, std::norm(h02));
+  Mat<R> t = res_prod(eD, eX);
+  t = res_prod(t, eY);
+  t = res_prod(t, eX);
+  return res_prod(t, eD);
+}
+
+template <class R> Mat<R> expm_lie_trotter_su3(const R a[NF], int tau) {
+  const R n = std::ldexp(R(1), tau);
+  Mat<R> m = trotter_factor_residual_su3(a, n);
+  for (int it = 0; it < tau; ++it) {
+    Mat<R> b = m;
+    for (int i = 0; i < 3; ++i) b.a[i][i] += R(2);          // a + 2I
+    m = mul(b, m);                                         // (a + 2I) a
+  }
+  for (int i = 0; i < 3; ++i) m.a[i][i] += R(1);
+  return m;
+}
+
+template <class R> Mat<R> exponentiate(int spin, int expo, int tau, const R a[NF]) {
   if (spin == HALF) return expm_su2(a[0], a[1], a[2]);
   if (expo == LIE_TROTTER) return expm_lie_trotter(a[0], a[1], a[2], a[3], tau);
+  if (expo == LIE_TROTTER_SU3) return expm_lie_trotter_su3(a, tau);
   return expm_spin1_analytic(a[0], a[1], a[2]);
 }
 
@@ -287,7 +390,7 @@ struct Config {
 };
 
 template <class R> void sample_in_frame(const Config& c, const double* p, double t_k, double off,
-                                        R omega_r, R f[4]) {
+                                        R omega_r, R f[NF]) {
   field_sample<R>(c.field, p, t_k, off, f);
   if (c.frame) to_rotating_frame<R>(f, (R)off, omega_r);       // applied at each sample
 }
@@ -299,14 +402,14 @@ template <class R> Mat<R> fine_step(const Config& c, const Grid& g, const double
     // Sample times t1,2 = t + ½(1 ∓ 1/√3)δt.
     const double off1 = grid_off(g, l, gauss_g1());
     const double off2 = grid_off(g, l, gauss_g2());
-    R f1[4], f2[4];
+    R f1[NF], f2[NF];
     sample_in_frame<R>(c, p, t_k, off1, omega_r, f1);
     sample_in_frame<R>(c, p, t_k, off2, omega_r, f2);
     // Weights (3 ± 2√3)/12 (Eqs. cf4_sample_1/2).
     const R wp = (R(3) + R(2) * std::sqrt(R(3))) / R(12);
     const R wm = (R(3) - R(2) * std::sqrt(R(3))) / R(12);
-    R a1[4], a2[4];
-    for (int j = 0; j < 4; ++j) {
+    R a1[NF], a2[NF];
+    for (int j = 0; j < NF; ++j) {
       a1[j] = (wp * f1[j] + wm * f2[j]) * dt;   // H̄1 δt
       a2[j] = (wm * f1[j] + wp * f2[j]) * dt;   // H̄2 δt
     }
@@ -314,17 +417,17 @@ template <class R> Mat<R> fine_step(const Config& c, const Grid& g, const double
     const Mat<R> e2 = exponentiate<R>(c.spin, c.expo, c.tau, a2);
     return mul(e2, e1);                          // exp(−iH̄2δt) exp(−iH̄1δt)  (Eq. cf4_implementation)
   }
-  R f[4];
+  R f[NF];
   if (c.method == MIDPOINT) {                    // "modified Euler": one sample at t + δt/2
     sample_in_frame<R>(c, p, t_k, grid_off(g, l, 0.5), omega_r, f);
   } else {                                       // HEUN, "improved Euler": average of H(t), H(t+δt)
-    R fa[4], fb[4];
+    R fa[NF], fb[NF];
     sample_in_frame<R>(c, p, t_k, grid_off(g, l, 0.0), omega_r, fa);
     sample_in_frame<R>(c, p, t_k, grid_off(g, l + 1, 0.0), omega_r, fb);
-    for (int j = 0; j < 4; ++j) f[j] = (fa[j] + fb[j]) / R(2);
+    for (int j = 0; j < NF; ++j) f[j] = (fa[j] + fb[j]) / R(2);
   }
-  R a[4];
-  for (int j = 0; j < 4; ++j) a[j] = f[j] * dt;
+  R a[NF];
+  for (int j = 0; j < NF; ++j) a[j] = f[j] * dt;
   return exponentiate<R>(c.spin, c.expo, c.tau, a);
 }
 
@@ -336,7 +439,7 @@ template <class R> Mat<R> interval_operator(const Config& c, const Grid& g, cons
   const double t_k = grid_tk(g, k);
   R omega_r = 0;
   if (c.frame) {                                 // ω_r = ω_z(t_{k} + Δt/2) from the lab field
-    R f[4];
+    R f[NF];
     field_sample<R>(c.field, p, t_k, 0.5 * g.dt_out, f);
     omega_r = f[2];
   }
@@ -435,8 +538,10 @@ using namespace oracle;
 static bool valid_config(const Config& c) {
   if (c.spin != HALF && c.spin != ONE) return false;
   if (c.method < CF4 || c.method > HEUN) return false;
-  if (c.expo != ANALYTIC && c.expo != LIE_TROTTER) return false;
+  if (c.expo != ANALYTIC && c.expo != LIE_TROTTER && c.expo != LIE_TROTTER_SU3) return false;
   if (c.spin == HALF && c.expo != ANALYTIC) return false;
+  // fields with U/V components need the su(3) exponentiator (the others would drop them)
+  if ((c.field == SU3_CONSTANT || c.field == SU3_DRIVE) && c.expo != LIE_TROTTER_SU3) return false;
   if (c.tau < 0 || c.tau > 60) return false;
   if (field_num_params(c.field) < 0) return false;
   return true;
@@ -467,34 +572,48 @@ int oracle_grid(double t0, double dt_out, double dt_int, long long k, long long 
   return 0;
 }
 
+// out: [8] (ωx, ωy, ωz, ωq, ωu1, ωu2, ωv1, ωv2)
 int oracle_field_sample(int field, const double* p, double t_k, double off, int use_ld, double* out) {
   if (field_num_params(field) < 0) return -1;
-  if (use_ld) { long double f[4]; field_sample<long double>(field, p, t_k, off, f); for (int j = 0; j < 4; ++j) out[j] = (double)f[j]; }
-  else { double f[4]; field_sample<double>(field, p, t_k, off, f); for (int j = 0; j < 4; ++j) out[j] = f[j]; }
+  if (use_ld) { long double f[NF]; field_sample<long double>(field, p, t_k, off, f); for (int j = 0; j < NF; ++j) out[j] = (double)f[j]; }
+  else { double f[NF]; field_sample<double>(field, p, t_k, off, f); for (int j = 0; j < NF; ++j) out[j] = f[j]; }
   return 0;
 }
 
+// f_in, out: [8]
 int oracle_rotating_frame(const double* f_in, double t_local, double omega_r, double* out) {
-  long double f[4] = {f_in[0], f_in[1], f_in[2], f_in[3]};
+  long double f[NF];
+  for (int j = 0; j < NF; ++j) f[j] = f_in[j];
   to_rotating_frame<long double>(f, t_local, omega_r);
-  for (int j = 0; j < 4; ++j) out[j] = (double)f[j];
+  for (int j = 0; j < NF; ++j) out[j] = (double)f[j];
   return 0;
 }
 
-// args: [n][4] (ax, ay, az, aq); out: [n][dim][dim] complex128
-int oracle_exponentiate(int spin, int expo, int tau, int use_ld, long long n, const double* args, double* out) {
+// args: [n][na] (ax, ay, az, aq[, au1, au2, av1, av2]), na = 4 or 8; out: [n][dim][dim] complex128
+int oracle_exponentiate(int spin, int expo, int tau, int use_ld, long long n, int na, const double* args,
+                        double* out) {
   Config c{spin, CF4, expo, tau, 0, CONSTANT};
-  if (!valid_config(c)) return -1;
+  if (!valid_config(c) || (na != 4 && na != NF)) return -1;
   const int dim = (spin == HALF) ? 2 : 3;
   for (long long i = 0; i < n; ++i) {
     if (use_ld) {
-      long double a[4] = {args[4 * i], args[4 * i + 1], args[4 * i + 2], args[4 * i + 3]};
+      long double a[NF] = {};
+      for (int j = 0; j < na; ++j) a[j] = args[na * i + j];
       store(exponentiate<long double>(spin, expo, tau, a), out + i * 2 * dim * dim);
     } else {
-      double a[4] = {args[4 * i], args[4 * i + 1], args[4 * i + 2], args[4 * i + 3]};
+      double a[NF] = {};
+      for (int j = 0; j < na; ++j) a[j] = args[na * i + j];
       store(exponentiate<double>(spin, expo, tau, a), out + i * 2 * dim * dim);
     }
   }
+  return 0;
+}
+
+// T − I of the general spin-one leapfrog factor for a[8] divided by n = 2^tau (long double).
+int oracle_trotter_residual_su3(const double* a, int tau, double* out) {
+  long double al[NF];
+  for (int j = 0; j < NF; ++j) al[j] = a[j];
+  store(trotter_factor_residual_su3<long double>(al, std::ldexp(1.0L, tau)), out);
   return 0;
 }
 

@@ -36,6 +36,17 @@ MUTANTS = {
     "su2_halfangle": ("const R c = std::cos(r / R(2));", "const R c = std::cos(r);"),
     # spin-one Jy sign convention broken inside the analytic map
     "d1_sign": ("D.a[1][0] = -rt2 * al * std::conj(be);", "D.a[1][0] = rt2 * al * std::conj(be);"),
+    # --- general spin-one (su(3)) exponentiator and fields (readings R19, R20) ---
+    # V1 enters the lower pair with the wrong sign
+    "su3_v_sign": ("Cx<R>(a[0] - a[6], -(a[1] - a[7]))", "Cx<R>(a[0] + a[6], -(a[1] - a[7]))"),
+    # U pair rotated by θ instead of 2θ in the frame
+    "su3_u_frame_angle": ("const R c2 = std::cos(R(2) * th), s2 = std::sin(R(2) * th);", "const R c2 = c, s2 = s;"),
+    # leapfrog half-step dropped on the tridiagonal part
+    "su3_x_half": ("Xh.a[0][1] = h01 / R(2);", "Xh.a[0][1] = h01;"),
+    # (0,2) coupling not Hermitian
+    "su3_y_conj": ("Y.a[2][0] = std::conj(h02);", "Y.a[2][0] = h02;"),
+    # two-photon drive at ω_d instead of 2ω_d
+    "su3_drive_2w": ("f[4] = (R)p[4] * std::cos(R(2) * ph);", "f[4] = (R)p[4] * std::cos(ph);"),
 }
 
 
@@ -53,6 +64,7 @@ def test_pins_kill_mutant(name):
                                cpp, "-o", so])
         env = dict(os.environ, SPINSIM_ORACLE_LIB=so)
         r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider",
-                            os.path.join(ROOT, "tests", "test_oracle_pins.py")],
+                            os.path.join(ROOT, "tests", "test_oracle_pins.py"),
+                            os.path.join(ROOT, "tests", "test_oracle_pins_su3.py")],
                            env=env, cwd=ROOT, capture_output=True, text=True, timeout=600)
         assert r.returncode != 0, f"mutant {name} survived the pins:\n{r.stdout[-2000:]}"

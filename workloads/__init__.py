@@ -12,6 +12,9 @@ Sweep-parameter layout per built-in field (same order on both sides):
   neural        [ω_bias, ω_rf, Ω, Ω_p, ω_sig, t_p, ω_q]
                 H = ω_bias Jz + 2Ω cos(ω_rf t) Jx + Ω_p sinp(ω_sig (t − t_p)) Jz + ω_q Q   (Eq. neural_pulse)
   gradient      [x, y]                          ω_z = x − 2y
+  su3_constant  [ωx, ωy, ωz, ωq, ωu1, ωu2, ωv1, ωv2]   general spin-one H, constant
+  su3_drive     [ω0, ω_q, Ω_x, Ω_v, Ω_u, ω_d]   H = ω0 Jz + ω_q Q + Ω_x(cos ω_d t Jx + sin ω_d t Jy)
+                + Ω_v(cos ω_d t V1 + sin ω_d t V2) + Ω_u(cos 2ω_d t U1 + sin 2ω_d t U2)   (reading R20)
 """
 from __future__ import annotations
 
@@ -29,7 +32,8 @@ OMEGA_PULSE = TWO_PI * 70.0
 # Quadratic shift for C2/C3 (reading R15: ⁸⁷Rb F=1, ≈72 Hz at the ≈1 G implied by 700 kHz).
 OMEGA_Q = TWO_PI * 72.0
 
-NUM_PARAMS = {"constant": 4, "rabi_linear": 2, "rabi_circular": 2, "neural": 7, "gradient": 2}
+NUM_PARAMS = {"constant": 4, "rabi_linear": 2, "rabi_circular": 2, "neural": 7, "gradient": 2, "su3_constant": 8,
+              "su3_drive": 6}
 
 
 def neural_params(omega_bias=OMEGA_BIAS, omega_rf=None, omega_dress=OMEGA_DRESS, omega_pulse=OMEGA_PULSE,
@@ -106,6 +110,21 @@ def random_exponent_args(n: int, scale: float, seed: int, quad: bool = True) -> 
     return a
 
 
+def random_exponent_args_su3(n: int, scale: float, seed: int) -> np.ndarray:
+    """All 8 su(3) coefficients (ax, ay, az, aq, au1, au2, av1, av2) uniform in [−scale, scale]^8."""
+    rng = np.random.default_rng(seed)
+    return rng.uniform(-scale, scale, size=(n, 8))
+
+
+def su3_drive_params(omega0=OMEGA_BIAS, omega_q=OMEGA_Q, omega_x=OMEGA_DRESS, omega_v=0.4 * OMEGA_DRESS,
+                     omega_u=0.25 * OMEGA_DRESS, omega_d=None) -> np.ndarray:
+    """[ω0, ω_q, Ω_x, Ω_v, Ω_u, ω_d]: unequal couplings of the upper/lower pairs (Ω_x ± Ω_v) plus a two-photon
+    drive Ω_u; ω_d = ω0 (resonant) unless given."""
+    if omega_d is None:
+        omega_d = omega0
+    return np.array([omega0, omega_q, omega_x, omega_v, omega_u, omega_d], dtype=np.float64)
+
+
 # ---------------------------------------------------------------------------------------------------------
 # BASELINE.json configs (SURVEY.md §8(d)).
 # ---------------------------------------------------------------------------------------------------------
@@ -162,4 +181,22 @@ def c5_matrix(expo: str = "lie_trotter", batch: int = 1) -> Workload:
                     basis_state(3, batch))
 
 
-CONFIGS = {"C1": c1_rabi, "C2": c2_neural, "C3": c3_batched, "C4": c4_long, "C5": c5_matrix}
+def g1_su3(batch: int = 8192, duration: float = 0.01) -> Workload:
+    """G1 (not a BASELINE config): a C3-shaped batched sweep of a general spin-one system —
+    the su3_drive field (upper/lower-pair couplings Ω_x ± Ω_v, two-photon drive Ω_u, quadratic shift) through the
+    su(3) Lie–Trotter exponentiator.  64 values Ω_v ∈ linspace(0, 0.8)·Ω_x × 128 drive detunings
+    Δ ∈ linspace(−2, 2)·2π kHz (ω_d = ω0 + Δ), Ω_x = 2π·1 kHz, Ω_u = 2π·250 Hz; 10 ms, δt = 100 ns, Δt = 1 µs."""
+    rows = []
+    for ov in np.linspace(0.0, 0.8, 64) * OMEGA_DRESS:
+        for de in np.linspace(-2.0, 2.0, 128) * TWO_PI * 1e3:
+            rows.append(su3_drive_params(omega_v=ov, omega_d=OMEGA_BIAS + de))
+    sweep = np.stack(rows)
+    if batch <= sweep.shape[0]:
+        sweep = sweep[:batch]
+    else:
+        sweep = np.concatenate([sweep] * int(math.ceil(batch / sweep.shape[0])))[:batch]
+    return Workload("G1", "one", "cf4", "lie_trotter_su3", 24, True, "su3_drive", 0.0, duration, 100e-9, 1e-6,
+                    np.ascontiguousarray(sweep), basis_state(3, sweep.shape[0]))
+
+
+CONFIGS = {"C1": c1_rabi, "C2": c2_neural, "C3": c3_batched, "C4": c4_long, "C5": c5_matrix, "G1": g1_su3}
