@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """bench.py — fine steps/s of the Spinsim hot path on B200 (BASELINE.json metric), one JSON line on rank 0.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C3|C2|C5|C4] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C3|C2|C5|C4|G1] [--impl ours|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...           (the driver's launch for N > 1)
 
 A "step" is one pass of the whole hot path (SURVEY §8(a) rows a1–a9: interval kernel + state scan) over one batch.
@@ -48,11 +48,13 @@ def algorithmic_flops_per_fine_step(spin: str, expo: str, tau: int, method: str 
     × τ per exponential, residual product b + a(I + b) = 219 (3×3) per exponential; field, frame, T − I construction
     and phases are not counted (a lower bound; ncu's executed count is in profiles/r01/).
     spin-half: per CF4 step 2 × (SU(2) series 26 + residual product 2×2 66) + CF4 weights 32 + two field samples 16 +
-    frame rotation 26 + phase steppers 12 + grid 2 = 272."""
+    frame rotation 26 + phase steppers 12 + grid 2 = 272.
+    general spin-one (lie_trotter_su3, readings R19/R20): dense residual squaring res_square3 = 159 flop (93 FP64
+    instructions) × τ, residual product 219; the T − I assembly (≈ 3 % of the step) is not counted."""
     n_exp = 2 if method == "cf4" else 1
     if spin == "one":
         prod = 219
-        per_exp = 99 * tau if expo == "lie_trotter" else 0
+        per_exp = {"lie_trotter": 99 * tau, "lie_trotter_su3": 159 * tau}.get(expo, 0)
         return n_exp * (per_exp + prod)
     return 272 if method == "cf4" else 136
 
@@ -62,7 +64,7 @@ def dense_equivalent_flops_per_fine_step(spin: str, expo: str, tau: int, method:
     201 flop each (context only)."""
     n_exp = 2 if method == "cf4" else 1
     if spin == "one":
-        return n_exp * ((201 * tau if expo == "lie_trotter" else 0) + 234)
+        return n_exp * ((201 * tau if expo in ("lie_trotter", "lie_trotter_su3") else 0) + 234)
     return n_exp * 72
 
 
@@ -89,6 +91,8 @@ def get_workload(name: str, batch: int) -> W.Workload:
         return W.c5_matrix("lie_trotter", batch=100)
     if name == "C4":
         return W.c4_long()
+    if name == "G1":
+        return W.g1_su3(batch=batch)
     raise ValueError(name)
 
 
@@ -483,7 +487,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["C3", "C2", "C5", "C4"], default="C3")
+    ap.add_argument("--workload", choices=["C3", "C2", "C5", "C4", "G1"], default="C3")
     ap.add_argument("--batch", type=int, default=8192, help="sweeps per rank (weak) or in total (strong), C3")
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
     ap.add_argument("--precision", choices=["fp64", "fp32"], default="fp64")

@@ -50,7 +50,13 @@ enum {
 
 enum ss_spin { SS_SPIN_HALF = 1, SS_SPIN_ONE = 2 };                 /* 2j */
 enum ss_integration { SS_CF4 = 0, SS_MIDPOINT = 1, SS_HEUN = 2 };   /* P:323; Euler samplers P:702-704 */
-enum ss_expo { SS_EXP_ANALYTIC = 0, SS_EXP_LIE_TROTTER = 1 };       /* P:359 / P:360-466 */
+/* SS_EXP_LIE_TROTTER_SU3: general spin-one Hamiltonians over the full su(3) basis (the paper
+ * ships such an exponentiator without describing it — DESIGN.md readings R19, R20):
+ *   H = ωx Jx + ωy Jy + ωz Jz + ωq Q + ωu1 U1 + ωu2 U2 + ωv1 V1 + ωv2 V2,
+ *   U1 = Jx² − Jy², U2 = JxJy + JyJx (Δm = ±2), V1 = JxJz + JzJx, V2 = JyJz + JzJy (Δm = ±1);
+ * Lie–Trotter U = T^n, n = 2^τ, T = e^{−iD/2} e^{−iX/2} e^{−iY} e^{−iX/2} e^{−iD/2} (D diagonal, X the (0,1)/(1,2)
+ * couplings, Y the (0,2) coupling, each ÷ n), τ dense residual squarings.  Spin-one only; accepts every field. */
+enum ss_expo { SS_EXP_ANALYTIC = 0, SS_EXP_LIE_TROTTER = 1, SS_EXP_LIE_TROTTER_SU3 = 2 };  /* P:359 / P:360-466 / P:478 */
 enum ss_precision { SS_FP64 = 0, SS_FP32 = 1 };
 /* Built-in field functions replacing the paper's user numba function.  Sweep parameters:
  *   SS_FIELD_CONSTANT       [ωx, ωy, ωz, ωq]
@@ -58,14 +64,21 @@ enum ss_precision { SS_FP64 = 0, SS_FP32 = 1 };
  *   SS_FIELD_RABI_CIRCULAR  [ω0, Ω]            H = ω0 Jz + Ω(cos(ω0 t) Jx + sin(ω0 t) Jy)
  *   SS_FIELD_NEURAL         [ω_bias, ω_rf, Ω, Ω_p, ω_sig, t_p, ω_q]
  *        H = ω_bias Jz + 2Ω cos(ω_rf t) Jx + Ω_p sinp(ω_sig (t − t_p)) Jz + ω_q Q   (Eq. neural_pulse)
- *   SS_FIELD_GRADIENT       [x, y]             ω_z = x − 2y                                      */
+ *   SS_FIELD_GRADIENT       [x, y]             ω_z = x − 2y
+ * General spin-one fields (only with SS_EXP_LIE_TROTTER_SU3):
+ *   SS_FIELD_SU3_CONSTANT   [ωx, ωy, ωz, ωq, ωu1, ωu2, ωv1, ωv2]
+ *   SS_FIELD_SU3_DRIVE      [ω0, ω_q, Ω_x, Ω_v, Ω_u, ω_d]
+ *        H = ω0 Jz + ω_q Q + Ω_x(cos ω_d t Jx + sin ω_d t Jy) + Ω_v(cos ω_d t V1 + sin ω_d t V2)
+ *            + Ω_u(cos 2ω_d t U1 + sin 2ω_d t U2)     (upper/lower-pair couplings Ω_x ± Ω_v, two-photon Ω_u) */
 enum ss_field {
   SS_FIELD_CONSTANT = 0,
   SS_FIELD_RABI_LINEAR = 1,
   SS_FIELD_RABI_CIRCULAR = 2,
   SS_FIELD_NEURAL = 3,
   SS_FIELD_GRADIENT = 4,
-  SS_FIELD_USER = 5         /* set by ss_create_user; not accepted by ss_create */
+  SS_FIELD_USER = 5,        /* set by ss_create_user; not accepted by ss_create */
+  SS_FIELD_SU3_CONSTANT = 6,
+  SS_FIELD_SU3_DRIVE = 7
 };
 
 /* Simulator description (mirrors spinsim.Simulator's constructor arguments). */
@@ -88,7 +101,8 @@ void ss_destroy(ss_sim* sim);
 /* Create a simulator whose field function is user code compiled at run time (the paper's
  * user-supplied field functions).  `field_source` is CUDA C++ that defines
  *     __device__ void user_field(double t_k, double off, const double* p, double f[4])
- * writing f = (ωx, ωy, ωz, ωq) in rad/s at time t_k + off (t_k = interval start, off = offset inside the interval,
+ * writing f = (ωx, ωy, ωz, ωq) — with SS_EXP_LIE_TROTTER_SU3 f has 8 entries, + (ωu1, ωu2, ωv1, ωv2) — in rad/s at
+ * time t_k + off (t_k = interval start, off = offset inside the interval,
  * kept apart so phases of fast drives can be formed accurately; f is zeroed before the call) for the sweep parameters
  * p[0 .. n_params), 1 ≤ n_params ≤ 64.  NVRTC compiles it with the library's own interval kernel for sm_100a (first call per simulator:
  * ~1 s); the rest of the description (spin, integration, exponentiation, τ, frame, precision) is honoured as for
@@ -166,8 +180,11 @@ int ss_chain_aggregate(int32_t dim, int64_t batch, int64_t k_count, const double
 int ss_compose_carry(int32_t dim, int64_t batch, int32_t n_parts, int32_t part, const double* d_aggregates,
                      const double* d_state_init, double* d_carry, void* stream);
 
-/* Building block for element-wise parity: exp(−i(ax Jx + ay Jy + az Jz + aq Q)) for d_args [n][4] float64,
- * with the simulator's spin / exponentiation / τ / precision; writes d_out [n][dim][dim] complex128. */
+/* Building block for element-wise parity: exp(−i(ax Jx + ay Jy + az Jz + aq Q)) for d_args [n][4] float64 (for
+ * SS_EXP_LIE_TROTTER_SU3: [n][8], + au1 U1 + au2 U2 + av1 V1 + av2 V2), with the simulator's spin / exponentiation /
+ * τ / precision; writes d_out [n][dim][dim] complex128. */
+/* Number of Hamiltonian coefficients per exponent argument / field sample: 8 for SS_EXP_LIE_TROTTER_SU3, else 4. */
+int ss_num_coefficients(const ss_sim* sim);
 int ss_exponentiate(const ss_sim* sim, int64_t n, const double* d_args, double* d_out, void* stream);
 
 /* Expected spin projection ⟨J⟩ = (ψ†Jxψ, ψ†Jyψ, ψ†Jzψ) for d_states [n][dim] complex128;

@@ -95,7 +95,8 @@ class Simulator:
         """field="user": `field_source` is CUDA C++ defining
         ``__device__ void user_field(double t_k, double off, const double* p, double f[4])`` (compiled at run time
         by NVRTC into the library's interval kernel; the paper's user field functions) and `n_params`
-        the number of sweep parameters it reads."""
+        the number of sweep parameters it reads.  exponentiation="lie_trotter_su3" (general spin-one)
+        takes 8 Hamiltonian coefficients: the su3_* fields, or a user field writing f[8]."""
         if exponentiation is None:
             exponentiation = "analytic" if spin == "half" else "lie_trotter"
         self.spin, self.integration, self.exponentiation = spin, integration, exponentiation
@@ -179,9 +180,17 @@ class Simulator:
               "ss_compute_unitaries")
         return U
 
+    @property
+    def num_coefficients(self) -> int:
+        """Hamiltonian coefficients per exponent argument: 8 for lie_trotter_su3, else 4."""
+        return int(self._lib.ss_num_coefficients(self._h))
+
     def exponentiate(self, args: torch.Tensor, stream=None) -> torch.Tensor:
-        """exp(−i(ax Jx + ay Jy + az Jz + aq Q)) for args [n][4] float64 (device) → [n][dim][dim] complex128."""
+        """exp(−i(ax Jx + ay Jy + az Jz + aq Q [+ au1 U1 + au2 U2 + av1 V1 + av2 V2])) for args [n][4] (or [n][8] for
+        lie_trotter_su3) float64 (device) → [n][dim][dim] complex128."""
         args = args.contiguous()
+        if args.dim() != 2 or args.shape[1] != self.num_coefficients:
+            raise ValueError(f"args must be [n][{self.num_coefficients}] for exponentiation {self.exponentiation!r}")
         out = torch.empty((args.shape[0], self.dim, self.dim), dtype=torch.complex128, device=args.device)
         check(self._lib.ss_exponentiate(self._h, args.shape[0], _dev_ptr(args, "args", torch.float64),
                                         _dev_ptr(out, "out"), _stream_ptr(stream)), "ss_exponentiate")

@@ -18,9 +18,10 @@ LIB_PATH = os.environ.get("SPINSIM_LIB") or os.path.join(HERE, "libspinsim_b200.
 SS_OK, SS_ERR_INVALID, SS_ERR_UNSUPPORTED, SS_ERR_CUDA, SS_ERR_NONFINITE = 0, -1, -2, -3, -4
 SPIN = {"half": 1, "one": 2}
 INTEGRATION = {"cf4": 0, "midpoint": 1, "heun": 2}
-EXPONENTIATION = {"analytic": 0, "lie_trotter": 1}
+EXPONENTIATION = {"analytic": 0, "lie_trotter": 1, "lie_trotter_su3": 2}
 PRECISION = {"fp64": 0, "fp32": 1}
-FIELD = {"constant": 0, "rabi_linear": 1, "rabi_circular": 2, "neural": 3, "gradient": 4}
+FIELD = {"constant": 0, "rabi_linear": 1, "rabi_circular": 2, "neural": 3, "gradient": 4, "su3_constant": 6,
+         "su3_drive": 7}
 
 # Every symbol include/spinsim_b200.h declares (tests/test_abi.py checks the header and the .so against this).
 EXPORTS = [
@@ -28,6 +29,7 @@ EXPORTS = [
     "ss_set_validation", "ss_compute_unitaries", "ss_scan_workspace_bytes", "ss_scan_states", "ss_scan_states_spin",
     "ss_aggregate_workspace_bytes", "ss_chain_aggregate", "ss_compose_carry", "ss_exponentiate",
     "ss_spin_projection", "ss_evaluate_host", "ss_kernel_launches", "ss_last_error", "ss_version",
+    "ss_num_coefficients",
 ]
 
 
@@ -80,6 +82,7 @@ def load() -> ctypes.CDLL:
         "ss_kernel_launches": (i64, []),
         "ss_last_error": (ctypes.c_char_p, []),
         "ss_version": (ctypes.c_int, []),
+        "ss_num_coefficients": (ctypes.c_int, [P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

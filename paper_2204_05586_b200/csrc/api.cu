@@ -43,9 +43,13 @@ int field_params(int field) {
     case SS_FIELD_RABI_CIRCULAR: return 2;
     case SS_FIELD_NEURAL: return 7;
     case SS_FIELD_GRADIENT: return 2;
+    case SS_FIELD_SU3_CONSTANT: return 8;
+    case SS_FIELD_SU3_DRIVE: return 6;
   }
   return -1;
 }
+
+bool is_su3_field(int field) { return field == SS_FIELD_SU3_CONSTANT || field == SS_FIELD_SU3_DRIVE; }
 
 // Column of the sweep table holding ω_q (must be 0 for the analytic spin-one exponentiator), or −1.
 int qcol_of(int field) {
@@ -87,6 +91,9 @@ ssb::IntervalLaunchFn pick_interval(const ss_sim_desc& d) {
   if (d.exponentiation == SS_EXP_LIE_TROTTER)
     return f32 ? ssb::interval_table_one_lt_f32(d.integration, d.field)
                : ssb::interval_table_one_lt_f64(d.integration, d.field);
+  if (d.exponentiation == SS_EXP_LIE_TROTTER_SU3)
+    return f32 ? ssb::interval_table_one_su3_f32(d.integration, d.field)
+               : ssb::interval_table_one_su3_f64(d.integration, d.field);
   return f32 ? ssb::interval_table_one_an_f32(d.integration, d.field) : ssb::interval_table_one_an_f64(d.integration, d.field);
 }
 
@@ -94,6 +101,8 @@ ssb::ExpoLaunchFn pick_expo(const ss_sim_desc& d) {
   const bool f32 = d.precision == SS_FP32;
   if (d.spin == SS_SPIN_HALF) return f32 ? ssb::expo_table_half_f32() : ssb::expo_table_half_f64();
   if (d.exponentiation == SS_EXP_LIE_TROTTER) return f32 ? ssb::expo_table_one_lt_f32() : ssb::expo_table_one_lt_f64();
+  if (d.exponentiation == SS_EXP_LIE_TROTTER_SU3)
+    return f32 ? ssb::expo_table_one_su3_f32() : ssb::expo_table_one_su3_f64();
   return f32 ? ssb::expo_table_one_an_f32() : ssb::expo_table_one_an_f64();
 }
 
@@ -171,7 +180,12 @@ int launch_interval_checked(ss_sim* s, const ssb::IntervalParams& p, cudaStream_
 
 extern "C" {
 
-int ss_version(void) { return 100; }
+int ss_version(void) { return 101; }
+
+int ss_num_coefficients(const ss_sim* s) {
+  if (!s) return fail(SS_ERR_INVALID, "sim is NULL");
+  return s->d.exponentiation == SS_EXP_LIE_TROTTER_SU3 ? 8 : 4;
+}
 
 const char* ss_last_error(void) { return g_err.c_str(); }
 
@@ -184,10 +198,13 @@ int ss_create(const ss_sim_desc* desc, ss_sim** out) {
   const ss_sim_desc& d = *desc;
   if (d.spin != SS_SPIN_HALF && d.spin != SS_SPIN_ONE) return fail(SS_ERR_INVALID, "spin must be 1 (half) or 2 (one), got %d", d.spin);
   if (d.integration < SS_CF4 || d.integration > SS_HEUN) return fail(SS_ERR_INVALID, "integration %d unknown", d.integration);
-  if (d.exponentiation != SS_EXP_ANALYTIC && d.exponentiation != SS_EXP_LIE_TROTTER)
+  if (d.exponentiation != SS_EXP_ANALYTIC && d.exponentiation != SS_EXP_LIE_TROTTER &&
+      d.exponentiation != SS_EXP_LIE_TROTTER_SU3)
     return fail(SS_ERR_INVALID, "exponentiation %d unknown", d.exponentiation);
   if (d.spin == SS_SPIN_HALF && d.exponentiation != SS_EXP_ANALYTIC)
     return fail(SS_ERR_UNSUPPORTED, "spin-half uses the analytic SU(2) exponentiator (P:359); Lie-Trotter is spin-one only");
+  if (is_su3_field(d.field) && d.exponentiation != SS_EXP_LIE_TROTTER_SU3)
+    return fail(SS_ERR_UNSUPPORTED, "field %d has U1/U2/V1/V2 components: it needs SS_EXP_LIE_TROTTER_SU3", d.field);
   if (d.trotter_cutoff < 0 || d.trotter_cutoff > 60) return fail(SS_ERR_INVALID, "trotter_cutoff %d outside 0..60", d.trotter_cutoff);
   if (d.use_rotating_frame != 0 && d.use_rotating_frame != 1) return fail(SS_ERR_INVALID, "use_rotating_frame must be 0 or 1");
   if (d.precision != SS_FP64 && d.precision != SS_FP32) return fail(SS_ERR_INVALID, "precision %d unknown", d.precision);

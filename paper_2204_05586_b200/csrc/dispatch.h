@@ -15,10 +15,14 @@ IntervalLaunchFn interval_table_one_lt_f64(int method, int field);
 IntervalLaunchFn interval_table_one_lt_f32(int method, int field);
 IntervalLaunchFn interval_table_one_an_f64(int method, int field);
 IntervalLaunchFn interval_table_one_an_f32(int method, int field);
+IntervalLaunchFn interval_table_one_su3_f64(int method, int field);
+IntervalLaunchFn interval_table_one_su3_f32(int method, int field);
 ExpoLaunchFn expo_table_half_f64();
 ExpoLaunchFn expo_table_half_f32();
 ExpoLaunchFn expo_table_one_lt_f64();
 ExpoLaunchFn expo_table_one_lt_f32();
 ExpoLaunchFn expo_table_one_an_f64();
 ExpoLaunchFn expo_table_one_an_f32();
+ExpoLaunchFn expo_table_one_su3_f64();
+ExpoLaunchFn expo_table_one_su3_f32();
 }  // namespace ssb

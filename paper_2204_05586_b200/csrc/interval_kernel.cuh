@@ -37,19 +37,28 @@ constexpr int kIntervalThreads = 128;
 #ifndef SS_INTERVAL_MINBLOCKS
 #define SS_INTERVAL_MINBLOCKS 4
 #endif
-template <int SPIN, typename T> constexpr int kIntervalMinBlocks() { return SS_INTERVAL_MINBLOCKS; }
+// The general spin-one kernel holds a dense 3×3 residual (18 reals) plus the squaring's output copy beside the
+// accumulator; SS_INTERVAL_MINBLOCKS_SU3 trades occupancy against spills for it (G1 on B200: 2 → 2.63e9, 3 → 2.74e9,
+// 4 (128 registers, 376 B spilled) → 2.70e9 fine steps/s; profiles/r01/su3).
+#ifndef SS_INTERVAL_MINBLOCKS_SU3
+#define SS_INTERVAL_MINBLOCKS_SU3 3
+#endif
+template <int SPIN, int EXPO, typename T> constexpr int kIntervalMinBlocks() {
+  return EXPO == EXP_LIE_TROTTER_SU3 ? SS_INTERVAL_MINBLOCKS_SU3 : SS_INTERVAL_MINBLOCKS;
+}
 
-template <int F>
+template <int NC, int F>
 __device__ __forceinline__ void sample_in_frame(const Field<F>& fld, double off, double omega_r, int frame,
-                                                double f[4]) {
+                                                double* f) {
   fld.sample(off, f);
-  if (frame) to_rotating_frame(f, off, omega_r);
+  if (frame) to_rotating_frame<NC>(f, off, omega_r);
 }
 
 template <int SPIN, int EXPO, int METHOD, int FIELD, typename T>
 __device__ __forceinline__ void interval_body(const IntervalParams& prm) {
   constexpr int D = SpinDim<SPIN>::D;
   constexpr int P = FieldParams<FIELD>::P;
+  constexpr int NC = NumCoeffs<EXPO>::N;             // 4, or 8 for the general spin-one exponentiator
   const int64_t gt = (int64_t)blockIdx.x * kIntervalThreads + threadIdx.x;
   const int S = prm.split;
   const int64_t i = gt / S;                          // interval index (sweep-major)
@@ -70,7 +79,7 @@ __device__ __forceinline__ void interval_body(const IntervalParams& prm) {
   fld.init(p, t_k);
   double omega_r = 0.0;
   if (prm.frame) {
-    double f[4];
+    double f[8];
     fld.sample(prm.half_dt_out, f);
     omega_r = f[2];
   }
@@ -91,16 +100,18 @@ __device__ __forceinline__ void interval_body(const IntervalParams& prm) {
     Res<D, T> u;
     if (METHOD == CF4) {
       // a2/a3: samples at t_k + (l + g1,2)δt, rotated into the frame.
-      double f1[4], f2[4];
+      double f1[NC], f2[NC];
+#pragma unroll
+      for (int j = 4; j < NC; ++j) f1[j] = f2[j] = 0.0;   // 4-coefficient fields under the su(3) exponentiator
       // exact sincos on anchor steps, rotation by e^{iωδt} in between (measured: +1.4 % on spin-one C3 despite
       // a few extra spill slots outside the squaring loops, +70 % on trig-bound spin-half)
       const bool anchor = ((l - l_begin) % kAnchor) == 0;
       fld.sample_cf4(base, anchor, __dadd_rn(base, prm.g1dt), __dadd_rn(base, prm.g2dt), f1, f2);
-      if (prm.frame) frame2.apply(base, anchor, f1, f2);
+      if (prm.frame) frame2.apply<NC>(base, anchor, f1, f2);
       // a4: H̄1 δt = (w+ f1 + w− f2) δt, H̄2 δt = (w− f1 + w+ f2) δt (Eqs. cf4_sample_1/2).
-      T a1[4], a2[4];
+      T a1[NC], a2[NC];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < NC; ++j) {
         a1[j] = (T)(fma(kWPlus, f1[j], kWMinus * f2[j]) * prm.dt);
         a2[j] = (T)(fma(kWMinus, f1[j], kWPlus * f2[j]) * prm.dt);
       }
@@ -130,6 +141,28 @@ __device__ __forceinline__ void interval_body(const IntervalParams& prm) {
         res_mul<D, T>(e, u, A);
         continue;
       }
+      if constexpr (SPIN == SPIN_ONE && EXPO == EXP_LIE_TROTTER_SU3 && sizeof(T) == 4) {
+        // FP32 mode, general spin-one: both exponentials' dense squarings in lockstep, one per float2 lane
+        Res<3, float> e1, e2;
+        trotter_init_su3<float>(a1, prm.tau, e1);
+        trotter_init_su3<float>(a2, prm.tau, e2);
+        Res<3, float2> m;
+#pragma unroll
+        for (int j = 0; j < 9; ++j) {
+          m.re[j] = make_float2(e1.re[j], e2.re[j]);
+          m.im[j] = make_float2(e1.im[j], e2.im[j]);
+        }
+#pragma unroll 1
+        for (int it = 0; it < prm.tau; ++it) res_square3<float2>(m);
+#pragma unroll
+        for (int j = 0; j < 9; ++j) {
+          e1.re[j] = m.re[j].x; e1.im[j] = m.im[j].x;
+          e2.re[j] = m.re[j].y; e2.im[j] = m.im[j].y;
+        }
+        res_mul<D, T>(e1, A, u);
+        res_mul<D, T>(e2, u, A);
+        continue;
+      }
       // a5/a6/a7: u·U_r = e2·(e1·U_r) (Eq. cf4_implementation), folded one exponential at a time so only
       // one exponential is live in registers (occupancy).  Residual form: A ← e + A + e·A.
       {
@@ -144,19 +177,23 @@ __device__ __forceinline__ void interval_body(const IntervalParams& prm) {
       }
       continue;
     } else {
-      double f[4];
+      double f[NC];
+#pragma unroll
+      for (int j = 4; j < NC; ++j) f[j] = 0.0;
       if (METHOD == MIDPOINT) {                       // one sample at t + δt/2 (reading R13)
-        sample_in_frame(fld, __dadd_rn(base, prm.half_dt), omega_r, prm.frame, f);
+        sample_in_frame<NC>(fld, __dadd_rn(base, prm.half_dt), omega_r, prm.frame, f);
       } else {                                        // HEUN: average of t and t + δt
-        double fa[4], fb[4];
-        sample_in_frame(fld, base, omega_r, prm.frame, fa);
-        sample_in_frame(fld, __dmul_rn((double)(l + 1), prm.dt), omega_r, prm.frame, fb);
+        double fa[NC], fb[NC];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) f[j] = 0.5 * (fa[j] + fb[j]);
+        for (int j = 4; j < NC; ++j) fa[j] = fb[j] = 0.0;
+        sample_in_frame<NC>(fld, base, omega_r, prm.frame, fa);
+        sample_in_frame<NC>(fld, __dmul_rn((double)(l + 1), prm.dt), omega_r, prm.frame, fb);
+#pragma unroll
+        for (int j = 0; j < NC; ++j) f[j] = 0.5 * (fa[j] + fb[j]);
       }
-      T a[4];
+      T a[NC];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) a[j] = (T)(f[j] * prm.dt);
+      for (int j = 0; j < NC; ++j) a[j] = (T)(f[j] * prm.dt);
       Expo<SPIN, EXPO, T>::run(a, prm.tau, u);
     }
     // a7: U_r ← u·U_r, residual form: A ← u + A + u·A.
@@ -206,7 +243,7 @@ __device__ __forceinline__ void interval_body(const IntervalParams& prm) {
 }
 
 template <int SPIN, int EXPO, int METHOD, int FIELD, typename T>
-__global__ void __launch_bounds__(kIntervalThreads, kIntervalMinBlocks<SPIN, T>())
+__global__ void __launch_bounds__(kIntervalThreads, kIntervalMinBlocks<SPIN, EXPO, T>())
 interval_kernel(const IntervalParams prm) {
   interval_body<SPIN, EXPO, METHOD, FIELD, T>(prm);
 }
@@ -224,11 +261,12 @@ cudaError_t launch_interval(const IntervalParams& prm, cudaStream_t stream) {
 template <int SPIN, int EXPO, typename T>
 __global__ void exponentiate_kernel(int64_t n, const double* args, int tau, double* out) {
   constexpr int D = SpinDim<SPIN>::D;
+  constexpr int NA = NumCoeffs<EXPO>::N;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  T a[4];
+  T a[NA];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) a[j] = (T)args[4 * i + j];
+  for (int j = 0; j < NA; ++j) a[j] = (T)args[NA * i + j];
   Res<D, T> e;
   Expo<SPIN, EXPO, T>::run(a, tau, e);
   double2* o = reinterpret_cast<double2*>(out) + i * D * D;

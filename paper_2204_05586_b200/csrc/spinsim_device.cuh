@@ -23,9 +23,13 @@ namespace ssb {
 
 enum { SPIN_HALF = 1, SPIN_ONE = 2 };
 enum { CF4 = 0, MIDPOINT = 1, HEUN = 2 };
-enum { EXP_ANALYTIC = 0, EXP_LIE_TROTTER = 1 };
+enum { EXP_ANALYTIC = 0, EXP_LIE_TROTTER = 1, EXP_LIE_TROTTER_SU3 = 2 };
 enum { FIELD_CONSTANT = 0, FIELD_RABI_LINEAR = 1, FIELD_RABI_CIRCULAR = 2, FIELD_NEURAL = 3, FIELD_GRADIENT = 4,
-       FIELD_USER = 5 };
+       FIELD_USER = 5, FIELD_SU3_CONSTANT = 6, FIELD_SU3_DRIVE = 7 };
+
+// Number of Hamiltonian coefficients a field sample carries for an exponentiator: 4 (ωx, ωy, ωz, ωq)
+// or 8 for the general spin-one exponentiator (+ ωu1, ωu2, ωv1, ωv2, reading R19).
+template <int EXPO> struct NumCoeffs { static constexpr int N = (EXPO == EXP_LIE_TROTTER_SU3) ? 8 : 4; };
 
 // ---- constants: correctly rounded doubles (reading R7) ------------------------------------------------
 constexpr double kG1 = 0x1.b0cb174df99c7p-3;       // ½(1 − 1/√3)  Gauss–Legendre node
@@ -47,6 +51,8 @@ template <> struct FieldParams<FIELD_RABI_LINEAR> { static constexpr int P = 2; 
 template <> struct FieldParams<FIELD_RABI_CIRCULAR> { static constexpr int P = 2; };
 template <> struct FieldParams<FIELD_NEURAL> { static constexpr int P = 7; };
 template <> struct FieldParams<FIELD_GRADIENT> { static constexpr int P = 2; };
+template <> struct FieldParams<FIELD_SU3_CONSTANT> { static constexpr int P = 8; };
+template <> struct FieldParams<FIELD_SU3_DRIVE> { static constexpr int P = 6; };
 
 // Series coefficients of cos(r/2) − 1 (÷ r², highest first) and sin(r/2)/r (highest first), constant bank.
 __constant__ double kSu2Series[10] = {-1.0 / 3715891200.0, 1.0 / 10321920.0, -1.0 / 46080.0, 1.0 / 384.0, -0.125,
@@ -223,14 +229,77 @@ template <> struct Field<FIELD_GRADIENT> {          // ω_z = x − 2y
   }
 };
 
+// General spin-one fields (readings R19, R20).
+template <> struct Field<FIELD_SU3_CONSTANT> {      // p = all 8 coefficients
+  double c[8];
+  __device__ __forceinline__ void init(const double* p, double) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) c[j] = p[j];
+  }
+  __device__ __forceinline__ void sample(double, double f[8]) const {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) f[j] = c[j];
+  }
+  __device__ __forceinline__ void init_cf4(double, double, double) {}
+  __device__ __forceinline__ void sample_cf4(double, bool, double o1, double o2, double g1[8], double g2[8]) {
+    sample(o1, g1); sample(o2, g2);
+  }
+};
+
+// H = ω0 Jz + ω_q Q + Ω_x(cos φ Jx + sin φ Jy) + Ω_v(cos φ V1 + sin φ V2) + Ω_u(cos 2φ U1 + sin 2φ U2), φ = ω_d t;
+// p = [ω0, ω_q, Ω_x, Ω_v, Ω_u, ω_d].  φ is reduced per interval in double-double (reading R8); 2φ by double angle.
+template <> struct Field<FIELD_SU3_DRIVE> {
+  double w0, wq, ox, ov, ou, wd, ph0, c1, s1, c2, s2;
+  PhaseStepper ps;
+  __device__ __forceinline__ void init(const double* p, double t_k) {
+    w0 = p[0]; wq = p[1]; ox = p[2]; ov = p[3]; ou = p[4]; wd = p[5];
+    ph0 = reduce_phase(p[5], t_k);
+  }
+  __device__ __forceinline__ void fill(double c, double s, double f[8]) const {
+    const double cc = fma(c, c, -s * s), ss = 2.0 * c * s;   // cos 2φ, sin 2φ
+    f[0] = ox * c;  f[1] = ox * s;  f[2] = w0;      f[3] = wq;
+    f[4] = ou * cc; f[5] = ou * ss; f[6] = ov * c;  f[7] = ov * s;
+  }
+  __device__ __forceinline__ void sample(double off, double f[8]) const {
+    double s, c;
+    sincos(fma(wd, off, ph0), &s, &c);
+    fill(c, s, f);
+  }
+  __device__ __forceinline__ void init_cf4(double g1dt, double g2dt, double dt) {
+    sincos(wd * g1dt, &s1, &c1); sincos(wd * g2dt, &s2, &c2);
+    ps.init(wd, ph0, dt);
+  }
+  __device__ __forceinline__ void sample_cf4(double base, bool anchor, double, double, double g1[8], double g2[8]) {
+    ps.next(base, anchor);
+    const double sb = ps.s, cb = ps.c;
+    fill(fma(cb, c1, -sb * s1), fma(sb, c1, cb * s1), g1);
+    fill(fma(cb, c2, -sb * s2), fma(sb, c2, cb * s2), g2);
+  }
+};
+
+// Frame rotation of the general spin-one coefficients (reading R19): conjugation by e^{iθJz} multiplies entry (i, j)
+// by e^{iθ(m_i − m_j)}, so (ωv1, ωv2) (Δm = ±1) rotate like (ωx, ωy) and (ωu1, ωu2) (Δm = ±2) by 2θ.
+template <int NC> __device__ __forceinline__ void rotate_quadrupoles(double* f, double c, double s) {
+  if constexpr (NC == 8) {
+    const double c2 = fma(c, c, -s * s), s2 = 2.0 * c * s;
+    const double u1 = f[4], u2 = f[5];
+    f[4] = fma(c2, u1, s2 * u2);
+    f[5] = fma(c2, u2, -s2 * u1);
+    const double v1 = f[6], v2 = f[7];
+    f[6] = fma(c, v1, s * v2);
+    f[7] = fma(c, v2, -s * v1);
+  }
+}
+
 // Rotating frame (reading R6): rotate (ωx, ωy) by θ = ω_r·t_local, shift ωz by −ω_r; ωq unchanged.
-__device__ __forceinline__ void to_rotating_frame(double f[4], double t_local, double omega_r) {
+template <int NC = 4> __device__ __forceinline__ void to_rotating_frame(double* f, double t_local, double omega_r) {
   double s, c;
   sincos(omega_r * t_local, &s, &c);
   const double fx = f[0], fy = f[1];
   f[0] = fma(c, fx, s * fy);
   f[1] = fma(c, fy, -s * fx);
   f[2] = f[2] - omega_r;
+  rotate_quadrupoles<NC>(f, c, s);
 }
 
 // Frame rotation for the two CF4 samples of one step: θ1,2 = ω_r·base + ω_r·g1,2δt, one sincos per step plus the
@@ -244,7 +313,8 @@ struct FrameCF4 {
     sincos(omega_r * g2dt, &s2, &c2);
     ps.init(omega_r, 0.0, dt);
   }
-  __device__ __forceinline__ void apply(double base, bool anchor, double f1[4], double f2[4]) {
+  template <int NC = 4>
+  __device__ __forceinline__ void apply(double base, bool anchor, double* f1, double* f2) {
     ps.next(base, anchor);
     const double sb = ps.s, cb = ps.c;
     const double ca = fma(cb, c1, -sb * s1), sa = fma(sb, c1, cb * s1);
@@ -253,6 +323,8 @@ struct FrameCF4 {
     f1[0] = fma(ca, fx, sa * fy); f1[1] = fma(ca, fy, -sa * fx); f1[2] -= wr;
     fx = f2[0]; fy = f2[1];
     f2[0] = fma(cc, fx, sc * fy); f2[1] = fma(cc, fy, -sc * fx); f2[2] -= wr;
+    rotate_quadrupoles<NC>(f1, ca, sa);
+    rotate_quadrupoles<NC>(f2, cc, sc);
   }
 };
 
@@ -529,12 +601,185 @@ template <typename T> __device__ __forceinline__ void expo_spin1_analytic(const 
   e.re[8] = dar * (dar + T(2)) - dai * dai;          e.im[8] = -(dai * (dar + T(2)) + dar * dai);
 }
 
+// ---- general spin-one exponentiator (readings R19, R20) -----------------------
+// exp(−iH) for H = Σ a_j A_j over (Jx, Jy, Jz, Q, U1, U2, V1, V2): Lie–Trotter U = T^n, n = 2^τ, with the leapfrog
+// factor T = e^{−iD/2} e^{−iX/2} e^{−iY} e^{−iX/2} e^{−iD/2} (arguments ÷ n), D = diagonal part, X = (0,1)/(1,2)
+// part, Y = (0,2) part; closed forms e^{−iX} = I − i (sin r/r) X + ((cos r − 1)/r²) X² (X³ = r² X).  At au = av = 0
+// it is the paper's T.  No symmetric-matrix shortcut exists for general su(3) (time-reversal is broken), so
+// the τ residual squarings are dense: res_square3, 93 FP64 instructions.
+
+// sin r / r and (cos r − 1)/r² from r² (both even): series for r ≤ 2^-4 (truncation < 1e-19 relative), else library.
+template <typename T> __device__ __forceinline__ void sinc_cosm1(T r2, T* sinc, T* cm) {
+  if (r2 <= T(0.00390625)) {
+    *sinc = fmaT(r2, fmaT(r2, fmaT(r2, fmaT(r2, T(1.0 / 362880.0), T(-1.0 / 5040.0)), T(1.0 / 120.0)), T(-1.0 / 6.0)),
+                 T(1));
+    *cm = fmaT(r2, fmaT(r2, fmaT(r2, fmaT(r2, T(-1.0 / 3628800.0), T(1.0 / 40320.0)), T(-1.0 / 720.0)),
+                         T(1.0 / 24.0)), T(-0.5));
+  } else {
+    const T r = sqrtT(r2);
+    T sh, ch;
+    sincosT(r * T(0.5), &sh, &ch);
+    *sinc = T(2) * sh * ch / r;
+    *cm = T(-2) * sh * sh / r2;
+  }
+}
+
+// (a + 2I)·a for a general 3×3 complex residual, 93 FP64 instructions: s_ii = (a_ii + 2) a_ii + Σ_{k≠i} a_ik a_ki;
+// s_ij = a_ij (a_ii + a_jj + 2) + a_ik a_kj (k the third index); the three pair sums a_ii + a_jj + 2 are shared.
+template <typename T> __device__ __forceinline__ void res_square3(Res<3, T>& a) {
+  const T two = splat<T>(2.0);
+  T d[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) d[i] = a.re[4 * i] + two;
+  T pr[3], pi[3];           // pair sums for (0,1), (0,2), (1,2)
+  pr[0] = d[0] + a.re[4]; pi[0] = a.im[0] + a.im[4];
+  pr[1] = d[0] + a.re[8]; pi[1] = a.im[0] + a.im[8];
+  pr[2] = d[1] + a.re[8]; pi[2] = a.im[4] + a.im[8];
+  Res<3, T> s;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const int ii = 4 * i;
+    T r = d[i] * a.re[ii], m = d[i] * a.im[ii];
+    r = fmaT(-a.im[ii], a.im[ii], r);
+    m = fmaT(a.im[ii], a.re[ii], m);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      if (k == i) continue;
+      const int ik = 3 * i + k, ki = 3 * k + i;
+      r = fmaT(a.re[ik], a.re[ki], r);
+      r = fmaT(-a.im[ik], a.im[ki], r);
+      m = fmaT(a.re[ik], a.im[ki], m);
+      m = fmaT(a.im[ik], a.re[ki], m);
+    }
+    s.re[ii] = r;
+    s.im[ii] = m;
+  }
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      if (i == j) continue;
+      const int k = 3 - i - j;
+      const int pj = (i + j == 1) ? 0 : (i + j == 2 ? 1 : 2);
+      const int ij = 3 * i + j, ik = 3 * i + k, kj = 3 * k + j;
+      T r = a.re[ik] * a.re[kj], m = a.re[ik] * a.im[kj];
+      r = fmaT(-a.im[ik], a.im[kj], r);
+      m = fmaT(a.im[ik], a.re[kj], m);
+      r = fmaT(a.re[ij], pr[pj], r);
+      r = fmaT(-a.im[ij], pi[pj], r);
+      m = fmaT(a.re[ij], pi[pj], m);
+      m = fmaT(a.im[ij], pr[pj], m);
+      s.re[ij] = r;
+      s.im[ij] = m;
+    }
+  a = s;
+}
+
+// T − I of the general leapfrog factor for coefficients a[8] (divided by n = 2^τ inside).
+template <typename T> __device__ __forceinline__ void trotter_init_su3(const T* a, int tau, Res<3, T>& out) {
+  const T inv_n = ldexp(T(1), -tau);
+  const T z = a[2] * inv_n, q = a[3] * inv_n;
+  const T th[3] = {z + q * T(kThird), T(-2) * q * T(kThird), q * T(kThird) - z};   // diag(D)
+  // half-angle phases e_i = e^{−iθ_i/2} = (ch_i, −sh_i)
+  T sh[3], ch[3];
+  {
+    const T big = fmax(fmax(fabs(th[0]), fabs(th[1])), fabs(th[2]));
+    if (big <= T(1.9073486328125e-06)) {          // half-angles ≤ 2^-20 (as trotter_init)
+#pragma unroll
+      for (int i = 0; i < 3; ++i) sincos_tiny<T>(th[i] * T(0.5), &sh[i], &ch[i]);
+    } else if (big <= T(0.03125)) {               // half-angles ≤ 2^-6
+#pragma unroll
+      for (int i = 0; i < 3; ++i) sincos_small<T>(th[i] * T(0.5), &sh[i], &ch[i]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 3; ++i) sincosT(th[i] * T(0.5), &sh[i], &ch[i]);
+    }
+  }
+  // X/2: α = H01/2, β = H12/2 with H01 = (ax + av1 − i(ay + av2))/√2, H12 = (ax − av1 − i(ay − av2))/√2
+  const T kx = inv_n * T(0.5 * kRsqrt2);
+  const T ar = (a[0] + a[6]) * kx, ai = -(a[1] + a[7]) * kx;
+  const T br = (a[0] - a[6]) * kx, bi = -(a[1] - a[7]) * kx;
+  const T na = fmaT(ar, ar, ai * ai), nb = fmaT(br, br, bi * bi);
+  T sx, cx;
+  sinc_cosm1<T>(na + nb, &sx, &cx);
+  // Y: γ = H02 = au1 − i au2
+  const T gr = a[4] * inv_n, gi = -a[5] * inv_n;
+  const T ng = fmaT(gr, gr, gi * gi);
+  T sy, cy;
+  sinc_cosm1<T>(ng, &sy, &cy);
+  // t = e^{−iX/2} − I = −i sinc X + cm X²;  u = e^{−iY} − I
+  Res<3, T> t;
+  t.re[0] = cx * na;          t.im[0] = T(0);
+  t.re[4] = cx * (na + nb);   t.im[4] = T(0);
+  t.re[8] = cx * nb;          t.im[8] = T(0);
+  t.re[1] = sx * ai;          t.im[1] = -sx * ar;          // −i sinc α
+  t.re[3] = -sx * ai;         t.im[3] = -sx * ar;          // −i sinc α*
+  t.re[5] = sx * bi;          t.im[5] = -sx * br;          // −i sinc β
+  t.re[7] = -sx * bi;         t.im[7] = -sx * br;          // −i sinc β*
+  t.re[2] = cx * fmaT(ar, br, -ai * bi);  t.im[2] = cx * fmaT(ar, bi, ai * br);    // cm αβ
+  t.re[6] = t.re[2];                      t.im[6] = -t.im[2];                      // cm α*β*
+  const T u0 = cy * ng;                                                            // u00 = u22 (real)
+  const T u02r = sy * gi, u02i = -sy * gr, u20r = -sy * gi, u20i = -sy * gr;       // −i sinc γ, −i sinc γ*
+  // w = t + u + t·u (u has entries only at (0,0), (0,2), (2,0), (2,2))
+  Res<3, T> w;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const T t0r = t.re[3 * i], t0i = t.im[3 * i], t2r = t.re[3 * i + 2], t2i = t.im[3 * i + 2];
+    // column 0: t_i0 (1 + u00) + t_i2 u20 + u_i0
+    T r = fmaT(t0r, u0, t0r), m = fmaT(t0i, u0, t0i);
+    r = fmaT(t2r, u20r, fmaT(-t2i, u20i, r));
+    m = fmaT(t2r, u20i, fmaT(t2i, u20r, m));
+    if (i == 0) r += u0;
+    if (i == 2) { r += u20r; m += u20i; }
+    w.re[3 * i] = r; w.im[3 * i] = m;
+    // column 2: t_i0 u02 + t_i2 (1 + u22) + u_i2
+    r = fmaT(t2r, u0, t2r); m = fmaT(t2i, u0, t2i);
+    r = fmaT(t0r, u02r, fmaT(-t0i, u02i, r));
+    m = fmaT(t0r, u02i, fmaT(t0i, u02r, m));
+    if (i == 2) r += u0;
+    if (i == 0) { r += u02r; m += u02i; }
+    w.re[3 * i + 2] = r; w.im[3 * i + 2] = m;
+    w.re[3 * i + 1] = t.re[3 * i + 1]; w.im[3 * i + 1] = t.im[3 * i + 1];
+  }
+  Res<3, T> mm;               // M − I = (I + w)(I + t) − I
+  res_mul<3, T>(w, t, mm);
+  // T − I = E_D M E_D − I: diagonal expm1(−iθ_i) + e^{−iθ_i} m_ii, off-diagonal e_i e_j m_ij
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const T xr = T(-2) * sh[i] * sh[i], xi = T(-2) * sh[i] * ch[i];       // expm1(−iθ_i)
+    const int ii = 4 * i;
+    const T mr = mm.re[ii], mi = mm.im[ii];
+    out.re[ii] = xr + mr + (xr * mr - xi * mi);
+    out.im[ii] = xi + mi + (xr * mi + xi * mr);
+  }
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      if (i == j) continue;
+      // e_i e_j = (ch_i − i sh_i)(ch_j − i sh_j)
+      const T er = ch[i] * ch[j] - sh[i] * sh[j], ei = -(sh[i] * ch[j] + ch[i] * sh[j]);
+      const int ij = 3 * i + j;
+      out.re[ij] = er * mm.re[ij] - ei * mm.im[ij];
+      out.im[ij] = er * mm.im[ij] + ei * mm.re[ij];
+    }
+}
+
+template <typename T> __device__ __forceinline__ void trotter_residual_su3(const T* a, int tau, Res<3, T>& e) {
+  trotter_init_su3<T>(a, tau, e);
+#pragma unroll 1
+  for (int it = 0; it < tau; ++it) res_square3<T>(e);
+}
+
 template <int SPIN, int EXPO, typename T> struct Expo;
 template <int EXPO, typename T> struct Expo<SPIN_HALF, EXPO, T> {
   __device__ __forceinline__ static void run(const T a[4], int, Res<2, T>& e) { expo_su2<T>(a, e); }
 };
 template <typename T> struct Expo<SPIN_ONE, EXP_LIE_TROTTER, T> {
   __device__ __forceinline__ static void run(const T a[4], int tau, Res<3, T>& e) { trotter_residual<T>(a, tau, e); }
+};
+template <typename T> struct Expo<SPIN_ONE, EXP_LIE_TROTTER_SU3, T> {
+  __device__ __forceinline__ static void run(const T* a, int tau, Res<3, T>& e) { trotter_residual_su3<T>(a, tau, e); }
 };
 template <typename T> struct Expo<SPIN_ONE, EXP_ANALYTIC, T> {
   __device__ __forceinline__ static void run(const T a[4], int, Res<3, T>& e) { expo_spin1_analytic<T>(a, e); }

@@ -56,9 +56,10 @@ def test_library_is_sm100a_only(lib):
 
 
 def test_version_and_params(lib):
-    assert lib.ss_version() == 100
+    assert lib.ss_version() == 101
     from paper_2204_05586_b200 import num_sweep_params
-    assert [num_sweep_params(f) for f in ("constant", "rabi_linear", "rabi_circular", "neural", "gradient")] == [4, 2, 2, 7, 2]
+    assert [num_sweep_params(f) for f in ("constant", "rabi_linear", "rabi_circular", "neural", "gradient",
+                                          "su3_constant", "su3_drive")] == [4, 2, 2, 7, 2, 8, 6]
     assert lib.ss_num_sweep_params(99) < 0
 
 
@@ -88,6 +89,19 @@ def test_create_validation(lib):
             for field in ("constant", "rabi_linear", "rabi_circular", "neural", "gradient"):
                 for prec in ("fp64", "fp32"):
                     Simulator(spin, method, expo, 24, True, prec, field)      # every instance exists
+    # general spin-one exponentiator: every field, and the su(3) fields only with it (readings R19, R20)
+    for method in ("cf4", "midpoint", "heun"):
+        for field in ("constant", "rabi_linear", "rabi_circular", "neural", "gradient", "su3_constant", "su3_drive"):
+            for prec in ("fp64", "fp32"):
+                assert Simulator("one", method, "lie_trotter_su3", 24, True, prec, field).num_coefficients == 8
+    for expo in ("lie_trotter", "analytic"):
+        with pytest.raises(SpinsimError) as e:
+            Simulator("one", "cf4", expo, 24, True, "fp64", "su3_drive")
+        assert e.value.code == SS_ERR_UNSUPPORTED
+    with pytest.raises(SpinsimError) as e:
+        Simulator("half", "cf4", "lie_trotter_su3", 24, True, "fp64", "constant")
+    assert e.value.code == SS_ERR_UNSUPPORTED
+    assert Simulator("one").num_coefficients == 4
 
 
 @pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU failure mode")
@@ -132,6 +146,10 @@ def test_user_field_compiles_without_gpu(lib):
     for spin, expo, prec in ((1, 0, 0), (2, 1, 0), (2, 1, 1)):
         d = _lib.ss_sim_desc(spin, 0, expo, 24, 1, prec, 0)
         assert lib.ss_compile_user_field(ctypes.byref(d), src, 1) == 0, lib.ss_last_error()
+    src8 = b"__device__ void user_field(double t_k, double off, const double* p, double f[8]) { f[2] = p[0]; f[5] = p[1]; }"
+    for prec in (0, 1):
+        d = _lib.ss_sim_desc(2, 0, 2, 24, 1, prec, 0)
+        assert lib.ss_compile_user_field(ctypes.byref(d), src8, 2) == 0, lib.ss_last_error()
     d = _lib.ss_sim_desc(1, 0, 0, 24, 1, 0, 0)
     assert lib.ss_compile_user_field(ctypes.byref(d), b"__device__ void user_field( {", 1) == _lib.SS_ERR_INVALID
     assert b"compilation failed" in lib.ss_last_error()

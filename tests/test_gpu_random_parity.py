@@ -12,11 +12,13 @@ pytestmark = pytest.mark.gpu
 FIELDS = ["constant", "rabi_linear", "rabi_circular", "neural", "gradient"]
 
 
-def random_config(seed):
-    rng = np.random.default_rng(1000 + seed)
-    spin = str(rng.choice(["half", "one"]))
+def random_config(seed, su3=False):
+    rng = np.random.default_rng(1000 + seed + (5000 if su3 else 0))
+    spin = "one" if su3 else str(rng.choice(["half", "one"]))
     expo = "analytic" if spin == "half" else str(rng.choice(["lie_trotter", "lie_trotter", "analytic"]))
-    field = str(rng.choice(FIELDS))
+    field = str(rng.choice(FIELDS + ["su3_constant", "su3_drive", "su3_drive"] if su3 else FIELDS))
+    if su3:
+        expo = "lie_trotter_su3"
     method = str(rng.choice(["cf4", "cf4", "midpoint", "heun"]))
     frame = bool(rng.integers(0, 2))
     tau = int(rng.choice([0, 3, 12, 24, 30]))
@@ -38,6 +40,14 @@ def random_config(seed):
                                 omega_dress=rng.uniform(0.5, 5) * two_pi * 1e3, omega_pulse=two_pi * 70 * rng.uniform(1, 50),
                                 omega_sig=two_pi * rng.uniform(1e3, 2e4), t_p=t0 + rng.uniform(0, K * dt_out),
                                 omega_q=two_pi * 72 * rng.uniform(0, 5))
+        elif field == "su3_constant":
+            p = rng.uniform(-1, 1, 8) * two_pi * 2e5
+        elif field == "su3_drive":
+            w0 = rng.uniform(0.3, 1.0) * two_pi * 7e5
+            p = W.su3_drive_params(omega0=w0, omega_q=two_pi * 72 * rng.uniform(0, 50),
+                                   omega_x=two_pi * rng.uniform(0.2, 5) * 1e3, omega_v=two_pi * rng.uniform(-3, 3) * 1e3,
+                                   omega_u=two_pi * rng.uniform(-3, 3) * 1e3,
+                                   omega_d=w0 + rng.uniform(-1, 1) * two_pi * 3e3)
         else:
             p = rng.uniform(-1, 1, 2) * two_pi * 3e5
         rows.append(p)
@@ -62,9 +72,9 @@ def ss():
     return ss
 
 
-@pytest.mark.parametrize("seed", range(48))
-def test_random_config_parity(ss, orc, seed):
-    w, prec = random_config(seed)
+@pytest.mark.parametrize("seed,su3", [(s, False) for s in range(48)] + [(s, True) for s in range(16)])
+def test_random_config_parity(ss, orc, seed, su3):
+    w, prec = random_config(seed, su3)
     sim = ss.Simulator(w.spin, w.method, w.expo, w.tau, w.frame, prec, w.field)
     res = sim.evaluate(torch.from_numpy(w.sweep).cuda(), w.t0, w.t1, w.dt_int, w.dt_out, torch.from_numpy(w.psi0).cuda())
     st_o, U_o = orc.evaluate(w.spin, w.method, w.expo, w.tau, w.frame, w.field, sweep=w.sweep, t0=w.t0, t1=w.t1,

@@ -26,7 +26,8 @@ def main():
     args = ap.parse_args()
     w = {"C3": lambda: W.c3_batched(batch=args.batch), "C2": lambda: W.c2_neural(),
          "C4": lambda: W.c4_long(), "C5": lambda: W.c5_matrix("lie_trotter", batch=100),
-         "C4S": lambda: W.c4_long(dt_int=1e-9, dt_out=10e-9, duration=1.0)}[args.workload]()
+         "C4S": lambda: W.c4_long(dt_int=1e-9, dt_out=10e-9, duration=1.0),
+         "G1": lambda: W.g1_su3(batch=args.batch)}[args.workload]()
     if args.duration:
         w = w.with_(t1=w.t0 + args.duration)
     sim = ss.Simulator(w.spin, w.method, w.expo, w.tau, w.frame, args.precision, w.field)
