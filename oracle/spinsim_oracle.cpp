@@ -240,6 +240,13 @@ template <class R> Mat<R> trotter_factor_residual(R Phi, R phi, R z, R q) {
   return a;
 }
 
+// One residual squaring: with T = I + a, T² − I = (a + 2I) a.
+template <class R> Mat<R> residual_square(const Mat<R>& a) {
+  Mat<R> b = a;
+  for (int i = 0; i < 3; ++i) b.a[i][i] += R(2);          // a + 2I
+  return mul(b, a);                                      // (a + 2I) a
+}
+
 // Lie–Trotter exponentiator: U = T^n, n = 2^τ, by τ residual squarings s = (a + 2I)a
 // (P:456-462), then the identity is added back.
 template <class R> Mat<R> expm_lie_trotter(R ax, R ay, R az, R aq, int tau) {
@@ -248,11 +255,7 @@ template <class R> Mat<R> expm_lie_trotter(R ax, R ay, R az, R aq, int tau) {
   const R phi = std::atan2(ay, ax);                        // atan2(0,0) = 0: reading R3
   const R z = az / n, q = aq / n;
   Mat<R> a = trotter_factor_residual(Phi, phi, z, q);
-  for (int it = 0; it < tau; ++it) {
-    Mat<R> b = a;
-    for (int i = 0; i < 3; ++i) b.a[i][i] += R(2);          // a + 2I
-    a = mul(b, a);                                         // (a + 2I) a
-  }
+  for (int it = 0; it < tau; ++it) a = residual_square(a);
   for (int i = 0; i < 3; ++i) a.a[i][i] += R(1);
   return a;
 }
@@ -338,11 +341,7 @@ template <class R> Mat<R> trotter_factor_residual_su3(const R a[NF], R n) {
 template <class R> Mat<R> expm_lie_trotter_su3(const R a[NF], int tau) {
   const R n = std::ldexp(R(1), tau);
   Mat<R> m = trotter_factor_residual_su3(a, n);
-  for (int it = 0; it < tau; ++it) {
-    Mat<R> b = m;
-    for (int i = 0; i < 3; ++i) b.a[i][i] += R(2);          // a + 2I
-    m = mul(b, m);                                         // (a + 2I) a
-  }
+  for (int it = 0; it < tau; ++it) m = residual_square(m);
   for (int i = 0; i < 3; ++i) m.a[i][i] += R(1);
   return m;
 }
