@@ -490,6 +490,15 @@ template <typename T> __device__ __forceinline__ void sym_square(Sym3<T>& a) {
   a = s;
 }
 
+// Below this bound on the entries of A = H/n (Σ|a_j|/n), the leapfrog factor's residual equals its second-order
+// Taylor polynomial to within rounding: a palindromic product of exponentials is exp(−iA + O(A³)) (symmetric
+// splitting), so T − I = −iA − A²/2 + O(A³), and the dropped terms are ≤ |A|²/6 ≈ 2^-56 (FP64) / 2^-26 (FP32)
+// relative to T − I — below one ulp.  Every physical step at τ = 24 takes this path (|a| ≲ 0.1 rad); the closed
+// forms remain for large arguments (item 9).
+template <typename T> __device__ __forceinline__ T taylor_bound();
+template <> __device__ __forceinline__ double taylor_bound<double>() { return 7.450580596923828e-09; }   // 2^-27
+template <> __device__ __forceinline__ float taylor_bound<float>() { return 2.44140625e-04f; }           // 2^-12
+
 // T₀ − I and the phase of φ (cos φ, sin φ) for exponent arguments a (divided by n = 2^τ inside).
 template <typename T>
 __device__ __forceinline__ void trotter_init(const T a[4], int tau, Sym3<T>& m, T& cphi, T& sphi) {
@@ -506,6 +515,19 @@ __device__ __forceinline__ void trotter_init(const T a[4], int tau, Sym3<T>& m, 
   }
   const T Phi = rxy * inv_n;
   const T z = a[2] * inv_n, q = a[3] * inv_n;
+  if ((fabs(a[0]) + fabs(a[1]) + fabs(a[2]) + fabs(a[3])) * inv_n <= taylor_bound<T>()) {
+    // T₀ − I = −iA₀ − A₀²/2, A₀ = D + Φ Jx (real symmetric): diag(D) = (z + q/3, −2q/3, q/3 − z), off-diagonal
+    // x = Φ/√2 on (0,1), (1,2).  A₀² = [[d0² + x², x(d0 + d1), x²], [·, d1² + 2x², x(d1 + d2)], [·, ·, d2² + x²]].
+    const T d0 = z + q * T(kThird), d1 = T(-2) * q * T(kThird), d2 = q * T(kThird) - z;
+    const T x = Phi * T(kRsqrt2), x2 = x * x, mh = T(-0.5);
+    m.r00 = mh * fmaT(d0, d0, x2);        m.i00 = -d0;
+    m.r11 = mh * fmaT(d1, d1, x2 + x2);   m.i11 = -d1;
+    m.r22 = mh * fmaT(d2, d2, x2);        m.i22 = -d2;
+    m.r01 = mh * x * (d0 + d1);           m.i01 = -x;
+    m.r12 = mh * x * (d1 + d2);           m.i12 = -x;
+    m.r02 = mh * x2;                      m.i02 = T(0);
+    return;
+  }
   const T th1 = z + q * T(kThird), th2 = T(2) * q * T(kThird), th3 = z - q * T(kThird);
   T s, c, s1, c1, s2, c2, s3, c3;
   const T big = fmax(fmax(Phi, fabs(th1)), fmax(fabs(th2), fabs(th3)));
@@ -680,6 +702,40 @@ template <typename T> __device__ __forceinline__ void trotter_init_su3(const T* 
   const T inv_n = ldexp(T(1), -tau);
   const T z = a[2] * inv_n, q = a[3] * inv_n;
   const T th[3] = {z + q * T(kThird), T(-2) * q * T(kThird), q * T(kThird) - z};   // diag(D)
+  {
+    T sum = T(0);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) sum += fabs(a[j]);
+    if (sum * inv_n <= taylor_bound<T>()) {
+      // T − I = −iA − A²/2 (palindromic product, see taylor_bound), A = H/n Hermitian with diagonal th[],
+      // A01 = α, A12 = β, A02 = γ:  (A²)_ii as below, (A²)01 = α(d0 + d1) + γβ*, (A²)12 = β(d1 + d2) + α*γ,
+      // (A²)02 = γ(d0 + d2) + αβ.
+      const T k2 = inv_n * T(kRsqrt2);
+      const T ar = (a[0] + a[6]) * k2, ai = -(a[1] + a[7]) * k2;
+      const T br = (a[0] - a[6]) * k2, bi = -(a[1] - a[7]) * k2;
+      const T gr = a[4] * inv_n, gi = -a[5] * inv_n;
+      const T na = fmaT(ar, ar, ai * ai), nb = fmaT(br, br, bi * bi), ng = fmaT(gr, gr, gi * gi);
+      const T mh = T(-0.5);
+      out.re[0] = mh * fmaT(th[0], th[0], na + ng);   out.im[0] = -th[0];
+      out.re[4] = mh * fmaT(th[1], th[1], na + nb);   out.im[4] = -th[1];
+      out.re[8] = mh * fmaT(th[2], th[2], nb + ng);   out.im[8] = -th[2];
+      const T s01 = th[0] + th[1], s12 = th[1] + th[2], s02 = th[0] + th[2];
+      // (A²)01 = α s01 + γ β*
+      const T p01r = fmaT(ar, s01, fmaT(gr, br, gi * bi)), p01i = fmaT(ai, s01, fmaT(gi, br, -gr * bi));
+      // (A²)12 = β s12 + α* γ
+      const T p12r = fmaT(br, s12, fmaT(ar, gr, ai * gi)), p12i = fmaT(bi, s12, fmaT(ar, gi, -ai * gr));
+      // (A²)02 = γ s02 + α β
+      const T p02r = fmaT(gr, s02, fmaT(ar, br, -ai * bi)), p02i = fmaT(gi, s02, fmaT(ar, bi, ai * br));
+      // (i,j): −i A_ij − (A²)_ij/2 ;  (j,i): −i conj(A_ij) − conj((A²)_ij)/2
+      out.re[1] = fmaT(mh, p01r, ai);    out.im[1] = fmaT(mh, p01i, -ar);
+      out.re[3] = fmaT(mh, p01r, -ai);   out.im[3] = fmaT(-mh, p01i, -ar);
+      out.re[5] = fmaT(mh, p12r, bi);    out.im[5] = fmaT(mh, p12i, -br);
+      out.re[7] = fmaT(mh, p12r, -bi);   out.im[7] = fmaT(-mh, p12i, -br);
+      out.re[2] = fmaT(mh, p02r, gi);    out.im[2] = fmaT(mh, p02i, -gr);
+      out.re[6] = fmaT(mh, p02r, -gi);   out.im[6] = fmaT(-mh, p02i, -gr);
+      return;
+    }
+  }
   // half-angle phases e_i = e^{−iθ_i/2} = (ch_i, −sh_i)
   T sh[3], ch[3];
   {

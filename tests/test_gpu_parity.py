@@ -51,6 +51,8 @@ def assert_parity(ss, orc, w, tol=TOL64, precision="fp64"):
 # ---- building blocks -------------------------------------------------------------------------------------------
 @pytest.mark.parametrize("spin,expo,scale", [("half", "analytic", 1.0), ("half", "analytic", 1e-6),
                                              ("one", "lie_trotter", 1.0), ("one", "lie_trotter", 1e-6),
+                                             # around the second-order Taylor bound of the factor (2^-27, §5 item 9)
+                                             ("one", "lie_trotter", 0.03), ("one", "lie_trotter", 0.02),
                                              ("one", "analytic", 1.0)])
 def test_exponentiator_parity(ss, orc, spin, expo, scale):
     a = W.random_exponent_args(5000, scale, seed=21, quad=(expo != "analytic" or spin == "half"))

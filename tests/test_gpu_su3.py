@@ -34,7 +34,7 @@ def parity(ss, orc, w, precision="fp64", tol=TOL64):
     return eU, eS
 
 
-@pytest.mark.parametrize("scale", [2.0, 1e-3, 1e-7])
+@pytest.mark.parametrize("scale", [2.0, 0.015, 0.01, 1e-3, 1e-7])      # 0.015 / 0.01 straddle the Taylor bound
 def test_su3_exponentiator_parity(ss, orc, scale):
     a = W.random_exponent_args_su3(5000, scale, seed=31)
     a[:2] = 0.0                                   # exact zero (identity)
