@@ -47,8 +47,8 @@ def algorithmic_flops_per_fine_step(spin: str, expo: str, tau: int, method: str 
     spin-one Lie–Trotter: residual squaring on the complex-symmetric leapfrog factor T₀ (6 unique entries) = 99 flop
     × τ per exponential, residual product b + a(I + b) = 219 (3×3) per exponential; field, frame, T − I construction
     and phases are not counted (a lower bound; ncu's executed count is in profiles/r01/).
-    spin-half: per CF4 step 2 × (SU(2) series 26 + residual product 2×2 66) + CF4 weights 32 + two field samples 16 +
-    frame rotation 26 + phase steppers 12 + grid 2 = 272.
+    spin-half: per CF4 step 2 × (SU(2) series 26 + SU(2)-parametrised residual product 36) + CF4 weights 32 + two
+    field samples 16 + frame rotation 26 + phase steppers 12 + grid 2 = 212 (ncu executes 211.7 per step).
     general spin-one (lie_trotter_su3, readings R19/R20): dense residual squaring res_square3 = 159 flop (93 FP64
     instructions) × τ, residual product 219; the T − I assembly (≈ 3 % of the step) is not counted."""
     n_exp = 2 if method == "cf4" else 1
@@ -56,7 +56,7 @@ def algorithmic_flops_per_fine_step(spin: str, expo: str, tau: int, method: str 
         prod = 219
         per_exp = {"lie_trotter": 99 * tau, "lie_trotter_su3": 159 * tau}.get(expo, 0)
         return n_exp * (per_exp + prod)
-    return 272 if method == "cf4" else 136
+    return 212 if method == "cf4" else 106
 
 
 def dense_equivalent_flops_per_fine_step(spin: str, expo: str, tau: int, method: str = "cf4") -> int:
@@ -426,6 +426,7 @@ def run_time_partition(args, rank, world, local, dev):
     states = torch.empty((1, kc + 1, D), dtype=torch.complex128, device=dev)
     lib = ss._lib.load()
     scan_ws = torch.empty(int(lib.ss_scan_workspace_bytes(D, 1, kc)), dtype=torch.uint8, device=dev)
+    A_zero = torch.zeros((1, D, D), dtype=torch.complex128, device=dev)
     stream = torch.cuda.current_stream()
     sim.evaluate(sweep, w.t0, w.t0 + 20 * w.dt_out, w.dt_int, w.dt_out, psi0)     # validation + warm-up
 
@@ -435,7 +436,8 @@ def run_time_partition(args, rank, world, local, dev):
         sim.compute_unitaries(sweep, w.t0, w.t1, w.dt_int, w.dt_out, k_begin=kb, k_count=kc, out=U)
         if ev is not None:
             ev[1].record(stream)
-        A = ss.chain_aggregate(U)
+        # the last partition's aggregate feeds no carry: it contributes zeros to the all-gather
+        A = ss.chain_aggregate(U) if rank < world - 1 else A_zero
         A_all = gather_aggregates(A) if world > 1 else A[None]
         carry = ss.compose_carry(A_all, psi0, rank)
         ss.scan_states(U, carry, out=states, workspace=scan_ws)

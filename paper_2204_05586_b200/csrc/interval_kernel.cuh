@@ -136,9 +136,9 @@ __device__ __forceinline__ void interval_body(const IntervalParams& prm) {
         m2.r11 = m.r11.y; m2.i11 = m.i11.y; m2.r12 = m.r12.y; m2.i12 = m.i12.y; m2.r22 = m.r22.y; m2.i22 = m.i22.y;
         Res<D, T> e;
         trotter_expand<T>(m1, c1, s1, e);
-        res_mul<D, T>(e, A, u);
+        res_mul(e, A, u);
         trotter_expand<T>(m2, c2, s2, e);
-        res_mul<D, T>(e, u, A);
+        res_mul(e, u, A);
         continue;
       }
       if constexpr (SPIN == SPIN_ONE && EXPO == EXP_LIE_TROTTER_SU3 && sizeof(T) == 4) {
@@ -159,8 +159,8 @@ __device__ __forceinline__ void interval_body(const IntervalParams& prm) {
           e1.re[j] = m.re[j].x; e1.im[j] = m.im[j].x;
           e2.re[j] = m.re[j].y; e2.im[j] = m.im[j].y;
         }
-        res_mul<D, T>(e1, A, u);
-        res_mul<D, T>(e2, u, A);
+        res_mul(e1, A, u);
+        res_mul(e2, u, A);
         continue;
       }
       // a5/a6/a7: u·U_r = e2·(e1·U_r) (Eq. cf4_implementation), folded one exponential at a time so only
@@ -168,12 +168,12 @@ __device__ __forceinline__ void interval_body(const IntervalParams& prm) {
       {
         Res<D, T> e;
         Expo<SPIN, EXPO, T>::run(a1, prm.tau, e);
-        res_mul<D, T>(e, A, u);
+        res_mul(e, A, u);
       }
       {
         Res<D, T> e;
         Expo<SPIN, EXPO, T>::run(a2, prm.tau, e);
-        res_mul<D, T>(e, u, A);
+        res_mul(e, u, A);
       }
       continue;
     } else {
@@ -198,7 +198,7 @@ __device__ __forceinline__ void interval_body(const IntervalParams& prm) {
     }
     // a7: U_r ← u·U_r, residual form: A ← u + A + u·A.
     Res<D, T> An;
-    res_mul<D, T>(u, A, An);
+    res_mul(u, A, An);
     A = An;
   }
 
@@ -206,15 +206,10 @@ __device__ __forceinline__ void interval_body(const IntervalParams& prm) {
   // (U_r = P_{S−1} ⋯ P_0, same samples, only the association of the product differs).
   if (S > 1) {
     for (int off = 1; off < S; off <<= 1) {
-      Res<D, T> B;
-#pragma unroll
-      for (int e = 0; e < D * D; ++e) {
-        B.re[e] = __shfl_down_sync(0xffffffffu, A.re[e], off);
-        B.im[e] = __shfl_down_sync(0xffffffffu, A.im[e], off);
-      }
+      const Res<D, T> B = res_shfl_down(A, off);
       if ((part & (2 * off - 1)) == 0) {
         Res<D, T> C;
-        res_mul<D, T>(B, A, C);
+        res_mul(B, A, C);
         A = C;
       }
     }
@@ -236,8 +231,8 @@ __device__ __forceinline__ void interval_body(const IntervalParams& prm) {
   for (int r = 0; r < D; ++r)
 #pragma unroll
     for (int cc = 0; cc < D; ++cc) {
-      const double mr = (double)A.re[r * D + cc] + (r == cc ? 1.0 : 0.0);
-      const double mi = (double)A.im[r * D + cc];
+      const double mr = (double)res_re(A, r, cc) + (r == cc ? 1.0 : 0.0);
+      const double mi = (double)res_im(A, r, cc);
       out[r * D + cc] = make_double2(ph_re[r] * mr - ph_im[r] * mi, ph_re[r] * mi + ph_im[r] * mr);
     }
 }
@@ -274,7 +269,7 @@ __global__ void exponentiate_kernel(int64_t n, const double* args, int tau, doub
   for (int r = 0; r < D; ++r)
 #pragma unroll
     for (int c = 0; c < D; ++c)
-      o[r * D + c] = make_double2((double)e.re[r * D + c] + (r == c ? 1.0 : 0.0), (double)e.im[r * D + c]);
+      o[r * D + c] = make_double2((double)res_re(e, r, c) + (r == c ? 1.0 : 0.0), (double)res_im(e, r, c));
 }
 
 template <int SPIN, int EXPO, typename T>

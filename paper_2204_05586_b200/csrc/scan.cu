@@ -1080,17 +1080,36 @@ static cudaError_t run_chain(int64_t batch, int64_t k_count, const double* U, co
 
 // Per-sweep product of the tile aggregates, in order: A[b] = T_{n−1} ⋯ T_0.
 template <int D>
-__global__ void combine_tiles_kernel(int64_t batch, int64_t tiles_per_sweep, const double2* tiles, double2* out) {
-  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= batch) return;
+__global__ void __launch_bounds__(256) combine_tiles_kernel(int64_t tiles_per_sweep, const double2* tiles,
+                                                            double2* out) {
+  // One block per sweep: thread t multiplies its contiguous run of tile aggregates (later·earlier), a warp shuffle
+  // tree and one pass over the 8 warp products give A = T_{n−1} ⋯ T_0.  (Was one thread per sweep walking all
+  // n ≈ 4e3 tiles of C4 serially: 0.62 ms; the fixed association is deterministic on every rank.)
+  __shared__ CM<D> warp_prod[8];
+  const int64_t b = blockIdx.x;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int64_t n = tiles_per_sweep;
+  const int64_t per = (n + 255) / 256;
+  const int64_t lo = (int64_t)t * per < n ? (int64_t)t * per : n, hi = lo + per < n ? lo + per : n;
   CM<D> A;
   cm_eye(A);
-  for (int64_t t = 0; t < tiles_per_sweep; ++t) {
+  for (int64_t k = lo; k < hi; ++k) {
     CM<D> T;
-    cm_load(tiles + ((size_t)b * tiles_per_sweep + t) * D * D, T);
+    cm_load(tiles + ((size_t)b * n + k) * D * D, T);
     A = cm_mul(T, A);
   }
-  cm_store(out + (size_t)b * D * D, A);
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const CM<D> B = cm_shfl_down(A, off);
+    if ((lane & (2 * off - 1)) == 0) A = cm_mul(B, A);
+  }
+  if (lane == 0) warp_prod[warp] = A;
+  __syncthreads();
+  if (t == 0) {
+    CM<D> R = warp_prod[0];
+    for (int w = 1; w < 8; ++w) R = cm_mul(warp_prod[w], R);
+    cm_store(out + (size_t)b * D * D, R);
+  }
 }
 
 // carry[b] = A_{part−1} ⋯ A_0 ψ0[b], applied to the state in increasing partition order.
@@ -1181,7 +1200,7 @@ static cudaError_t run_scan(int64_t batch, int64_t k_count, const double* U, con
   ++*launches;
   e = cudaGetLastError();
   if (e != cudaSuccess || SCAN) return e;
-  combine_tiles_kernel<D><<<(unsigned)((batch + 127) / 128), 128, 0, s>>>(batch, L.tiles_per_sweep, a.agg,
+  combine_tiles_kernel<D><<<(unsigned)batch, 256, 0, s>>>(L.tiles_per_sweep, a.agg,
                                                                           reinterpret_cast<double2*>(aggregate));
   ++*launches;
   return cudaGetLastError();

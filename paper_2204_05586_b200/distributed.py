@@ -64,8 +64,13 @@ def time_partitioned(steps: PartitionSteps, K: int, psi0: torch.Tensor, rank: in
     where local states[:, 0] is ψ(t_{k_begin}) and local states[:, i] is ψ(t_{k_begin + i})."""
     k_begin, k_count = partition_bounds(K, world, rank)
     U = steps.compute_unitaries(k_begin, k_count)
-    A = steps.chain_aggregate(U)
-    A_all = gather(A)                       # the only exchange: dim² complex128 per sweep per rank
+    if rank == world - 1:
+        # The last partition's aggregate feeds no carry (carry_g uses A_0 … A_{g−1}): contribute zeros to the
+        # collective instead of reducing U; with one rank there is no exchange at all.
+        A = torch.zeros((U.shape[0], U.shape[2], U.shape[3]), dtype=U.dtype, device=U.device)
+    else:
+        A = steps.chain_aggregate(U)
+    A_all = gather(A) if world > 1 else A[None]      # the only exchange: dim² complex128 per sweep per rank
     carry = steps.compose_carry(A_all, psi0, rank)
     return k_begin, steps.scan_states(U, carry)
 
