@@ -50,8 +50,12 @@ def algorithmic_flops_per_fine_step(spin: str, expo: str, tau: int, method: str 
     spin-half: per CF4 step 2 × (SU(2) series 26 + SU(2)-parametrised residual product 36) + CF4 weights 32 + two
     field samples 16 + frame rotation 26 + phase steppers 12 + grid 2 = 212 (ncu executes 211.7 per step).
     general spin-one (lie_trotter_su3, readings R19/R20): dense residual squaring res_square3 = 159 flop (93 FP64
-    instructions) × τ, residual product 219; the T − I assembly (≈ 3 % of the step) is not counted."""
+    instructions) × τ, residual product 219; the T − I assembly (≈ 3 % of the step) is not counted.
+    spin-one analytic (reading R14): accumulated in SU(2) form and mapped by D¹ once per interval (DESIGN.md §5
+    item 11), so its fine step is the spin-half step: 212."""
     n_exp = 2 if method == "cf4" else 1
+    if spin == "one" and expo == "analytic":
+        spin = "half"
     if spin == "one":
         prod = 219
         per_exp = {"lie_trotter": 99 * tau, "lie_trotter_su3": 159 * tau}.get(expo, 0)
@@ -82,13 +86,13 @@ def scan_bytes_per_interval(dim: int) -> int:
     return (2 * dim * dim + 2 * dim) * 8       # read U_k, write ψ_{k+1}
 
 
-def get_workload(name: str, batch: int) -> W.Workload:
+def get_workload(name: str, batch: int, expo: str | None = None) -> W.Workload:
     if name == "C3":
         return W.c3_batched(batch=batch)
     if name == "C2":
         return W.c2_neural(dt_int=100e-9)
     if name == "C5":
-        return W.c5_matrix("lie_trotter", batch=100)
+        return W.c5_matrix(expo or "lie_trotter", batch=100)
     if name == "C4":
         return W.c4_long()
     if name == "G1":
@@ -235,7 +239,7 @@ def run_reference(args, rank, world):
     """The reference arm of this tier: the CPU oracle, timed as it stands on the host cores (rank 0 only)."""
     if rank != 0:
         return
-    w = get_workload(args.workload, args.batch)
+    w = get_workload(args.workload, args.batch, args.expo)
     run, n_sw, k_end, cores = cpu_oracle_sample(w, target_s=args.ref_step_seconds)
     for _ in range(args.warmup):
         run(n_sw, k_end)
@@ -293,10 +297,10 @@ def run_ours(args, rank, world, local):
         return run_time_partition(args, rank, world, local, dev)
     # sweep shard of this rank
     if args.scaling == "weak":
-        full = get_workload(args.workload, args.batch * world)
+        full = get_workload(args.workload, args.batch * world, args.expo)
         lo, hi = rank * args.batch, (rank + 1) * args.batch
     else:
-        full = get_workload(args.workload, args.batch)
+        full = get_workload(args.workload, args.batch, args.expo)
         per = (full.batch + world - 1) // world
         lo, hi = rank * per, min(full.batch, (rank + 1) * per)
     w = full.with_(sweep=np.ascontiguousarray(full.sweep[lo:hi]), psi0=np.ascontiguousarray(full.psi0[lo:hi]))
@@ -493,6 +497,8 @@ def main():
     ap.add_argument("--batch", type=int, default=8192, help="sweeps per rank (weak) or in total (strong), C3")
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
     ap.add_argument("--precision", choices=["fp64", "fp32"], default="fp64")
+    ap.add_argument("--expo", choices=["analytic", "lie_trotter"], default=None,
+                    help="C5 only: the exponentiator column of the accuracy/throughput matrix (default lie_trotter)")
     ap.add_argument("--chunks", type=int, default=10, help="batch chunks of the pipelined host-buffer (e2e) call")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-step-seconds", type=float, default=8.0)

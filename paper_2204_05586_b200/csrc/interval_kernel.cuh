@@ -90,14 +90,15 @@ __device__ __forceinline__ void interval_body(const IntervalParams& prm) {
     frame2.init(omega_r, prm.g1dt, prm.g2dt, prm.dt);
   }
 
-  Res<D, T> A;   // U_r − I, U_r initialised to the identity
+  constexpr int DA = AccDim<SPIN, EXPO>::D;         // accumulated residual: SU(2) form (2) or dense 3×3
+  Res<DA, T> A;   // U_r − I, U_r initialised to the identity
   res_zero(A);
 
   const int64_t l_begin = (prm.L * part) / S, l_end = active ? (prm.L * (part + 1)) / S : l_begin;
 #pragma unroll 1
   for (int64_t l = l_begin; l < l_end; ++l) {
     const double base = __dmul_rn((double)l, prm.dt);
-    Res<D, T> u;
+    Res<DA, T> u;
     if (METHOD == CF4) {
       // a2/a3: samples at t_k + (l + g1,2)δt, rotated into the frame.
       double f1[NC], f2[NC];
@@ -166,12 +167,12 @@ __device__ __forceinline__ void interval_body(const IntervalParams& prm) {
       // a5/a6/a7: u·U_r = e2·(e1·U_r) (Eq. cf4_implementation), folded one exponential at a time so only
       // one exponential is live in registers (occupancy).  Residual form: A ← e + A + e·A.
       {
-        Res<D, T> e;
+        Res<DA, T> e;
         Expo<SPIN, EXPO, T>::run(a1, prm.tau, e);
         res_mul(e, A, u);
       }
       {
-        Res<D, T> e;
+        Res<DA, T> e;
         Expo<SPIN, EXPO, T>::run(a2, prm.tau, e);
         res_mul(e, u, A);
       }
@@ -197,7 +198,7 @@ __device__ __forceinline__ void interval_body(const IntervalParams& prm) {
       Expo<SPIN, EXPO, T>::run(a, prm.tau, u);
     }
     // a7: U_r ← u·U_r, residual form: A ← u + A + u·A.
-    Res<D, T> An;
+    Res<DA, T> An;
     res_mul(u, A, An);
     A = An;
   }
@@ -206,9 +207,9 @@ __device__ __forceinline__ void interval_body(const IntervalParams& prm) {
   // (U_r = P_{S−1} ⋯ P_0, same samples, only the association of the product differs).
   if (S > 1) {
     for (int off = 1; off < S; off <<= 1) {
-      const Res<D, T> B = res_shfl_down(A, off);
+      const Res<DA, T> B = res_shfl_down(A, off);
       if ((part & (2 * off - 1)) == 0) {
-        Res<D, T> C;
+        Res<DA, T> C;
         res_mul(B, A, C);
         A = C;
       }
@@ -226,13 +227,15 @@ __device__ __forceinline__ void interval_body(const IntervalParams& prm) {
     ph_re[D - 1] = c; ph_im[D - 1] = s;               // m = −1 (or −½)
     if (D == 3) { ph_re[1] = 1.0; ph_im[1] = 0.0; }   // m = 0
   }
+  Res<D, T> Ad;                                      // D¹ map of the SU(2) accumulator (analytic spin-one)
+  acc_to_dim<T>(A, Ad);
   double2* out = reinterpret_cast<double2*>(prm.unitaries) + i * (D * D);
 #pragma unroll
   for (int r = 0; r < D; ++r)
 #pragma unroll
     for (int cc = 0; cc < D; ++cc) {
-      const double mr = (double)res_re(A, r, cc) + (r == cc ? 1.0 : 0.0);
-      const double mi = (double)res_im(A, r, cc);
+      const double mr = (double)res_re(Ad, r, cc) + (r == cc ? 1.0 : 0.0);
+      const double mi = (double)res_im(Ad, r, cc);
       out[r * D + cc] = make_double2(ph_re[r] * mr - ph_im[r] * mi, ph_re[r] * mi + ph_im[r] * mr);
     }
 }
@@ -262,8 +265,10 @@ __global__ void exponentiate_kernel(int64_t n, const double* args, int tau, doub
   T a[NA];
 #pragma unroll
   for (int j = 0; j < NA; ++j) a[j] = (T)args[NA * i + j];
+  Res<AccDim<SPIN, EXPO>::D, T> e0;
+  Expo<SPIN, EXPO, T>::run(a, tau, e0);
   Res<D, T> e;
-  Expo<SPIN, EXPO, T>::run(a, tau, e);
+  acc_to_dim<T>(e0, e);
   double2* o = reinterpret_cast<double2*>(out) + i * D * D;
 #pragma unroll
   for (int r = 0; r < D; ++r)

@@ -659,9 +659,7 @@ template <typename T> __device__ __forceinline__ void trotter_residual(const T a
 
 // Spin-one "analytic" exponential (reading R14): D¹ of the SU(2) closed form, valid iff aq = 0.
 // With α = 1 + δα, β (from expo_su2): D¹ − I = [[δα(δα+2), √2αβ, β²], [−√2αβ*, −2|β|², √2α*β], [β*², −√2α*β*, δα*(δα*+2)]].
-template <typename T> __device__ __forceinline__ void expo_spin1_analytic(const T a[4], Res<3, T>& e) {
-  Res<2, T> u;
-  expo_su2<T>(a, u);
+template <typename T> __device__ __forceinline__ void su2_to_spin1(const Res<2, T>& u, Res<3, T>& e) {
   const T dar = u.ar, dai = u.ai;                    // δα = α − 1
   const T ar = T(1) + dar, ai = dai;                 // α
   const T br = u.br, bi = u.bi;                      // β
@@ -900,8 +898,24 @@ template <typename T> struct Expo<SPIN_ONE, EXP_LIE_TROTTER, T> {
 template <typename T> struct Expo<SPIN_ONE, EXP_LIE_TROTTER_SU3, T> {
   __device__ __forceinline__ static void run(const T* a, int tau, Res<3, T>& e) { trotter_residual_su3<T>(a, tau, e); }
 };
+template <typename T> __device__ __forceinline__ void expo_spin1_analytic(const T a[4], Res<3, T>& e) {
+  Res<2, T> u;
+  expo_su2<T>(a, u);
+  su2_to_spin1<T>(u, e);
+}
+// The analytic spin-one path accumulates in SU(2) and maps once: D¹ is a homomorphism, so D¹(u_L)⋯D¹(u_1) =
+// D¹(u_L⋯u_1) — the same interval operator, exactly (DESIGN.md §5 item 11).  Expo returns the SU(2) residual.
 template <typename T> struct Expo<SPIN_ONE, EXP_ANALYTIC, T> {
-  __device__ __forceinline__ static void run(const T a[4], int, Res<3, T>& e) { expo_spin1_analytic<T>(a, e); }
+  __device__ __forceinline__ static void run(const T a[4], int, Res<2, T>& e) { expo_su2<T>(a, e); }
 };
+
+// Dimension of the residual the interval kernel accumulates: 2 (SU(2) form) for spin-half and for the analytic
+// spin-one exponentiator, 3 otherwise.
+template <int SPIN, int EXPO> struct AccDim {
+  static constexpr int D = (SPIN == SPIN_HALF || EXPO == EXP_ANALYTIC) ? 2 : 3;
+};
+template <typename T> __device__ __forceinline__ void acc_to_dim(const Res<2, T>& a, Res<2, T>& o) { o = a; }
+template <typename T> __device__ __forceinline__ void acc_to_dim(const Res<2, T>& a, Res<3, T>& o) { su2_to_spin1<T>(a, o); }
+template <typename T> __device__ __forceinline__ void acc_to_dim(const Res<3, T>& a, Res<3, T>& o) { o = a; }
 
 }  // namespace ssb
