@@ -597,8 +597,11 @@ __global__ void __launch_bounds__(Scan2Cfg<D>::NT) scan2_kernel(const Scan2Args 
 #ifndef SS_SCAN3_MAXST
 #define SS_SCAN3_MAXST 16   // stages per pass in the largest tile
 #endif
+#ifndef SS_SCAN3_NSTAGE
+#define SS_SCAN3_NSTAGE 5   // TMA ring depth; shallower rings fit 2 CTAs per SM (tuning knob)
+#endif
 template <int D> struct Scan3Cfg {
-  static constexpr int NT = 128, NW = NT / 32, C = (D == 2) ? 4 : 2, NSTAGE = 5, MAXST = SS_SCAN3_MAXST;
+  static constexpr int NT = 128, NW = NT / 32, C = (D == 2) ? 4 : 2, NSTAGE = SS_SCAN3_NSTAGE, MAXST = SS_SCAN3_MAXST;
   static constexpr int SU = C * D * D + 1;   // slot pitch in double2: odd → conflict-free per-thread reads
   static constexpr int SS = C * D + 1;       // state staging pitch in double2
 };
