@@ -46,3 +46,17 @@ def test_device_arm_contract():
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] == 2 * d["steps"]
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
+
+
+def test_flop_model():
+    """The per-fine-step flop counts bench.py reports, re-derived from the instruction mix of each
+    formulation: symmetric squaring 36 DFMA + 12 DMUL + 15 DADD = 99 flop, dense su(3) squaring 66 DFMA + 18 DMUL +
+    9 DADD = 159, 3×3 residual product 219, SU(2) group-law product 16 DFMA + 4 DADD = 36."""
+    sys.path.insert(0, ROOT)
+    import bench
+    sym, dense3, prod3, prod2 = 2 * 36 + 12 + 15, 2 * 66 + 18 + 9, 219, 2 * 16 + 4
+    assert bench.algorithmic_flops_per_fine_step("one", "lie_trotter", 24) == 2 * (24 * sym + prod3)
+    assert bench.algorithmic_flops_per_fine_step("one", "lie_trotter_su3", 24) == 2 * (24 * dense3 + prod3)
+    half = 2 * (26 + prod2) + 32 + 16 + 26 + 12 + 2
+    assert bench.algorithmic_flops_per_fine_step("half", "analytic", 24) == half == 212
+    assert bench.algorithmic_flops_per_fine_step("one", "analytic", 24) == half      # SU(2) accumulation + D¹ map
