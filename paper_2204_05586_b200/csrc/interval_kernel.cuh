@@ -95,8 +95,10 @@ __device__ __forceinline__ void interval_body(const IntervalParams& prm) {
   res_zero(A);
 
   const int64_t l_begin = (prm.L * part) / S, l_end = active ? (prm.L * (part + 1)) / S : l_begin;
-#pragma unroll 1
-  for (int64_t l = l_begin; l < l_end; ++l) {
+  // One fine step.  ANCHOR (exact sincos of the phase steppers, every kAnchor-th step) and PULSE (this interval can
+  // meet the neural field's pulse window) are compile-time, so the step body carries no per-step branches for them.
+  auto step = [&](int64_t l, auto anchor_c, auto pulse_c) {
+    const bool ANCHOR = anchor_c.value, PULSE = pulse_c.value;   // compile-time for BoolC, run-time for RtBool
     const double base = __dmul_rn((double)l, prm.dt);
     Res<DA, T> u;
     if (METHOD == CF4) {
@@ -106,9 +108,8 @@ __device__ __forceinline__ void interval_body(const IntervalParams& prm) {
       for (int j = 4; j < NC; ++j) f1[j] = f2[j] = 0.0;   // 4-coefficient fields under the su(3) exponentiator
       // exact sincos on anchor steps, rotation by e^{iωδt} in between (measured: +1.4 % on spin-one C3 despite
       // a few extra spill slots outside the squaring loops, +70 % on trig-bound spin-half)
-      const bool anchor = ((l - l_begin) % kAnchor) == 0;
-      fld.sample_cf4(base, anchor, __dadd_rn(base, prm.g1dt), __dadd_rn(base, prm.g2dt), f1, f2);
-      if (prm.frame) frame2.apply<NC>(base, anchor, f1, f2);
+      fld.sample_cf4(base, ANCHOR, PULSE, __dadd_rn(base, prm.g1dt), __dadd_rn(base, prm.g2dt), f1, f2);
+      if (prm.frame) frame2.apply<NC>(base, ANCHOR, f1, f2);
       // a4: H̄1 δt = (w+ f1 + w− f2) δt, H̄2 δt = (w− f1 + w+ f2) δt (Eqs. cf4_sample_1/2).
       T a1[NC], a2[NC];
 #pragma unroll
@@ -140,7 +141,7 @@ __device__ __forceinline__ void interval_body(const IntervalParams& prm) {
         res_mul(e, A, u);
         trotter_expand<T>(m2, c2, s2, e);
         res_mul(e, u, A);
-        continue;
+        return;
       }
       if constexpr (SPIN == SPIN_ONE && EXPO == EXP_LIE_TROTTER_SU3 && sizeof(T) == 4) {
         // FP32 mode, general spin-one: both exponentials' dense squarings in lockstep, one per float2 lane
@@ -162,7 +163,7 @@ __device__ __forceinline__ void interval_body(const IntervalParams& prm) {
         }
         res_mul(e1, A, u);
         res_mul(e2, u, A);
-        continue;
+        return;
       }
       // a5/a6/a7: u·U_r = e2·(e1·U_r) (Eq. cf4_implementation), folded one exponential at a time so only
       // one exponential is live in registers (occupancy).  Residual form: A ← e + A + e·A.
@@ -176,7 +177,7 @@ __device__ __forceinline__ void interval_body(const IntervalParams& prm) {
         Expo<SPIN, EXPO, T>::run(a2, prm.tau, e);
         res_mul(e, u, A);
       }
-      continue;
+      return;
     } else {
       double f[NC];
 #pragma unroll
@@ -201,6 +202,24 @@ __device__ __forceinline__ void interval_body(const IntervalParams& prm) {
     Res<DA, T> An;
     res_mul(u, A, An);
     A = An;
+  };
+  auto run_steps = [&](auto pulse_c) {
+#pragma unroll 1
+    for (int64_t l0 = l_begin; l0 < l_end; l0 += kAnchor) {
+      step(l0, BoolC<true>{}, pulse_c);
+      const int64_t l1 = l0 + kAnchor < l_end ? l0 + kAnchor : l_end;
+#pragma unroll 1
+      for (int64_t l = l0 + 1; l < l1; ++l) step(l, BoolC<false>{}, pulse_c);
+    }
+  };
+  if constexpr (DA == 2) {
+    // spin-half / analytic spin-one (short, trig-heavy steps): specialised bodies, C4 1.05e11 → 1.24e11 fine steps/s
+    if (field_pulse_possible(fld, prm.dt_out, 0)) run_steps(BoolC<true>{});
+    else run_steps(BoolC<false>{});
+  } else {
+    // 3×3 paths: one body with a run-time anchor test (four specialised copies spill more: C3 −2.5 %, measured)
+#pragma unroll 1
+    for (int64_t l = l_begin; l < l_end; ++l) step(l, RtBool{((l - l_begin) % kAnchor) == 0}, BoolC<true>{});
   }
 
   // Sub-interval split: lane p holds the partial product of its fine steps; combine later·earlier in a shuffle tree

@@ -138,7 +138,7 @@ template <> struct Field<FIELD_CONSTANT> {
   __device__ __forceinline__ void init(const double* p, double) { f0 = p[0]; f1 = p[1]; f2 = p[2]; f3 = p[3]; }
   __device__ __forceinline__ void sample(double, double f[4]) const { f[0] = f0; f[1] = f1; f[2] = f2; f[3] = f3; }
   __device__ __forceinline__ void init_cf4(double, double, double) {}
-  __device__ __forceinline__ void sample_cf4(double, bool, double o1, double o2, double g1[4], double g2[4]) {
+  __device__ __forceinline__ void sample_cf4(double, bool, bool, double o1, double o2, double g1[4], double g2[4]) {
     sample(o1, g1); sample(o2, g2);
   }
 };
@@ -156,7 +156,7 @@ template <> struct Field<FIELD_RABI_LINEAR> {        // ω0 Jz + 2Ω cos(ω0 t) 
     sincos(w0 * g1dt, &s1, &c1); sincos(w0 * g2dt, &s2, &c2);
     ps.init(w0, ph0, dt);
   }
-  __device__ __forceinline__ void sample_cf4(double base, bool anchor, double, double, double g1[4], double g2[4]) {
+  __device__ __forceinline__ void sample_cf4(double base, bool anchor, bool, double, double, double g1[4], double g2[4]) {
     ps.next(base, anchor);
     const double sb = ps.s, cb = ps.c;
     g1[0] = two_om * fma(cb, c1, -sb * s1); g1[1] = 0.0; g1[2] = w0; g1[3] = 0.0;
@@ -179,7 +179,7 @@ template <> struct Field<FIELD_RABI_CIRCULAR> {      // ω0 Jz + Ω(cos(ω0 t) J
     sincos(w0 * g1dt, &s1, &c1); sincos(w0 * g2dt, &s2, &c2);
     ps.init(w0, ph0, dt);
   }
-  __device__ __forceinline__ void sample_cf4(double base, bool anchor, double, double, double g1[4], double g2[4]) {
+  __device__ __forceinline__ void sample_cf4(double base, bool anchor, bool, double, double, double g1[4], double g2[4]) {
     ps.next(base, anchor);
     const double sb = ps.s, cb = ps.c;
     g1[0] = om * fma(cb, c1, -sb * s1); g1[1] = om * fma(sb, c1, cb * s1); g1[2] = w0; g1[3] = 0.0;
@@ -190,6 +190,14 @@ template <> struct Field<FIELD_RABI_CIRCULAR> {      // ω0 Jz + Ω(cos(ω0 t) J
 template <> struct Field<FIELD_NEURAL> {
   // p = [ω_bias, ω_rf, Ω, Ω_p, ω_sig, t_p, ω_q] (reading R16)
   double wb, wrf, two_om, op, ws, wq, ph0, dtk, c1, s1, c2, s2;
+  // Can a sample of this interval fall inside the signal pulse's single cycle (sinp ≠ 0)?  x = ω_sig(t_k − t_p + off)
+  // is monotone in off ∈ [0, Δt]; the margin covers the rounding of the per-sample arguments.  Intervals outside
+  // the window take the pulse-free step body (no per-sample window test).
+  __device__ __forceinline__ bool pulse_possible(double dt_out) const {
+    const double x0 = ws * dtk, x1 = ws * (dtk + dt_out);
+    const double lo = fmin(x0, x1), hi = fmax(x0, x1), m = 1e-12 * (fabs(x0) + fabs(x1)) + 1e-300;
+    return !(hi < -m || lo > kTwoPi1 + m);
+  }
   __device__ __forceinline__ void init(const double* p, double t_k) {
     wb = p[0]; wrf = p[1]; two_om = 2.0 * p[2]; op = p[3]; ws = p[4]; wq = p[6];
     ph0 = reduce_phase(p[1], t_k);
@@ -211,11 +219,11 @@ template <> struct Field<FIELD_NEURAL> {
     sincos(wrf * g1dt, &s1, &c1); sincos(wrf * g2dt, &s2, &c2);
     ps.init(wrf, ph0, dt);
   }
-  __device__ __forceinline__ void sample_cf4(double base, bool anchor, double o1, double o2, double g1[4], double g2[4]) {
+  __device__ __forceinline__ void sample_cf4(double base, bool anchor, bool pulse, double o1, double o2, double g1[4], double g2[4]) {
     ps.next(base, anchor);                         // e^{i ω_rf (t_k + base)}, reduced
     const double sb = ps.s, cb = ps.c;
-    g1[0] = two_om * fma(cb, c1, -sb * s1); g1[1] = 0.0; g1[2] = pulse_z(o1); g1[3] = wq;
-    g2[0] = two_om * fma(cb, c2, -sb * s2); g2[1] = 0.0; g2[2] = pulse_z(o2); g2[3] = wq;
+    g1[0] = two_om * fma(cb, c1, -sb * s1); g1[1] = 0.0; g1[2] = pulse ? pulse_z(o1) : wb; g1[3] = wq;
+    g2[0] = two_om * fma(cb, c2, -sb * s2); g2[1] = 0.0; g2[2] = pulse ? pulse_z(o2) : wb; g2[3] = wq;
   }
 };
 
@@ -224,7 +232,7 @@ template <> struct Field<FIELD_GRADIENT> {          // ω_z = x − 2y
   __device__ __forceinline__ void init(const double* p, double) { wz = fma(-2.0, p[1], p[0]); }
   __device__ __forceinline__ void sample(double, double f[4]) const { f[0] = 0.0; f[1] = 0.0; f[2] = wz; f[3] = 0.0; }
   __device__ __forceinline__ void init_cf4(double, double, double) {}
-  __device__ __forceinline__ void sample_cf4(double, bool, double o1, double o2, double g1[4], double g2[4]) {
+  __device__ __forceinline__ void sample_cf4(double, bool, bool, double o1, double o2, double g1[4], double g2[4]) {
     sample(o1, g1); sample(o2, g2);
   }
 };
@@ -241,7 +249,7 @@ template <> struct Field<FIELD_SU3_CONSTANT> {      // p = all 8 coefficients
     for (int j = 0; j < 8; ++j) f[j] = c[j];
   }
   __device__ __forceinline__ void init_cf4(double, double, double) {}
-  __device__ __forceinline__ void sample_cf4(double, bool, double o1, double o2, double g1[8], double g2[8]) {
+  __device__ __forceinline__ void sample_cf4(double, bool, bool, double o1, double o2, double g1[8], double g2[8]) {
     sample(o1, g1); sample(o2, g2);
   }
 };
@@ -269,7 +277,7 @@ template <> struct Field<FIELD_SU3_DRIVE> {
     sincos(wd * g1dt, &s1, &c1); sincos(wd * g2dt, &s2, &c2);
     ps.init(wd, ph0, dt);
   }
-  __device__ __forceinline__ void sample_cf4(double base, bool anchor, double, double, double g1[8], double g2[8]) {
+  __device__ __forceinline__ void sample_cf4(double base, bool anchor, bool, double, double, double g1[8], double g2[8]) {
     ps.next(base, anchor);
     const double sb = ps.s, cb = ps.c;
     fill(fma(cb, c1, -sb * s1), fma(sb, c1, cb * s1), g1);
@@ -290,6 +298,15 @@ template <int NC> __device__ __forceinline__ void rotate_quadrupoles(double* f, 
     f[7] = fma(c, v2, -s * v1);
   }
 }
+
+// Only the neural field has a pulse window (pulse_possible above); every other field's step body is pulse-free.
+template <class F> __device__ __forceinline__ auto field_pulse_possible(const F& f, double dt_out, int)
+    -> decltype(f.pulse_possible(dt_out)) { return f.pulse_possible(dt_out); }
+template <class F> __device__ __forceinline__ bool field_pulse_possible(const F&, double, long) { return false; }
+
+// Compile-time booleans for the interval kernel's specialised step bodies (no <type_traits> under NVRTC).
+template <bool B> struct BoolC { static constexpr bool value = B; };
+struct RtBool { bool value; };
 
 // Rotating frame (reading R6): rotate (ωx, ωy) by θ = ω_r·t_local, shift ωz by −ω_r; ωq unchanged.
 template <int NC = 4> __device__ __forceinline__ void to_rotating_frame(double* f, double t_local, double omega_r) {
