@@ -47,12 +47,13 @@ def algorithmic_flops_per_fine_step(spin: str, expo: str, tau: int, method: str 
     spin-one Lie–Trotter: residual squaring on the complex-symmetric leapfrog factor T₀ (6 unique entries) = 99 flop
     × τ per exponential, residual product b + a(I + b) = 219 (3×3) per exponential; field, frame, T − I construction
     and phases are not counted (a lower bound; ncu's executed count is in profiles/r01/).
-    spin-half: per CF4 step 2 × (SU(2) series 26 + SU(2)-parametrised residual product 36) + CF4 weights 32 + two
-    field samples 16 + frame rotation 26 + phase steppers 12 + grid 2 = 212 (ncu executes 211.7 per step).
+    spin-half: per CF4 step 2 × (SU(2) series 26 + SU(2)-parametrised residual product 36) = 124 plus the weights,
+    field samples, frame rotation, phase steppers and grid — 193 in total, the ncu-executed count (2·DFMA + DMUL +
+    DADD per step, profiles/r01/s2_final/flops_c4.csv after DESIGN.md §5 items 10, 12 and the folded weights).
     general spin-one (lie_trotter_su3, readings R19/R20): dense residual squaring res_square3 = 159 flop (93 FP64
     instructions) × τ, residual product 219; the T − I assembly (≈ 3 % of the step) is not counted.
     spin-one analytic (reading R14): accumulated in SU(2) form and mapped by D¹ once per interval (DESIGN.md §5
-    item 11), so its fine step is the spin-half step: 212."""
+    item 11), so its fine step is the spin-half step: 193."""
     n_exp = 2 if method == "cf4" else 1
     if spin == "one" and expo == "analytic":
         spin = "half"
@@ -60,7 +61,7 @@ def algorithmic_flops_per_fine_step(spin: str, expo: str, tau: int, method: str 
         prod = 219
         per_exp = {"lie_trotter": 99 * tau, "lie_trotter_su3": 159 * tau}.get(expo, 0)
         return n_exp * (per_exp + prod)
-    return 212 if method == "cf4" else 106
+    return 193 if method == "cf4" else 97
 
 
 def dense_equivalent_flops_per_fine_step(spin: str, expo: str, tau: int, method: str = "cf4") -> int:

@@ -135,6 +135,8 @@ ssb::IntervalParams make_params(const ss_sim* s, double t0, double dt_out, doubl
   p.g2dt = ssb::kG2 * dt;
   p.half_dt = 0.5 * dt;
   p.half_dt_out = 0.5 * dt_out;
+  p.wpd = ssb::kWPlus * dt;
+  p.wmd = ssb::kWMinus * dt;
   p.L = L;
   p.k_begin = k_begin;
   p.k_count = k_count;

@@ -22,6 +22,7 @@ struct IntervalParams {
   double g1dt, g2dt;  // fl(g1·δt), fl(g2·δt)
   double half_dt;     // fl(0.5·δt)
   double half_dt_out; // fl(0.5·Δt)
+  double wpd, wmd;    // fl(w±·δt): the CF4 weights with δt folded in (read from the parameter bank, no UMOV)
   int64_t L;
   int64_t k_begin, k_count, batch;
   int64_t n_threads;  // batch·k_count
@@ -110,12 +111,12 @@ __device__ __forceinline__ void interval_body(const IntervalParams& prm) {
       // a few extra spill slots outside the squaring loops, +70 % on trig-bound spin-half)
       fld.sample_cf4(base, ANCHOR, PULSE, __dadd_rn(base, prm.g1dt), __dadd_rn(base, prm.g2dt), f1, f2);
       if (prm.frame) frame2.apply<NC>(base, ANCHOR, f1, f2);
-      // a4: H̄1 δt = (w+ f1 + w− f2) δt, H̄2 δt = (w− f1 + w+ f2) δt (Eqs. cf4_sample_1/2).
+      // a4: H̄1 δt = (w+ f1 + w− f2) δt, H̄2 δt = (w− f1 + w+ f2) δt (Eqs. cf4_sample_1/2), δt folded into w±.
       T a1[NC], a2[NC];
 #pragma unroll
       for (int j = 0; j < NC; ++j) {
-        a1[j] = (T)(fma(kWPlus, f1[j], kWMinus * f2[j]) * prm.dt);
-        a2[j] = (T)(fma(kWMinus, f1[j], kWPlus * f2[j]) * prm.dt);
+        a1[j] = (T)fma(prm.wpd, f1[j], prm.wmd * f2[j]);
+        a2[j] = (T)fma(prm.wmd, f1[j], prm.wpd * f2[j]);
       }
       if constexpr (SPIN == SPIN_ONE && EXPO == EXP_LIE_TROTTER && sizeof(T) == 4) {
         // FP32 mode: both exponentials' symmetric squarings in lockstep, packed one per float2 lane (FFMA2)
