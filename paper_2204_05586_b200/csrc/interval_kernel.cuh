@@ -48,6 +48,10 @@ template <int SPIN, int EXPO, typename T> constexpr int kIntervalMinBlocks() {
   return EXPO == EXP_LIE_TROTTER_SU3 ? SS_INTERVAL_MINBLOCKS_SU3 : SS_INTERVAL_MINBLOCKS;
 }
 
+#ifndef SS_STEP_UNROLL
+#define SS_STEP_UNROLL 1    // unroll of the rotated-phase steps between anchors (SU(2)-form paths; tuning knob)
+#endif
+
 template <int NC, int F>
 __device__ __forceinline__ void sample_in_frame(const Field<F>& fld, double off, double omega_r, int frame,
                                                 double* f) {
@@ -209,7 +213,7 @@ __device__ __forceinline__ void interval_body(const IntervalParams& prm) {
     for (int64_t l0 = l_begin; l0 < l_end; l0 += kAnchor) {
       step(l0, BoolC<true>{}, pulse_c);
       const int64_t l1 = l0 + kAnchor < l_end ? l0 + kAnchor : l_end;
-#pragma unroll 1
+      SS_UNROLL(SS_STEP_UNROLL)
       for (int64_t l = l0 + 1; l < l1; ++l) step(l, BoolC<false>{}, pulse_c);
     }
   };
