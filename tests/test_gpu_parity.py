@@ -327,3 +327,22 @@ def test_cuda_graph_capture_replay(ss):
         g.replay()
     torch.cuda.synchronize()
     assert torch.equal(states, ref.state) and torch.equal(U, ref.time_evolution)
+
+
+@pytest.mark.parametrize("spin,expo", [("half", "analytic"), ("one", "analytic"), ("one", "lie_trotter")])
+def test_pulse_window_edges_parity(ss, orc, spin, expo):
+    """The specialised pulse-free step body (DESIGN.md §5 item 12) is taken only for intervals that provably miss the
+    sinp cycle: put the window's start and end exactly on interval boundaries, on fine-step boundaries and between
+    the two Gauss points of a step, over many sweeps, and compare element by element with the oracle."""
+    dt_out, L = 1e-6, 8
+    dt = dt_out / L
+    ws = 2 * np.pi / (5 * dt_out)                         # one sinp cycle = 5 intervals
+    t_ps = [10 * dt_out, 10 * dt_out + dt, 10 * dt_out + 0.5 * dt, 10 * dt_out + 0.2113 * dt,
+            10 * dt_out - 1e-15, 13 * dt_out + 3 * dt, 12.5 * dt_out]
+    rows = [W.neural_params(omega_bias=2 * np.pi * 7e5, omega_dress=2 * np.pi * 20e3, omega_pulse=2 * np.pi * 30e3,
+                            omega_sig=ws, t_p=tp, omega_q=(2 * np.pi * 72 if expo == "lie_trotter" else 0.0))
+            for tp in t_ps]
+    d = 2 if spin == "half" else 3
+    w = W.Workload("pulse_edges", spin, "cf4", expo, 24, True, "neural", 0.0, 24 * dt_out, dt, dt_out,
+                   np.stack(rows), W.random_states(len(rows), d, seed=41))
+    assert_parity(ss, orc, w)
