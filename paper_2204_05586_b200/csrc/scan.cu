@@ -963,7 +963,10 @@ __global__ void __launch_bounds__(Scan3Cfg<D>::NT, 1)
 #endif
 constexpr int kChainThreads = SS_CHAIN_THREADS;
 constexpr int64_t kChainMinBatch = 4096;
-template <int D> struct ChainCfg { static constexpr int CH = 8; };
+#ifndef SS_CHAIN_CH
+#define SS_CHAIN_CH 8
+#endif
+template <int D> struct ChainCfg { static constexpr int CH = SS_CHAIN_CH; };
 // Per-lane slot: 2 stages of CH operators, stride padded to an odd number of 16-byte words so the 32 lanes' LDS.128
 // at the same offset hit distinct banks (an unpadded stride is a multiple of 128 B: a 32-way conflict).
 template <int D> __host__ __device__ constexpr int chain_slot_stride() { return (2 * ChainCfg<D>::CH * D * D) | 1; }
