@@ -125,8 +125,39 @@ int plan_grid(double t0, double t1, double dt_int, double dt_out, int64_t* K, in
   return SS_OK;
 }
 
+// Sub-interval split (DESIGN.md §5 item 8): S = 1, 2, 4, … ≤ 32 adjacent lanes share an interval (S | L), each
+// running L/S fine steps.  S minimises the modelled time ⌈n·S/R⌉ · (L/S + c0 + c1·log2 S): n intervals, R resident
+// threads (SMs × resident blocks × 128), c0 the per-thread setup and c1 the per-level combine cost in fine steps
+// (short SU(2)-form steps: 2.5 / 0.17; 3×3 Lie–Trotter steps: 0.15 / 0.03).  n is the WHOLE problem (batch × K of
+// the grid), never the launched part, so partitions and host-API chunks pick the same S and reproduce the same
+// operators bit for bit.  C4 (1e6 intervals × 1000 steps): S = 4, 14 → 53 rounds of a quarter the length (−4.5 %).
+#ifndef SS_FORCE_SPLIT
+#define SS_FORCE_SPLIT 0    // tuning experiments only: a fixed S (must divide L)
+#endif
+int choose_split(const ss_sim* s, int64_t n_total, int64_t L) {
+  if (SS_FORCE_SPLIT > 0 && L % SS_FORCE_SPLIT == 0) return SS_FORCE_SPLIT;
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) !=
+                                                   cudaSuccess || sms <= 0)
+      sms = 148;
+  }
+  const bool su3 = s->d.exponentiation == SS_EXP_LIE_TROTTER_SU3;
+  const bool short_steps = s->dim == 2 || s->d.exponentiation == SS_EXP_ANALYTIC;
+  const double R = (double)sms * (su3 ? SS_INTERVAL_MINBLOCKS_SU3 : SS_INTERVAL_MINBLOCKS) * ssb::kIntervalThreads;
+  const double c0 = short_steps ? 2.5 : 0.15, c1 = short_steps ? 0.17 : 0.03;
+  int best = 1;
+  double best_t = 0.0;
+  for (int S = 1, lev = 0; S <= 32 && L % S == 0; S *= 2, ++lev) {
+    const double t = std::ceil((double)n_total * S / R) * ((double)L / S + c0 + c1 * lev);
+    if (S == 1 || t < best_t * 0.995) { best = S; best_t = t; }
+  }
+  return best;
+}
+
 ssb::IntervalParams make_params(const ss_sim* s, double t0, double dt_out, double dt, int64_t L, int64_t k_begin,
-                                int64_t k_count, int64_t batch, const double* sweep, double* U) {
+                                int64_t k_count, int64_t batch, const double* sweep, double* U, int64_t n_total) {
   ssb::IntervalParams p;
   p.t0 = t0;
   p.dt_out = dt_out;
@@ -144,15 +175,7 @@ ssb::IntervalParams make_params(const ss_sim* s, double t0, double dt_out, doubl
   p.n_threads = batch * k_count;
   p.tau = s->d.trotter_cutoff;
   p.frame = s->d.use_rotating_frame;
-  // Sub-interval split: when batch·K intervals fill fewer than ~2 waves of resident threads
-  // (148 SMs × 512), let S = 2, 4, … adjacent lanes share an interval.  S divides L (no ragged lanes in a warp) and
-  // S ≤ 32.  C3-sized batches keep S = 1.
-  {
-    const int64_t target = (int64_t)2 * 148 * 512;
-    int S = 1;
-    while (S < 32 && L % (2 * S) == 0 && p.n_threads * S < target) S *= 2;
-    p.split = S;
-  }
+  p.split = choose_split(s, n_total, L);
   p.sweep = sweep;
   p.unitaries = U;
   return p;
@@ -339,7 +362,7 @@ int ss_compute_unitaries(ss_sim* s, double t0, double t1, double dt_int, double 
                 (long long)(k_begin + k_count), (long long)K);
   if ((rc = check_device_ptr(d_sweep, "d_sweep")) || (rc = check_device_ptr(d_U, "d_unitaries"))) return rc;
   if ((rc = ensure_device())) return rc;
-  const auto p = make_params(s, t0, dt_out, dt, L, k_begin, k_count, batch, d_sweep, d_U);
+  const auto p = make_params(s, t0, dt_out, dt, L, k_begin, k_count, batch, d_sweep, d_U, batch * K);
   return launch_interval_checked(s, p, static_cast<cudaStream_t>(stream));
 }
 
@@ -435,7 +458,7 @@ int ss_evaluate(ss_sim* s, double t0, double t1, double dt_int, double dt_out, i
   void* scan_ws = w + 256;
   double* U = d_U ? d_U : reinterpret_cast<double*>(w + 256 + align256(ssb::scan_workspace_bytes(s->dim, batch, K)));
   if (s->validate && (rc = validate_inputs(s, batch, d_sweep, d_psi0, reinterpret_cast<int*>(w), st))) return rc;
-  const auto p = make_params(s, t0, dt_out, dt, L, 0, K, batch, d_sweep, U);
+  const auto p = make_params(s, t0, dt_out, dt, L, 0, K, batch, d_sweep, U, batch * K);
   if ((rc = launch_interval_checked(s, p, st))) return rc;
   return ss_scan_states(s->dim, batch, K, U, d_psi0, d_states, scan_ws, need - 256, stream);
 }
@@ -553,7 +576,7 @@ int ss_evaluate_host(ss_sim* s, double t0, double t1, double dt_int, double dt_o
     if ((e = cudaMemcpyAsync(d_sweep, h_sweep + b0 * s->P, sizeof(double) * s->P * cb, cudaMemcpyHostToDevice, cs)) ||
         (e = cudaMemcpyAsync(d_psi0, h_psi0 + b0 * 2 * D, sizeof(double) * 2 * D * cb, cudaMemcpyHostToDevice, cs)))
       return cuda_fail(e, "H2D copy");
-    const auto p = make_params(s, t0, dt_out, dt, L, 0, K, cb, d_sweep, d_U);
+    const auto p = make_params(s, t0, dt_out, dt, L, 0, K, cb, d_sweep, d_U, batch * K);   // S of the whole batch
     if ((rc = launch_interval_checked(s, p, cs))) return rc;
     int n = 0;
     if ((e = ssb::launch_scan(D, cb, K, d_U, d_psi0, d_states, d_scan, cs, &n)) != cudaSuccess)
