@@ -1,6 +1,6 @@
 # session-2 evidence: all GPU tests, smoke, bench lines, reference arm, torchrun, launch list, ncu captures + counters
 export PATH=/usr/local/cuda/bin:$PATH
-O=gpurun_out/s2f
+O=${OUT:-gpurun_out/s2f}
 mkdir -p $O
 timeout 1200 python -m pytest tests -m gpu -q 2>&1 | tail -3 > $O/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1
@@ -11,6 +11,8 @@ timeout 300 python bench.py --workload C5 --no-e2e --no-cpu-baseline 2>&1 | tail
 timeout 300 python bench.py --workload C5 --precision fp32 --no-e2e --no-cpu-baseline 2>&1 | tail -1 > $O/bench_c5_lt_fp32.jsonl
 timeout 300 python bench.py --workload C5 --expo analytic --no-e2e --no-cpu-baseline 2>&1 | tail -1 > $O/bench_c5_an_fp64.jsonl
 timeout 300 python bench.py --workload G1 --no-e2e --no-cpu-baseline 2>&1 | tail -1 > $O/bench_g1.jsonl
+timeout 300 python bench.py --workload C5 --expo analytic --precision fp32 --no-e2e --no-cpu-baseline 2>&1 | tail -1 > $O/bench_c5_an_fp32.jsonl
+timeout 300 python bench.py --workload G1 --precision fp32 --no-e2e --no-cpu-baseline 2>&1 | tail -1 > $O/bench_g1_fp32.jsonl
 timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29513 bench.py --gpus 1 --steps 3 --no-cpu-baseline 2>&1 | tail -1 > $O/bench_torchrun1.jsonl
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 2>&1 | tail -1 > $O/bench_reference.jsonl
 timeout 400 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c3.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-probe > /dev/null 2>&1
