@@ -33,7 +33,10 @@ struct IntervalParams {
   double* unitaries;    // [batch][k_count][D][D] complex128
 };
 
-constexpr int kIntervalThreads = 128;
+#ifndef SS_INTERVAL_THREADS
+#define SS_INTERVAL_THREADS 128
+#endif
+constexpr int kIntervalThreads = SS_INTERVAL_THREADS;
 // Resident blocks per SM requested from ptxas: 16 warps/SM (128 registers) without spills for every instance.
 #ifndef SS_INTERVAL_MINBLOCKS
 #define SS_INTERVAL_MINBLOCKS 4
