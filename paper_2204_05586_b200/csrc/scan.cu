@@ -962,6 +962,9 @@ __global__ void __launch_bounds__(Scan3Cfg<D>::NT, 1)
 #define SS_CHAIN_THREADS 64
 #endif
 constexpr int kChainThreads = SS_CHAIN_THREADS;
+#ifndef SS_CHAIN_FULL_CTAS
+#define SS_CHAIN_FULL_CTAS 0   // 1: the round-1 launch (kChainThreads sweeps per CTA), for comparison
+#endif
 constexpr int64_t kChainMinBatch = 4096;
 #ifndef SS_CHAIN_CH
 #define SS_CHAIN_CH 8
@@ -978,6 +981,7 @@ struct ChainArgs {
   const double2* psi0;
   double2* states;   // [batch][K+1][D] or NULL
   double* spin;      // [batch][K+1][3] or NULL (⟨J⟩ fused into the write-out)
+  int spc;           // sweeps per CTA (≤ kChainThreads): spreads the batch over every SM
 };
 
 template <int D>
@@ -986,8 +990,8 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(const ChainArgs a)
   extern __shared__ __align__(128) double2 smem3[];
   __shared__ __align__(8) uint64_t sBar[kChainThreads / 32][2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t b = (int64_t)blockIdx.x * kChainThreads + tid;
-  const bool valid = b < a.batch;
+  const int64_t b = (int64_t)blockIdx.x * a.spc + tid;
+  const bool valid = tid < a.spc && b < a.batch;
   double2* slot[2] = {smem3 + (size_t)tid * chain_slot_stride<D>(), smem3 + (size_t)tid * chain_slot_stride<D>() + CH * D * D};
   if (lane == 0) {
     mbar_init(&sBar[warp][0], 32);
@@ -1077,9 +1081,21 @@ static cudaError_t run_chain(int64_t batch, int64_t k_count, const double* U, co
     if (e != cudaSuccess) return e;
     attr = true;
   }
+  // Sweeps per CTA: at most kChainThreads, and few enough that the CTAs cover every SM (8192 sweeps: 56 per CTA on
+  // 147 CTAs instead of 64 on 128 — the per-SM TMA/L1 path, not HBM, limited the 128-CTA launch).
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) !=
+                                                   cudaSuccess || sms <= 0)
+      sms = 148;
+  }
+  int spc = (int)std::min<int64_t>(kChainThreads, (batch + sms - 1) / sms);
+  if (SS_CHAIN_FULL_CTAS) spc = kChainThreads;
+  if (spc < 1) spc = 1;
   ChainArgs a{batch, k_count, reinterpret_cast<const double2*>(U), reinterpret_cast<const double2*>(psi0),
-              reinterpret_cast<double2*>(states), spin};
-  chain_kernel<D><<<(unsigned)((batch + kChainThreads - 1) / kChainThreads), kChainThreads, smem, s>>>(a);
+              reinterpret_cast<double2*>(states), spin, spc};
+  chain_kernel<D><<<(unsigned)((batch + spc - 1) / spc), kChainThreads, smem, s>>>(a);
   ++*launches;
   return cudaGetLastError();
 }
