@@ -967,7 +967,7 @@ constexpr int kChainThreads = SS_CHAIN_THREADS;
 #endif
 constexpr int64_t kChainMinBatch = 4096;
 #ifndef SS_CHAIN_CH
-#define SS_CHAIN_CH 8
+#define SS_CHAIN_CH 12   // operators per bulk copy: 4 / 8 / 12 → 2.9 / 5.2 / 5.4 TB/s on C3 (14 exceeds shared memory)
 #endif
 template <int D> struct ChainCfg { static constexpr int CH = SS_CHAIN_CH; };
 // Per-lane slot: 2 stages of CH operators, stride padded to an odd number of 16-byte words so the 32 lanes' LDS.128
