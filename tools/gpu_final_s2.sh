@@ -6,7 +6,7 @@ timeout 1200 python -m pytest tests -m gpu -q 2>&1 | tail -3 > $O/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1
 timeout 900 python bench.py 2>&1 | tail -1 > $O/bench_default.jsonl
 timeout 300 python bench.py --workload C4 2>&1 | tail -1 > $O/bench_c4.jsonl
-timeout 300 python bench.py --workload C2 --no-e2e --no-cpu-baseline 2>&1 | tail -1 > $O/bench_c2.jsonl
+timeout 300 python bench.py --workload C2 --no-cpu-baseline 2>&1 | tail -1 > $O/bench_c2.jsonl
 timeout 300 python bench.py --workload C5 --no-e2e --no-cpu-baseline 2>&1 | tail -1 > $O/bench_c5_lt_fp64.jsonl
 timeout 300 python bench.py --workload C5 --precision fp32 --no-e2e --no-cpu-baseline 2>&1 | tail -1 > $O/bench_c5_lt_fp32.jsonl
 timeout 300 python bench.py --workload C5 --expo analytic --no-e2e --no-cpu-baseline 2>&1 | tail -1 > $O/bench_c5_an_fp64.jsonl
