@@ -83,6 +83,19 @@ def ncu_traffic(kernel: str, workload: str, full_size: bool):
     return e["bytes"] if e else None
 
 
+def hbm_peak_gbs():
+    """HBM roofline denominator: MEASURED_PEAKS.json's STREAM-style copy (driver-written), else the profiling guide's
+    fallback 6.65 TB/s (B200_PROFILING.md) — returned with which one it is."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        v = float(d["hbm_gbs"])
+        if v > 0:
+            return v, "of measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, ValueError, KeyError, TypeError):
+        pass
+    return 6650.0, "of fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
 def scan_bytes_per_interval(dim: int) -> int:
     return (2 * dim * dim + 2 * dim) * 8       # read U_k, write ψ_{k+1}
 
@@ -403,7 +416,8 @@ def run_ours(args, rank, world, local):
                          "measured_dfma_peak_tflops": measured_peak,
                          "frac_at_observed_clock": (achieved / (peak * clocks["sm_mhz"] / SM_MAX_MHZ)
                                                     if clocks.get("sm_mhz") else None)},
-            "scan": {"bound": "hbm", "achieved": scan_gbs, "unit": "GB/s", "ms_per_launch": t_scan,
+            "scan": {"bound": "hbm", "achieved": scan_gbs, "unit": "GB/s", "peak": hbm_peak_gbs()[0],
+                     "frac": scan_gbs / hbm_peak_gbs()[0], "peak_basis": hbm_peak_gbs()[1], "ms_per_launch": t_scan,
                      "bytes_per_launch": B * K * scan_bytes_per_interval(D)},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
             "fine_steps_per_step": total_steps,
