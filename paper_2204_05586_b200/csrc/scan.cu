@@ -14,6 +14,7 @@
 //      shared memory (coalesced).
 // HBM traffic per interval: read U_k (2·dim² doubles) + write ψ_{k+1} (2·dim doubles) — 192 B (spin-one) /
 // 96 B (spin-half): the kernel is HBM bound.
+#include <cooperative_groups.h>
 #include <cuda/atomic>
 
 #include <algorithm>
@@ -952,6 +953,147 @@ __global__ void __launch_bounds__(Scan3Cfg<D>::NT, 1)
   bulk_wait_all();
 }
 
+// ---- small problems: one cooperative wave with two grid-wide barriers instead of look-back -------------------------
+//
+// For problems whose operators fit in L2 (B·K·dim²·16 B ≤ 64 MB) and with few sweeps (C1, C2, C4's 1e6-interval
+// sweep), the tile scan's decoupled look-back is latency-bound: every tile of one sweep runs in the same wave, so the
+// last tile multiplies ~all predecessor aggregates (C2: 30 µs for 19 MB).  Here each sweep gets `cps` CTAs, CTA c owns
+// a contiguous interval range and thread i of it a contiguous sub-range:
+//   1. P_i = product of thread i's operators (HBM → L2), block Kogge–Stone → exclusive prefixes X_i, CTA aggregate G_c;
+//   2. grid barrier; every CTA multiplies the ≤ cps − 1 aggregates of its sweep's predecessors (128 per round, one
+//      ordered tree per round) into ψ_in = G_{c−1} ⋯ G_{first} ψ0;
+//   3. y = X_i ψ_in, then thread i re-reads its operators (L2) and writes its states.
+// All CTAs are co-resident (cooperative launch), so the barrier cannot deadlock.
+struct CoopArgs {
+  int64_t batch, k_count;
+  int cps;                 // CTAs per sweep
+  const double2* U;
+  const double2* psi0;
+  double2* states;         // or NULL
+  double* spin;            // or NULL
+  double2* agg;            // [grid][D·D] CTA aggregates (workspace)
+};
+
+template <int D>
+__global__ void __launch_bounds__(128) scan_coop_kernel(const CoopArgs a) {
+  namespace cg = cooperative_groups;
+  constexpr int NT = 128, NW = NT / 32;
+  __shared__ double2 sWarpTot[NW][D * D];
+  __shared__ double2 sPsiIn[D];
+  __shared__ double2 sM[D * D];
+  const int c = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t K = a.k_count;
+  const int64_t b = c / a.cps;
+  const int part = c - (int)b * a.cps;
+  const bool has = b < a.batch;
+  const int64_t per = (K + a.cps - 1) / a.cps;
+  const int64_t k0 = has ? min((int64_t)part * per, K) : 0, k1 = has ? min(k0 + per, K) : 0;
+  const int64_t m = (k1 - k0 + NT - 1) / NT;
+  const int64_t t0 = min(k0 + (int64_t)tid * m, k1), t1 = min(t0 + m, k1);
+  const double2* gU = a.U + (size_t)(has ? b : 0) * K * D * D;
+  // 1. thread product and block exclusive scan
+  CM<D> P;
+  cm_eye(P);
+  // unrolled so several operators' loads are in flight per thread (the products are a dependent chain)
+#pragma unroll 4
+  for (int64_t k = t0; k < t1; ++k) {
+    CM<D> u;
+    cm_load(gU + (size_t)k * D * D, u);
+    P = cm_mul(u, P);
+  }
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const CM<D> o = cm_shfl_up(P, off);
+    if (lane >= off) P = cm_mul(P, o);
+  }
+  CM<D> X = cm_shfl_up(P, 1);
+  if (lane == 0) cm_eye(X);
+  if (lane == 31) cm_store(sWarpTot[warp], P);
+  __syncthreads();
+  {
+    CM<D> W, T;
+    cm_eye(W);
+    for (int w = 0; w < warp; ++w) { cm_load(sWarpTot[w], T); W = cm_mul(T, W); }
+    X = cm_mul(X, W);
+    if (tid == 0) {
+      CM<D> tot;
+      cm_eye(tot);
+      for (int w = 0; w < NW; ++w) { cm_load(sWarpTot[w], T); tot = cm_mul(T, tot); }
+      cm_store(a.agg + (size_t)c * D * D, tot);
+      cm_eye(tot);
+      cm_store(sM, tot);
+    }
+  }
+  cg::this_grid().sync();
+  // 2. ψ_in: ordered product of the predecessors' aggregates (latest first), NT per round
+  for (int q0 = part - 1; q0 >= 0; q0 -= NT) {
+    const int q = q0 - tid;                                  // thread t holds G_{q0 − t} (later on the left)
+    CM<D> Ag;
+    if (q >= 0) cm_load_cg(a.agg + (size_t)(c - part + q) * D * D, Ag); else cm_eye(Ag);
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const CM<D> o = cm_shfl_down(Ag, off);
+      if ((lane & (2 * off - 1)) == 0) Ag = cm_mul(Ag, o);
+    }
+    __syncthreads();                                         // sWarpTot reuse
+    if (lane == 0) cm_store(sWarpTot[warp], Ag);
+    __syncthreads();
+    if (tid == 0) {
+      CM<D> M, T;
+      cm_load(sM, M);
+      for (int w = 0; w < NW; ++w) { cm_load(sWarpTot[w], T); M = cm_mul(M, T); }
+      cm_store(sM, M);
+    }
+  }
+  __syncthreads();
+  if (tid == 0 && has) {
+    CM<D> M;
+    cm_load(sM, M);
+    double xr[D], xi[D], yr[D], yi[D];
+    for (int d = 0; d < D; ++d) { xr[d] = a.psi0[b * D + d].x; xi[d] = a.psi0[b * D + d].y; }
+    cm_apply(M, xr, xi, yr, yi);
+    for (int d = 0; d < D; ++d) sPsiIn[d] = make_double2(yr[d], yi[d]);
+    if (part == 0) {
+      if (a.states)
+        for (int d = 0; d < D; ++d) a.states[(size_t)b * (K + 1) * D + d] = make_double2(xr[d], xi[d]);
+      if (a.spin) {
+        double jj3[3];
+        spin_of<D>(xr, xi, jj3);
+        for (int e = 0; e < 3; ++e) a.spin[(size_t)b * (K + 1) * 3 + e] = jj3[e];
+      }
+    }
+  }
+  __syncthreads();
+  if (!has) return;
+  // 3. states of this thread's intervals
+  double yr[D], yi[D];
+  {
+    double xr[D], xi[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) { xr[d] = sPsiIn[d].x; xi[d] = sPsiIn[d].y; }
+    cm_apply(X, xr, xi, yr, yi);
+  }
+  double2* gS = a.states ? a.states + (size_t)b * (K + 1) * D : nullptr;
+  double* gJ = a.spin ? a.spin + (size_t)b * (K + 1) * 3 : nullptr;
+#pragma unroll 4
+  for (int64_t k = t0; k < t1; ++k) {
+    CM<D> u;
+    cm_load(gU + (size_t)k * D * D, u);
+    double zr[D], zi[D];
+    cm_apply(u, yr, yi, zr, zi);
+#pragma unroll
+    for (int d = 0; d < D; ++d) { yr[d] = zr[d]; yi[d] = zi[d]; }
+    if (gS)
+#pragma unroll
+      for (int d = 0; d < D; ++d) __stcs(gS + (k + 1) * D + d, make_double2(zr[d], zi[d]));
+    if (gJ) {
+      double jj3[3];
+      spin_of<D>(zr, zi, jj3);
+      for (int e = 0; e < 3; ++e) __stcs(gJ + (k + 1) * 3 + e, jj3[e]);
+    }
+  }
+}
+
 // ---- state chain for large batches: one thread per sweep, TMA-streamed ------------------------------------------
 //
 // With batch ≥ kChainMinBatch the sweeps alone give enough parallelism to saturate HBM, so each thread runs its own
@@ -962,6 +1104,12 @@ __global__ void __launch_bounds__(Scan3Cfg<D>::NT, 1)
 #define SS_CHAIN_THREADS 64
 #endif
 constexpr int kChainThreads = SS_CHAIN_THREADS;
+#ifndef SS_SCAN_COOP
+#define SS_SCAN_COOP 1         // 0: small problems keep the round-1 tile scan (comparison builds)
+#endif
+#ifndef SS_COOP_MAXCPS
+#define SS_COOP_MAXCPS 128     // CTAs per sweep of the cooperative scan (one predecessor round)
+#endif
 #ifndef SS_CHAIN_FULL_CTAS
 #define SS_CHAIN_FULL_CTAS 0   // 1: the round-1 launch (kChainThreads sweeps per CTA), for comparison
 #endif
@@ -1180,9 +1328,42 @@ __global__ void validate_kernel(int64_t n_sweep, const double* sweep, int P, int
 // ---- host launchers -------------------------------------------------------------------------------------------
 template <int D> size_t scan_ws_bytes(int64_t batch, int64_t k_count) { return ScanLayout<D>(batch, k_count).total; }
 
+constexpr int kCoopMaxGrid = 1024;
 size_t scan_workspace_bytes(int dim, int64_t batch, int64_t k_count) {
-  return dim == 2 ? std::max(Scan2Layout<2>(batch, k_count).total, Scan3Layout<2>(batch, k_count, 1).total)
-                  : std::max(Scan2Layout<3>(batch, k_count).total, Scan3Layout<3>(batch, k_count, 1).total);
+  const size_t coop = sizeof(double2) * (size_t)dim * dim * kCoopMaxGrid;
+  return std::max(coop, dim == 2 ? std::max(Scan2Layout<2>(batch, k_count).total, Scan3Layout<2>(batch, k_count, 1).total)
+                                 : std::max(Scan2Layout<3>(batch, k_count).total, Scan3Layout<3>(batch, k_count, 1).total));
+}
+
+// Cooperative small-problem scan (scan_coop_kernel): returns cudaErrorNotSupported when the problem is not eligible.
+template <int D>
+static cudaError_t run_scan_coop(int64_t batch, int64_t k_count, const double* U, const double* psi0, double* states,
+                                 double* spin, void* ws, cudaStream_t s, int* launches) {
+  static int max_grid = -1;
+  if (max_grid < 0) {
+    int dev = 0, sms = 0, per_sm = 0, coop = 0;
+    max_grid = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev) == cudaSuccess && coop &&
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scan_coop_kernel<D>, 128, 0) == cudaSuccess)
+      max_grid = std::min(kCoopMaxGrid, sms * std::max(per_sm, 0));
+  }
+  const double bytes = (double)batch * (double)k_count * D * D * sizeof(double2);
+  if (SS_SCAN_COOP == 0 || max_grid < 2 || batch * 2 > max_grid || bytes > 64.0 * (1 << 20))
+    return cudaErrorNotSupported;
+  // CTAs per sweep: fill the resident grid, but keep ≥ 256 intervals per CTA
+  // (measured: C2's 1e5 intervals prefer 128 CTAs — one predecessor round — C4's 1e6 prefer 256: shorter thread chains)
+  const int64_t cap = (k_count > (int64_t)SS_COOP_MAXCPS * 4096) ? 2 * SS_COOP_MAXCPS : SS_COOP_MAXCPS;
+  int cps = (int)std::min<int64_t>(std::min<int64_t>(max_grid / batch, cap), (k_count + 255) / 256);
+  if (cps < 1) cps = 1;
+  CoopArgs a{batch, k_count, cps, reinterpret_cast<const double2*>(U), reinterpret_cast<const double2*>(psi0),
+             reinterpret_cast<double2*>(states), spin, static_cast<double2*>(ws)};
+  void* args[] = {&a};
+  const cudaError_t e = cudaLaunchCooperativeKernel((const void*)scan_coop_kernel<D>, dim3((unsigned)(batch * cps)),
+                                                    dim3(128), args, 0, s);
+  if (e == cudaSuccess) ++*launches;
+  return e;
 }
 
 size_t aggregate_workspace_bytes(int dim, int64_t batch, int64_t k_count) {
@@ -1371,6 +1552,11 @@ static cudaError_t run_scan3(int64_t batch, int64_t k_count, const double* U, co
 
 cudaError_t launch_scan(int dim, int64_t batch, int64_t k_count, const double* U, const double* psi0, double* states,
                         void* ws, cudaStream_t s, int* launches, double* spin) {
+  {
+    const cudaError_t e = dim == 2 ? run_scan_coop<2>(batch, k_count, U, psi0, states, spin, ws, s, launches)
+                                   : run_scan_coop<3>(batch, k_count, U, psi0, states, spin, ws, s, launches);
+    if (e != cudaErrorNotSupported) return e;
+  }
   // scan3 amortises its look-back over big tiles; below ~4 stages per tile (small problems) scan2's single pass wins
   if (SS_SCAN_VERSION == 3 && batch < kChainMinBatch &&
       (dim == 2 ? scan3_nst<2>(batch, k_count, scan3_grid<2>()) : scan3_nst<3>(batch, k_count, scan3_grid<3>())) >= 4)
