@@ -267,9 +267,12 @@ def test_host_api_matches_device_api(ss):
         assert np.array_equal(st_h, st_d) and np.array_equal(U_h, U_d)
 
 
-def test_partition_reproduces_unitaries_bitwise(ss):
-    """The time grid uses the global k, so computing a sub-range reproduces those U_k bit for bit."""
-    w = W.c4_long(duration=1e-3)
+@pytest.mark.parametrize("which", ["C4", "C2", "G1"])
+def test_partition_reproduces_unitaries_bitwise(ss, which):
+    """The time grid uses the global k (and the sub-interval split is chosen from the whole problem), so computing a
+    sub-range reproduces those U_k bit for bit — for the SU(2)-form, Lie–Trotter and general spin-one kernels."""
+    w = {"C4": lambda: W.c4_long(duration=1e-3), "C2": lambda: W.c2_neural(duration=1e-3),
+         "G1": lambda: W.g1_su3(batch=3, duration=1e-3)}[which]()
     sim = ss.Simulator(w.spin, w.method, w.expo, w.tau, w.frame, "fp64", w.field)
     sweep = torch.from_numpy(w.sweep).cuda()
     full = sim.compute_unitaries(sweep, w.t0, w.t1, w.dt_int, w.dt_out)
