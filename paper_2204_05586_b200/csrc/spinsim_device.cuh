@@ -442,37 +442,6 @@ template <typename T> __device__ __forceinline__ Res<3, T> res_shfl_down(const R
   return r;
 }
 
-// a ← (a + 2I)·a, i.e. (I+a)² − I.  3 adds + 18 mul + 90 fma for D = 3.
-template <int D, typename T> __device__ __forceinline__ void res_square(Res<D, T>& a) {
-  T d[D];
-#pragma unroll
-  for (int i = 0; i < D; ++i) d[i] = a.re[i * D + i] + T(2);
-  Res<D, T> s;
-#pragma unroll
-  for (int i = 0; i < D; ++i)
-#pragma unroll
-    for (int j = 0; j < D; ++j) {
-      T r = T(0), m = T(0);
-#pragma unroll
-      for (int k = 0; k < D; ++k) {
-        const T br = (k == i) ? d[i] : a.re[i * D + k];
-        const T bi = a.im[i * D + k];
-        if (k == 0) {
-          r = br * a.re[k * D + j];
-          m = br * a.im[k * D + j];
-        } else {
-          r = fmaT(br, a.re[k * D + j], r);
-          m = fmaT(br, a.im[k * D + j], m);
-        }
-        r = fmaT(-bi, a.im[k * D + j], r);
-        m = fmaT(bi, a.re[k * D + j], m);
-      }
-      s.re[i * D + j] = r;
-      s.im[i * D + j] = m;
-    }
-  a = s;
-}
-
 // ---- exponentiators: residual of exp(−i(ax Jx + ay Jy + az Jz + aq Q)) -----------------------------------------
 
 // Spin-half closed form: exp(−i a·σ/2) = cos(r/2) I − i (sin(r/2)/r) a·σ.  cos(r/2) − 1 = −2 sin²(r/4).
