@@ -223,6 +223,17 @@ def dist_setup(n_gpus: int):
     return rank, world, local
 
 
+def cpu_model() -> str:
+    """Host CPU model (state the core count and CPU model beside the CPU baseline)."""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_oracle_sample(w: W.Workload, target_s: float):
     """Time the oracle (double instantiation, all host cores) on a bounded sample of workload w: sweeps strided
     across the batch, each over its first k_end intervals, sized from a calibration run to ≈ target_s seconds."""
@@ -270,7 +281,8 @@ def run_reference(args, rank, world):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
             "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": config_of(w, args, world),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
+                             "cpu": cpu_model()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -394,7 +406,7 @@ def run_ours(args, rank, world, local):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         run, n_sw, k_end, cores = cpu_oracle_sample(w, target_s=args.cpu_seconds)
         dt, n = run(n_sw, k_end)
-        cpu = {"value": n / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+        cpu = {"value": n / dt, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu": cpu_model(),
                "sample": f"{n_sw} of {B} sweeps x first {k_end} of {K} intervals x L={L} = {n} fine steps, "
                          f"oracle<double>, std::thread x {cores}, {dt:.1f} s"}
 
