@@ -187,6 +187,15 @@ int ss_compose_carry(int32_t dim, int64_t batch, int32_t n_parts, int32_t part, 
 int ss_num_coefficients(const ss_sim* sim);
 int ss_exponentiate(const ss_sim* sim, int64_t n, const double* d_args, double* d_out, void* stream);
 
+/* Advisory Magnus-convergence diagnostic ("∫‖H‖₂ < ξ ≈ 1.08686870"; never blocks execution): for every fine
+ * step the two-point Gauss–Legendre estimate δt·(‖H(t₁)‖₂ + ‖H(t₂)‖₂)/2 of ∫‖H‖₂ over the step, on the CF4 sample
+ * times and in the frame the simulator integrates in, with the exact spectral norm; d_out[b] (device, [batch]
+ * float64) = the maximum over the steps of sweep b.  Convergence is indicated by d_out[b] < SS_MAGNUS_XI.  Built-in
+ * fields only (SS_ERR_UNSUPPORTED for user fields). */
+#define SS_MAGNUS_XI 1.08686870
+int ss_magnus_bound(ss_sim* sim, double time_start, double time_end, double time_step_integration,
+                    double time_step_output, int64_t batch, const double* d_sweep, double* d_out, void* stream);
+
 /* Expected spin projection ⟨J⟩ = (ψ†Jxψ, ψ†Jyψ, ψ†Jzψ) for d_states [n][dim] complex128;
  * writes d_out [n][3] float64. */
 int ss_spin_projection(int32_t spin, int64_t n, const double* d_states, double* d_out, void* stream);

@@ -70,6 +70,8 @@ def _load():
     lib.oracle_chain.argtypes = [i, ll, ll, P, P, P, P]
     lib.oracle_spin_projection.argtypes = [i, ll, P, P]
     lib.oracle_rms_error.argtypes = [ll, i, P, P]
+    lib.oracle_magnus_bound.argtypes = [i, i, i, d, d, d, d, ll, P, P]
+    lib.oracle_spectral_norm.argtypes = [i, P, P]
     lib.oracle_rms_error.restype = d
     _lib = lib
     return lib
@@ -232,3 +234,26 @@ def rms_error(a, b) -> float:
     b = _c128(b)
     assert a.shape == b.shape
     return _load().oracle_rms_error(a.shape[0], a.shape[1], _ptr(a), _ptr(b))
+
+
+MAGNUS_XI = 1.08686870
+
+
+def magnus_bound(spin, frame, field, *, sweep, t0, t1, dt_int, dt_out) -> np.ndarray:
+    """Per sweep: max over fine steps of δt·(‖H(t₁)‖₂ + ‖H(t₂)‖₂)/2 in the integration frame (P:304 diagnostic)."""
+    sw = _f64(sweep).reshape(-1, num_params(field))
+    out = np.zeros(sw.shape[0])
+    rc = _load().oracle_magnus_bound(SPIN[spin], int(frame), FIELD[field], t0, t1, dt_int, dt_out, sw.shape[0],
+                                     _ptr(sw), _ptr(out))
+    if rc != 0:
+        raise ValueError("oracle_magnus_bound rejected its arguments")
+    return out
+
+
+def spectral_norm(spin, f) -> float:
+    """‖Σ f_j A_j‖₂ for 8 coefficients (spin-half uses the first three)."""
+    f8 = np.zeros(8)
+    f8[: len(f)] = f
+    out = np.zeros(1)
+    _load().oracle_spectral_norm(SPIN[spin], _ptr(f8), _ptr(out))
+    return float(out[0])

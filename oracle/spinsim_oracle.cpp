@@ -458,6 +458,90 @@ template <class R> Mat<R> interval_operator(const Config& c, const Grid& g, cons
   return U;
 }
 
+// ------------------------------------------------------------------------------------------------
+// Advisory Magnus-convergence diagnostic (the Magnus series of a step converges if ∫‖H‖₂ < ξ ≈ 1.08686870).
+// Per fine step: δt·(‖H(t₁)‖₂ + ‖H(t₂)‖₂)/2, the two-point Gauss–Legendre estimate of ∫‖H‖₂ on the CF4 sample times,
+// with H the field in the integration frame; the result is the maximum over the sweep.  H is assembled as the
+// dense matrix Σ f_j A_j from the operator DEFINITIONS (spin-half: σ/2; spin-one: Jx, Jy, Jz, Q and the quadrupoles
+// U1 = Jx² − Jy², U2 = {Jx, Jy}, V1 = {Jx, Jz}, V2 = {Jy, Jz} of reading R19, multiplied out here), and ‖H‖₂ is the
+// largest |eigenvalue|, from the roots of the characteristic polynomial.
+// ------------------------------------------------------------------------------------------------
+template <class R> Mat<R> dense_hamiltonian(int spin, const R f[NF]) {
+  const Cx<R> I(0, 1);
+  if (spin == HALF) {
+    Mat<R> h = Mat<R>::zero(2);
+    h.a[0][0] = f[2] / R(2);                 h.a[1][1] = -f[2] / R(2);
+    h.a[0][1] = Cx<R>(f[0], -f[1]) / R(2);   h.a[1][0] = Cx<R>(f[0], f[1]) / R(2);
+    return h;
+  }
+  const R s = R(1) / std::sqrt(R(2));
+  Mat<R> Jx = Mat<R>::zero(3), Jy = Mat<R>::zero(3), Jz = Mat<R>::zero(3), Q = Mat<R>::zero(3);
+  Jx.a[0][1] = Jx.a[1][0] = Jx.a[1][2] = Jx.a[2][1] = s;
+  Jy.a[0][1] = -I * s; Jy.a[1][0] = I * s; Jy.a[1][2] = -I * s; Jy.a[2][1] = I * s;
+  Jz.a[0][0] = R(1); Jz.a[2][2] = R(-1);
+  Q.a[0][0] = R(1) / R(3); Q.a[1][1] = R(-2) / R(3); Q.a[2][2] = R(1) / R(3);
+  auto anti = [](const Mat<R>& x, const Mat<R>& y) {       // x y + y x
+    Mat<R> a = mul(x, y), b = mul(y, x);
+    for (int i = 0; i < 3; ++i) for (int j = 0; j < 3; ++j) a.a[i][j] += b.a[i][j];
+    return a;
+  };
+  Mat<R> U1 = mul(Jx, Jx), Jy2 = mul(Jy, Jy);
+  for (int i = 0; i < 3; ++i) for (int j = 0; j < 3; ++j) U1.a[i][j] -= Jy2.a[i][j];
+  const Mat<R> U2 = anti(Jx, Jy), V1 = anti(Jx, Jz), V2 = anti(Jy, Jz);
+  const Mat<R>* A[NF] = {&Jx, &Jy, &Jz, &Q, &U1, &U2, &V1, &V2};
+  Mat<R> h = Mat<R>::zero(3);
+  for (int j = 0; j < NF; ++j)
+    for (int r = 0; r < 3; ++r) for (int c = 0; c < 3; ++c) h.a[r][c] += f[j] * A[j]->a[r][c];
+  return h;
+}
+
+template <class R> R spectral_norm(const Mat<R>& h) {
+  if (h.n == 2) {   // λ = (tr ± √(tr² − 4 det))/2 (real for Hermitian h)
+    const R tr = (h.a[0][0] + h.a[1][1]).real();
+    const R det = (h.a[0][0] * h.a[1][1] - h.a[0][1] * h.a[1][0]).real();
+    const R disc = std::sqrt(std::max(R(0), tr * tr - R(4) * det));
+    return std::max(std::fabs((tr + disc) / R(2)), std::fabs((tr - disc) / R(2)));
+  }
+  // λ = μ + tr/3 with μ the roots of μ³ − pμ − q, B = h − (tr/3)I, p = tr(B²)/2, q = det B (trigonometric form)
+  const R m = (h.a[0][0] + h.a[1][1] + h.a[2][2]).real() / R(3);
+  Mat<R> B = h;
+  for (int i = 0; i < 3; ++i) B.a[i][i] -= m;
+  const Mat<R> B2 = mul(B, B);
+  const R p = (B2.a[0][0] + B2.a[1][1] + B2.a[2][2]).real() / R(2);
+  const R q = (B.a[0][0] * (B.a[1][1] * B.a[2][2] - B.a[1][2] * B.a[2][1]) -
+               B.a[0][1] * (B.a[1][0] * B.a[2][2] - B.a[1][2] * B.a[2][0]) +
+               B.a[0][2] * (B.a[1][0] * B.a[2][1] - B.a[1][1] * B.a[2][0])).real();
+  if (!(p > R(0))) return std::fabs(m);
+  const R r = R(2) * std::sqrt(p / R(3));
+  const R c = std::min(R(1), std::max(R(-1), (R(3) * q / (R(2) * p)) * std::sqrt(R(3) / p)));
+  const R phi = std::acos(c) / R(3), two_pi_3 = R(2) * std::acos(R(-1)) / R(3);
+  R best = 0;
+  for (int k = 0; k < 3; ++k) best = std::max(best, std::fabs(r * std::cos(phi - two_pi_3 * k) + m));
+  return best;
+}
+
+template <class R> R magnus_bound(const Config& c, const Grid& g, const double* p) {
+  R worst = 0;
+  for (long long k = 0; k < g.K; ++k) {
+    const double t_k = grid_tk(g, k);
+    R omega_r = 0;
+    if (c.frame) {
+      R f[NF];
+      field_sample<R>(c.field, p, t_k, 0.5 * g.dt_out, f);
+      omega_r = f[2];
+    }
+    for (long long l = 0; l < g.L; ++l) {
+      R f1[NF], f2[NF];
+      sample_in_frame<R>(c, p, t_k, grid_off(g, l, gauss_g1()), omega_r, f1);
+      sample_in_frame<R>(c, p, t_k, grid_off(g, l, gauss_g2()), omega_r, f2);
+      const R n = (R)g.dt_int * (spectral_norm(dense_hamiltonian<R>(c.spin, f1)) +
+                                 spectral_norm(dense_hamiltonian<R>(c.spin, f2))) / R(2);
+      worst = std::max(worst, n);
+    }
+  }
+  return worst;
+}
+
 // Validation and planning: K = (t1−t0)/Δt and L = Δt/δt must be integral (reading R10).
 inline int plan(double t0, double t1, double dt_int, double dt_out, long long* K, long long* L, double* dt) {
   if (!(t1 > t0) || !(dt_int > 0) || !(dt_out > 0)) return -1;
@@ -719,6 +803,25 @@ int oracle_spin_projection(int spin, long long n, const double* states, double* 
       out[3 * s + a] = (double)acc.real();
     }
   }
+  return 0;
+}
+
+// Magnus diagnostic per sweep (long double); f_in: [8] field coefficients for a direct spectral-norm query.
+int oracle_magnus_bound(int spin, int frame, int field, double t0, double t1, double dt_int, double dt_out,
+                        long long batch, const double* sweep, double* out) {
+  Config c{spin, CF4, spin == HALF ? ANALYTIC : LIE_TROTTER_SU3, 24, frame, field};
+  if (field_num_params(field) < 0 || (spin != HALF && spin != ONE)) return -1;
+  Grid g{t0, dt_out, 0, 0, 0};
+  if (plan(t0, t1, dt_int, dt_out, &g.K, &g.L, &g.dt_int) != 0) return -1;
+  const int np = field_num_params(field);
+  for (long long b = 0; b < batch; ++b) out[b] = (double)magnus_bound<long double>(c, g, sweep + b * np);
+  return 0;
+}
+
+int oracle_spectral_norm(int spin, const double* f_in, double* out) {
+  long double f[NF];
+  for (int j = 0; j < NF; ++j) f[j] = f_in[j];
+  *out = (double)spectral_norm(dense_hamiltonian<long double>(spin, f));
   return 0;
 }
 

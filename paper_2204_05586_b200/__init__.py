@@ -196,6 +196,18 @@ class Simulator:
                                         _dev_ptr(out, "out"), _stream_ptr(stream)), "ss_exponentiate")
         return out
 
+    def magnus_bound(self, sweep: torch.Tensor, time_start, time_end, time_step_integration, time_step_output,
+                     stream=None) -> torch.Tensor:
+        """Advisory Magnus-convergence diagnostic: per sweep, the largest Gauss–Legendre estimate of ∫‖H‖₂
+        over one fine step (in the integration frame); the expansion converges where it is < SS_MAGNUS_XI."""
+        B = sweep.shape[0]
+        _dev_ptr(sweep, "sweep", torch.float64)
+        out = torch.empty(B, dtype=torch.float64, device=sweep.device)
+        check(self._lib.ss_magnus_bound(self._h, time_start, time_end, time_step_integration, time_step_output, B,
+                                        _dev_ptr(sweep, "sweep"), _dev_ptr(out, "out"), _stream_ptr(stream)),
+              "ss_magnus_bound")
+        return out
+
     def evaluate_host(self, sweep: np.ndarray, time_start, time_end, time_step_integration, time_step_output,
                       state_init: np.ndarray, out_states: np.ndarray | None = None, want_unitaries=False,
                       n_chunks: int = 4):

@@ -16,6 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SPINSIM_LIB") or os.path.join(HERE, "libspinsim_b200.so")
 
 SS_OK, SS_ERR_INVALID, SS_ERR_UNSUPPORTED, SS_ERR_CUDA, SS_ERR_NONFINITE = 0, -1, -2, -3, -4
+SS_MAGNUS_XI = 1.08686870          # Magnus convergence radius
 SPIN = {"half": 1, "one": 2}
 INTEGRATION = {"cf4": 0, "midpoint": 1, "heun": 2}
 EXPONENTIATION = {"analytic": 0, "lie_trotter": 1, "lie_trotter_su3": 2}
@@ -29,7 +30,7 @@ EXPORTS = [
     "ss_set_validation", "ss_compute_unitaries", "ss_scan_workspace_bytes", "ss_scan_states", "ss_scan_states_spin",
     "ss_aggregate_workspace_bytes", "ss_chain_aggregate", "ss_compose_carry", "ss_exponentiate",
     "ss_spin_projection", "ss_evaluate_host", "ss_kernel_launches", "ss_last_error", "ss_version",
-    "ss_num_coefficients",
+    "ss_num_coefficients", "ss_magnus_bound",
 ]
 
 
@@ -83,6 +84,7 @@ def load() -> ctypes.CDLL:
         "ss_last_error": (ctypes.c_char_p, []),
         "ss_version": (ctypes.c_int, []),
         "ss_num_coefficients": (ctypes.c_int, [P]),
+        "ss_magnus_bound": (ctypes.c_int, [P, d, d, d, d, i64, P, P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

@@ -97,6 +97,16 @@ ssb::IntervalLaunchFn pick_interval(const ss_sim_desc& d) {
   return f32 ? ssb::interval_table_one_an_f32(d.integration, d.field) : ssb::interval_table_one_an_f64(d.integration, d.field);
 }
 
+ssb::MagnusLaunchFn pick_magnus(const ss_sim_desc& d) {
+  const bool f32 = d.precision == SS_FP32;
+  if (d.spin == SS_SPIN_HALF) return f32 ? ssb::magnus_table_half_f32(d.field) : ssb::magnus_table_half_f64(d.field);
+  if (d.exponentiation == SS_EXP_LIE_TROTTER)
+    return f32 ? ssb::magnus_table_one_lt_f32(d.field) : ssb::magnus_table_one_lt_f64(d.field);
+  if (d.exponentiation == SS_EXP_LIE_TROTTER_SU3)
+    return f32 ? ssb::magnus_table_one_su3_f32(d.field) : ssb::magnus_table_one_su3_f64(d.field);
+  return f32 ? ssb::magnus_table_one_an_f32(d.field) : ssb::magnus_table_one_an_f64(d.field);
+}
+
 ssb::ExpoLaunchFn pick_expo(const ss_sim_desc& d) {
   const bool f32 = d.precision == SS_FP32;
   if (d.spin == SS_SPIN_HALF) return f32 ? ssb::expo_table_half_f32() : ssb::expo_table_half_f64();
@@ -471,6 +481,29 @@ int ss_exponentiate(const ss_sim* s, int64_t n, const double* d_args, double* d_
   if ((rc = ensure_device())) return rc;
   const cudaError_t e = s->expo(n, d_args, s->d.trotter_cutoff, d_out, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "exponentiate launch");
+  g_launches.fetch_add(1);
+  return SS_OK;
+}
+
+int ss_magnus_bound(ss_sim* s, double t0, double t1, double dt_int, double dt_out, int64_t batch,
+                    const double* d_sweep, double* d_out, void* stream) {
+  if (!s) return fail(SS_ERR_INVALID, "sim is NULL");
+  if (s->user) return fail(SS_ERR_UNSUPPORTED, "the Magnus diagnostic is available for built-in fields only");
+  int64_t K, L;
+  double dt;
+  int rc = plan_grid(t0, t1, dt_int, dt_out, &K, &L, &dt);
+  if (rc) return rc;
+  if (batch < 1) return fail(SS_ERR_INVALID, "batch must be >= 1");
+  if ((rc = check_device_ptr(d_sweep, "d_sweep"))) return rc;
+  if (!d_out || (reinterpret_cast<uintptr_t>(d_out) & 7) != 0) return fail(SS_ERR_INVALID, "d_out must be 8-byte aligned");
+  if ((rc = ensure_device())) return rc;
+  const ssb::MagnusLaunchFn fn = pick_magnus(s->d);
+  if (!fn) return fail(SS_ERR_UNSUPPORTED, "no Magnus diagnostic instance for this combination");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemsetAsync(d_out, 0, sizeof(double) * (size_t)batch, st);
+  if (e != cudaSuccess) return cuda_fail(e, "magnus memset");
+  const auto p = make_params(s, t0, dt_out, dt, L, 0, K, batch, d_sweep, nullptr, batch * K);
+  if ((e = fn(p, d_out, st)) != cudaSuccess) return cuda_fail(e, "magnus launch");
   g_launches.fetch_add(1);
   return SS_OK;
 }

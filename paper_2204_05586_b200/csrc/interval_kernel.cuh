@@ -282,6 +282,77 @@ cudaError_t launch_interval(const IntervalParams& prm, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
+// ---- advisory Magnus-convergence diagnostic --------------------------------------------------
+// The Magnus series of a step converges if ∫‖H‖₂ over it < ξ ≈ 1.08686870.  For every fine step this estimates
+// the integral by the two-point Gauss–Legendre rule on the CF4 sample times, δt·(‖H(t₁)‖₂ + ‖H(t₂)‖₂)/2, in the frame
+// the integrator uses, and out[b] = the maximum over sweep b (atomic max on the non-negative doubles' bit patterns).
+// ‖H‖₂ is exact: |ω|/2 for spin-half; for spin-one the largest |eigenvalue| of the traceless Hermitian 3×3 from the
+// roots of λ³ − pλ − q (p = tr H²/2, q = det H) in trigonometric form.
+template <int SPIN, int NC> __device__ __forceinline__ double spectral_norm(const double* f) {
+  if constexpr (SPIN == SPIN_HALF) {
+    return 0.5 * sqrt(fma(f[0], f[0], fma(f[1], f[1], f[2] * f[2])));
+  } else {
+    const double d0 = f[2] + f[3] * kThird, d1 = -2.0 * f[3] * kThird, d2 = f[3] * kThird - f[2];
+    double ur = 0.0, ui = 0.0, vr = 0.0, vi = 0.0;
+    if constexpr (NC == 8) { ur = f[4]; ui = -f[5]; vr = f[6]; vi = -f[7]; }
+    const double ar = (f[0] + vr) * kRsqrt2, ai = (-f[1] + vi) * kRsqrt2;      // H01
+    const double br = (f[0] - vr) * kRsqrt2, bi = (-f[1] - vi) * kRsqrt2;      // H12
+    const double na = ar * ar + ai * ai, nb = br * br + bi * bi, ng = ur * ur + ui * ui;   // |H01|², |H12|², |H02|²
+    const double p = 0.5 * (d0 * d0 + d1 * d1 + d2 * d2) + na + nb + ng;
+    // det H = d0 d1 d2 + 2 Re(H01 H12 conj(H02)) − d0|H12|² − d1|H02|² − d2|H01|²
+    const double pr = ar * br - ai * bi, pim = ar * bi + ai * br;
+    const double q = d0 * d1 * d2 + 2.0 * (pr * ur + pim * ui) - d0 * nb - d1 * ng - d2 * na;
+    if (!(p > 0.0)) return 0.0;
+    const double r = 2.0 * sqrt(p / 3.0);
+    double c = 1.5 * q / p * sqrt(3.0 / p);
+    c = fmin(1.0, fmax(-1.0, c));
+    const double phi = acos(c) / 3.0;
+    const double l0 = r * cos(phi), l2 = r * cos(phi + 2.0943951023931957);   // largest and smallest eigenvalues
+    return fmax(fabs(l0), fabs(l2));
+  }
+}
+
+template <int SPIN, int EXPO, int FIELD>
+__global__ void __launch_bounds__(128) magnus_kernel(const IntervalParams prm, double* out) {
+  constexpr int P = FieldParams<FIELD>::P;
+  constexpr int NC = NumCoeffs<EXPO>::N;
+  const int64_t i = (int64_t)blockIdx.x * 128 + threadIdx.x;
+  if (i >= prm.n_threads) return;
+  const int64_t b = i / prm.k_count;
+  const int64_t k = prm.k_begin + (i - b * prm.k_count);
+  double p[P];
+#pragma unroll
+  for (int j = 0; j < P; ++j) p[j] = __ldg(prm.sweep + b * P + j);
+  const double t_k = __dadd_rn(prm.t0, __dmul_rn((double)k, prm.dt_out));
+  Field<FIELD> fld;
+  fld.init(p, t_k);
+  double omega_r = 0.0;
+  if (prm.frame) {
+    double f[8];
+    fld.sample(prm.half_dt_out, f);
+    omega_r = f[2];
+  }
+  double m = 0.0;
+  for (int64_t l = 0; l < prm.L; ++l) {
+    const double base = __dmul_rn((double)l, prm.dt);
+    double f1[8] = {0, 0, 0, 0, 0, 0, 0, 0}, f2[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    sample_in_frame<NC>(fld, __dadd_rn(base, prm.g1dt), omega_r, prm.frame, f1);
+    sample_in_frame<NC>(fld, __dadd_rn(base, prm.g2dt), omega_r, prm.frame, f2);
+    m = fmax(m, 0.5 * prm.dt * (spectral_norm<SPIN, NC>(f1) + spectral_norm<SPIN, NC>(f2)));
+  }
+  atomicMax(reinterpret_cast<unsigned long long*>(out) + b, (unsigned long long)__double_as_longlong(m));
+}
+
+#ifndef __CUDACC_RTC__
+template <int SPIN, int EXPO, int FIELD>
+cudaError_t launch_magnus(const IntervalParams& prm, double* out, cudaStream_t stream) {
+  const int64_t blocks = (prm.n_threads + 127) / 128;
+  if (blocks <= 0) return cudaSuccess;
+  magnus_kernel<SPIN, EXPO, FIELD><<<(unsigned)blocks, 128, 0, stream>>>(prm, out);
+  return cudaGetLastError();
+}
+#endif
+
 // Small kernel for element-wise parity of the exponentiators (ss_exponentiate).
 template <int SPIN, int EXPO, typename T>
 __global__ void exponentiate_kernel(int64_t n, const double* args, int tau, double* out) {

@@ -47,6 +47,11 @@ MUTANTS = {
     "su3_y_conj": ("Y.a[2][0] = std::conj(h02);", "Y.a[2][0] = h02;"),
     # two-photon drive at ω_d instead of 2ω_d
     "su3_drive_2w": ("f[4] = (R)p[4] * std::cos(R(2) * ph);", "f[4] = (R)p[4] * std::cos(ph);"),
+    # --- Magnus diagnostic ---
+    # coarse instead of fine step in the ∫‖H‖ estimate
+    "magnus_dt": ("const R n = (R)g.dt_int * (spectral_norm", "const R n = (R)g.dt_out * (spectral_norm"),
+    # wrong angle in the trigonometric cubic roots
+    "spectral_root": ("const R phi = std::acos(c) / R(3),", "const R phi = std::acos(c) / R(2),"),
 }
 
 

@@ -212,3 +212,56 @@ def test_su3_drive_detuned_fourth_order(orc):
     r = [a / b for a, b in zip(errs, errs[1:])]
     assert all(10 <= x <= 24 for x in r), (errs, r)
     assert errs[-1] > 1e-11
+
+
+# ---- Magnus-convergence diagnostic ------------------------------------------------------------
+def test_spectral_norm_vs_eigvalsh(orc):
+    """‖H‖₂ of the oracle's dense Hamiltonian (assembled from the operator definitions) = max |eigvalsh| of the
+    test's own H8 (spin-one) / σ/2 (spin-half), over random coefficients."""
+    rng = np.random.default_rng(51)
+    for _ in range(300):
+        f = rng.standard_normal(8) * rng.choice([1e-3, 1.0, 1e4])
+        ref = np.abs(np.linalg.eigvalsh(H8(f))).max()
+        assert abs(orc.spectral_norm("one", f) - ref) <= 1e-12 * ref
+        h2 = 0.5 * (f[0] * np.array([[0, 1], [1, 0]]) + f[1] * np.array([[0, -1j], [1j, 0]])
+                    + f[2] * np.diag([1.0, -1.0]))
+        ref2 = np.abs(np.linalg.eigvalsh(h2)).max()
+        assert abs(orc.spectral_norm("half", f[:3]) - ref2) <= 1e-12 * ref2
+
+
+def test_magnus_bound_spec_examples(orc):
+    """S:161-169 examples: field-norm bound × δt against ξ = 1.08686870.  Constant spin-half field with
+    ‖H‖₂ = |ω|/2 = 2π·1e6 rad/s, frame off: 0.628 at δt = 100 ns (converges), 1.257 at 200 ns (does not)."""
+    w = 2 * 2 * np.pi * 1e6
+    for dt, conv in ((1e-7, True), (2e-7, False)):
+        mb = orc.magnus_bound("half", False, "constant", sweep=[[w, 0, 0, 0]], t0=0.0, t1=4e-6, dt_int=dt,
+                              dt_out=4e-7)[0]
+        assert mb == pytest.approx(np.pi * 2e6 * dt, rel=1e-15)
+        assert (mb < orc.MAGNUS_XI) == conv
+    # the frame removes the bias: a pure z field has zero in-frame norm; the quadratic shift keeps 2|ωq|/3
+    mb = orc.magnus_bound("one", True, "constant", sweep=[[0, 0, 4.4e6, 3e3]], t0=0.0, t1=2e-6, dt_int=1e-7,
+                          dt_out=1e-6)[0]
+    assert mb == pytest.approx(2 / 3 * 3e3 * 1e-7, rel=1e-12)
+
+
+def test_magnus_bound_is_max_gauss_estimate(orc):
+    """Brute force: the diagnostic equals the maximum over steps of the Gauss–Legendre estimate rebuilt here from the
+    oracle's field samples, frame rotation and numpy eigenvalues."""
+    w = W.g1_su3(batch=2, duration=4e-6)
+    p = w.sweep[1]
+    g1, g2 = orc.constants()["g1"], orc.constants()["g2"]
+    dt = w.dt_int
+    worst = 0.0
+    for k in range(w.K):
+        t_k = k * w.dt_out
+        wr = orc.field_sample("su3_drive", p, t_k, 0.5 * w.dt_out)[2]
+        for l in range(w.L):
+            n = []
+            for g in (g1, g2):
+                off = l * dt + g * dt
+                f = orc.rotating_frame(orc.field_sample("su3_drive", p, t_k, off), off, wr)
+                n.append(np.abs(np.linalg.eigvalsh(H8(f))).max())
+            worst = max(worst, dt * (n[0] + n[1]) / 2)
+    got = orc.magnus_bound("one", True, "su3_drive", sweep=w.sweep, t0=w.t0, t1=w.t1, dt_int=w.dt_int,
+                           dt_out=w.dt_out)[1]
+    assert got == pytest.approx(worst, rel=1e-9)
