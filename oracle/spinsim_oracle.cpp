@@ -433,15 +433,18 @@ template <class R> Mat<R> fine_step(const Config& c, const Grid& g, const double
 // ------------------------------------------------------------------------------------------------
 // Interval operator U_k (§parallelization; Fig. architecture; frame P:539-545).
 // ------------------------------------------------------------------------------------------------
+// Frame rate of interval k: ω_r = ω_z(t_k + Δt/2) from the lab field, 0 with the frame off.
+template <class R> R frame_omega(const Config& c, const Grid& g, const double* p, double t_k) {
+  if (!c.frame) return R(0);
+  R f[NF];
+  field_sample<R>(c.field, p, t_k, 0.5 * g.dt_out, f);
+  return f[2];
+}
+
 template <class R> Mat<R> interval_operator(const Config& c, const Grid& g, const double* p, long long k) {
   const int dim = (c.spin == HALF) ? 2 : 3;
   const double t_k = grid_tk(g, k);
-  R omega_r = 0;
-  if (c.frame) {                                 // ω_r = ω_z(t_{k} + Δt/2) from the lab field
-    R f[NF];
-    field_sample<R>(c.field, p, t_k, 0.5 * g.dt_out, f);
-    omega_r = f[2];
-  }
+  const R omega_r = frame_omega<R>(c, g, p, t_k);
   Mat<R> U = Mat<R>::eye(dim);                   // U_r initialised to the identity
   for (long long l = 0; l < g.L; ++l) {
     const Mat<R> u = fine_step<R>(c, g, p, t_k, l, omega_r);
@@ -524,12 +527,7 @@ template <class R> R magnus_bound(const Config& c, const Grid& g, const double* 
   R worst = 0;
   for (long long k = 0; k < g.K; ++k) {
     const double t_k = grid_tk(g, k);
-    R omega_r = 0;
-    if (c.frame) {
-      R f[NF];
-      field_sample<R>(c.field, p, t_k, 0.5 * g.dt_out, f);
-      omega_r = f[2];
-    }
+    const R omega_r = frame_omega<R>(c, g, p, t_k);
     for (long long l = 0; l < g.L; ++l) {
       R f1[NF], f2[NF];
       sample_in_frame<R>(c, p, t_k, grid_off(g, l, gauss_g1()), omega_r, f1);
