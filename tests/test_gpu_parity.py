@@ -349,3 +349,32 @@ def test_pulse_window_edges_parity(ss, orc, spin, expo):
     w = W.Workload("pulse_edges", spin, "cf4", expo, 24, True, "neural", 0.0, 24 * dt_out, dt, dt_out,
                    np.stack(rows), W.random_states(len(rows), d, seed=41))
     assert_parity(ss, orc, w)
+
+
+# ---- degenerate and minimal problems -------------------------------------------------------------------------------
+@pytest.mark.parametrize("spin,expo,field,nc", [("half", "analytic", "constant", 4), ("one", "lie_trotter", "constant", 4),
+                                                ("one", "analytic", "constant", 4),
+                                                ("one", "lie_trotter_su3", "su3_constant", 8)])
+@pytest.mark.parametrize("frame", [True, False])
+def test_zero_field_is_identity(ss, spin, expo, field, nc, frame):
+    """H ≡ 0: every exponential, product and frame factor is exactly the identity, so ψ_k = ψ0 bit for bit and every
+    U_k is exactly I (any stray term in a residual formula would show)."""
+    d = 2 if spin == "half" else 3
+    w = W.Workload("zero", spin, "cf4", expo, 24, frame, field, 0.0, 7e-6, 0.5e-6, 1e-6, np.zeros((3, nc)),
+                   W.random_states(3, d, seed=61))
+    st, U = gpu_run(ss, w)
+    assert np.array_equal(U, np.broadcast_to(np.eye(d, dtype=complex), U.shape))
+    assert np.array_equal(st, np.broadcast_to(w.psi0[:, None, :], st.shape))
+
+
+@pytest.mark.parametrize("spin,expo", [("half", "analytic"), ("one", "lie_trotter"), ("one", "analytic"),
+                                       ("one", "lie_trotter_su3")])
+@pytest.mark.parametrize("K,L", [(1, 1), (1, 1000), (3, 1)])
+def test_minimal_grids_parity(ss, orc, spin, expo, K, L):
+    """Smallest grids (one interval, one fine step; one interval of 1000 steps — the widest sub-interval split)
+    through every exponentiator, against the oracle."""
+    d = 2 if spin == "half" else 3
+    p = W.neural_params(t_p=0.0, omega_q=(0.0 if expo == "analytic" else W.OMEGA_Q))
+    w = W.Workload("min", spin, "cf4", expo, 24, True, "neural", 0.0, K * 1e-6, 1e-6 / L, 1e-6, p[None, :],
+                   W.random_states(1, d, seed=62))
+    assert_parity(ss, orc, w)
