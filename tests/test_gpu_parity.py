@@ -212,9 +212,11 @@ def _fast_unitaries(B, K, d, seed):
                                         (2, 1, 1300001, True),          # nst = 4, ragged last tile
                                         (2, 7, 300000, False),          # several sweeps, j-major look-back
                                         (3, 1, 4096 * 592, True),       # tiles of 4096, all full
-                                        (3, 3, 700001, False)])         # nst = 8, ragged, several sweeps
+                                        (3, 3, 700001, False),          # nst = 8, ragged, several sweeps
+                                        (3, 1, 600001, True)])          # > 64 MB, < 4 stages per tile: scan2
 def test_scan_large_single_sweep_path(ss, orc, d, B, K, spin):
-    """Sizes that select the super-tile scan (scan3: tensor-TMA stage boxes, one look-back per tile) against the
+    """Sizes that select the super-tile scan (scan3: tensor-TMA stage boxes, one look-back per tile) — and, last, the
+    round-1 tile scan (scan2), which the cooperative scan left to single sweeps past the L2-sized bound — against the
     oracle's sequential long-double chain, element by element; with the fused ⟨J⟩ where `spin`."""
     U = _fast_unitaries(B, K, d, seed=K + B)
     psi0 = W.random_states(B, d, seed=33)
