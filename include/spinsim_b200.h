@@ -190,8 +190,8 @@ int ss_exponentiate(const ss_sim* sim, int64_t n, const double* d_args, double* 
 /* Advisory Magnus-convergence diagnostic ("∫‖H‖₂ < ξ ≈ 1.08686870"; never blocks execution): for every fine
  * step the two-point Gauss–Legendre estimate δt·(‖H(t₁)‖₂ + ‖H(t₂)‖₂)/2 of ∫‖H‖₂ over the step, on the CF4 sample
  * times and in the frame the simulator integrates in, with the exact spectral norm; d_out[b] (device, [batch]
- * float64) = the maximum over the steps of sweep b.  Convergence is indicated by d_out[b] < SS_MAGNUS_XI.  Built-in
- * fields only (SS_ERR_UNSUPPORTED for user fields). */
+ * float64) = the maximum over the steps of sweep b.  Convergence is indicated by d_out[b] < SS_MAGNUS_XI.  Works for
+ * built-in and user (NVRTC) fields. */
 #define SS_MAGNUS_XI 1.08686870
 int ss_magnus_bound(ss_sim* sim, double time_start, double time_end, double time_step_integration,
                     double time_step_output, int64_t batch, const double* d_sweep, double* d_out, void* stream);

@@ -488,7 +488,6 @@ int ss_exponentiate(const ss_sim* s, int64_t n, const double* d_args, double* d_
 int ss_magnus_bound(ss_sim* s, double t0, double t1, double dt_int, double dt_out, int64_t batch,
                     const double* d_sweep, double* d_out, void* stream) {
   if (!s) return fail(SS_ERR_INVALID, "sim is NULL");
-  if (s->user) return fail(SS_ERR_UNSUPPORTED, "the Magnus diagnostic is available for built-in fields only");
   int64_t K, L;
   double dt;
   int rc = plan_grid(t0, t1, dt_int, dt_out, &K, &L, &dt);
@@ -497,13 +496,14 @@ int ss_magnus_bound(ss_sim* s, double t0, double t1, double dt_int, double dt_ou
   if ((rc = check_device_ptr(d_sweep, "d_sweep"))) return rc;
   if (!d_out || (reinterpret_cast<uintptr_t>(d_out) & 7) != 0) return fail(SS_ERR_INVALID, "d_out must be 8-byte aligned");
   if ((rc = ensure_device())) return rc;
-  const ssb::MagnusLaunchFn fn = pick_magnus(s->d);
-  if (!fn) return fail(SS_ERR_UNSUPPORTED, "no Magnus diagnostic instance for this combination");
+  const ssb::MagnusLaunchFn fn = s->user ? nullptr : pick_magnus(s->d);
+  if (!s->user && !fn) return fail(SS_ERR_UNSUPPORTED, "no Magnus diagnostic instance for this combination");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t e = cudaMemsetAsync(d_out, 0, sizeof(double) * (size_t)batch, st);
   if (e != cudaSuccess) return cuda_fail(e, "magnus memset");
   const auto p = make_params(s, t0, dt_out, dt, L, 0, K, batch, d_sweep, nullptr, batch * K);
-  if ((e = fn(p, d_out, st)) != cudaSuccess) return cuda_fail(e, "magnus launch");
+  e = s->user ? ssb::launch_user_magnus(s->user_kernel, p, d_out, st) : fn(p, d_out, st);
+  if (e != cudaSuccess) return cuda_fail(e, "magnus launch");
   g_launches.fetch_add(1);
   return SS_OK;
 }

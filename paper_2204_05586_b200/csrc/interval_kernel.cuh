@@ -281,6 +281,7 @@ cudaError_t launch_interval(const IntervalParams& prm, cudaStream_t stream) {
   interval_kernel<SPIN, EXPO, METHOD, FIELD, T><<<(unsigned)blocks, kIntervalThreads, 0, stream>>>(prm);
   return cudaGetLastError();
 }
+#endif  // !__CUDACC_RTC__
 
 // ---- advisory Magnus-convergence diagnostic --------------------------------------------------
 // The Magnus series of a step converges if ∫‖H‖₂ over it < ξ ≈ 1.08686870.  For every fine step this estimates
@@ -313,7 +314,7 @@ template <int SPIN, int NC> __device__ __forceinline__ double spectral_norm(cons
 }
 
 template <int SPIN, int EXPO, int FIELD>
-__global__ void __launch_bounds__(128) magnus_kernel(const IntervalParams prm, double* out) {
+__device__ __forceinline__ void magnus_body(const IntervalParams& prm, double* out) {
   constexpr int P = FieldParams<FIELD>::P;
   constexpr int NC = NumCoeffs<EXPO>::N;
   const int64_t i = (int64_t)blockIdx.x * 128 + threadIdx.x;
@@ -343,6 +344,11 @@ __global__ void __launch_bounds__(128) magnus_kernel(const IntervalParams prm, d
   atomicMax(reinterpret_cast<unsigned long long*>(out) + b, (unsigned long long)__double_as_longlong(m));
 }
 
+template <int SPIN, int EXPO, int FIELD>
+__global__ void __launch_bounds__(128) magnus_kernel(const IntervalParams prm, double* out) {
+  magnus_body<SPIN, EXPO, FIELD>(prm, out);
+}
+
 #ifndef __CUDACC_RTC__
 template <int SPIN, int EXPO, int FIELD>
 cudaError_t launch_magnus(const IntervalParams& prm, double* out, cudaStream_t stream) {
@@ -353,6 +359,7 @@ cudaError_t launch_magnus(const IntervalParams& prm, double* out, cudaStream_t s
 }
 #endif
 
+#ifndef __CUDACC_RTC__
 // Small kernel for element-wise parity of the exponentiators (ss_exponentiate).
 template <int SPIN, int EXPO, typename T>
 __global__ void exponentiate_kernel(int64_t n, const double* args, int tau, double* out) {

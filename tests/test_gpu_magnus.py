@@ -51,3 +51,24 @@ def test_magnus_threshold_example(ss):
     b = sim.magnus_bound(sweep, 0.0, 4e-6, 2e-7, 4e-7).item()
     assert a == pytest.approx(0.2 * np.pi, rel=1e-14) and a < SS_MAGNUS_XI
     assert b == pytest.approx(0.4 * np.pi, rel=1e-14) and b > SS_MAGNUS_XI
+
+
+def test_magnus_bound_user_field(ss, orc):
+    """The diagnostic through a run-time compiled (NVRTC) user field equals the built-in field's (same Eq.
+    neural_pulse transcription) and the oracle's."""
+    src = r"""
+__device__ void user_field(double t_k, double off, const double* p, double f[4]) {
+  const double t = t_k + off;
+  f[0] = 2.0 * p[2] * cos(p[1] * t);
+  const double x = p[4] * ((t_k - p[5]) + off);
+  f[2] = p[0] + p[3] * ((x >= 0.0 && x <= 6.283185307179586) ? sin(x) : 0.0);
+  f[3] = p[6];
+}"""
+    w = W.c2_neural(duration=0.2e-3).with_(sweep=W.neural_params(t_p=0.05e-3)[None, :])
+    sim_u = ss.Simulator("one", "cf4", "lie_trotter", 24, True, "fp64", "user", field_source=src, n_params=7)
+    sim_b = ss.Simulator("one", "cf4", "lie_trotter", 24, True, "fp64", "neural")
+    sw = torch.from_numpy(w.sweep).cuda()
+    mu = sim_u.magnus_bound(sw, w.t0, w.t1, w.dt_int, w.dt_out).item()
+    mb = sim_b.magnus_bound(sw, w.t0, w.t1, w.dt_int, w.dt_out).item()
+    ref = orc.magnus_bound("one", True, "neural", sweep=w.sweep, t0=w.t0, t1=w.t1, dt_int=w.dt_int, dt_out=w.dt_out)[0]
+    assert mu == pytest.approx(ref, rel=1e-9) and mb == pytest.approx(ref, rel=1e-11)
