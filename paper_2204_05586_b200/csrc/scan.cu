@@ -1362,6 +1362,10 @@ static cudaError_t run_scan_coop(int64_t batch, int64_t k_count, const double* U
   void* args[] = {&a};
   const cudaError_t e = cudaLaunchCooperativeKernel((const void*)scan_coop_kernel<D>, dim3((unsigned)(batch * cps)),
                                                     dim3(128), args, 0, s);
+  if (e == cudaErrorCooperativeLaunchTooLarge) {   // SMs taken by another context (MPS, green contexts): tile scan
+    (void)cudaGetLastError();
+    return cudaErrorNotSupported;
+  }
   if (e == cudaSuccess) ++*launches;
   return e;
 }
