@@ -42,10 +42,11 @@ constexpr int kIntervalThreads = SS_INTERVAL_THREADS;
 #define SS_INTERVAL_MINBLOCKS 4
 #endif
 // The general spin-one kernel holds a dense 3×3 residual (18 reals) plus the squaring's output copy beside the
-// accumulator; SS_INTERVAL_MINBLOCKS_SU3 trades occupancy against spills for it (G1 on B200: 2 → 2.63e9, 3 → 2.74e9,
-// 4 (128 registers, 376 B spilled) → 2.70e9 fine steps/s; profiles/r01/su3).
+// accumulator; SS_INTERVAL_MINBLOCKS_SU3 trades occupancy against spills for it (G1 on B200 with the closed-form
+// factor: 2 → 2.63e9, 3 → 2.74e9, 4 → 2.70e9 fine steps/s; with the Taylor factor of §5 item 9: 3 → 3.08e9,
+// 4 (128 registers, 316 B spilled) → 3.11e9).
 #ifndef SS_INTERVAL_MINBLOCKS_SU3
-#define SS_INTERVAL_MINBLOCKS_SU3 3
+#define SS_INTERVAL_MINBLOCKS_SU3 4
 #endif
 template <int SPIN, int EXPO, typename T> constexpr int kIntervalMinBlocks() {
   return EXPO == EXP_LIE_TROTTER_SU3 ? SS_INTERVAL_MINBLOCKS_SU3 : SS_INTERVAL_MINBLOCKS;
