@@ -140,7 +140,7 @@ __device__ __forceinline__ void interval_body(const IntervalParams& prm) {
         m.r12 = make_float2(m1.r12, m2.r12); m.i12 = make_float2(m1.i12, m2.i12);
         m.r22 = make_float2(m1.r22, m2.r22); m.i22 = make_float2(m1.i22, m2.i22);
 #pragma unroll 2
-        for (int it = 0; it < prm.tau; ++it) sym_square<float2>(m);
+        for (int it = 0; it < prm.tau; ++it) lt_square<float2>(m);
         m1.r00 = m.r00.x; m1.i00 = m.i00.x; m1.r01 = m.r01.x; m1.i01 = m.i01.x; m1.r02 = m.r02.x; m1.i02 = m.i02.x;
         m1.r11 = m.r11.x; m1.i11 = m.i11.x; m1.r12 = m.r12.x; m1.i12 = m.i12.x; m1.r22 = m.r22.x; m1.i22 = m.i22.x;
         m2.r00 = m.r00.y; m2.i00 = m.i00.y; m2.r01 = m.r01.y; m2.i01 = m.i01.y; m2.r02 = m.r02.y; m2.i02 = m.i02.y;

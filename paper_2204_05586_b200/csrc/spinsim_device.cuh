@@ -542,6 +542,42 @@ template <typename T> __device__ __forceinline__ T taylor_bound();
 template <> __device__ __forceinline__ double taylor_bound<double>() { return 7.450580596923828e-09; }   // 2^-27
 template <> __device__ __forceinline__ float taylor_bound<float>() { return 2.44140625e-04f; }           // 2^-12
 
+// The same squaring in double-angle form.  T₀ is complex symmetric AND unitary, so with T₀ = X + iY (X, Y real
+// symmetric) unitarity T₀T₀* = I reads X² + Y² = I and XY = YX; every power keeps both properties.  Then
+//   T₀² = X² − Y² + 2iXY = (I − 2Y²) + 2i XY,
+// i.e. for the residual a = x + iy (x = X − I, y = Y):  x' = −2y²,  y' = 2y + 2xy  — the double-angle formulas
+// cos 2Θ = 1 − 2 sin²Θ, sin 2Θ = 2 sin Θ cos Θ of T₀ = e^{iΘ}.  Exactly the residual squaring s = (a + 2I)a of
+// P:456-462 for a unitary symmetric T₀ (the dropped term x² + 2x + y² is T₀'s unitarity defect, zero up to rounding):
+// two real symmetric products instead of a complex one, 48 FP64 instructions instead of 63 (DESIGN.md §5 item 13).
+template <typename T> __device__ __forceinline__ void sym_square_u(Sym3<T>& a) {
+  const T m2 = splat<T>(-2.0), p2 = splat<T>(2.0);
+  // w = −2y, u = 2x
+  const T w00 = m2 * a.i00, w01 = m2 * a.i01, w02 = m2 * a.i02, w11 = m2 * a.i11, w12 = m2 * a.i12, w22 = m2 * a.i22;
+  const T u00 = p2 * a.r00, u01 = p2 * a.r01, u02 = p2 * a.r02, u11 = p2 * a.r11, u12 = p2 * a.r12, u22 = p2 * a.r22;
+  const T y00 = a.i00, y01 = a.i01, y02 = a.i02, y11 = a.i11, y12 = a.i12, y22 = a.i22;
+  // x' = w·y (symmetric: w and y commute up to rounding)
+  a.r00 = fmaT(w00, y00, fmaT(w01, y01, w02 * y02));
+  a.r01 = fmaT(w00, y01, fmaT(w01, y11, w02 * y12));
+  a.r02 = fmaT(w00, y02, fmaT(w01, y12, w02 * y22));
+  a.r11 = fmaT(w01, y01, fmaT(w11, y11, w12 * y12));
+  a.r12 = fmaT(w01, y02, fmaT(w11, y12, w12 * y22));
+  a.r22 = fmaT(w02, y02, fmaT(w12, y12, w22 * y22));
+  // y' = 2y + u·y = u·y − w
+  a.i00 = fmaT(u00, y00, fmaT(u01, y01, fmaT(u02, y02, -w00)));
+  a.i01 = fmaT(u00, y01, fmaT(u01, y11, fmaT(u02, y12, -w01)));
+  a.i02 = fmaT(u00, y02, fmaT(u01, y12, fmaT(u02, y22, -w02)));
+  a.i11 = fmaT(u01, y01, fmaT(u11, y11, fmaT(u12, y12, -w11)));
+  a.i12 = fmaT(u01, y02, fmaT(u11, y12, fmaT(u12, y22, -w12)));
+  a.i22 = fmaT(u02, y02, fmaT(u12, y12, fmaT(u22, y22, -w22)));
+}
+
+#ifndef SS_SQUARE_U
+#define SS_SQUARE_U 1       // 1: double-angle squaring (sym_square_u); 0: the complex form (sym_square), for comparison
+#endif
+template <typename T> __device__ __forceinline__ void lt_square(Sym3<T>& a) {
+  if constexpr (SS_SQUARE_U) sym_square_u<T>(a); else sym_square<T>(a);
+}
+
 // T₀ − I and the phase of φ (cos φ, sin φ) for exponent arguments a (divided by n = 2^τ inside).
 template <typename T>
 __device__ __forceinline__ void trotter_init(const T a[4], int tau, Sym3<T>& m, T& cphi, T& sphi) {
@@ -639,7 +675,7 @@ template <typename T> __device__ __forceinline__ void trotter_residual(const T a
   T cphi, sphi;
   trotter_init<T>(a, tau, m, cphi, sphi);
   SS_UNROLL(SS_SQ_UNROLL)
-  for (int it = 0; it < tau; ++it) sym_square<T>(m);
+  for (int it = 0; it < tau; ++it) lt_square<T>(m);
   trotter_expand<T>(m, cphi, sphi, e);
 }
 
