@@ -44,10 +44,10 @@ def algorithmic_flops_per_fine_step(spin: str, expo: str, tau: int, method: str 
     """Arithmetic of one fine step in this implementation's formulation, counting every real +, −, ×
     once (an FMA is 2).
 
-    spin-one Lie–Trotter: residual squaring of the complex-symmetric unitary leapfrog factor T₀ in double-angle form
-    (x' = −2y², y' = 2y + 2xy on its 6 unique entries, DESIGN.md §5 item 13) = 78 flop (48 FP64 instructions) × τ per
-    exponential, residual product b + a(I + b) = 219 (3×3) per exponential; field, frame, T − I construction and
-    phases are not counted (a lower bound; ncu's executed count is in profiles/r01/).
+    spin-one Lie–Trotter: residual squaring of the complex-symmetric unitary leapfrog factor T₀ in scaled double-angle
+    form (x̃' = −ỹ², ỹ' = (x̃ + 2I)ỹ on its 6 unique entries, DESIGN.md §5 item 13) = 63 flop (39 FP64 instructions)
+    × τ per exponential, residual product b + a(I + b) = 219 (3×3) per exponential; field, frame, T − I construction
+    and phases are not counted (a lower bound; ncu's executed count is in profiles/r01/).
     spin-half: per CF4 step 2 × (SU(2) series 26 + SU(2)-parametrised residual product 36) = 124 plus the weights,
     field samples, frame rotation, phase steppers and grid — 193 in total, the ncu-executed count (2·DFMA + DMUL +
     DADD per step, profiles/r01/s2_final/flops_c4.csv after DESIGN.md §5 items 10, 12 and the folded weights).
@@ -60,7 +60,7 @@ def algorithmic_flops_per_fine_step(spin: str, expo: str, tau: int, method: str 
         spin = "half"
     if spin == "one":
         prod = 219
-        per_exp = {"lie_trotter": 78 * tau, "lie_trotter_su3": 159 * tau}.get(expo, 0)
+        per_exp = {"lie_trotter": 63 * tau, "lie_trotter_su3": 159 * tau}.get(expo, 0)
         return n_exp * (per_exp + prod)
     return 193 if method == "cf4" else 97
 
