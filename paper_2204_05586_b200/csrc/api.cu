@@ -73,13 +73,14 @@ struct ss_sim {
   ssb::UserKernel user_kernel;
   // ss_evaluate_host pipeline: streams[0] computes, streams[1] copies; two staging slots; events order them
   cudaStream_t streams[2] = {nullptr, nullptr};
-  cudaEvent_t computed[2] = {nullptr, nullptr};   // slot's kernels done → its D2H may start
-  cudaEvent_t drained[2] = {nullptr, nullptr};    // slot's D2H done → its buffers may be reused
+  static constexpr int kSlots = 3;
+  cudaEvent_t computed[kSlots] = {};   // slot's kernels done → its D2H may start
+  cudaEvent_t drained[kSlots] = {};    // slot's D2H done → its buffers may be reused
   int device = -1;
   struct Slot {
     void* buf = nullptr;
     size_t cap = 0;
-  } slots[2];
+  } slots[kSlots], aux;   // aux: sweep table + running carry of the time-chunked pipeline
 };
 
 namespace {
@@ -302,9 +303,10 @@ void ss_destroy(ss_sim* s) {
   if (s->user) ssb::destroy_user_kernel(&s->user_kernel);
   for (auto& sl : s->slots)
     if (sl.buf) cudaFree(sl.buf);
+  if (s->aux.buf) cudaFree(s->aux.buf);
   for (auto& st : s->streams)
     if (st) cudaStreamDestroy(st);
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < ss_sim::kSlots; ++k) {
     if (s->computed[k]) cudaEventDestroy(s->computed[k]);
     if (s->drained[k]) cudaEventDestroy(s->drained[k]);
   }
@@ -548,19 +550,97 @@ int ss_evaluate_host(ss_sim* s, double t0, double t1, double dt_int, double dt_o
   if (s->device != dev) {  // (re)create per-device streams/events and drop buffers of another device
     for (auto& st : s->streams) if (st) cudaStreamDestroy(st), st = nullptr;
     for (auto& sl : s->slots) if (sl.buf) cudaFree(sl.buf), sl.buf = nullptr, sl.cap = 0;
-    for (int k = 0; k < 2; ++k) {
+    if (s->aux.buf) cudaFree(s->aux.buf), s->aux.buf = nullptr, s->aux.cap = 0;
+    for (int k = 0; k < ss_sim::kSlots; ++k) {
       if (s->computed[k]) cudaEventDestroy(s->computed[k]), s->computed[k] = nullptr;
       if (s->drained[k]) cudaEventDestroy(s->drained[k]), s->drained[k] = nullptr;
     }
     for (auto& st : s->streams)
       if ((e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)) != cudaSuccess) return cuda_fail(e, "stream create");
-    for (int k = 0; k < 2; ++k)
+    for (int k = 0; k < ss_sim::kSlots; ++k)
       if ((e = cudaEventCreateWithFlags(&s->computed[k], cudaEventDisableTiming)) != cudaSuccess ||
           (e = cudaEventCreateWithFlags(&s->drained[k], cudaEventDisableTiming)) != cudaSuccess)
         return cuda_fail(e, "event create");
     s->device = dev;
   }
   const int D = s->dim;
+  auto ensure = [&](ss_sim::Slot& sl, size_t bytes) -> cudaError_t {
+    if (sl.cap >= bytes) return cudaSuccess;
+    if (sl.buf) cudaFree(sl.buf);
+    sl.buf = nullptr;
+    sl.cap = 0;
+    const cudaError_t r = cudaMalloc(&sl.buf, bytes);
+    if (r == cudaSuccess) sl.cap = bytes;
+    return r;
+  };
+  cudaStream_t cs = s->streams[0], xs = s->streams[1];
+  if (batch >= ssb::chain_min_batch() && n_chunks >= 6 && K >= 4 * (int64_t)n_chunks) {
+    // Large batches: chunk the TIME axis, all sweeps per chunk (the per-sweep chain kernel stays at full width and is
+    // sequential per sweep, so the states are bit-identical to one ss_evaluate).  Chunk c = intervals [k0, k0 + kc)
+    // of every sweep, started from the running carry (the previous chunk's last states).  Tent-shaped sizes — small
+    // first chunks so the device→host copies start early, small last ones so little copy is left exposed — with
+    // weights 1, 2, 3, …, 3, 1, ½, ¼, ¼ and three staging slots (the copy of chunk c overlaps chunks c+1 and c+2).
+    std::vector<double> w = {1.0, 2.0};
+    while ((int)w.size() < n_chunks - 4) w.push_back(3.0);
+    for (double x : {1.0, 0.5, 0.25, 0.25}) w.push_back(x);
+    double wsum = 0;
+    for (double x : w) wsum += x;
+    std::vector<int64_t> ks;
+    int64_t used = 0, kc_max = 0;
+    for (size_t c = 0; c < w.size(); ++c) {
+      const int64_t kc = (c + 1 == w.size()) ? K - used : std::max<int64_t>(1, (int64_t)std::llround(K * w[c] / wsum));
+      ks.push_back(kc);
+      used += kc;
+      kc_max = std::max(kc_max, kc);
+    }
+    const size_t sweep_b = align256(sizeof(double) * s->P * batch), carry_b = align256(sizeof(double) * 2 * D * batch);
+    const size_t states_b = align256(sizeof(double) * 2 * D * (size_t)batch * (kc_max + 1));
+    const size_t U_b = align256(sizeof(double) * 2 * D * D * (size_t)batch * kc_max);
+    const size_t scan_b = align256(ssb::scan_workspace_bytes(D, batch, kc_max));
+    if ((e = ensure(s->aux, sweep_b + carry_b)) != cudaSuccess) return cuda_fail(e, "cudaMalloc (host-API staging)");
+    for (int k = 0; k < ss_sim::kSlots; ++k)
+      if ((e = ensure(s->slots[k], states_b + U_b + scan_b)) != cudaSuccess)
+        return cuda_fail(e, "cudaMalloc (host-API staging)");
+    double* d_sweep = static_cast<double*>(s->aux.buf);
+    double* d_carry = reinterpret_cast<double*>(static_cast<char*>(s->aux.buf) + sweep_b);
+    if ((e = cudaMemcpyAsync(d_sweep, h_sweep, sizeof(double) * s->P * batch, cudaMemcpyHostToDevice, cs)) ||
+        (e = cudaMemcpyAsync(d_carry, h_psi0, sizeof(double) * 2 * D * batch, cudaMemcpyHostToDevice, cs)))
+      return cuda_fail(e, "H2D copy");
+    const size_t row = sizeof(double) * 2 * D;                   // one state
+    for (size_t c = 0, k0 = 0; c < ks.size(); k0 += ks[c], ++c) {
+      const int64_t kc = ks[c];
+      const int k = (int)(c % ss_sim::kSlots);
+      char* base = static_cast<char*>(s->slots[k].buf);
+      double* d_states = reinterpret_cast<double*>(base);
+      double* d_U = reinterpret_cast<double*>(base + states_b);
+      void* d_scan = base + states_b + U_b;
+      if (c >= (size_t)ss_sim::kSlots && (e = cudaStreamWaitEvent(cs, s->drained[k], 0)) != cudaSuccess)
+        return cuda_fail(e, "event wait");
+      const auto p = make_params(s, t0, dt_out, dt, L, (int64_t)k0, kc, batch, d_sweep, d_U, batch * K);
+      if ((rc = launch_interval_checked(s, p, cs))) return rc;
+      int n = 0;
+      if ((e = ssb::launch_scan(D, batch, kc, d_U, d_carry, d_states, d_scan, cs, &n)) != cudaSuccess)
+        return cuda_fail(e, "scan launch");
+      g_launches.fetch_add(n);
+      // carry ← states[:, kc]
+      if ((e = cudaMemcpy2DAsync(d_carry, row, d_states + (size_t)kc * 2 * D, row * (kc + 1), row, batch,
+                                 cudaMemcpyDeviceToDevice, cs)))
+        return cuda_fail(e, "carry copy");
+      if ((e = cudaEventRecord(s->computed[k], cs)) || (e = cudaStreamWaitEvent(xs, s->computed[k], 0)))
+        return cuda_fail(e, "event record/wait");
+      const size_t first = (c == 0) ? 0 : 1;                     // states[:, 0] of chunk c > 0 is the carry
+      if ((e = cudaMemcpy2DAsync(h_states + (k0 + first) * 2 * D, row * (K + 1), d_states + first * 2 * D,
+                                 row * (kc + 1), row * (kc + 1 - first), batch, cudaMemcpyDeviceToHost, xs)))
+        return cuda_fail(e, "D2H copy (states)");
+      if (h_U && (e = cudaMemcpy2DAsync(h_U + k0 * 2 * D * D, row * D * K, d_U, row * D * kc, row * D * kc, batch,
+                                        cudaMemcpyDeviceToHost, xs)))
+        return cuda_fail(e, "D2H copy (unitaries)");
+      if ((e = cudaEventRecord(s->drained[k], xs))) return cuda_fail(e, "event record");
+    }
+    for (int k = 0; k < 2; ++k)
+      if ((e = cudaStreamSynchronize(s->streams[k])) != cudaSuccess) return cuda_fail(e, "stream synchronize");
+    return SS_OK;
+  }
   // Geometric chunks (B/2, B/4, …, the last two equal): early chunks are big (full-speed chain scan, long compute
   // that hides the previous chunk's D2H), the final chunk — whose D2H cannot be hidden — is small.
   std::vector<int64_t> sizes;
@@ -581,20 +661,11 @@ int ss_evaluate_host(ss_sim* s, double t0, double t1, double dt_int, double dt_o
   const size_t scan_b = align256(ssb::scan_workspace_bytes(D, cb_max, K));
   const size_t slot_bytes = sweep_b + psi0_b + states_b + U_b + scan_b;
   const int nslots = n_chunks > 1 ? 2 : 1;
-  for (int k = 0; k < nslots; ++k) {
-    auto& sl = s->slots[k];
-    if (sl.cap < slot_bytes) {
-      if (sl.buf) cudaFree(sl.buf);
-      sl.buf = nullptr;
-      sl.cap = 0;
-      if ((e = cudaMalloc(&sl.buf, slot_bytes)) != cudaSuccess) return cuda_fail(e, "cudaMalloc (host-API staging)");
-      sl.cap = slot_bytes;
-    }
-  }
+  for (int k = 0; k < nslots; ++k)
+    if ((e = ensure(s->slots[k], slot_bytes)) != cudaSuccess) return cuda_fail(e, "cudaMalloc (host-API staging)");
   // Chunk c: [compute stream] wait drained[slot] (its D2H two chunks ago) → H2D inputs → kernels → record
   // computed[slot];  [copy stream] wait computed[slot] → D2H → record drained[slot].  Compute stays serial over
   // chunks (each chunk fills the GPU), so the D2H of chunk c overlaps the kernels of chunk c+1.
-  cudaStream_t cs = s->streams[0], xs = s->streams[1];
   for (int64_t c = 0, b0 = 0; c < n_chunks; ++c) {
     const int64_t cb = sizes[c];
     if (cb <= 0) break;

@@ -8,6 +8,7 @@
 
 namespace ssb {
 size_t scan_workspace_bytes(int dim, int64_t batch, int64_t k_count);
+int64_t chain_min_batch();   // batches from this size take the per-sweep chain kernel (sequential, chunk-invariant)
 size_t aggregate_workspace_bytes(int dim, int64_t batch, int64_t k_count);
 cudaError_t launch_scan(int dim, int64_t batch, int64_t k_count, const double* U, const double* psi0, double* states,
                         void* ws, cudaStream_t s, int* launches, double* spin = nullptr);

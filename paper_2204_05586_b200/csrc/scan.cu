@@ -1328,6 +1328,8 @@ __global__ void validate_kernel(int64_t n_sweep, const double* sweep, int P, int
 // ---- host launchers -------------------------------------------------------------------------------------------
 template <int D> size_t scan_ws_bytes(int64_t batch, int64_t k_count) { return ScanLayout<D>(batch, k_count).total; }
 
+int64_t chain_min_batch() { return kChainMinBatch; }
+
 constexpr int kCoopMaxGrid = 1024;
 size_t scan_workspace_bytes(int dim, int64_t batch, int64_t k_count) {
   const size_t coop = sizeof(double2) * (size_t)dim * dim * kCoopMaxGrid;

@@ -269,6 +269,18 @@ def test_host_api_matches_device_api(ss):
         assert np.array_equal(st_h, st_d) and np.array_equal(U_h, U_d)
 
 
+def test_host_api_time_chunks_match_device_api(ss):
+    """Large batches (≥ 4096 sweeps) pipeline the host-buffer call over time chunks started from a running carry:
+    the per-sweep chain scan is sequential, so states and operators equal one device evaluate() bit for bit."""
+    w = W.c3_batched(batch=4096, duration=0.2e-3)
+    st_d, U_d = gpu_run(ss, w)
+    sim = ss.Simulator(w.spin, w.method, w.expo, w.tau, w.frame, "fp64", w.field)
+    for chunks in (6, 10):
+        st_h, U_h = sim.evaluate_host(w.sweep, w.t0, w.t1, w.dt_int, w.dt_out, w.psi0, want_unitaries=True,
+                                      n_chunks=chunks)
+        assert np.array_equal(st_h, st_d) and np.array_equal(U_h, U_d)
+
+
 @pytest.mark.parametrize("which", ["C4", "C2", "G1"])
 def test_partition_reproduces_unitaries_bitwise(ss, which):
     """The time grid uses the global k (and the sub-interval split is chosen from the whole problem), so computing a
