@@ -288,18 +288,31 @@ template <class R> Mat<R> expm_spin1_analytic(R ax, R ay, R az) {
 // i.e. the Hermitian matrix with
 //   diagonal (az + aq/3, −2aq/3, −az + aq/3),
 //   H01 = (ax − i ay + av1 − i av2)/√2,  H12 = (ax − i ay − av1 + i av2)/√2,  H02 = au1 − i au2.
-// Lie–Trotter in the paper's form: U = T^n, n = 2^τ, with the symmetric (leapfrog) factor
-//   T = e^{−iD/2} e^{−iX/2} e^{−iY} e^{−iX/2} e^{−iD/2}     (all arguments divided by n),
-// D = diagonal part, X = the (0,1)/(1,2) part, Y = the (0,2) part.  X and Y each have a closed-form exponential
-// (X³ = r² X with r² = |H01|² + |H12|²; Y³ = |H02|² Y):  e^{−iX} = I − i (sin r / r) X + ((cos r − 1)/r²) X².
-// With au = av = 0, Y = 0 and X = Φ Jφ, so T is exactly the paper's factor of Eq. lie_trotter_4.
-// T − I is assembled from the factors' residuals (cos − 1 = −2 sin²(·/2), expm1 diagonals) by the
-// residual product (I + x)(I + y) − I = x + y + xy; then τ residual squarings s = (a + 2I)a.
+// Lie–Trotter in the paper's form, reading R20: the paper's factor is built for a matrix
+// whose only couplings are (0,1) and (1,2) with one common phase (Eq. lie_trotter_4: e^{−iD/2} e^{−iΦJφ} e^{−iD/2},
+// the phase removed by a diagonal similarity R_φ).  A general H is first brought to that shape by a unitary
+// similarity W that fixes the m = +1 basis vector: W = diag(1, G)·diag(1, 1, e^{iψ}) with
+//   G = [[H01*, −H02], [H02*, H01]] / r,   r = √(|H01|² + |H02|²)    (G = I at r = 0),
+// which zeroes the (0,2) entry and makes the (0,1) entry r ≥ 0, and the phase e^{iψ} = B12*/|B12| (B = W†HW before
+// the phase; := 1 at B12 = 0) that makes the (1,2) entry real ≥ 0.  S = W†HW is then real symmetric tridiagonal
+// (the first steps of the Lanczos process started at the m = +1 vector), and
+//   T = W T₀ W†,   T₀ = e^{−iD/2} e^{−iX} e^{−iD/2}     (all arguments divided by n = 2^τ),
+// D = diag(S), X = S − D.  X has a closed-form exponential (X³ = ρ² X, ρ² = S01² + S12²):
+// e^{−iX} = I − i (sin ρ / ρ) X + ((cos ρ − 1)/ρ²) X².  With au = av = 0, W = e^{iφ}·R_φ up to a global phase and
+// T₀ is exactly the paper's factor of Eq. lie_trotter_4.  T − I is assembled from the factors' residuals
+// (cos − 1 = −2 sin²(·/2), expm1 diagonals) by the residual product (I + x)(I + y) − I = x + y + xy and
+// conjugated, T − I = W (T₀ − I) W†; then τ residual squarings s = (a + 2I)a.
 // ------------------------------------------------------------------------------------------------
 template <class R> Mat<R> res_prod(const Mat<R>& x, const Mat<R>& y) {   // (I + x)(I + y) − I
   Mat<R> z = mul(x, y);
   for (int i = 0; i < 3; ++i) for (int j = 0; j < 3; ++j) z.a[i][j] += x.a[i][j] + y.a[i][j];
   return z;
+}
+
+template <class R> Mat<R> adjoint(const Mat<R>& x) {
+  Mat<R> y = Mat<R>::zero(x.n);
+  for (int i = 0; i < x.n; ++i) for (int j = 0; j < x.n; ++j) y.a[i][j] = std::conj(x.a[j][i]);
+  return y;
 }
 
 // residual of exp(−iX) for a Hermitian X with X³ = r² X (r² given)
@@ -315,27 +328,50 @@ template <class R> Mat<R> rodrigues_residual(const Mat<R>& X, R r2) {
   return a;
 }
 
-template <class R> Mat<R> trotter_factor_residual_su3(const R a[NF], R n) {
-  const Cx<R> I(0, 1);
+template <class R> Mat<R> su3_hamiltonian(const R a[NF], R n) {      // H/n over the basis above (reading R19)
   const R rt2 = std::sqrt(R(2));
   const R z = a[2] / n, q = a[3] / n;
-  const R d[3] = {z + q / R(3), -R(2) * q / R(3), -z + q / R(3)};
-  const Cx<R> h01 = Cx<R>(a[0] + a[6], -(a[1] + a[7])) / (rt2 * n);
-  const Cx<R> h12 = Cx<R>(a[0] - a[6], -(a[1] - a[7])) / (rt2 * n);
-  const Cx<R> h02 = Cx<R>(a[4], -a[5]) / n;
+  Mat<R> H = Mat<R>::zero(3);
+  H.a[0][0] = z + q / R(3);
+  H.a[1][1] = -R(2) * q / R(3);
+  H.a[2][2] = -z + q / R(3);
+  H.a[0][1] = Cx<R>(a[0] + a[6], -(a[1] + a[7])) / (rt2 * n);
+  H.a[1][2] = Cx<R>(a[0] - a[6], -(a[1] - a[7])) / (rt2 * n);
+  H.a[0][2] = Cx<R>(a[4], -a[5]) / n;
+  for (int i = 0; i < 3; ++i) for (int j = 0; j < i; ++j) H.a[i][j] = std::conj(H.a[j][i]);
+  return H;
+}
+
+// The similarity W of reading R20 (W†HW real symmetric tridiagonal, W e0 = e0).
+template <class R> Mat<R> su3_tridiagonaliser(const Mat<R>& H) {
+  const Cx<R> h01 = H.a[0][1], h02 = H.a[0][2];
+  const R r = std::sqrt(std::norm(h01) + std::norm(h02));
+  Mat<R> W = Mat<R>::eye(3);
+  if (r > R(0)) {
+    W.a[1][1] = std::conj(h01) / r;  W.a[1][2] = -h02 / r;
+    W.a[2][1] = std::conj(h02) / r;  W.a[2][2] = h01 / r;
+  }
+  const Cx<R> b12 = mul(adjoint(W), mul(H, W)).a[1][2];
+  if (std::abs(b12) > R(0)) {
+    const Cx<R> ph = std::conj(b12) / std::abs(b12);
+    W.a[1][2] *= ph;
+    W.a[2][2] *= ph;
+  }
+  return W;
+}
+
+template <class R> Mat<R> trotter_factor_residual_su3(const R a[NF], R n) {
+  const Mat<R> H = su3_hamiltonian(a, n);
+  const Mat<R> W = su3_tridiagonaliser(H);
+  const Mat<R> S = mul(adjoint(W), mul(H, W));      // real symmetric tridiagonal up to rounding
   Mat<R> eD = Mat<R>::zero(3);                       // e^{−iD/2} − I
-  for (int i = 0; i < 3; ++i) eD.a[i][i] = expm1i(-d[i] / R(2));
-  Mat<R> Xh = Mat<R>::zero(3);                       // X/2
-  Xh.a[0][1] = h01 / R(2); Xh.a[1][0] = std::conj(h01) / R(2);
-  Xh.a[1][2] = h12 / R(2); Xh.a[2][1] = std::conj(h12) / R(2);
-  Mat<R> Y = Mat<R>::zero(3);
-  Y.a[0][2] = h02; Y.a[2][0] = std::conj(h02);
-  const Mat<R> eX = rodrigues_residual(Xh, (std::norm(h01) + std::norm(h12)) / R(4));
-  const Mat<R> eY = rodrigues_residual(Y, std::norm(h02));
-  Mat<R> t = res_prod(eD, eX);
-  t = res_prod(t, eY);
-  t = res_prod(t, eX);
-  return res_prod(t, eD);
+  for (int i = 0; i < 3; ++i) eD.a[i][i] = expm1i(-S.a[i][i].real() / R(2));
+  Mat<R> X = Mat<R>::zero(3);
+  X.a[0][1] = X.a[1][0] = S.a[0][1].real();
+  X.a[1][2] = X.a[2][1] = S.a[1][2].real();
+  const Mat<R> eX = rodrigues_residual(X, std::norm(X.a[0][1]) + std::norm(X.a[1][2]));
+  const Mat<R> t0 = res_prod(res_prod(eD, eX), eD);  // T₀ − I
+  return mul(W, mul(t0, adjoint(W)));                // T − I = W (T₀ − I) W†
 }
 
 template <class R> Mat<R> expm_lie_trotter_su3(const R a[NF], int tau) {

@@ -41,10 +41,16 @@ MUTANTS = {
     "su3_v_sign": ("Cx<R>(a[0] - a[6], -(a[1] - a[7]))", "Cx<R>(a[0] + a[6], -(a[1] - a[7]))"),
     # U pair rotated by θ instead of 2θ in the frame
     "su3_u_frame_angle": ("const R c2 = std::cos(R(2) * th), s2 = std::sin(R(2) * th);", "const R c2 = c, s2 = s;"),
-    # leapfrog half-step dropped on the tridiagonal part
-    "su3_x_half": ("Xh.a[0][1] = h01 / R(2);", "Xh.a[0][1] = h01;"),
+    # leapfrog half-step dropped on the diagonal part
+    "su3_d_half": ("expm1i(-S.a[i][i].real() / R(2))", "expm1i(-S.a[i][i].real())"),
     # (0,2) coupling not Hermitian
-    "su3_y_conj": ("Y.a[2][0] = std::conj(h02);", "Y.a[2][0] = h02;"),
+    "su3_h02_conj": ("H.a[0][2] = Cx<R>(a[4], -a[5]) / n;", "H.a[0][2] = Cx<R>(a[4], a[5]) / n;"),
+    # tridiagonalising rotation built from H01 instead of its conjugate
+    "su3_w_conj": ("W.a[1][1] = std::conj(h01) / r;", "W.a[1][1] = h01 / r;"),
+    # phase e^{iψ} applied with the wrong sign
+    "su3_w_phase": ("const Cx<R> ph = std::conj(b12) / std::abs(b12);", "const Cx<R> ph = b12 / std::abs(b12);"),
+    # factor conjugated the wrong way round: W† (T₀ − I) W
+    "su3_w_side": ("return mul(W, mul(t0, adjoint(W)));", "return mul(adjoint(W), mul(t0, W));"),
     # two-photon drive at ω_d instead of 2ω_d
     "su3_drive_2w": ("f[4] = (R)p[4] * std::cos(R(2) * ph);", "f[4] = (R)p[4] * std::cos(ph);"),
     # --- Magnus diagnostic ---

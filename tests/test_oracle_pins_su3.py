@@ -93,27 +93,61 @@ def _mp_expm_residual(H, s):
         return np.array([[complex(E[i, j]) for j in range(3)] for i in range(3)])
 
 
+def _mp_lanczos(Hm):
+    """Lanczos from the m = +1 basis vector in mpmath: W = [q0, q1, q2] with W†HW real tridiagonal, positive
+    off-diagonals (a construction independent of the oracle's explicit Givens-plus-phase W)."""
+    q0 = mpmath.matrix([1, 0, 0])
+    dot = lambda u, v: sum(mpmath.conj(u[i]) * v[i] for i in range(3))
+    w = Hm * q0
+    w = w - dot(q0, w) * q0
+    b1 = mpmath.sqrt(mpmath.re(dot(w, w)))
+    q1 = w / b1
+    w = Hm * q1
+    w = w - dot(q0, w) * q0 - dot(q1, w) * q1
+    q2 = w / mpmath.sqrt(mpmath.re(dot(w, w)))
+    return mpmath.matrix([[q[i] for q in (q0, q1, q2)] for i in range(3)])
+
+
 def test_su3_factor_residual_vs_mpmath(orc):
-    """T − I = e^{−iD/2n} e^{−iX/2n} e^{−iY/n} e^{−iX/2n} e^{−iD/2n} − I (reading R20) against 40-digit products
-    of the five exponentials, elementwise RELATIVE accuracy (the residual form keeps the digits P:463-466 asks for),
-    at a large and a tiny argument scale."""
+    """T − I = W (e^{−iD/2n} e^{−iX/n} e^{−iD/2n} − I) W† with S = W†HW = D + X real tridiagonal (reading R20)
+    against 40-digit arithmetic with W from the Lanczos process (mpmath) — elementwise RELATIVE accuracy (the
+    residual form keeps the digits P:463-466 asks for), at a large and a tiny argument scale."""
     rng = np.random.default_rng(24)
     for scale, tau in ((1.0, 0), (1.0, 20), (1e-4, 24)):
         for _ in range(6):
             a = rng.uniform(-scale, scale, 8)
             n = 2.0 ** tau
-            D = a[2] * JZ + a[3] * Q
             Hfull = H8(a)
-            X = np.triu(Hfull, 1) - np.triu(Hfull, 2) + np.tril(Hfull, -1) - np.tril(Hfull, -2)   # (0,1),(1,2) part
-            Y = Hfull - D - X                                                                     # (0,2) part
             with mpmath.workdps(40):
-                def ex(Hm, s):
-                    return mpmath.expm(mpmath.matrix([[mpmath.mpc(complex(Hm[i, j])) * (-1j) * s / n
-                                                       for j in range(3)] for i in range(3)]))
-                T = ex(D, 0.5) * ex(X, 0.5) * ex(Y, 1.0) * ex(X, 0.5) * ex(D, 0.5) - mpmath.eye(3)
+                Hm = mpmath.matrix([[mpmath.mpc(complex(Hfull[i, j])) for j in range(3)] for i in range(3)])
+                Wm = _mp_lanczos(Hm)
+                S = Wm.H * Hm * Wm
+                assert abs(S[0, 2]) < mpmath.mpf(10) ** -35 and abs(mpmath.im(S[1, 2])) < mpmath.mpf(10) ** -35
+                D = mpmath.diag([mpmath.re(S[i, i]) for i in range(3)])
+                X = mpmath.matrix(3, 3)
+                X[0, 1] = X[1, 0] = mpmath.re(S[0, 1])
+                X[1, 2] = X[2, 1] = mpmath.re(S[1, 2])
+                ex = lambda M, s: mpmath.expm(M * (-1j) * s / n)
+                T = Wm * ex(D, 0.5) * ex(X, 1.0) * ex(D, 0.5) * Wm.H - mpmath.eye(3)
                 ref = np.array([[complex(T[i, j]) for j in range(3)] for i in range(3)])
             got = orc.trotter_residual_su3(a, tau)
             assert np.all(np.abs(got - ref) <= 1e-15 * np.abs(ref) + 1e-16 * scale / n), (scale, tau, got - ref)
+
+
+def test_su3_factor_special_cases(orc):
+    """The reading-R20 factor's special shapes: (i) no (0,1)/(0,2) coupling (r = 0, W = phase only), (ii) no (1,2)
+    coupling after the rotation (B12 = 0), (iii) Δm = ±2 coupling only — each against the 40-digit Lanczos factor's
+    defining property: T unitary, and T = exp(−iH/n) + O(|H/n|³) with the Strang constant (halving H divides the
+    error by ≈ 8)."""
+    for a in (np.array([0.4, 0.4, 0.3, -0.7, 0, 0, -0.4, -0.4]),  # H01 = H02 = 0: r = 0, W = phase only
+              np.array([0.5, 0.2, 0.1, 0.3, 0, 0, 0.5, 0.2]),     # H12 = 0 (ax = av1, ay = av2)
+              np.array([0, 0, 0.2, 0.1, 0.8, -0.6, 0, 0])):       # U pair only: H01 = H12 = 0
+        errs = []
+        for s in (1.0, 0.5, 0.25):
+            T = orc.trotter_residual_su3(s * a, 0) + np.eye(3)
+            assert np.abs(T.conj().T @ T - np.eye(3)).max() < 1e-15
+            errs.append(np.abs(T - sl.expm(-1j * H8(s * a))).max())
+        assert 6 < errs[0] / errs[1] < 10 and 6 < errs[1] / errs[2] < 10, errs
 
 
 def test_su3_structure(orc):
