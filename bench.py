@@ -51,8 +51,9 @@ def algorithmic_flops_per_fine_step(spin: str, expo: str, tau: int, method: str 
     spin-half: per CF4 step 2 × (SU(2) series 26 + SU(2)-parametrised residual product 36) = 124 plus the weights,
     field samples, frame rotation, phase steppers and grid — 193 in total, the ncu-executed count (2·DFMA + DMUL +
     DADD per step, profiles/r01/s2_final/flops_c4.csv after DESIGN.md §5 items 10, 12 and the folded weights).
-    general spin-one (lie_trotter_su3, readings R19/R20): dense residual squaring res_square3 = 159 flop (93 FP64
-    instructions) × τ, residual product 219; the T − I assembly (≈ 3 % of the step) is not counted.
+    general spin-one (lie_trotter_su3, readings R19/R20): the same 63-flop symmetric squaring × τ on the
+    tridiagonalised factor T₀, the conjugation W (T₀^n − I) W† = 24 complex multiply-adds = 192 flop, residual product
+    219; the tridiagonalisation and T₀ construction are not counted.
     spin-one analytic (reading R14): accumulated in SU(2) form and mapped by D¹ once per interval (DESIGN.md §5
     item 11), so its fine step is the spin-half step: 193."""
     n_exp = 2 if method == "cf4" else 1
@@ -60,7 +61,7 @@ def algorithmic_flops_per_fine_step(spin: str, expo: str, tau: int, method: str 
         spin = "half"
     if spin == "one":
         prod = 219
-        per_exp = {"lie_trotter": 63 * tau, "lie_trotter_su3": 159 * tau}.get(expo, 0)
+        per_exp = {"lie_trotter": 63 * tau, "lie_trotter_su3": 63 * tau + 192}.get(expo, 0)
         return n_exp * (per_exp + prod)
     return 193 if method == "cf4" else 97
 

@@ -132,19 +132,10 @@ __device__ __forceinline__ void interval_body(const IntervalParams& prm) {
         float c1, s1, c2, s2;
         trotter_init<float>(a1, prm.tau, m1, c1, s1);
         trotter_init<float>(a2, prm.tau, m2, c2, s2);
-        Sym3<float2> m;
-        m.r00 = make_float2(m1.r00, m2.r00); m.i00 = make_float2(m1.i00, m2.i00);
-        m.r01 = make_float2(m1.r01, m2.r01); m.i01 = make_float2(m1.i01, m2.i01);
-        m.r02 = make_float2(m1.r02, m2.r02); m.i02 = make_float2(m1.i02, m2.i02);
-        m.r11 = make_float2(m1.r11, m2.r11); m.i11 = make_float2(m1.i11, m2.i11);
-        m.r12 = make_float2(m1.r12, m2.r12); m.i12 = make_float2(m1.i12, m2.i12);
-        m.r22 = make_float2(m1.r22, m2.r22); m.i22 = make_float2(m1.i22, m2.i22);
+        Sym3<float2> m = sym_pack(m1, m2);
 #pragma unroll 2
         for (int it = 0; it < prm.tau; ++it) lt_square<float2>(m);
-        m1.r00 = m.r00.x; m1.i00 = m.i00.x; m1.r01 = m.r01.x; m1.i01 = m.i01.x; m1.r02 = m.r02.x; m1.i02 = m.i02.x;
-        m1.r11 = m.r11.x; m1.i11 = m.i11.x; m1.r12 = m.r12.x; m1.i12 = m.i12.x; m1.r22 = m.r22.x; m1.i22 = m.i22.x;
-        m2.r00 = m.r00.y; m2.i00 = m.i00.y; m2.r01 = m.r01.y; m2.i01 = m.i01.y; m2.r02 = m.r02.y; m2.i02 = m.i02.y;
-        m2.r11 = m.r11.y; m2.i11 = m.i11.y; m2.r12 = m.r12.y; m2.i12 = m.i12.y; m2.r22 = m.r22.y; m2.i22 = m.i22.y;
+        sym_unpack(m, m1, m2);
         Res<D, T> e;
         trotter_expand<T>(m1, c1, s1, e);
         res_mul(e, A, u);
@@ -153,25 +144,20 @@ __device__ __forceinline__ void interval_body(const IntervalParams& prm) {
         return;
       }
       if constexpr (SPIN == SPIN_ONE && EXPO == EXP_LIE_TROTTER_SU3 && sizeof(T) == 4) {
-        // FP32 mode, general spin-one: both exponentials' dense squarings in lockstep, one per float2 lane
-        Res<3, float> e1, e2;
-        trotter_init_su3<float>(a1, prm.tau, e1);
-        trotter_init_su3<float>(a2, prm.tau, e2);
-        Res<3, float2> m;
-#pragma unroll
-        for (int j = 0; j < 9; ++j) {
-          m.re[j] = make_float2(e1.re[j], e2.re[j]);
-          m.im[j] = make_float2(e1.im[j], e2.im[j]);
-        }
-#pragma unroll 1
-        for (int it = 0; it < prm.tau; ++it) res_square3<float2>(m);
-#pragma unroll
-        for (int j = 0; j < 9; ++j) {
-          e1.re[j] = m.re[j].x; e1.im[j] = m.im[j].x;
-          e2.re[j] = m.re[j].y; e2.im[j] = m.im[j].y;
-        }
-        res_mul(e1, A, u);
-        res_mul(e2, u, A);
+        // FP32 mode, general spin-one: the same lockstep squarings on the tridiagonalised factors (reading R20)
+        Sym3<float> m1, m2;
+        Su3W<float> w1, w2;
+        su3_init<float>(a1, prm.tau, m1, w1);
+        su3_init<float>(a2, prm.tau, m2, w2);
+        Sym3<float2> m = sym_pack(m1, m2);
+#pragma unroll 2
+        for (int it = 0; it < prm.tau; ++it) lt_square<float2>(m);
+        sym_unpack(m, m1, m2);
+        Res<D, T> e;
+        su3_expand<T>(m1, w1, e);
+        res_mul(e, A, u);
+        su3_expand<T>(m2, w2, e);
+        res_mul(e, u, A);
         return;
       }
       // a5/a6/a7: u·U_r = e2·(e1·U_r) (Eq. cf4_implementation), folded one exponential at a time so only

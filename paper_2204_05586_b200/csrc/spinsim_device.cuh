@@ -606,6 +606,25 @@ template <typename T> __device__ __forceinline__ void lt_square(Sym3<T>& a) {
   else sym_square<T>(a);
 }
 
+// Two FP32 symmetric residuals packed one per float2 lane (FP32 mode squares both exponentials of a CF4 step in
+// lockstep with packed FFMA2).
+__device__ __forceinline__ Sym3<float2> sym_pack(const Sym3<float>& a, const Sym3<float>& b) {
+  Sym3<float2> m;
+  m.r00 = make_float2(a.r00, b.r00); m.i00 = make_float2(a.i00, b.i00);
+  m.r01 = make_float2(a.r01, b.r01); m.i01 = make_float2(a.i01, b.i01);
+  m.r02 = make_float2(a.r02, b.r02); m.i02 = make_float2(a.i02, b.i02);
+  m.r11 = make_float2(a.r11, b.r11); m.i11 = make_float2(a.i11, b.i11);
+  m.r12 = make_float2(a.r12, b.r12); m.i12 = make_float2(a.i12, b.i12);
+  m.r22 = make_float2(a.r22, b.r22); m.i22 = make_float2(a.i22, b.i22);
+  return m;
+}
+__device__ __forceinline__ void sym_unpack(const Sym3<float2>& m, Sym3<float>& a, Sym3<float>& b) {
+  a.r00 = m.r00.x; a.i00 = m.i00.x; a.r01 = m.r01.x; a.i01 = m.i01.x; a.r02 = m.r02.x; a.i02 = m.i02.x;
+  a.r11 = m.r11.x; a.i11 = m.i11.x; a.r12 = m.r12.x; a.i12 = m.i12.x; a.r22 = m.r22.x; a.i22 = m.i22.x;
+  b.r00 = m.r00.y; b.i00 = m.i00.y; b.r01 = m.r01.y; b.i01 = m.i01.y; b.r02 = m.r02.y; b.i02 = m.i02.y;
+  b.r11 = m.r11.y; b.i11 = m.i11.y; b.r12 = m.r12.y; b.i12 = m.i12.y; b.r22 = m.r22.y; b.i22 = m.i22.y;
+}
+
 // T₀ − I and the phase of φ (cos φ, sin φ) for exponent arguments a (divided by n = 2^τ inside).
 template <typename T>
 __device__ __forceinline__ void trotter_init(const T a[4], int tau, Sym3<T>& m, T& cphi, T& sphi) {
@@ -761,11 +780,12 @@ template <typename T> __device__ __forceinline__ void su2_to_spin1(const Res<2, 
 }
 
 // ---- general spin-one exponentiator (readings R19, R20) -----------------------
-// exp(−iH) for H = Σ a_j A_j over (Jx, Jy, Jz, Q, U1, U2, V1, V2): Lie–Trotter U = T^n, n = 2^τ, with the leapfrog
-// factor T = e^{−iD/2} e^{−iX/2} e^{−iY} e^{−iX/2} e^{−iD/2} (arguments ÷ n), D = diagonal part, X = (0,1)/(1,2)
-// part, Y = (0,2) part; closed forms e^{−iX} = I − i (sin r/r) X + ((cos r − 1)/r²) X² (X³ = r² X).  At au = av = 0
-// it is the paper's T.  No symmetric-matrix shortcut exists for general su(3) (time-reversal is broken), so
-// the τ residual squarings are dense: res_square3, 93 FP64 instructions.
+// exp(−iH) for H = Σ a_j A_j over (Jx, Jy, Jz, Q, U1, U2, V1, V2): Lie–Trotter U = T^n, n = 2^τ.  H is brought to
+// real symmetric tridiagonal form S = W†HW by W = diag(1, g), g = G·diag(1, e^{iψ}) with
+// G = [[H01*, −H02], [H02*, H01]]/r, r = √(|H01|² + |H02|²), and e^{iψ} = B12*/|B12| for B = G†H_blk G (reading R20);
+// the factor is T = W T₀ W†, T₀ = e^{−iD/2} e^{−iX} e^{−iD/2} on S/n (the paper's Eq. lie_trotter_4 shape).  T₀ is
+// complex symmetric and unitary, so its τ squarings take the scaled double-angle form (39 instructions, §5 item 13)
+// and W is applied once at the end: (W T₀ W†)^n − I = W (T₀^n − I) W† (DESIGN.md §5 item 14).
 
 // sin r / r and (cos r − 1)/r² from r² (both even): series for r ≤ 2^-4 (truncation < 1e-19 relative), else library.
 template <typename T> __device__ __forceinline__ void sinc_cosm1(T r2, T* sinc, T* cm) {
@@ -783,185 +803,169 @@ template <typename T> __device__ __forceinline__ void sinc_cosm1(T r2, T* sinc, 
   }
 }
 
-// (a + 2I)·a for a general 3×3 complex residual, 93 FP64 instructions: s_ii = (a_ii + 2) a_ii + Σ_{k≠i} a_ik a_ki;
-// s_ij = a_ij (a_ii + a_jj + 2) + a_ik a_kj (k the third index); the three pair sums a_ii + a_jj + 2 are shared.
-template <typename T> __device__ __forceinline__ void res_square3(Res<3, T>& a) {
-  const T two = splat<T>(2.0);
-  T d[3];
-#pragma unroll
-  for (int i = 0; i < 3; ++i) d[i] = a.re[4 * i] + two;
-  T pr[3], pi[3];           // pair sums for (0,1), (0,2), (1,2)
-  pr[0] = d[0] + a.re[4]; pi[0] = a.im[0] + a.im[4];
-  pr[1] = d[0] + a.re[8]; pi[1] = a.im[0] + a.im[8];
-  pr[2] = d[1] + a.re[8]; pi[2] = a.im[4] + a.im[8];
-  Res<3, T> s;
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    const int ii = 4 * i;
-    T r = d[i] * a.re[ii], m = d[i] * a.im[ii];
-    r = fmaT(-a.im[ii], a.im[ii], r);
-    m = fmaT(a.im[ii], a.re[ii], m);
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      if (k == i) continue;
-      const int ik = 3 * i + k, ki = 3 * k + i;
-      r = fmaT(a.re[ik], a.re[ki], r);
-      r = fmaT(-a.im[ik], a.im[ki], r);
-      m = fmaT(a.re[ik], a.im[ki], m);
-      m = fmaT(a.im[ik], a.re[ki], m);
-    }
-    s.re[ii] = r;
-    s.im[ii] = m;
+template <typename T> struct Su3W {   // the (1,2) block g of W = diag(1, g), pre-scaled by ½ (see su3_expand)
+  T g11r, g11i, g12r, g12i, g21r, g21i, g22r, g22i;
+};
+
+// S = W†HW from the unscaled coefficients a[8]: diagonal (s0, s1, s2), off-diagonals al = S01 = r, be = S12 ≥ 0.
+// With P = H01 H12 H02*:  B11 = (|H01|² d1 + |H02|² d2 + 2 Re P)/r²,  B22 = d1 + d2 − B11 (trace kept exact),
+// B12 = (H01 H02 (d2 − d1) + H01² H12 − H02² H12*)/r².
+template <typename T>
+__device__ __forceinline__ void su3_tridiagonalise(const T* a, T& s0, T& s1, T& s2, T& al, T& be, Su3W<T>& w) {
+  const T k = T(kRsqrt2);
+  const T d0 = a[2] + a[3] * T(kThird), d1 = T(-2) * a[3] * T(kThird), d2 = a[3] * T(kThird) - a[2];
+  const T ar = (a[0] + a[6]) * k, ai = -(a[1] + a[7]) * k;        // H01
+  const T br = (a[0] - a[6]) * k, bi = -(a[1] - a[7]) * k;        // H12
+  const T gr = a[4], gi = -a[5];                                  // H02
+  const T n01 = fmaT(ar, ar, ai * ai), n02 = fmaT(gr, gr, gi * gi), r2 = n01 + n02;
+  T b12r = br, b12i = bi;
+  s0 = d0; s1 = d1; s2 = d2; al = T(0);
+  w.g11r = T(0.5); w.g11i = T(0); w.g12r = T(0); w.g12i = T(0);
+  w.g21r = T(0);   w.g21i = T(0); w.g22r = T(0.5); w.g22i = T(0);
+  if (r2 > T(0)) {
+    const T ir = rsqrtT(r2), ir2 = ir * ir;
+    al = r2 * ir;
+    // H01·H12, then Re(H01 H12 H02*)
+    const T pr = fmaT(ar, br, -ai * bi), pi = fmaT(ar, bi, ai * br);
+    const T reP = fmaT(pr, gr, pi * gi);
+    s1 = fmaT(n01, d1, fmaT(n02, d2, reP + reP)) * ir2;
+    s2 = (d1 + d2) - s1;
+    // B12·r² = H01 H02 (d2 − d1) + H01² H12 − H02² H12*
+    const T dd = d2 - d1;
+    const T agr = fmaT(ar, gr, -ai * gi), agi = fmaT(ar, gi, ai * gr);        // H01 H02
+    const T a2r = fmaT(ar, ar, -ai * ai), a2i = T(2) * ar * ai;              // H01²
+    const T g2r = fmaT(gr, gr, -gi * gi), g2i = T(2) * gr * gi;              // H02²
+    T xr = fmaT(agr, dd, fmaT(a2r, br, -a2i * bi));
+    T xi = fmaT(agi, dd, fmaT(a2r, bi, a2i * br));
+    xr = fmaT(-g2r, br, fmaT(-g2i, bi, xr));                                 // − H02² H12*  (H12* = br − i bi)
+    xi = fmaT(-g2i, br, fmaT(g2r, bi, xi));
+    b12r = xr * ir2; b12i = xi * ir2;
+    const T hr = T(0.5) * ir;
+    w.g11r = ar * hr;  w.g11i = -ai * hr;        // H01*/r
+    w.g21r = gr * hr;  w.g21i = -gi * hr;        // H02*/r
+    w.g12r = -gr * hr; w.g12i = -gi * hr;        // −H02/r
+    w.g22r = ar * hr;  w.g22i = ai * hr;         // H01/r
   }
-#pragma unroll
-  for (int i = 0; i < 3; ++i)
-#pragma unroll
-    for (int j = 0; j < 3; ++j) {
-      if (i == j) continue;
-      const int k = 3 - i - j;
-      const int pj = (i + j == 1) ? 0 : (i + j == 2 ? 1 : 2);
-      const int ij = 3 * i + j, ik = 3 * i + k, kj = 3 * k + j;
-      T r = a.re[ik] * a.re[kj], m = a.re[ik] * a.im[kj];
-      r = fmaT(-a.im[ik], a.im[kj], r);
-      m = fmaT(a.im[ik], a.re[kj], m);
-      r = fmaT(a.re[ij], pr[pj], r);
-      r = fmaT(-a.im[ij], pi[pj], r);
-      m = fmaT(a.re[ij], pi[pj], m);
-      m = fmaT(a.im[ij], pr[pj], m);
-      s.re[ij] = r;
-      s.im[ij] = m;
-    }
-  a = s;
+  const T nb = fmaT(b12r, b12r, b12i * b12i);
+  be = T(0);
+  if (nb > T(0)) {                               // column 2 of g times e^{iψ} = B12*/|B12|
+    const T ib = rsqrtT(nb);
+    be = nb * ib;
+    const T er = b12r * ib, ei = -b12i * ib;
+    const T x12r = fmaT(w.g12r, er, -w.g12i * ei), x12i = fmaT(w.g12r, ei, w.g12i * er);
+    const T x22r = fmaT(w.g22r, er, -w.g22i * ei), x22i = fmaT(w.g22r, ei, w.g22i * er);
+    w.g12r = x12r; w.g12i = x12i; w.g22r = x22r; w.g22i = x22i;
+  }
 }
 
-// T − I of the general leapfrog factor for coefficients a[8] (divided by n = 2^τ inside).
-template <typename T> __device__ __forceinline__ void trotter_init_su3(const T* a, int tau, Res<3, T>& out) {
+// T₀ − I for T₀ = e^{−iD/2} e^{−iX} e^{−iD/2}, D = diag(s)/n, X = tridiagonal (al, be)/n, in the scaled form (2x, −2y)
+// that sym_square_s carries.  Taylor branch as trotter_init (T₀ − I = −iA − A²/2 below taylor_bound); otherwise
+// T₀_ij = e_i E_ij e_j with e_i = e^{−is_i/2}, E = e^{−iX} = I − iσX + K X² (σ = sin ρ/ρ, K = (cos ρ − 1)/ρ²,
+// ρ² = al² + be²; X² = [[al², 0, al·be], [0, ρ², 0], [al·be, 0, be²]]).
+template <typename T>
+__device__ __forceinline__ void su3_init(const T* a, int tau, Sym3<T>& m, Su3W<T>& w) {
+  T s0, s1, s2, al, be;
+  su3_tridiagonalise<T>(a, s0, s1, s2, al, be, w);
   const T inv_n = ldexp(T(1), -tau);
-  const T z = a[2] * inv_n, q = a[3] * inv_n;
-  const T th[3] = {z + q * T(kThird), T(-2) * q * T(kThird), q * T(kThird) - z};   // diag(D)
-  {
-    T sum = T(0);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) sum += fabs(a[j]);
-    if (sum * inv_n <= taylor_bound<T>()) {
-      // T − I = −iA − A²/2 (palindromic product, see taylor_bound), A = H/n Hermitian with diagonal th[],
-      // A01 = α, A12 = β, A02 = γ:  (A²)_ii as below, (A²)01 = α(d0 + d1) + γβ*, (A²)12 = β(d1 + d2) + α*γ,
-      // (A²)02 = γ(d0 + d2) + αβ.
-      const T k2 = inv_n * T(kRsqrt2);
-      const T ar = (a[0] + a[6]) * k2, ai = -(a[1] + a[7]) * k2;
-      const T br = (a[0] - a[6]) * k2, bi = -(a[1] - a[7]) * k2;
-      const T gr = a[4] * inv_n, gi = -a[5] * inv_n;
-      const T na = fmaT(ar, ar, ai * ai), nb = fmaT(br, br, bi * bi), ng = fmaT(gr, gr, gi * gi);
-      const T mh = T(-0.5);
-      out.re[0] = mh * fmaT(th[0], th[0], na + ng);   out.im[0] = -th[0];
-      out.re[4] = mh * fmaT(th[1], th[1], na + nb);   out.im[4] = -th[1];
-      out.re[8] = mh * fmaT(th[2], th[2], nb + ng);   out.im[8] = -th[2];
-      const T s01 = th[0] + th[1], s12 = th[1] + th[2], s02 = th[0] + th[2];
-      // (A²)01 = α s01 + γ β*
-      const T p01r = fmaT(ar, s01, fmaT(gr, br, gi * bi)), p01i = fmaT(ai, s01, fmaT(gi, br, -gr * bi));
-      // (A²)12 = β s12 + α* γ
-      const T p12r = fmaT(br, s12, fmaT(ar, gr, ai * gi)), p12i = fmaT(bi, s12, fmaT(ar, gi, -ai * gr));
-      // (A²)02 = γ s02 + α β
-      const T p02r = fmaT(gr, s02, fmaT(ar, br, -ai * bi)), p02i = fmaT(gi, s02, fmaT(ar, bi, ai * br));
-      // (i,j): −i A_ij − (A²)_ij/2 ;  (j,i): −i conj(A_ij) − conj((A²)_ij)/2
-      out.re[1] = fmaT(mh, p01r, ai);    out.im[1] = fmaT(mh, p01i, -ar);
-      out.re[3] = fmaT(mh, p01r, -ai);   out.im[3] = fmaT(-mh, p01i, -ar);
-      out.re[5] = fmaT(mh, p12r, bi);    out.im[5] = fmaT(mh, p12i, -br);
-      out.re[7] = fmaT(mh, p12r, -bi);   out.im[7] = fmaT(-mh, p12i, -br);
-      out.re[2] = fmaT(mh, p02r, gi);    out.im[2] = fmaT(mh, p02i, -gr);
-      out.re[6] = fmaT(mh, p02r, -gi);   out.im[6] = fmaT(-mh, p02i, -gr);
-      return;
-    }
+  s0 *= inv_n; s1 *= inv_n; s2 *= inv_n; al *= inv_n; be *= inv_n;
+  if ((fabs(s0) + fabs(s1) + fabs(s2) + T(2) * (al + be)) <= taylor_bound<T>()) {
+    // (2x, −2y) = (−A², 2A), A = S/n:  A² = [[s0² + al², al(s0 + s1), al·be], [·, s1² + al² + be², be(s1 + s2)],
+    // [·, ·, s2² + be²]]
+    const T al2 = al * al, be2 = be * be;
+    m.r00 = -fmaT(s0, s0, al2);         m.i00 = s0 + s0;
+    m.r11 = -fmaT(s1, s1, al2 + be2);   m.i11 = s1 + s1;
+    m.r22 = -fmaT(s2, s2, be2);         m.i22 = s2 + s2;
+    m.r01 = -(al * (s0 + s1));          m.i01 = al + al;
+    m.r12 = -(be * (s1 + s2));          m.i12 = be + be;
+    m.r02 = -(al * be);                 m.i02 = T(0);
+    return;
   }
-  // half-angle phases e_i = e^{−iθ_i/2} = (ch_i, −sh_i)
   T sh[3], ch[3];
-  {
-    const T big = fmax(fmax(fabs(th[0]), fabs(th[1])), fabs(th[2]));
-    if (big <= T(1.9073486328125e-06)) {          // half-angles ≤ 2^-20 (as trotter_init)
+  const T sd[3] = {s0, s1, s2};
+  const T big = fmax(fmax(fabs(s0), fabs(s1)), fabs(s2));
+  if (big <= T(1.9073486328125e-06)) {          // half-angles ≤ 2^-20 (as trotter_init)
 #pragma unroll
-      for (int i = 0; i < 3; ++i) sincos_tiny<T>(th[i] * T(0.5), &sh[i], &ch[i]);
-    } else if (big <= T(0.03125)) {               // half-angles ≤ 2^-6
+    for (int i = 0; i < 3; ++i) sincos_tiny<T>(sd[i] * T(0.5), &sh[i], &ch[i]);
+  } else if (big <= T(0.03125)) {                // half-angles ≤ 2^-6: polynomial
 #pragma unroll
-      for (int i = 0; i < 3; ++i) sincos_small<T>(th[i] * T(0.5), &sh[i], &ch[i]);
-    } else {
+    for (int i = 0; i < 3; ++i) sincos_small<T>(sd[i] * T(0.5), &sh[i], &ch[i]);
+  } else {
 #pragma unroll
-      for (int i = 0; i < 3; ++i) sincosT(th[i] * T(0.5), &sh[i], &ch[i]);
-    }
+    for (int i = 0; i < 3; ++i) sincosT(sd[i] * T(0.5), &sh[i], &ch[i]);
   }
-  // X/2: α = H01/2, β = H12/2 with H01 = (ax + av1 − i(ay + av2))/√2, H12 = (ax − av1 − i(ay − av2))/√2
-  const T kx = inv_n * T(0.5 * kRsqrt2);
-  const T ar = (a[0] + a[6]) * kx, ai = -(a[1] + a[7]) * kx;
-  const T br = (a[0] - a[6]) * kx, bi = -(a[1] - a[7]) * kx;
-  const T na = fmaT(ar, ar, ai * ai), nb = fmaT(br, br, bi * bi);
-  T sx, cx;
-  sinc_cosm1<T>(na + nb, &sx, &cx);
-  // Y: γ = H02 = au1 − i au2
-  const T gr = a[4] * inv_n, gi = -a[5] * inv_n;
-  const T ng = fmaT(gr, gr, gi * gi);
-  T sy, cy;
-  sinc_cosm1<T>(ng, &sy, &cy);
-  // t = e^{−iX/2} − I = −i sinc X + cm X²;  u = e^{−iY} − I
-  Res<3, T> t;
-  t.re[0] = cx * na;          t.im[0] = T(0);
-  t.re[4] = cx * (na + nb);   t.im[4] = T(0);
-  t.re[8] = cx * nb;          t.im[8] = T(0);
-  t.re[1] = sx * ai;          t.im[1] = -sx * ar;          // −i sinc α
-  t.re[3] = -sx * ai;         t.im[3] = -sx * ar;          // −i sinc α*
-  t.re[5] = sx * bi;          t.im[5] = -sx * br;          // −i sinc β
-  t.re[7] = -sx * bi;         t.im[7] = -sx * br;          // −i sinc β*
-  t.re[2] = cx * fmaT(ar, br, -ai * bi);  t.im[2] = cx * fmaT(ar, bi, ai * br);    // cm αβ
-  t.re[6] = t.re[2];                      t.im[6] = -t.im[2];                      // cm α*β*
-  const T u0 = cy * ng;                                                            // u00 = u22 (real)
-  const T u02r = sy * gi, u02i = -sy * gr, u20r = -sy * gi, u20i = -sy * gr;       // −i sinc γ, −i sinc γ*
-  // w = t + u + t·u (u has entries only at (0,0), (0,2), (2,0), (2,2))
-  Res<3, T> w;
+  T sg, K;
+  sinc_cosm1<T>(fmaT(al, al, be * be), &sg, &K);
+  const T Ed[3] = {K * al * al, K * fmaT(al, al, be * be), K * be * be};      // E_ii − 1
+  T dr[3], di[3];
 #pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    const T t0r = t.re[3 * i], t0i = t.im[3 * i], t2r = t.re[3 * i + 2], t2i = t.im[3 * i + 2];
-    // column 0: t_i0 (1 + u00) + t_i2 u20 + u_i0
-    T r = fmaT(t0r, u0, t0r), m = fmaT(t0i, u0, t0i);
-    r = fmaT(t2r, u20r, fmaT(-t2i, u20i, r));
-    m = fmaT(t2r, u20i, fmaT(t2i, u20r, m));
-    if (i == 0) r += u0;
-    if (i == 2) { r += u20r; m += u20i; }
-    w.re[3 * i] = r; w.im[3 * i] = m;
-    // column 2: t_i0 u02 + t_i2 (1 + u22) + u_i2
-    r = fmaT(t2r, u0, t2r); m = fmaT(t2i, u0, t2i);
-    r = fmaT(t0r, u02r, fmaT(-t0i, u02i, r));
-    m = fmaT(t0r, u02i, fmaT(t0i, u02r, m));
-    if (i == 2) r += u0;
-    if (i == 0) { r += u02r; m += u02i; }
-    w.re[3 * i + 2] = r; w.im[3 * i + 2] = m;
-    w.re[3 * i + 1] = t.re[3 * i + 1]; w.im[3 * i + 1] = t.im[3 * i + 1];
+  for (int i = 0; i < 3; ++i) {                  // e_i² E_ii − 1 = (v − i s2)(1 + E) + E, v − i s2 = expm1(−is_i)
+    const T v = T(-2) * sh[i] * sh[i], s2i = T(2) * sh[i] * ch[i];
+    dr[i] = fmaT(v, Ed[i], v + Ed[i]);
+    di[i] = -s2i * (T(1) + Ed[i]);
   }
-  Res<3, T> mm;               // M − I = (I + w)(I + t) − I
-  res_mul<3, T>(w, t, mm);
-  // T − I = E_D M E_D − I: diagonal expm1(−iθ_i) + e^{−iθ_i} m_ii, off-diagonal e_i e_j m_ij
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    const T xr = T(-2) * sh[i] * sh[i], xi = T(-2) * sh[i] * ch[i];       // expm1(−iθ_i)
-    const int ii = 4 * i;
-    const T mr = mm.re[ii], mi = mm.im[ii];
-    out.re[ii] = xr + mr + (xr * mr - xi * mi);
-    out.im[ii] = xi + mi + (xr * mi + xi * mr);
-  }
-#pragma unroll
-  for (int i = 0; i < 3; ++i)
-#pragma unroll
-    for (int j = 0; j < 3; ++j) {
-      if (i == j) continue;
-      // e_i e_j = (ch_i − i sh_i)(ch_j − i sh_j)
-      const T er = ch[i] * ch[j] - sh[i] * sh[j], ei = -(sh[i] * ch[j] + ch[i] * sh[j]);
-      const int ij = 3 * i + j;
-      out.re[ij] = er * mm.re[ij] - ei * mm.im[ij];
-      out.im[ij] = er * mm.im[ij] + ei * mm.re[ij];
-    }
+  // e_i e_j = (c_ij, −s_ij), c_ij = cos((s_i + s_j)/2), s_ij = sin((s_i + s_j)/2)
+  const T c01 = fmaT(ch[0], ch[1], -sh[0] * sh[1]), s01 = fmaT(sh[0], ch[1], ch[0] * sh[1]);
+  const T c12 = fmaT(ch[1], ch[2], -sh[1] * sh[2]), s12 = fmaT(sh[1], ch[2], ch[1] * sh[2]);
+  const T c02 = fmaT(ch[0], ch[2], -sh[0] * sh[2]), s02 = fmaT(sh[0], ch[2], ch[0] * sh[2]);
+  const T xa = sg * al, xb = sg * be, kab = K * al * be;
+  // scaled: real parts ×2, imaginary parts ×(−2)
+  m.r00 = T(2) * dr[0];  m.i00 = T(-2) * di[0];
+  m.r11 = T(2) * dr[1];  m.i11 = T(-2) * di[1];
+  m.r22 = T(2) * dr[2];  m.i22 = T(-2) * di[2];
+  m.r01 = T(-2) * xa * s01;  m.i01 = T(2) * xa * c01;      // (c − is)(−iσal) = σal(−s − ic)
+  m.r12 = T(-2) * xb * s12;  m.i12 = T(2) * xb * c12;
+  m.r02 = T(2) * kab * c02;  m.i02 = T(2) * kab * s02;     // (c − is) K al be
+}
+
+// e = W (T₀^n − I) W† from the scaled symmetric residual (x̃, ỹ): Z̃ = x̃ − iỹ = 2(T₀^n − I), and g in w already
+// carries the ½, so e = diag(½, g/2)·Z̃·diag(1, g)†.  24 complex multiply-adds.
+template <typename T>
+__device__ __forceinline__ void su3_expand(const Sym3<T>& m, const Su3W<T>& w, Res<3, T>& e) {
+  // z_ij = (m.rij, −m.iij)
+  const T z01r = m.r01, z01i = -m.i01, z02r = m.r02, z02i = -m.i02;
+  const T z11r = m.r11, z11i = -m.i11, z12r = m.r12, z12i = -m.i12, z22r = m.r22, z22i = -m.i22;
+  // full g = 2·(w) for the right factor g†
+  const T G11r = T(2) * w.g11r, G11i = T(2) * w.g11i, G12r = T(2) * w.g12r, G12i = T(2) * w.g12i;
+  const T G21r = T(2) * w.g21r, G21i = T(2) * w.g21i, G22r = T(2) * w.g22r, G22i = T(2) * w.g22i;
+  e.re[0] = T(0.5) * m.r00;  e.im[0] = T(-0.5) * m.i00;
+  // row 0: M0j = ½ Σ_k z0k conj(G_jk)
+  const T hz01r = T(0.5) * z01r, hz01i = T(0.5) * z01i, hz02r = T(0.5) * z02r, hz02i = T(0.5) * z02i;
+  e.re[1] = fmaT(hz01r, G11r, fmaT(hz01i, G11i, fmaT(hz02r, G12r, hz02i * G12i)));
+  e.im[1] = fmaT(hz01i, G11r, fmaT(-hz01r, G11i, fmaT(hz02i, G12r, -hz02r * G12i)));
+  e.re[2] = fmaT(hz01r, G21r, fmaT(hz01i, G21i, fmaT(hz02r, G22r, hz02i * G22i)));
+  e.im[2] = fmaT(hz01i, G21r, fmaT(-hz01r, G21i, fmaT(hz02i, G22r, -hz02r * G22i)));
+  // column 0: Mj0 = Σ_k (g_jk/2) zk0
+  e.re[3] = fmaT(w.g11r, z01r, fmaT(-w.g11i, z01i, fmaT(w.g12r, z02r, -w.g12i * z02i)));
+  e.im[3] = fmaT(w.g11r, z01i, fmaT(w.g11i, z01r, fmaT(w.g12r, z02i, w.g12i * z02r)));
+  e.re[6] = fmaT(w.g21r, z01r, fmaT(-w.g21i, z01i, fmaT(w.g22r, z02r, -w.g22i * z02i)));
+  e.im[6] = fmaT(w.g21r, z01i, fmaT(w.g21i, z01r, fmaT(w.g22r, z02i, w.g22i * z02r)));
+  // block: N = (g/2) Zb, Mb = N g†
+  const T n11r = fmaT(w.g11r, z11r, fmaT(-w.g11i, z11i, fmaT(w.g12r, z12r, -w.g12i * z12i)));
+  const T n11i = fmaT(w.g11r, z11i, fmaT(w.g11i, z11r, fmaT(w.g12r, z12i, w.g12i * z12r)));
+  const T n12r = fmaT(w.g11r, z12r, fmaT(-w.g11i, z12i, fmaT(w.g12r, z22r, -w.g12i * z22i)));
+  const T n12i = fmaT(w.g11r, z12i, fmaT(w.g11i, z12r, fmaT(w.g12r, z22i, w.g12i * z22r)));
+  const T n21r = fmaT(w.g21r, z11r, fmaT(-w.g21i, z11i, fmaT(w.g22r, z12r, -w.g22i * z12i)));
+  const T n21i = fmaT(w.g21r, z11i, fmaT(w.g21i, z11r, fmaT(w.g22r, z12i, w.g22i * z12r)));
+  const T n22r = fmaT(w.g21r, z12r, fmaT(-w.g21i, z12i, fmaT(w.g22r, z22r, -w.g22i * z22i)));
+  const T n22i = fmaT(w.g21r, z12i, fmaT(w.g21i, z12r, fmaT(w.g22r, z22i, w.g22i * z22r)));
+  // M_jl = N_j1 conj(G_l1) + N_j2 conj(G_l2)
+  e.re[4] = fmaT(n11r, G11r, fmaT(n11i, G11i, fmaT(n12r, G12r, n12i * G12i)));
+  e.im[4] = fmaT(n11i, G11r, fmaT(-n11r, G11i, fmaT(n12i, G12r, -n12r * G12i)));
+  e.re[5] = fmaT(n11r, G21r, fmaT(n11i, G21i, fmaT(n12r, G22r, n12i * G22i)));
+  e.im[5] = fmaT(n11i, G21r, fmaT(-n11r, G21i, fmaT(n12i, G22r, -n12r * G22i)));
+  e.re[7] = fmaT(n21r, G11r, fmaT(n21i, G11i, fmaT(n22r, G12r, n22i * G12i)));
+  e.im[7] = fmaT(n21i, G11r, fmaT(-n21r, G11i, fmaT(n22i, G12r, -n22r * G12i)));
+  e.re[8] = fmaT(n21r, G21r, fmaT(n21i, G21i, fmaT(n22r, G22r, n22i * G22i)));
+  e.im[8] = fmaT(n21i, G21r, fmaT(-n21r, G21i, fmaT(n22i, G22r, -n22r * G22i)));
 }
 
 template <typename T> __device__ __forceinline__ void trotter_residual_su3(const T* a, int tau, Res<3, T>& e) {
-  trotter_init_su3<T>(a, tau, e);
+  Sym3<T> m;
+  Su3W<T> w;
+  su3_init<T>(a, tau, m, w);
   SS_UNROLL(SS_SQ_UNROLL)
-  for (int it = 0; it < tau; ++it) res_square3<T>(e);
+  for (int it = 0; it < tau; ++it) lt_square<T>(m);
+  su3_expand<T>(m, w, e);
 }
 
 template <int SPIN, int EXPO, typename T> struct Expo;

@@ -50,14 +50,14 @@ def test_device_arm_contract():
 
 def test_flop_model():
     """The per-fine-step flop counts bench.py reports, re-derived from the instruction mix of each
-    formulation: scaled double-angle symmetric squaring 24 DFMA + 12 DMUL + 3 DADD = 63 flop, dense su(3) squaring
-    66 DFMA + 18 DMUL +
-    9 DADD = 159, 3×3 residual product 219, SU(2) group-law product 16 DFMA + 4 DADD = 36."""
+    formulation: scaled double-angle symmetric squaring 24 DFMA + 12 DMUL + 3 DADD = 63 flop (also on the
+    tridiagonalised su(3) factor, plus its conjugation by W: 24 complex multiply-adds × 8 = 192), 3×3 residual product
+    219, SU(2) group-law product 16 DFMA + 4 DADD = 36."""
     sys.path.insert(0, ROOT)
     import bench
-    sym, dense3, prod3, prod2 = 2 * 24 + 12 + 3, 2 * 66 + 18 + 9, 219, 2 * 16 + 4
+    sym, conj3, prod3, prod2 = 2 * 24 + 12 + 3, 24 * 8, 219, 2 * 16 + 4
     assert bench.algorithmic_flops_per_fine_step("one", "lie_trotter", 24) == 2 * (24 * sym + prod3)
-    assert bench.algorithmic_flops_per_fine_step("one", "lie_trotter_su3", 24) == 2 * (24 * dense3 + prod3)
+    assert bench.algorithmic_flops_per_fine_step("one", "lie_trotter_su3", 24) == 2 * (24 * sym + conj3 + prod3)
     half = 193                         # ncu-executed per spin-half step (2 × (26 + prod2) = 124 of it in the products)
     assert 2 * (26 + prod2) < half
     assert bench.algorithmic_flops_per_fine_step("half", "analytic", 24) == half
