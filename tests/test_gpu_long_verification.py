@@ -49,3 +49,15 @@ def test_c3_sampled_sweeps_every_state(orc):
     err = np.abs(st_g[idx] - st_o).max()
     print(f"\nC3: 32 sweeps x 10001 states: max |dpsi| = {err:.3e}")
     assert err <= 1e-10
+
+
+def test_g1_sampled_sweeps_every_state(orc):
+    """G1 (general spin-one, su(3) Lie–Trotter) complete GPU run; 32 sweeps compared state by state with the oracle."""
+    w = W.g1_su3()
+    st_g = _run(w)
+    idx = np.linspace(0, w.batch - 1, 32).astype(int)
+    st_o, _ = orc.evaluate(w.spin, w.method, w.expo, w.tau, w.frame, w.field, sweep=w.sweep[idx], t0=w.t0, t1=w.t1,
+                           dt_int=w.dt_int, dt_out=w.dt_out, psi0=w.psi0[idx], want_unitaries=False)
+    err = np.abs(st_g[idx] - st_o).max()
+    print(f"\nG1: 32 sweeps x {st_g.shape[1]} states: max |dpsi| = {err:.3e}")
+    assert err <= 1e-10
