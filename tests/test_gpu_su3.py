@@ -34,13 +34,18 @@ def parity(ss, orc, w, precision="fp64", tol=TOL64):
     return eU, eS
 
 
-@pytest.mark.parametrize("scale", [2.0, 0.015, 0.01, 1e-3, 1e-7])      # 0.015 / 0.01 straddle the Taylor bound
+@pytest.mark.parametrize("scale", [2.0, 0.03, 0.025, 0.01, 1e-3, 1e-7])   # 0.03 / 0.025 straddle the Taylor bound
 def test_su3_exponentiator_parity(ss, orc, scale):
     a = W.random_exponent_args_su3(5000, scale, seed=31)
     a[:2] = 0.0                                   # exact zero (identity)
     a[2, [0, 1, 4, 5, 6, 7]] = 0.0                # diagonal only
     a[3, [4, 5]] = 0.0                            # no (0,2) coupling
     a[4, [0, 1, 6, 7]] = 0.0                      # (0,2) coupling only
+    a[5, [4, 5]] = 0.0                            # H01 = H02 = 0 (r = 0: W is the phase alone, reading R20)
+    a[5, [6, 7]] = -a[5, [0, 1]]
+    a[6, [6, 7]] = a[6, [0, 1]]                   # H12 = 0
+    a[7, [6, 7]] = a[7, [0, 1]]                   # H12 = 0 and H02 = 0: B12 = 0 (no phase)
+    a[7, [4, 5]] = 0.0
     ref = orc.exponentiate("one", a, "lie_trotter_su3", 24)
     for prec, tol in (("fp64", 4e-15 * max(1.0, scale)), ("fp32", 2e-6)):
         sim = ss.Simulator("one", "cf4", "lie_trotter_su3", 24, True, prec, "su3_constant")
