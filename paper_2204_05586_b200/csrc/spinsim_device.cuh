@@ -807,51 +807,81 @@ template <typename T> struct Su3W {   // the (1,2) block g of W = diag(1, g), pr
   T g11r, g11i, g12r, g12i, g21r, g21i, g22r, g22i;
 };
 
+// v ← v/|v|, returns |v| (0 for v = 0, v then unchanged).  When |v|² leaves the normal range (components below
+// ≈ 1e-19 in FP32 / 1e-154 in FP64, where a subnormal |v|² keeps only a few bits and W would stop being unitary) the
+// components are first rescaled by an exact power of two.
+template <typename T> __device__ __forceinline__ T norm_lo();
+template <typename T> __device__ __forceinline__ T norm_hi();
+template <> __device__ __forceinline__ double norm_lo<double>() { return 0x1p-960; }
+template <> __device__ __forceinline__ double norm_hi<double>() { return 0x1p960; }
+template <> __device__ __forceinline__ float norm_lo<float>() { return 0x1p-100f; }
+template <> __device__ __forceinline__ float norm_hi<float>() { return 0x1p100f; }
+template <int N, typename T> __device__ __forceinline__ T unit_vec(T (&v)[N]) {
+  T r2 = v[0] * v[0];
+#pragma unroll
+  for (int i = 1; i < N; ++i) r2 = fmaT(v[i], v[i], r2);
+  if (r2 >= norm_lo<T>() && r2 <= norm_hi<T>()) {
+    const T ir = rsqrtT(r2);
+#pragma unroll
+    for (int i = 0; i < N; ++i) v[i] *= ir;
+    return r2 * ir;
+  }
+  T m = fabs(v[0]);
+#pragma unroll
+  for (int i = 1; i < N; ++i) m = fmax(m, fabs(v[i]));
+  if (!(m > T(0))) return T(0);
+  const int e = ilogb(m);
+  const T sc = ldexp(T(1), -e);
+#pragma unroll
+  for (int i = 0; i < N; ++i) v[i] *= sc;
+  r2 = v[0] * v[0];
+#pragma unroll
+  for (int i = 1; i < N; ++i) r2 = fmaT(v[i], v[i], r2);
+  const T ir = rsqrtT(r2);
+#pragma unroll
+  for (int i = 0; i < N; ++i) v[i] *= ir;
+  return ldexp(r2 * ir, e);
+}
+
 // S = W†HW from the unscaled coefficients a[8]: diagonal (s0, s1, s2), off-diagonals al = S01 = r, be = S12 ≥ 0.
-// With P = H01 H12 H02*:  B11 = (|H01|² d1 + |H02|² d2 + 2 Re P)/r²,  B22 = d1 + d2 − B11 (trace kept exact),
-// B12 = (H01 H02 (d2 − d1) + H01² H12 − H02² H12*)/r².
+// With the unit pair u1 = H01/r, u2 = H02/r (all products below stay O(|H|)):
+// B11 = |u1|² d1 + |u2|² d2 + 2 Re(u1 H12 u2*),  B22 = d1 + d2 − B11 (trace kept exact),
+// B12 = u1 u2 (d2 − d1) + u1² H12 − u2² H12*.
 template <typename T>
 __device__ __forceinline__ void su3_tridiagonalise(const T* a, T& s0, T& s1, T& s2, T& al, T& be, Su3W<T>& w) {
   const T k = T(kRsqrt2);
   const T d0 = a[2] + a[3] * T(kThird), d1 = T(-2) * a[3] * T(kThird), d2 = a[3] * T(kThird) - a[2];
-  const T ar = (a[0] + a[6]) * k, ai = -(a[1] + a[7]) * k;        // H01
   const T br = (a[0] - a[6]) * k, bi = -(a[1] - a[7]) * k;        // H12
-  const T gr = a[4], gi = -a[5];                                  // H02
-  const T n01 = fmaT(ar, ar, ai * ai), n02 = fmaT(gr, gr, gi * gi), r2 = n01 + n02;
+  T u[4] = {(a[0] + a[6]) * k, -(a[1] + a[7]) * k, a[4], -a[5]};  // (H01, H02), normalised below
   T b12r = br, b12i = bi;
-  s0 = d0; s1 = d1; s2 = d2; al = T(0);
+  s0 = d0; s1 = d1; s2 = d2;
   w.g11r = T(0.5); w.g11i = T(0); w.g12r = T(0); w.g12i = T(0);
   w.g21r = T(0);   w.g21i = T(0); w.g22r = T(0.5); w.g22i = T(0);
-  if (r2 > T(0)) {
-    const T ir = rsqrtT(r2), ir2 = ir * ir;
-    al = r2 * ir;
-    // H01·H12, then Re(H01 H12 H02*)
-    const T pr = fmaT(ar, br, -ai * bi), pi = fmaT(ar, bi, ai * br);
-    const T reP = fmaT(pr, gr, pi * gi);
-    s1 = fmaT(n01, d1, fmaT(n02, d2, reP + reP)) * ir2;
+  al = unit_vec<4, T>(u);
+  if (al > T(0)) {
+    const T ur = u[0], ui = u[1], vr = u[2], vi = u[3];                     // u1 = H01/r, u2 = H02/r
+    const T pr = fmaT(ur, br, -ui * bi), pi = fmaT(ur, bi, ui * br);        // u1 H12
+    const T reP = fmaT(pr, vr, pi * vi);                                    // Re(u1 H12 u2*)
+    s1 = fmaT(fmaT(ur, ur, ui * ui), d1, fmaT(fmaT(vr, vr, vi * vi), d2, reP + reP));
     s2 = (d1 + d2) - s1;
-    // B12·r² = H01 H02 (d2 − d1) + H01² H12 − H02² H12*
     const T dd = d2 - d1;
-    const T agr = fmaT(ar, gr, -ai * gi), agi = fmaT(ar, gi, ai * gr);        // H01 H02
-    const T a2r = fmaT(ar, ar, -ai * ai), a2i = T(2) * ar * ai;              // H01²
-    const T g2r = fmaT(gr, gr, -gi * gi), g2i = T(2) * gr * gi;              // H02²
-    T xr = fmaT(agr, dd, fmaT(a2r, br, -a2i * bi));
-    T xi = fmaT(agi, dd, fmaT(a2r, bi, a2i * br));
-    xr = fmaT(-g2r, br, fmaT(-g2i, bi, xr));                                 // − H02² H12*  (H12* = br − i bi)
-    xi = fmaT(-g2i, br, fmaT(g2r, bi, xi));
-    b12r = xr * ir2; b12i = xi * ir2;
-    const T hr = T(0.5) * ir;
-    w.g11r = ar * hr;  w.g11i = -ai * hr;        // H01*/r
-    w.g21r = gr * hr;  w.g21i = -gi * hr;        // H02*/r
-    w.g12r = -gr * hr; w.g12i = -gi * hr;        // −H02/r
-    w.g22r = ar * hr;  w.g22i = ai * hr;         // H01/r
+    const T uvr = fmaT(ur, vr, -ui * vi), uvi = fmaT(ur, vi, ui * vr);      // u1 u2
+    const T u2r = fmaT(ur, ur, -ui * ui), u2i = T(2) * ur * ui;             // u1²
+    const T v2r = fmaT(vr, vr, -vi * vi), v2i = T(2) * vr * vi;             // u2²
+    const T xr = fmaT(uvr, dd, fmaT(u2r, br, -u2i * bi));
+    const T xi = fmaT(uvi, dd, fmaT(u2r, bi, u2i * br));
+    b12r = fmaT(-v2r, br, fmaT(-v2i, bi, xr));                              // − u2² H12*  (H12* = br − i bi)
+    b12i = fmaT(-v2i, br, fmaT(v2r, bi, xi));
+    const T h = T(0.5);
+    w.g11r = h * ur;   w.g11i = -h * ui;         // H01*/r
+    w.g21r = h * vr;   w.g21i = -h * vi;         // H02*/r
+    w.g12r = -h * vr;  w.g12i = -h * vi;         // −H02/r
+    w.g22r = h * ur;   w.g22i = h * ui;          // H01/r
   }
-  const T nb = fmaT(b12r, b12r, b12i * b12i);
-  be = T(0);
-  if (nb > T(0)) {                               // column 2 of g times e^{iψ} = B12*/|B12|
-    const T ib = rsqrtT(nb);
-    be = nb * ib;
-    const T er = b12r * ib, ei = -b12i * ib;
+  T q[2] = {b12r, b12i};
+  be = unit_vec<2, T>(q);
+  if (be > T(0)) {                               // column 2 of g times e^{iψ} = B12*/|B12|
+    const T er = q[0], ei = -q[1];
     const T x12r = fmaT(w.g12r, er, -w.g12i * ei), x12i = fmaT(w.g12r, ei, w.g12i * er);
     const T x22r = fmaT(w.g22r, er, -w.g22i * ei), x22i = fmaT(w.g22r, ei, w.g22i * er);
     w.g12r = x12r; w.g12i = x12i; w.g22r = x22r; w.g22i = x22i;

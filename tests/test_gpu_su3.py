@@ -53,6 +53,26 @@ def test_su3_exponentiator_parity(ss, orc, scale):
         assert np.abs(got - ref).max() <= tol, (prec, np.abs(got - ref).max())
 
 
+def test_su3_tiny_couplings(ss, orc):
+    """Couplings down to 1e-30 next to O(1) diagonals (FP32 subnormal range for |H01|², |H02|²): the similarity W of
+    reading R20 stays finite and unitary, so the exponential is the diagonal one plus the tiny coupling."""
+    a = np.zeros((6, 8))
+    a[:, 2], a[:, 3] = 0.7, -0.4
+    a[0, [0, 1]] = [1e-30, -2e-30]                 # H01 = H12 tiny
+    a[1, [4, 5]] = [3e-21, 1e-21]                  # H02 tiny
+    a[2, [0, 6]] = [1e-19, 1e-19]                  # H01 tiny-ish, H12 = 0
+    a[3, [0, 6]] = [0.3, -0.3 + 1e-18]             # H01 ≈ 1e-18, H12 ≈ 0.42
+    a[4, :] = 0.0
+    a[4, 4] = 1e-300                               # FP64 only: H02 at the bottom of the double range
+    a[5, [0, 4, 7]] = [1e-25, 0.2, 1e-25]
+    ref = orc.exponentiate("one", a, "lie_trotter_su3", 24)
+    for prec, tol in (("fp64", 4e-15), ("fp32", 2e-6)):
+        sim = ss.Simulator("one", "cf4", "lie_trotter_su3", 24, True, prec, "su3_constant")
+        got = sim.exponentiate(torch.from_numpy(a).cuda()).cpu().numpy()
+        assert np.isfinite(got).all(), prec
+        assert np.abs(got - ref).max() <= tol, (prec, np.abs(got - ref).max(axis=(1, 2)))
+
+
 @pytest.mark.parametrize("tau", [0, 1, 9, 24, 33])
 def test_su3_tau_parity(ss, orc, tau):
     a = W.random_exponent_args_su3(500, 0.5, seed=32)
