@@ -145,8 +145,8 @@ int plan_grid(double t0, double t1, double dt_int, double dt_out, int64_t* K, in
 #ifndef SS_FORCE_SPLIT
 #define SS_FORCE_SPLIT 0    // tuning experiments only: a fixed S (must divide L)
 #endif
-int choose_split(const ss_sim* s, int64_t n_total, int64_t L) {
-  if (SS_FORCE_SPLIT > 0 && L % SS_FORCE_SPLIT == 0) return SS_FORCE_SPLIT;
+// Interval-kernel threads resident on the device at once (one wave).
+double resident_threads(const ss_sim* s) {
   static int sms = 0;
   if (sms == 0) {
     int dev = 0;
@@ -155,8 +155,13 @@ int choose_split(const ss_sim* s, int64_t n_total, int64_t L) {
       sms = 148;
   }
   const bool su3 = s->d.exponentiation == SS_EXP_LIE_TROTTER_SU3;
+  return (double)sms * (su3 ? SS_INTERVAL_MINBLOCKS_SU3 : SS_INTERVAL_MINBLOCKS) * ssb::kIntervalThreads;
+}
+
+int choose_split(const ss_sim* s, int64_t n_total, int64_t L) {
+  if (SS_FORCE_SPLIT > 0 && L % SS_FORCE_SPLIT == 0) return SS_FORCE_SPLIT;
   const bool short_steps = s->dim == 2 || s->d.exponentiation == SS_EXP_ANALYTIC;
-  const double R = (double)sms * (su3 ? SS_INTERVAL_MINBLOCKS_SU3 : SS_INTERVAL_MINBLOCKS) * ssb::kIntervalThreads;
+  const double R = resident_threads(s);
   const double c0 = short_steps ? 2.5 : 0.15, c1 = short_steps ? 0.17 : 0.03;
   int best = 1;
   double best_t = 0.0;
@@ -533,7 +538,6 @@ int ss_evaluate_host(ss_sim* s, double t0, double t1, double dt_int, double dt_o
   if (batch < 1) return fail(SS_ERR_INVALID, "batch must be >= 1");
   if (!h_sweep || !h_psi0 || !h_states) return fail(SS_ERR_INVALID, "h_sweep, h_state_init, h_states must be non-NULL");
   if (n_chunks < 1) n_chunks = 1;
-  if (n_chunks > batch) n_chunks = (int32_t)batch;
   // host-side input validation (host data: no device round trip needed)
   const int qcol = (s->dim == 3 && s->d.exponentiation == SS_EXP_ANALYTIC) ? qcol_of(s->d.field) : -1;
   for (int64_t i = 0; i < batch * s->P; ++i) {
@@ -574,9 +578,15 @@ int ss_evaluate_host(ss_sim* s, double t0, double t1, double dt_int, double dt_o
     return r;
   };
   cudaStream_t cs = s->streams[0], xs = s->streams[1];
-  if (batch >= ssb::chain_min_batch() && n_chunks >= 6 && K >= 4 * (int64_t)n_chunks) {
-    // Large batches: chunk the TIME axis, all sweeps per chunk (the per-sweep chain kernel stays at full width and is
-    // sequential per sweep, so the states are bit-identical to one ss_evaluate).  Chunk c = intervals [k0, k0 + kc)
+  // Time chunks: large batches (the chain scan is sequential per sweep — bit-identical to ss_evaluate), and long
+  // sweeps of small batches whose interval work spans ≥ 6 waves per chunk on average (one sweep of 1e6 intervals,
+  // C4); there the single-sweep scan restarts from the carry each chunk, so states agree with ss_evaluate to
+  // rounding (a different product order), not bit for bit.
+  const bool big_batch = batch >= ssb::chain_min_batch();
+  const double waves = (double)batch * K * choose_split(s, batch * K, L) / resident_threads(s);
+  if (n_chunks >= 6 && K >= 4 * (int64_t)n_chunks && (big_batch || waves >= 6.0 * n_chunks)) {
+    // Chunk the TIME axis, all sweeps per chunk (for large batches the per-sweep chain kernel stays at full width and
+    // is sequential per sweep, so the states are bit-identical to one ss_evaluate).  Chunk c = intervals [k0, k0 + kc)
     // of every sweep, started from the running carry (the previous chunk's last states).  Tent-shaped sizes — small
     // first chunks so the device→host copies start early, small last ones so little copy is left exposed — with
     // weights 1, 2, 3, …, 3, 1, ½, ¼, ¼ and three staging slots (the copy of chunk c overlaps chunks c+1 and c+2).
@@ -643,6 +653,7 @@ int ss_evaluate_host(ss_sim* s, double t0, double t1, double dt_int, double dt_o
   }
   // Geometric chunks (B/2, B/4, …, the last two equal): early chunks are big (full-speed chain scan, long compute
   // that hides the previous chunk's D2H), the final chunk — whose D2H cannot be hidden — is small.
+  if (n_chunks > batch) n_chunks = (int32_t)batch;
   std::vector<int64_t> sizes;
   {
     int64_t left = batch;

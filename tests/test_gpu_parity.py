@@ -281,6 +281,22 @@ def test_host_api_time_chunks_match_device_api(ss):
         assert np.array_equal(st_h, st_d) and np.array_equal(U_h, U_d)
 
 
+def test_host_api_time_chunks_long_sweep(ss):
+    """A single long sweep (C4: 1e6 intervals, ≥ 6 waves of interval work per chunk) also takes the time-chunked host
+    pipeline: the operators are bit-identical to the device call, the states equal to rounding (the scan restarts
+    from the carry)."""
+    w = W.c4_long()
+    st_d, U_d = gpu_run(ss, w)
+    sim = ss.Simulator(w.spin, w.method, w.expo, w.tau, w.frame, "fp64", w.field)
+    for chunks in (6, 8):
+        st_h, U_h = sim.evaluate_host(w.sweep, w.t0, w.t1, w.dt_int, w.dt_out, w.psi0, want_unitaries=True,
+                                      n_chunks=chunks)
+        assert np.array_equal(U_h, U_d)
+        # two FP64 product orders over 1e6 intervals: each drifts ≈ 3e-11 from the exact chain (SURVEY §0.7,
+        # profiles/r01/long_verification*.txt); measured difference 5.5e-13
+        assert np.abs(st_h - st_d).max() <= 1e-11
+
+
 @pytest.mark.parametrize("which", ["C4", "C2", "G1"])
 def test_partition_reproduces_unitaries_bitwise(ss, which):
     """The time grid uses the global k (and the sub-interval split is chosen from the whole problem), so computing a
