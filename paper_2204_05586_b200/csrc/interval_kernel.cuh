@@ -118,7 +118,7 @@ __device__ __forceinline__ void interval_body(const IntervalParams& prm) {
       // exact sincos on anchor steps, rotation by e^{iωδt} in between (measured: +1.4 % on spin-one C3 despite
       // a few extra spill slots outside the squaring loops, +70 % on trig-bound spin-half)
       fld.sample_cf4(base, ANCHOR, PULSE, __dadd_rn(base, prm.g1dt), __dadd_rn(base, prm.g2dt), f1, f2);
-      if (prm.frame) frame2.apply<NC>(base, ANCHOR, f1, f2);
+      if (prm.frame) frame2.apply<NC, zero_y_of<Field<FIELD>>(nullptr)>(base, ANCHOR, f1, f2);
       // a4: H̄1 δt = (w+ f1 + w− f2) δt, H̄2 δt = (w− f1 + w+ f2) δt (Eqs. cf4_sample_1/2), δt folded into w±.
       T a1[NC], a2[NC];
 #pragma unroll

@@ -133,6 +133,11 @@ struct PhaseStepper {
 // starts at t_k + base (off1,2 = fl(base + fl(g1,2·δt))).  Fields with an RF phase evaluate one sincos at the step
 // base and reach both Gauss points by rotating with per-interval constants e^{iω g1,2 δt} (init_cf4) — the same
 // angle up to ~1e-15 rad at half the trigonometric work.
+// Fields whose y coefficient is identically zero declare kZeroY: the frame rotation then skips the terms in f[1]
+// (fma(c, 0, ·) and s·0 cannot be folded by the compiler under IEEE semantics; the result is the same to the bit).
+template <class F> __device__ constexpr bool zero_y_of(decltype(F::kZeroY)*) { return F::kZeroY; }
+template <class F> __device__ constexpr bool zero_y_of(...) { return false; }
+
 template <> struct Field<FIELD_CONSTANT> {
   double f0, f1, f2, f3;
   __device__ __forceinline__ void init(const double* p, double) { f0 = p[0]; f1 = p[1]; f2 = p[2]; f3 = p[3]; }
@@ -144,6 +149,7 @@ template <> struct Field<FIELD_CONSTANT> {
 };
 
 template <> struct Field<FIELD_RABI_LINEAR> {        // ω0 Jz + 2Ω cos(ω0 t) Jx
+  static constexpr bool kZeroY = true;               // f[1] ≡ 0 (the frame rotation specialises on it)
   double w0, two_om, ph0, c1, s1, c2, s2;
   PhaseStepper ps;
   __device__ __forceinline__ void init(const double* p, double t_k) {
@@ -189,6 +195,7 @@ template <> struct Field<FIELD_RABI_CIRCULAR> {      // ω0 Jz + Ω(cos(ω0 t) J
 
 template <> struct Field<FIELD_NEURAL> {
   // p = [ω_bias, ω_rf, Ω, Ω_p, ω_sig, t_p, ω_q] (reading R16)
+  static constexpr bool kZeroY = true;               // f[1] ≡ 0
   double wb, wrf, two_om, op, ws, wq, ph0, dtk, c1, s1, c2, s2;
   // Can a sample of this interval fall inside the signal pulse's single cycle (sinp ≠ 0)?  x = ω_sig(t_k − t_p + off)
   // is monotone in off ∈ [0, Δt]; the margin covers the rounding of the per-sample arguments.  Intervals outside
@@ -228,6 +235,7 @@ template <> struct Field<FIELD_NEURAL> {
 };
 
 template <> struct Field<FIELD_GRADIENT> {          // ω_z = x − 2y
+  static constexpr bool kZeroY = true;               // f[1] ≡ 0
   double wz;
   __device__ __forceinline__ void init(const double* p, double) { wz = fma(-2.0, p[1], p[0]); }
   __device__ __forceinline__ void sample(double, double f[4]) const { f[0] = 0.0; f[1] = 0.0; f[2] = wz; f[3] = 0.0; }
@@ -330,16 +338,20 @@ struct FrameCF4 {
     sincos(omega_r * g2dt, &s2, &c2);
     ps.init(omega_r, 0.0, dt);
   }
-  template <int NC = 4>
+  template <int NC = 4, bool ZERO_Y = false>
   __device__ __forceinline__ void apply(double base, bool anchor, double* f1, double* f2) {
     ps.next(base, anchor);
     const double sb = ps.s, cb = ps.c;
     const double ca = fma(cb, c1, -sb * s1), sa = fma(sb, c1, cb * s1);
     const double cc = fma(cb, c2, -sb * s2), sc = fma(sb, c2, cb * s2);
     double fx = f1[0], fy = f1[1];
-    f1[0] = fma(ca, fx, sa * fy); f1[1] = fma(ca, fy, -sa * fx); f1[2] -= wr;
+    if constexpr (ZERO_Y) { f1[0] = ca * fx; f1[1] = -(sa * fx); }
+    else { f1[0] = fma(ca, fx, sa * fy); f1[1] = fma(ca, fy, -sa * fx); }
+    f1[2] -= wr;
     fx = f2[0]; fy = f2[1];
-    f2[0] = fma(cc, fx, sc * fy); f2[1] = fma(cc, fy, -sc * fx); f2[2] -= wr;
+    if constexpr (ZERO_Y) { f2[0] = cc * fx; f2[1] = -(sc * fx); }
+    else { f2[0] = fma(cc, fx, sc * fy); f2[1] = fma(cc, fy, -sc * fx); }
+    f2[2] -= wr;
     rotate_quadrupoles<NC>(f1, ca, sa);
     rotate_quadrupoles<NC>(f2, cc, sc);
   }
