@@ -467,10 +467,16 @@ template <typename T> __device__ __forceinline__ void expo_su2(const T a[4], Res
     // FP64 coefficients come from the constant bank (DFMA c[][] operands) instead of being rematerialised in
     // uniform registers every step (measured: 37 UMOV per spin-half fine step).
     if constexpr (sizeof(T) == 8) {
-      cm1 = r2 * fma(r2, fma(r2, fma(r2, fma(r2, kSu2Series[0], kSu2Series[1]), kSu2Series[2]), kSu2Series[3]),
-                     kSu2Series[4]);
-      s = fma(r2, fma(r2, fma(r2, fma(r2, kSu2Series[5], kSu2Series[6]), kSu2Series[7]), kSu2Series[8]),
-              kSu2Series[9]);
+      if (r2 <= 1.4901161193847656e-08) {
+        // r ≤ 2^-13 (e.g. C4's 1 ns steps): two terms each — the dropped r⁶/46080 and r⁴/3840 are < 1.2e-19 relative
+        cm1 = r2 * fma(r2, kSu2Series[3], kSu2Series[4]);
+        s = fma(r2, kSu2Series[8], kSu2Series[9]);
+      } else {
+        cm1 = r2 * fma(r2, fma(r2, fma(r2, fma(r2, kSu2Series[0], kSu2Series[1]), kSu2Series[2]), kSu2Series[3]),
+                       kSu2Series[4]);
+        s = fma(r2, fma(r2, fma(r2, fma(r2, kSu2Series[5], kSu2Series[6]), kSu2Series[7]), kSu2Series[8]),
+                kSu2Series[9]);
+      }
     } else {
       cm1 = r2 * fmaT(r2, fmaT(r2, fmaT(r2, fmaT(r2, T(-1.0 / 3715891200.0), T(1.0 / 10321920.0)),
                                           T(-1.0 / 46080.0)), T(1.0 / 384.0)), T(-0.125));
