@@ -48,14 +48,16 @@ def algorithmic_flops_per_fine_step(spin: str, expo: str, tau: int, method: str 
     form (x̃' = −ỹ², ỹ' = (x̃ + 2I)ỹ on its 6 unique entries, DESIGN.md §5 item 13) = 63 flop (39 FP64 instructions)
     × τ per exponential, residual product b + a(I + b) = 219 (3×3) per exponential; field, frame, T − I construction
     and phases are not counted (a lower bound; ncu's executed count is in profiles/r01/).
-    spin-half: per CF4 step 2 × (SU(2) series 26 + SU(2)-parametrised residual product 36) = 124 plus the weights,
-    field samples, frame rotation, phase steppers and grid — 193 in total, the ncu-executed count (2·DFMA + DMUL +
-    DADD per step, profiles/r01/s2_final/flops_c4.csv after DESIGN.md §5 items 10, 12 and the folded weights).
+    spin-half: per CF4 step 2 × (SU(2) closed form + SU(2)-parametrised residual product 36) plus the weights, field
+    samples, frame rotation, phase steppers and grid — 163 in total, the ncu-executed count on C4 (2·DFMA + DMUL +
+    DADD per step: 61.1 DFMA + 32.3 DMUL + 8.1 DADD, profiles/r01/s8_final/flops_c4.csv, after DESIGN.md §5 items
+    10, 12, 15 and the folded weights).  Steps with r > 2^-13 (longer series, e.g. C5 at 100 ns) execute ≈ 26 more,
+    so their reported fraction is a lower bound.
     general spin-one (lie_trotter_su3, readings R19/R20): the same 63-flop symmetric squaring × τ on the
     tridiagonalised factor T₀, the conjugation W (T₀^n − I) W† = 24 complex multiply-adds = 192 flop, residual product
     219; the tridiagonalisation and T₀ construction are not counted.
     spin-one analytic (reading R14): accumulated in SU(2) form and mapped by D¹ once per interval (DESIGN.md §5
-    item 11), so its fine step is the spin-half step: 193."""
+    item 11), so its fine step is the spin-half step: 163."""
     n_exp = 2 if method == "cf4" else 1
     if spin == "one" and expo == "analytic":
         spin = "half"
@@ -63,7 +65,7 @@ def algorithmic_flops_per_fine_step(spin: str, expo: str, tau: int, method: str 
         prod = 219
         per_exp = {"lie_trotter": 63 * tau, "lie_trotter_su3": 63 * tau + 192}.get(expo, 0)
         return n_exp * (per_exp + prod)
-    return 193 if method == "cf4" else 97
+    return 163 if method == "cf4" else 82
 
 
 def dense_equivalent_flops_per_fine_step(spin: str, expo: str, tau: int, method: str = "cf4") -> int:

@@ -58,7 +58,7 @@ def test_flop_model():
     sym, conj3, prod3, prod2 = 2 * 24 + 12 + 3, 24 * 8, 219, 2 * 16 + 4
     assert bench.algorithmic_flops_per_fine_step("one", "lie_trotter", 24) == 2 * (24 * sym + prod3)
     assert bench.algorithmic_flops_per_fine_step("one", "lie_trotter_su3", 24) == 2 * (24 * sym + conj3 + prod3)
-    half = 193                         # ncu-executed per spin-half step (2 × (26 + prod2) = 124 of it in the products)
-    assert 2 * (26 + prod2) < half
+    half = 163                         # ncu-executed per spin-half C4 step (2 × (9 + prod2) = 90 of it in the products)
+    assert 2 * (9 + prod2) < half
     assert bench.algorithmic_flops_per_fine_step("half", "analytic", 24) == half
     assert bench.algorithmic_flops_per_fine_step("one", "analytic", 24) == half      # SU(2) accumulation + D¹ map
