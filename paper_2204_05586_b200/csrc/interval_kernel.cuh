@@ -52,6 +52,9 @@ template <int SPIN, int EXPO, typename T> constexpr int kIntervalMinBlocks() {
   return EXPO == EXP_LIE_TROTTER_SU3 ? SS_INTERVAL_MINBLOCKS_SU3 : SS_INTERVAL_MINBLOCKS;
 }
 
+#ifndef SS_SU2_SHORT_BODIES
+#define SS_SU2_SHORT_BODIES 1   // SU(2) short-series choice as specialised step bodies (1) or a run-time flag (0)
+#endif
 #ifndef SS_STEP_UNROLL
 #define SS_STEP_UNROLL 1    // unroll of the rotated-phase steps between anchors (SU(2)-form paths; tuning knob)
 #endif
@@ -100,14 +103,21 @@ __device__ __forceinline__ void interval_body(const IntervalParams& prm) {
   }
 
   constexpr int DA = AccDim<SPIN, EXPO>::D;         // accumulated residual: SU(2) form (2) or dense 3×3
+  // SU(2) closed form: |a| ≤ (|w+| + |w−|)·|f| (CF4) or δt·|f| ≤ 2^-13 on every step of this interval ⇒ short series
+  bool su2_short = false;
+  if constexpr (DA == 2 && sizeof(T) == 8) {
+    const double rb = (METHOD == CF4 ? fabs(prm.wpd) + fabs(prm.wmd) : prm.dt) * field_bound(fld, omega_r, 0);
+    su2_short = rb * 1.01 <= 1.220703125e-04;        // 2^-13 with a margin for the rounding of a and of the bound
+  }
   Res<DA, T> A;   // U_r − I, U_r initialised to the identity
   res_zero(A);
 
   const int64_t l_begin = (prm.L * part) / S, l_end = active ? (prm.L * (part + 1)) / S : l_begin;
   // One fine step.  ANCHOR (exact sincos of the phase steppers, every kAnchor-th step) and PULSE (this interval can
   // meet the neural field's pulse window) are compile-time, so the step body carries no per-step branches for them.
-  auto step = [&](int64_t l, auto anchor_c, auto pulse_c) {
+  auto step = [&](int64_t l, auto anchor_c, auto pulse_c, auto short_c) {
     const bool ANCHOR = anchor_c.value, PULSE = pulse_c.value;   // compile-time for BoolC, run-time for RtBool
+    const bool SHORT = short_c.value;
     const double base = __dmul_rn((double)l, prm.dt);
     Res<DA, T> u;
     if (METHOD == CF4) {
@@ -164,12 +174,12 @@ __device__ __forceinline__ void interval_body(const IntervalParams& prm) {
       // one exponential is live in registers (occupancy).  Residual form: A ← e + A + e·A.
       {
         Res<DA, T> e;
-        Expo<SPIN, EXPO, T>::run(a1, prm.tau, e);
+        Expo<SPIN, EXPO, T>::run(a1, prm.tau, e, SHORT);
         res_mul(e, A, u);
       }
       {
         Res<DA, T> e;
-        Expo<SPIN, EXPO, T>::run(a2, prm.tau, e);
+        Expo<SPIN, EXPO, T>::run(a2, prm.tau, e, SHORT);
         res_mul(e, u, A);
       }
       return;
@@ -191,30 +201,40 @@ __device__ __forceinline__ void interval_body(const IntervalParams& prm) {
       T a[NC];
 #pragma unroll
       for (int j = 0; j < NC; ++j) a[j] = (T)(f[j] * prm.dt);
-      Expo<SPIN, EXPO, T>::run(a, prm.tau, u);
+      Expo<SPIN, EXPO, T>::run(a, prm.tau, u, SHORT);
     }
     // a7: U_r ← u·U_r, residual form: A ← u + A + u·A.
     Res<DA, T> An;
     res_mul(u, A, An);
     A = An;
   };
-  auto run_steps = [&](auto pulse_c) {
+  auto run_steps = [&](auto pulse_c, auto short_c) {
 #pragma unroll 1
     for (int64_t l0 = l_begin; l0 < l_end; l0 += kAnchor) {
-      step(l0, BoolC<true>{}, pulse_c);
+      step(l0, BoolC<true>{}, pulse_c, short_c);
       const int64_t l1 = l0 + kAnchor < l_end ? l0 + kAnchor : l_end;
       SS_UNROLL(SS_STEP_UNROLL)
-      for (int64_t l = l0 + 1; l < l1; ++l) step(l, BoolC<false>{}, pulse_c);
+      for (int64_t l = l0 + 1; l < l1; ++l) step(l, BoolC<false>{}, pulse_c, short_c);
     }
   };
   if constexpr (DA == 2) {
-    // spin-half / analytic spin-one (short, trig-heavy steps): specialised bodies, C4 1.05e11 → 1.24e11 fine steps/s
-    if (field_pulse_possible(fld, prm.dt_out, 0)) run_steps(BoolC<true>{});
-    else run_steps(BoolC<false>{});
+    // spin-half / analytic spin-one (short, trig-heavy steps): specialised bodies, C4 1.05e11 → 1.24e11 fine steps/s;
+    // the short-series choice too (SS_SU2_SHORT_BODIES)
+    auto with_pulse = [&](auto pulse_c) {
+      if constexpr (SS_SU2_SHORT_BODIES && sizeof(T) == 8) {
+        if (su2_short) run_steps(pulse_c, BoolC<true>{});
+        else run_steps(pulse_c, BoolC<false>{});
+      } else {
+        run_steps(pulse_c, RtBool{su2_short});
+      }
+    };
+    if (field_pulse_possible(fld, prm.dt_out, 0)) with_pulse(BoolC<true>{});
+    else with_pulse(BoolC<false>{});
   } else {
     // 3×3 paths: one body with a run-time anchor test (four specialised copies spill more: C3 −2.5 %, measured)
 #pragma unroll 1
-    for (int64_t l = l_begin; l < l_end; ++l) step(l, RtBool{((l - l_begin) % kAnchor) == 0}, BoolC<true>{});
+    for (int64_t l = l_begin; l < l_end; ++l)
+      step(l, RtBool{((l - l_begin) % kAnchor) == 0}, BoolC<true>{}, BoolC<false>{});
   }
 
   // Sub-interval split: lane p holds the partial product of its fine steps; combine later·earlier in a shuffle tree

@@ -137,10 +137,17 @@ struct PhaseStepper {
 // (fma(c, 0, ·) and s·0 cannot be folded by the compiler under IEEE semantics; the result is the same to the bit).
 template <class F> __device__ constexpr bool zero_y_of(decltype(F::kZeroY)*) { return F::kZeroY; }
 template <class F> __device__ constexpr bool zero_y_of(...) { return false; }
+// Upper bound on |(fx, fy, fz)| over the interval in the frame rotating at wr (0: frame off) — transverse magnitudes
+// are rotation invariant, fz shifts by −wr.  Fields without mag_bound (su(3), user fields): no bound.
+template <class F> __device__ __forceinline__ auto field_bound(const F& f, double wr, int) -> decltype(f.mag_bound(wr)) {
+  return f.mag_bound(wr);
+}
+template <class F> __device__ __forceinline__ double field_bound(const F&, double, long) { return 1e300; }
 
 template <> struct Field<FIELD_CONSTANT> {
   double f0, f1, f2, f3;
   __device__ __forceinline__ void init(const double* p, double) { f0 = p[0]; f1 = p[1]; f2 = p[2]; f3 = p[3]; }
+  __device__ __forceinline__ double mag_bound(double wr) const { return fabs(f0) + fabs(f1) + fabs(f2 - wr); }
   __device__ __forceinline__ void sample(double, double f[4]) const { f[0] = f0; f[1] = f1; f[2] = f2; f[3] = f3; }
   __device__ __forceinline__ void init_cf4(double, double, double) {}
   __device__ __forceinline__ void sample_cf4(double, bool, bool, double o1, double o2, double g1[4], double g2[4]) {
@@ -168,6 +175,7 @@ template <> struct Field<FIELD_RABI_LINEAR> {        // ω0 Jz + 2Ω cos(ω0 t) 
     g1[0] = two_om * fma(cb, c1, -sb * s1); g1[1] = 0.0; g1[2] = w0; g1[3] = 0.0;
     g2[0] = two_om * fma(cb, c2, -sb * s2); g2[1] = 0.0; g2[2] = w0; g2[3] = 0.0;
   }
+  __device__ __forceinline__ double mag_bound(double wr) const { return fabs(two_om) + fabs(w0 - wr); }
 };
 
 template <> struct Field<FIELD_RABI_CIRCULAR> {      // ω0 Jz + Ω(cos(ω0 t) Jx + sin(ω0 t) Jy)
@@ -191,6 +199,7 @@ template <> struct Field<FIELD_RABI_CIRCULAR> {      // ω0 Jz + Ω(cos(ω0 t) J
     g1[0] = om * fma(cb, c1, -sb * s1); g1[1] = om * fma(sb, c1, cb * s1); g1[2] = w0; g1[3] = 0.0;
     g2[0] = om * fma(cb, c2, -sb * s2); g2[1] = om * fma(sb, c2, cb * s2); g2[2] = w0; g2[3] = 0.0;
   }
+  __device__ __forceinline__ double mag_bound(double wr) const { return fabs(om) + fabs(w0 - wr); }
 };
 
 template <> struct Field<FIELD_NEURAL> {
@@ -232,12 +241,14 @@ template <> struct Field<FIELD_NEURAL> {
     g1[0] = two_om * fma(cb, c1, -sb * s1); g1[1] = 0.0; g1[2] = pulse ? pulse_z(o1) : wb; g1[3] = wq;
     g2[0] = two_om * fma(cb, c2, -sb * s2); g2[1] = 0.0; g2[2] = pulse ? pulse_z(o2) : wb; g2[3] = wq;
   }
+  __device__ __forceinline__ double mag_bound(double wr) const { return fabs(two_om) + fabs(wb - wr) + fabs(op); }
 };
 
 template <> struct Field<FIELD_GRADIENT> {          // ω_z = x − 2y
   static constexpr bool kZeroY = true;               // f[1] ≡ 0
   double wz;
   __device__ __forceinline__ void init(const double* p, double) { wz = fma(-2.0, p[1], p[0]); }
+  __device__ __forceinline__ double mag_bound(double wr) const { return fabs(wz - wr); }
   __device__ __forceinline__ void sample(double, double f[4]) const { f[0] = 0.0; f[1] = 0.0; f[2] = wz; f[3] = 0.0; }
   __device__ __forceinline__ void init_cf4(double, double, double) {}
   __device__ __forceinline__ void sample_cf4(double, bool, bool, double o1, double o2, double g1[4], double g2[4]) {
@@ -457,26 +468,28 @@ template <typename T> __device__ __forceinline__ Res<3, T> res_shfl_down(const R
 // ---- exponentiators: residual of exp(−i(ax Jx + ay Jy + az Jz + aq Q)) -----------------------------------------
 
 // Spin-half closed form: exp(−i a·σ/2) = cos(r/2) I − i (sin(r/2)/r) a·σ.  cos(r/2) − 1 = −2 sin²(r/4).
-template <typename T> __device__ __forceinline__ void expo_su2(const T a[4], Res<2, T>& e) {
+// short_series: the caller guarantees r ≤ 2^-13 for this argument (interval_body bounds |a| once per interval from
+// the field's magnitude bound, field_bound): then two series terms each suffice — the dropped r⁶/46080 and r⁴/3840
+// are < 1.2e-19 relative (DESIGN.md §5 item 15).  A per-step test instead costs an FP64 compare per exponential and,
+// where lanes straddle the bound (C5's 100 ns steps), both series.
+template <typename T>
+__device__ __forceinline__ void expo_su2(const T a[4], Res<2, T>& e, bool short_series = false) {
   const T r2 = a[0] * a[0] + a[1] * a[1] + a[2] * a[2];
   T cm1, s;
-  if (r2 <= T(0.00390625)) {
+  if (sizeof(T) == 8 && short_series) {
+    cm1 = r2 * fmaT(r2, T(kSu2Series[3]), T(kSu2Series[4]));
+    s = fmaT(r2, T(kSu2Series[8]), T(kSu2Series[9]));
+  } else if (r2 <= T(0.00390625)) {
     // r ≤ 2^-4 (every fine step of the configs): both functions are even, so series in r² need no sqrt, sincos
     // or division.  cos(r/2) − 1 = −r²/8 + r⁴/384 − r⁶/46080 + r⁸/10321920 − r¹⁰/3715891200,
     // sin(r/2)/r = 1/2 − r²/48 + r⁴/3840 − r⁶/645120 + r⁸/185794560 (truncation < 1e-19 relative).
     // FP64 coefficients come from the constant bank (DFMA c[][] operands) instead of being rematerialised in
     // uniform registers every step (measured: 37 UMOV per spin-half fine step).
     if constexpr (sizeof(T) == 8) {
-      if (r2 <= 1.4901161193847656e-08) {
-        // r ≤ 2^-13 (e.g. C4's 1 ns steps): two terms each — the dropped r⁶/46080 and r⁴/3840 are < 1.2e-19 relative
-        cm1 = r2 * fma(r2, kSu2Series[3], kSu2Series[4]);
-        s = fma(r2, kSu2Series[8], kSu2Series[9]);
-      } else {
-        cm1 = r2 * fma(r2, fma(r2, fma(r2, fma(r2, kSu2Series[0], kSu2Series[1]), kSu2Series[2]), kSu2Series[3]),
-                       kSu2Series[4]);
-        s = fma(r2, fma(r2, fma(r2, fma(r2, kSu2Series[5], kSu2Series[6]), kSu2Series[7]), kSu2Series[8]),
-                kSu2Series[9]);
-      }
+      cm1 = r2 * fma(r2, fma(r2, fma(r2, fma(r2, kSu2Series[0], kSu2Series[1]), kSu2Series[2]), kSu2Series[3]),
+                     kSu2Series[4]);
+      s = fma(r2, fma(r2, fma(r2, fma(r2, kSu2Series[5], kSu2Series[6]), kSu2Series[7]), kSu2Series[8]),
+              kSu2Series[9]);
     } else {
       cm1 = r2 * fmaT(r2, fmaT(r2, fmaT(r2, fmaT(r2, T(-1.0 / 3715891200.0), T(1.0 / 10321920.0)),
                                           T(-1.0 / 46080.0)), T(1.0 / 384.0)), T(-0.125));
@@ -1017,14 +1030,20 @@ template <typename T> __device__ __forceinline__ void trotter_residual_su3(const
 }
 
 template <int SPIN, int EXPO, typename T> struct Expo;
+// run(a, τ, e, short_series): short_series (the caller's per-interval bound r ≤ 2^-13) only matters for the SU(2)
+// closed form.
 template <int EXPO, typename T> struct Expo<SPIN_HALF, EXPO, T> {
-  __device__ __forceinline__ static void run(const T a[4], int, Res<2, T>& e) { expo_su2<T>(a, e); }
+  __device__ __forceinline__ static void run(const T a[4], int, Res<2, T>& e, bool sh = false) { expo_su2<T>(a, e, sh); }
 };
 template <typename T> struct Expo<SPIN_ONE, EXP_LIE_TROTTER, T> {
-  __device__ __forceinline__ static void run(const T a[4], int tau, Res<3, T>& e) { trotter_residual<T>(a, tau, e); }
+  __device__ __forceinline__ static void run(const T a[4], int tau, Res<3, T>& e, bool = false) {
+    trotter_residual<T>(a, tau, e);
+  }
 };
 template <typename T> struct Expo<SPIN_ONE, EXP_LIE_TROTTER_SU3, T> {
-  __device__ __forceinline__ static void run(const T* a, int tau, Res<3, T>& e) { trotter_residual_su3<T>(a, tau, e); }
+  __device__ __forceinline__ static void run(const T* a, int tau, Res<3, T>& e, bool = false) {
+    trotter_residual_su3<T>(a, tau, e);
+  }
 };
 template <typename T> __device__ __forceinline__ void expo_spin1_analytic(const T a[4], Res<3, T>& e) {
   Res<2, T> u;
@@ -1034,7 +1053,7 @@ template <typename T> __device__ __forceinline__ void expo_spin1_analytic(const 
 // The analytic spin-one path accumulates in SU(2) and maps once: D¹ is a homomorphism, so D¹(u_L)⋯D¹(u_1) =
 // D¹(u_L⋯u_1) — the same interval operator, exactly (DESIGN.md §5 item 11).  Expo returns the SU(2) residual.
 template <typename T> struct Expo<SPIN_ONE, EXP_ANALYTIC, T> {
-  __device__ __forceinline__ static void run(const T a[4], int, Res<2, T>& e) { expo_su2<T>(a, e); }
+  __device__ __forceinline__ static void run(const T a[4], int, Res<2, T>& e, bool sh = false) { expo_su2<T>(a, e, sh); }
 };
 
 // Dimension of the residual the interval kernel accumulates: 2 (SU(2) form) for spin-half and for the analytic
