@@ -493,20 +493,20 @@ def run_time_partition(args, rank, world, local, dev):
     t_rest = float(np.mean([e[1].elapsed_time(e[2]) for e in evs]))
     elapsed_ms, t_interval, t_rest = reduce_max([elapsed_ms, t_interval, t_rest], dev, world)
     # e2e at N = 1: the single simulation through the host-buffer C-ABI call (pinned; H2D of the sweep and ψ0, D2H of
-    # all 1e6 + 1 states inside the timed region), pipelined over 6 time chunks.  A time partition over N > 1 ranks has no host-buffer entry point.
+    # all 1e6 + 1 states inside the timed region), pipelined over --c4-chunks time chunks.  A time partition over N > 1 ranks has no host-buffer entry point.
     e2e = None
     if world == 1 and not args.no_e2e:
         h_sweep = torch.from_numpy(w.sweep).pin_memory().numpy()
         h_psi0 = torch.from_numpy(w.psi0).pin_memory().numpy()
         h_states = torch.empty((1, K + 1, D), dtype=torch.complex128).pin_memory().numpy()
-        sim.evaluate_host(h_sweep, w.t0, w.t1, w.dt_int, w.dt_out, h_psi0, out_states=h_states, n_chunks=6)
+        sim.evaluate_host(h_sweep, w.t0, w.t1, w.dt_int, w.dt_out, h_psi0, out_states=h_states, n_chunks=args.c4_chunks)
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            sim.evaluate_host(h_sweep, w.t0, w.t1, w.dt_int, w.dt_out, h_psi0, out_states=h_states, n_chunks=6)
+            sim.evaluate_host(h_sweep, w.t0, w.t1, w.dt_int, w.dt_out, h_psi0, out_states=h_states, n_chunks=args.c4_chunks)
         e2e_s = time.perf_counter() - t0
         e2e = {"value": w.fine_steps * args.steps / e2e_s, "unit": UNIT,
                "h2d_bytes_per_step": int(h_sweep.nbytes + h_psi0.nbytes), "d2h_bytes_per_step": int(h_states.nbytes),
-               "n_chunks": 6}
+               "n_chunks": args.c4_chunks}
     value = w.fine_steps * args.steps / (elapsed_ms * 1e-3)
     flops_launch = algorithmic_flops_per_fine_step(w.spin, w.expo, w.tau, w.method) * kc * L
     achieved = flops_launch / (t_interval * 1e-3) / 1e12
@@ -545,9 +545,11 @@ def main():
     ap.add_argument("--precision", choices=["fp64", "fp32"], default="fp64")
     ap.add_argument("--expo", choices=["analytic", "lie_trotter"], default=None,
                     help="C5 only: the exponentiator column of the accuracy/throughput matrix (default lie_trotter)")
-    ap.add_argument("--chunks", type=int, default=10, help="batch chunks of the pipelined host-buffer (e2e) call")
+    ap.add_argument("--chunks", type=int, default=40,
+                    help="chunks of the pipelined host-buffer (e2e) call (time chunks for large batches; 0: automatic)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-step-seconds", type=float, default=8.0)
+    ap.add_argument("--c4-chunks", type=int, default=6, help="time chunks of C4's host-buffer (e2e) call")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-probe", action="store_true")

@@ -202,7 +202,8 @@ int ss_spin_projection(int32_t spin, int64_t n, const double* d_states, double* 
 
 /* End-to-end call on HOST buffers: copies h_sweep/h_state_init to the device, runs the path and copies the states
  * (and unitaries if h_unitaries != NULL) back, pipelined over `n_chunks` chunks on an internal compute stream and
- * copy stream so device→host copies overlap compute: batch chunks of geometrically shrinking size (B/2, B/4, …), or —
+ * copy stream so device→host copies overlap compute (n_chunks ≤ 0: automatic — ≈ 40 time chunks where they apply,
+ * else 4 batch chunks): batch chunks of geometrically shrinking size (B/2, B/4, …), or —
  * for n_chunks ≥ 6 and either batch ≥ 4096 or long sweeps (≥ 6 waves of interval work per chunk, e.g. one sweep of
  * 1e6 intervals) — time chunks of all sweeps continued from a running carry (bit-identical to ss_evaluate for
  * batch ≥ 4096; equal to rounding otherwise: the single-sweep scan restarts from the carry).  Synchronous: returns after the results are in host memory.  Device

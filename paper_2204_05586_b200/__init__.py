@@ -210,8 +210,9 @@ class Simulator:
 
     def evaluate_host(self, sweep: np.ndarray, time_start, time_end, time_step_integration, time_step_output,
                       state_init: np.ndarray, out_states: np.ndarray | None = None, want_unitaries=False,
-                      n_chunks: int = 4):
-        """End-to-end call on host arrays (pinned for full bandwidth): H2D, kernels, D2H inside the library."""
+                      n_chunks: int = 0):
+        """End-to-end call on host arrays (pinned for full bandwidth): H2D, kernels, D2H inside the library, pipelined
+        over n_chunks chunks (0: automatic)."""
         K, _, _ = plan(time_start, time_end, time_step_integration, time_step_output)
         sweep = np.ascontiguousarray(sweep, dtype=np.float64)
         state_init = np.ascontiguousarray(state_init, dtype=np.complex128)

@@ -537,7 +537,6 @@ int ss_evaluate_host(ss_sim* s, double t0, double t1, double dt_int, double dt_o
   if (rc) return rc;
   if (batch < 1) return fail(SS_ERR_INVALID, "batch must be >= 1");
   if (!h_sweep || !h_psi0 || !h_states) return fail(SS_ERR_INVALID, "h_sweep, h_state_init, h_states must be non-NULL");
-  if (n_chunks < 1) n_chunks = 1;
   // host-side input validation (host data: no device round trip needed)
   const int qcol = (s->dim == 3 && s->d.exponentiation == SS_EXP_ANALYTIC) ? qcol_of(s->d.field) : -1;
   for (int64_t i = 0; i < batch * s->P; ++i) {
@@ -584,6 +583,11 @@ int ss_evaluate_host(ss_sim* s, double t0, double t1, double dt_int, double dt_o
   // rounding (a different product order), not bit for bit.
   const bool big_batch = batch >= ssb::chain_min_batch();
   const double waves = (double)batch * K * choose_split(s, batch * K, L) / resident_threads(s);
+  if (n_chunks <= 0) {        // auto: ≈ 40 time chunks where they apply (measured best for C3: e2e 0.97 of device),
+    int64_t tc = std::min<int64_t>(40, K / 4);            // else 4 geometric batch chunks
+    if (!big_batch) tc = std::min<int64_t>(tc, (int64_t)(waves / 8.0));   // C4: 6 (measured best)
+    n_chunks = tc >= 6 ? (int32_t)tc : 4;
+  }
   if (n_chunks >= 6 && K >= 4 * (int64_t)n_chunks && (big_batch || waves >= 6.0 * n_chunks)) {
     // Chunk the TIME axis, all sweeps per chunk (for large batches the per-sweep chain kernel stays at full width and
     // is sequential per sweep, so the states are bit-identical to one ss_evaluate).  Chunk c = intervals [k0, k0 + kc)
@@ -595,13 +599,21 @@ int ss_evaluate_host(ss_sim* s, double t0, double t1, double dt_int, double dt_o
     for (double x : {1.0, 0.5, 0.25, 0.25}) w.push_back(x);
     double wsum = 0;
     for (double x : w) wsum += x;
+    // chunk boundaries from the cumulative weights (rounding errors do not accumulate), every chunk ≥ 1 interval
     std::vector<int64_t> ks;
-    int64_t used = 0, kc_max = 0;
-    for (size_t c = 0; c < w.size(); ++c) {
-      const int64_t kc = (c + 1 == w.size()) ? K - used : std::max<int64_t>(1, (int64_t)std::llround(K * w[c] / wsum));
-      ks.push_back(kc);
-      used += kc;
-      kc_max = std::max(kc_max, kc);
+    int64_t kc_max = 0;
+    {
+      const int64_t nc = (int64_t)w.size();
+      double cum = 0.0;
+      int64_t b = 0;
+      for (int64_t c = 0; c < nc; ++c) {
+        cum += w[c];
+        int64_t nb = (c + 1 == nc) ? K : (int64_t)std::llround(K * cum / wsum);
+        nb = std::min(std::max(nb, b + 1), K - (nc - c - 1));
+        ks.push_back(nb - b);
+        kc_max = std::max(kc_max, nb - b);
+        b = nb;
+      }
     }
     const size_t sweep_b = align256(sizeof(double) * s->P * batch), carry_b = align256(sizeof(double) * 2 * D * batch);
     const size_t states_b = align256(sizeof(double) * 2 * D * (size_t)batch * (kc_max + 1));

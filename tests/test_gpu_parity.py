@@ -275,7 +275,7 @@ def test_host_api_time_chunks_match_device_api(ss):
     w = W.c3_batched(batch=4096, duration=0.2e-3)
     st_d, U_d = gpu_run(ss, w)
     sim = ss.Simulator(w.spin, w.method, w.expo, w.tau, w.frame, "fp64", w.field)
-    for chunks in (6, 10):
+    for chunks in (6, 10, 50):                      # 50: K = 200 = 4·50, chunks of 1–5 intervals
         st_h, U_h = sim.evaluate_host(w.sweep, w.t0, w.t1, w.dt_int, w.dt_out, w.psi0, want_unitaries=True,
                                       n_chunks=chunks)
         assert np.array_equal(st_h, st_d) and np.array_equal(U_h, U_d)
