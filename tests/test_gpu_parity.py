@@ -102,6 +102,16 @@ def test_c4_spin_half_parity_short(ss, orc):
     assert_parity(ss, orc, W.c4_long(duration=2e-3).with_(sweep=W.neural_params(t_p=1e-3, omega_q=0.0)[None, :]))
 
 
+@pytest.mark.parametrize("spin,method", [("half", "midpoint"), ("one", "cf4"), ("one", "heun")])
+def test_short_su2_series_parity(ss, orc, spin, method):
+    """1 ns steps put every SU(2) exponential below the per-interval bound r ≤ 2^-13 (two-term series, DESIGN.md §5
+    item 15) — spin-half with a midpoint sampler and the analytic spin-one path (ω_q = 0)."""
+    w = W.c4_long(duration=0.4e-3).with_(spin=spin, method=method, expo="analytic",
+                                         sweep=W.neural_params(t_p=0.2e-3, omega_q=0.0)[None, :],
+                                         psi0=W.random_states(1, 2 if spin == "half" else 3, seed=27))
+    assert_parity(ss, orc, w)
+
+
 @pytest.mark.parametrize("expo", ["lie_trotter", "analytic"])
 def test_c5_parity_short(ss, orc, expo):
     w = W.c5_matrix(expo, batch=3)
