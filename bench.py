@@ -199,6 +199,9 @@ def timed_loop(step, steps, stream, local, barrier):
         start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         launches0 = ss.kernel_launches()
         with ClockSampler(local) as clk:
+            # ≈ 1 ms device-side spin before the region: the host enqueues the first steps meanwhile, so no event of
+            # the region waits on host launch latency (matters only for sub-millisecond steps such as C2's)
+            torch.cuda._sleep(2_000_000)
             start.record(stream)
             for i in range(steps):
                 step(evs[i])
