@@ -206,7 +206,10 @@ int ss_spin_projection(int32_t spin, int64_t n, const double* d_states, double* 
  * else 4 batch chunks): batch chunks of geometrically shrinking size (B/2, B/4, …), or —
  * for n_chunks ≥ 6 and either batch ≥ 4096 or long sweeps (≥ 6 waves of interval work per chunk, e.g. one sweep of
  * 1e6 intervals) — time chunks of all sweeps continued from a running carry (bit-identical to ss_evaluate for
- * batch ≥ 4096; equal to rounding otherwise: the single-sweep scan restarts from the carry).  Synchronous: returns after the results are in host memory.  Device
+ * batch ≥ 4096; equal to rounding otherwise: the single-sweep scan restarts from the carry).  Batches of ≤ 4 sweeps
+ * whose interval work spans ≥ 1.2 waves but is too short for time chunks (the paper's benchmark, one sweep of 1e5
+ * intervals) take two wave-aligned time chunks instead — all whole waves but the last, then the rest — unless
+ * n_chunks == 1 (one chunk, no pipelining).  Synchronous: returns after the results are in host memory.  Device
  * buffers are allocated once and cached in `sim`.  Pinned host buffers give full copy bandwidth. */
 int ss_evaluate_host(ss_sim* sim, double time_start, double time_end, double time_step_integration,
                      double time_step_output, int64_t batch, const double* h_sweep, const double* h_state_init,

@@ -583,12 +583,21 @@ int ss_evaluate_host(ss_sim* s, double t0, double t1, double dt_int, double dt_o
   // rounding (a different product order), not bit for bit.
   const bool big_batch = batch >= ssb::chain_min_batch();
   const double waves = (double)batch * K * choose_split(s, batch * K, L) / resident_threads(s);
+  const bool single = n_chunks == 1;                       // the caller asked for one chunk
   if (n_chunks <= 0) {        // auto: ≈ 40 time chunks where they apply (measured best for C3: e2e 0.97 of device),
     int64_t tc = std::min<int64_t>(40, K / 4);            // else 4 geometric batch chunks
     if (!big_batch) tc = std::min<int64_t>(tc, (int64_t)(waves / 8.0));   // C4: 6 (measured best)
     n_chunks = tc >= 6 ? (int32_t)tc : 4;
   }
-  if (n_chunks >= 6 && K >= 4 * (int64_t)n_chunks && (big_batch || waves >= 6.0 * n_chunks)) {
+  const bool tent = n_chunks >= 6 && K >= 4 * (int64_t)n_chunks && (big_batch || waves >= 6.0 * n_chunks);
+  // Wave-aligned pair (C2: one sweep of 1e5 intervals = 2.6 waves, too short for the tent): chunk A holds the whole
+  // waves but the last, chunk B the rest.  Interval work still takes ⌈waves⌉ wave-times in total, and the D2H of
+  // chunk A (most of the states) overlaps chunk B's kernels; only chunk B's copy is left exposed.
+  const int64_t wave_iv = (int64_t)(resident_threads(s) / choose_split(s, batch * K, L)) / batch;   // intervals/wave
+  const int64_t pair_waves = (int64_t)std::ceil(waves) - 1;
+  const bool pair = !tent && !single && !big_batch && batch <= 4 && waves >= 1.2 && wave_iv >= 1 && pair_waves >= 1 &&
+                    pair_waves * wave_iv < K;
+  if (tent || pair) {
     // Chunk the TIME axis, all sweeps per chunk (for large batches the per-sweep chain kernel stays at full width and
     // is sequential per sweep, so the states are bit-identical to one ss_evaluate).  Chunk c = intervals [k0, k0 + kc)
     // of every sweep, started from the running carry (the previous chunk's last states).  Tent-shaped sizes — small
@@ -602,7 +611,10 @@ int ss_evaluate_host(ss_sim* s, double t0, double t1, double dt_int, double dt_o
     // chunk boundaries from the cumulative weights (rounding errors do not accumulate), every chunk ≥ 1 interval
     std::vector<int64_t> ks;
     int64_t kc_max = 0;
-    {
+    if (pair) {
+      ks = {pair_waves * wave_iv, K - pair_waves * wave_iv};
+      kc_max = std::max(ks[0], ks[1]);
+    } else {
       const int64_t nc = (int64_t)w.size();
       double cum = 0.0;
       int64_t b = 0;

@@ -307,6 +307,29 @@ def test_host_api_time_chunks_long_sweep(ss):
         assert np.abs(st_h - st_d).max() <= 1e-11
 
 
+@pytest.mark.parametrize("batch", [1, 3])
+def test_host_api_wave_pair_c2(ss, batch):
+    """The paper's benchmark shape (C2: 1e5 intervals per sweep, 2.6 waves of interval work for one sweep) takes the
+    wave-aligned two-chunk host pipeline: operators bit-identical to the device call, states equal to rounding (the
+    scan restarts from the carry at the chunk boundary)."""
+    w = W.c2_neural()
+    if batch > 1:
+        w = w.with_(sweep=np.repeat(w.sweep, batch, axis=0) * np.linspace(1.0, 1.01, batch)[:, None],
+                    psi0=W.random_states(batch, 3, seed=33))
+    n0 = ss.kernel_launches()
+    st_d, U_d = gpu_run(ss, w)
+    n_dev = ss.kernel_launches() - n0
+    sim = ss.Simulator(w.spin, w.method, w.expo, w.tau, w.frame, "fp64", w.field)
+    for chunks in (0, 40):
+        n0 = ss.kernel_launches()
+        st_h, U_h = sim.evaluate_host(w.sweep, w.t0, w.t1, w.dt_int, w.dt_out, w.psi0, want_unitaries=True,
+                                      n_chunks=chunks)
+        assert ss.kernel_launches() - n0 > n_dev        # two chunks: interval + scan launches for each
+        assert np.array_equal(U_h, U_d)
+        # two FP64 product orders over 1e5 spin-one intervals (each ≈ 5e-12 from the exact chain, §9.0c)
+        assert np.abs(st_h - st_d).max() <= 1e-11
+
+
 @pytest.mark.parametrize("which", ["C4", "C2", "G1"])
 def test_partition_reproduces_unitaries_bitwise(ss, which):
     """The time grid uses the global k (and the sub-interval split is chosen from the whole problem), so computing a
