@@ -118,8 +118,23 @@ def get_workload(name: str, batch: int, expo: str | None = None) -> W.Workload:
     raise ValueError(name)
 
 
+def _nvml_handle(index: int):
+    """NVML handle of CUDA device `index` (by UUID, so CUDA_VISIBLE_DEVICES remapping is respected), or None."""
+    try:
+        import pynvml
+        import torch
+        pynvml.nvmlInit()
+        try:
+            return pynvml.nvmlDeviceGetHandleByUUID("GPU-" + str(torch.cuda.get_device_properties(index).uuid))
+        except Exception:
+            return pynvml.nvmlDeviceGetHandleByIndex(index)
+    except Exception:
+        return None
+
+
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region, plus NVML polled every 2 ms
+    by a host thread (so sub-second regions such as C2's and C4's also carry clock samples)."""
     QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -129,7 +144,31 @@ class ClockSampler:
         self.proc = None
         self.lines = []
 
+    def _poll_nvml(self):
+        import pynvml
+        R = pynvml
+        bits = {"hw_slowdown": R.nvmlClocksEventReasonHwSlowdown,
+                "hw_thermal_slowdown": R.nvmlClocksEventReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": R.nvmlClocksEventReasonSwThermalSlowdown,
+                "sw_power_cap": R.nvmlClocksEventReasonSwPowerCap}
+        while not self.stop.is_set():
+            try:
+                sm = R.nvmlDeviceGetClockInfo(self.h, R.NVML_CLOCK_SM)
+                mx = R.nvmlDeviceGetMaxClockInfo(self.h, R.NVML_CLOCK_SM)
+                pw = R.nvmlDeviceGetPowerUsage(self.h) / 1000.0
+                rs = R.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.nvml.append((float(sm), float(mx), pw, sorted(n for n, b in bits.items() if rs & b)))
+            except Exception:
+                return
+            self.stop.wait(0.002)
+
     def __enter__(self):
+        self.nvml = []
+        self.stop = threading.Event()
+        self.h = _nvml_handle(self.index)
+        if self.h is not None:
+            self.nvml_thread = threading.Thread(target=self._poll_nvml, daemon=True)
+            self.nvml_thread.start()
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}",
                                           "--format=csv,noheader,nounits", "-lms", "200"],
@@ -145,6 +184,9 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *exc):
+        self.stop.set()
+        if self.h is not None:
+            self.nvml_thread.join(timeout=1)
         if self.proc:
             self.proc.terminate()
             try:
@@ -168,10 +210,17 @@ class ClockSampler:
             for n, v in zip(names, f[5:9]):
                 if v.lower() == "active":
                     reasons.add(n)
+        n_smi = len(sm)
+        for (a, b, c, r) in self.nvml:
+            sm.append(a)
+            mx.append(b)
+            power.append(c)
+            reasons.update(r)
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm), "power_w_median": float(np.median(power))}
+                "samples": len(sm), "samples_nvidia_smi": n_smi, "samples_nvml": len(self.nvml),
+                "power_w_median": float(np.median(power))}
 
 
 BAD_REASONS = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
