@@ -215,6 +215,14 @@ int ss_evaluate_host(ss_sim* sim, double time_start, double time_end, double tim
                      double time_step_output, int64_t batch, const double* h_sweep, const double* h_state_init,
                      double* h_states, double* h_unitaries, int32_t n_chunks);
 
+/* The chunk plan ss_evaluate_host uses for these arguments (pure host logic; needs no GPU — the SM count defaults to
+ * 148 without one).  *kind: 0 = batch chunks (sizes[c] = sweeps), 1 = tent-shaped time chunks, 2 = the wave-aligned
+ * time pair (sizes[c] = intervals of every sweep); *count = number of chunks.  sizes[0..cap) is caller-owned host
+ * memory; SS_ERR_INVALID if cap < *count (then *count is still set) or on the time-grid errors of ss_plan. */
+int ss_host_chunk_plan(const ss_sim* sim, double time_start, double time_end, double time_step_integration,
+                       double time_step_output, int64_t batch, int32_t n_chunks, int32_t* kind, int64_t* sizes,
+                       int32_t cap, int32_t* count);
+
 /* Number of CUDA kernels this library has launched in the process so far (launch accounting for bench.py). */
 int64_t ss_kernel_launches(void);
 

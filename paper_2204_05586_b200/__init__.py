@@ -225,6 +225,17 @@ class Simulator:
                                          vp(U.ctypes.data) if U is not None else None, n_chunks), "ss_evaluate_host")
         return states, U
 
+    def host_chunk_plan(self, time_start, time_end, time_step_integration, time_step_output, batch: int,
+                        n_chunks: int = 0):
+        """(kind, sizes) of the pipeline evaluate_host would run: kind "batch" (sizes in sweeps), "time" (tent) or
+        "wave_pair" (sizes in intervals)."""
+        kind, count = ctypes.c_int32(0), ctypes.c_int32(0)
+        sizes = (ctypes.c_int64 * 64)()
+        check(self._lib.ss_host_chunk_plan(self._h, time_start, time_end, time_step_integration, time_step_output,
+                                           batch, n_chunks, ctypes.byref(kind), sizes, 64, ctypes.byref(count)),
+              "ss_host_chunk_plan")
+        return {0: "batch", 1: "time", 2: "wave_pair"}[kind.value], [int(x) for x in sizes[:count.value]]
+
 
 def scan_states(unitaries: torch.Tensor, state_init: torch.Tensor, out=None, workspace=None, stream=None) -> torch.Tensor:
     """ψ[b][0] = ψ0[b], ψ[b][k+1] = U[b][k] ψ[b][k] (decoupled look-back scan, row a9)."""

@@ -30,7 +30,7 @@ EXPORTS = [
     "ss_set_validation", "ss_compute_unitaries", "ss_scan_workspace_bytes", "ss_scan_states", "ss_scan_states_spin",
     "ss_aggregate_workspace_bytes", "ss_chain_aggregate", "ss_compose_carry", "ss_exponentiate",
     "ss_spin_projection", "ss_evaluate_host", "ss_kernel_launches", "ss_last_error", "ss_version",
-    "ss_num_coefficients", "ss_magnus_bound",
+    "ss_num_coefficients", "ss_magnus_bound", "ss_host_chunk_plan",
 ]
 
 
@@ -80,6 +80,7 @@ def load() -> ctypes.CDLL:
         "ss_exponentiate": (ctypes.c_int, [P, i64, P, P, P]),
         "ss_spin_projection": (ctypes.c_int, [i32, i64, P, P, P]),
         "ss_evaluate_host": (ctypes.c_int, [P, d, d, d, d, i64, P, P, P, P, i32]),
+        "ss_host_chunk_plan": (ctypes.c_int, [P, d, d, d, d, i64, i32, P, P, i32, P]),
         "ss_kernel_launches": (i64, []),
         "ss_last_error": (ctypes.c_char_p, []),
         "ss_version": (ctypes.c_int, []),

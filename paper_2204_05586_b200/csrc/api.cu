@@ -528,6 +528,74 @@ int ss_spin_projection(int32_t spin, int64_t n, const double* d_states, double* 
   return SS_OK;
 }
 
+// Host-buffer pipeline plan (ss_evaluate_host, ss_host_chunk_plan): pure host logic, no device calls beyond the SM
+// count.  kind 0: batch chunks of geometrically shrinking size (sizes = sweeps); kind 1: tent-shaped time chunks,
+// kind 2: the wave-aligned time pair (sizes = intervals).
+//
+// Time chunks: large batches (the chain scan is sequential per sweep — bit-identical to ss_evaluate), and long
+// sweeps of small batches whose interval work spans ≥ 6 waves per chunk on average (one sweep of 1e6 intervals,
+// C4); there the single-sweep scan restarts from the carry each chunk, so states agree with ss_evaluate to
+// rounding (a different product order), not bit for bit.
+static int plan_host_chunks(const ss_sim* s, int64_t K, int64_t L, int64_t batch, int32_t n_chunks, int32_t* kind,
+                     std::vector<int64_t>& ks) {
+  ks.clear();
+  const bool big_batch = batch >= ssb::chain_min_batch();
+  const double waves = (double)batch * K * choose_split(s, batch * K, L) / resident_threads(s);
+  const bool single = n_chunks == 1;                       // the caller asked for one chunk
+  if (n_chunks <= 0) {        // auto: ≈ 40 time chunks where they apply (measured best for C3: e2e 0.97 of device),
+    int64_t tc = std::min<int64_t>(40, K / 4);            // else 4 geometric batch chunks
+    if (!big_batch) tc = std::min<int64_t>(tc, (int64_t)(waves / 8.0));   // C4: 6 (measured best)
+    n_chunks = tc >= 6 ? (int32_t)tc : 4;
+  }
+  const bool tent = n_chunks >= 6 && K >= 4 * (int64_t)n_chunks && (big_batch || waves >= 6.0 * n_chunks);
+  // Wave-aligned pair (C2: one sweep of 1e5 intervals = 2.6 waves, too short for the tent): chunk A holds the whole
+  // waves but the last, chunk B the rest.  Interval work still takes ⌈waves⌉ wave-times in total, and the D2H of
+  // chunk A (most of the states) overlaps chunk B's kernels; only chunk B's copy is left exposed.
+  const int64_t wave_iv = (int64_t)(resident_threads(s) / choose_split(s, batch * K, L)) / batch;   // intervals/wave
+  const int64_t pair_waves = (int64_t)std::ceil(waves) - 1;
+  const bool pair = !tent && !single && !big_batch && batch <= 4 && waves >= 1.2 && wave_iv >= 1 && pair_waves >= 1 &&
+                    pair_waves * wave_iv < K;
+  if (pair) {
+    *kind = 2;
+    ks = {pair_waves * wave_iv, K - pair_waves * wave_iv};
+    return SS_OK;
+  }
+  if (tent) {
+    // Tent-shaped sizes — small first chunks so the device→host copies start early, small last ones so little copy
+    // is left exposed — with weights 1, 2, 3, …, 3, 1, ½, ¼, ¼ (three staging slots: the copy of chunk c overlaps
+    // chunks c+1 and c+2); boundaries from the cumulative weights (rounding errors do not accumulate), every chunk
+    // ≥ 1 interval.
+    *kind = 1;
+    std::vector<double> w = {1.0, 2.0};
+    while ((int)w.size() < n_chunks - 4) w.push_back(3.0);
+    for (double x : {1.0, 0.5, 0.25, 0.25}) w.push_back(x);
+    double wsum = 0;
+    for (double x : w) wsum += x;
+    const int64_t nc = (int64_t)w.size();
+    double cum = 0.0;
+    int64_t b = 0;
+    for (int64_t c = 0; c < nc; ++c) {
+      cum += w[c];
+      int64_t nb = (c + 1 == nc) ? K : (int64_t)std::llround(K * cum / wsum);
+      nb = std::min(std::max(nb, b + 1), K - (nc - c - 1));
+      ks.push_back(nb - b);
+      b = nb;
+    }
+    return SS_OK;
+  }
+  // Geometric batch chunks (B/2, B/4, …, the last two equal): early chunks are big (full-speed chain scan, long
+  // compute that hides the previous chunk's D2H), the final chunk — whose D2H cannot be hidden — is small.
+  *kind = 0;
+  if (n_chunks > batch) n_chunks = (int32_t)batch;
+  int64_t left = batch;
+  for (int c = 0; c < n_chunks && left > 0; ++c) {
+    const int64_t cb = (c == n_chunks - 1) ? left : std::max<int64_t>(1, (left + 1) / 2);
+    ks.push_back(cb);
+    left -= cb;
+  }
+  return SS_OK;
+}
+
 int ss_evaluate_host(ss_sim* s, double t0, double t1, double dt_int, double dt_out, int64_t batch, const double* h_sweep,
                      const double* h_psi0, double* h_states, double* h_U, int32_t n_chunks) {
   if (!s) return fail(SS_ERR_INVALID, "sim is NULL");
@@ -577,56 +645,15 @@ int ss_evaluate_host(ss_sim* s, double t0, double t1, double dt_int, double dt_o
     return r;
   };
   cudaStream_t cs = s->streams[0], xs = s->streams[1];
-  // Time chunks: large batches (the chain scan is sequential per sweep — bit-identical to ss_evaluate), and long
-  // sweeps of small batches whose interval work spans ≥ 6 waves per chunk on average (one sweep of 1e6 intervals,
-  // C4); there the single-sweep scan restarts from the carry each chunk, so states agree with ss_evaluate to
-  // rounding (a different product order), not bit for bit.
-  const bool big_batch = batch >= ssb::chain_min_batch();
-  const double waves = (double)batch * K * choose_split(s, batch * K, L) / resident_threads(s);
-  const bool single = n_chunks == 1;                       // the caller asked for one chunk
-  if (n_chunks <= 0) {        // auto: ≈ 40 time chunks where they apply (measured best for C3: e2e 0.97 of device),
-    int64_t tc = std::min<int64_t>(40, K / 4);            // else 4 geometric batch chunks
-    if (!big_batch) tc = std::min<int64_t>(tc, (int64_t)(waves / 8.0));   // C4: 6 (measured best)
-    n_chunks = tc >= 6 ? (int32_t)tc : 4;
-  }
-  const bool tent = n_chunks >= 6 && K >= 4 * (int64_t)n_chunks && (big_batch || waves >= 6.0 * n_chunks);
-  // Wave-aligned pair (C2: one sweep of 1e5 intervals = 2.6 waves, too short for the tent): chunk A holds the whole
-  // waves but the last, chunk B the rest.  Interval work still takes ⌈waves⌉ wave-times in total, and the D2H of
-  // chunk A (most of the states) overlaps chunk B's kernels; only chunk B's copy is left exposed.
-  const int64_t wave_iv = (int64_t)(resident_threads(s) / choose_split(s, batch * K, L)) / batch;   // intervals/wave
-  const int64_t pair_waves = (int64_t)std::ceil(waves) - 1;
-  const bool pair = !tent && !single && !big_batch && batch <= 4 && waves >= 1.2 && wave_iv >= 1 && pair_waves >= 1 &&
-                    pair_waves * wave_iv < K;
-  if (tent || pair) {
+  int32_t kind = 0;
+  std::vector<int64_t> ks;
+  plan_host_chunks(s, K, L, batch, n_chunks, &kind, ks);
+  if (kind != 0) {
     // Chunk the TIME axis, all sweeps per chunk (for large batches the per-sweep chain kernel stays at full width and
     // is sequential per sweep, so the states are bit-identical to one ss_evaluate).  Chunk c = intervals [k0, k0 + kc)
-    // of every sweep, started from the running carry (the previous chunk's last states).  Tent-shaped sizes — small
-    // first chunks so the device→host copies start early, small last ones so little copy is left exposed — with
-    // weights 1, 2, 3, …, 3, 1, ½, ¼, ¼ and three staging slots (the copy of chunk c overlaps chunks c+1 and c+2).
-    std::vector<double> w = {1.0, 2.0};
-    while ((int)w.size() < n_chunks - 4) w.push_back(3.0);
-    for (double x : {1.0, 0.5, 0.25, 0.25}) w.push_back(x);
-    double wsum = 0;
-    for (double x : w) wsum += x;
-    // chunk boundaries from the cumulative weights (rounding errors do not accumulate), every chunk ≥ 1 interval
-    std::vector<int64_t> ks;
+    // of every sweep, started from the running carry (the previous chunk's last states).
     int64_t kc_max = 0;
-    if (pair) {
-      ks = {pair_waves * wave_iv, K - pair_waves * wave_iv};
-      kc_max = std::max(ks[0], ks[1]);
-    } else {
-      const int64_t nc = (int64_t)w.size();
-      double cum = 0.0;
-      int64_t b = 0;
-      for (int64_t c = 0; c < nc; ++c) {
-        cum += w[c];
-        int64_t nb = (c + 1 == nc) ? K : (int64_t)std::llround(K * cum / wsum);
-        nb = std::min(std::max(nb, b + 1), K - (nc - c - 1));
-        ks.push_back(nb - b);
-        kc_max = std::max(kc_max, nb - b);
-        b = nb;
-      }
-    }
+    for (int64_t x : ks) kc_max = std::max(kc_max, x);
     const size_t sweep_b = align256(sizeof(double) * s->P * batch), carry_b = align256(sizeof(double) * 2 * D * batch);
     const size_t states_b = align256(sizeof(double) * 2 * D * (size_t)batch * (kc_max + 1));
     const size_t U_b = align256(sizeof(double) * 2 * D * D * (size_t)batch * kc_max);
@@ -675,19 +702,9 @@ int ss_evaluate_host(ss_sim* s, double t0, double t1, double dt_int, double dt_o
       if ((e = cudaStreamSynchronize(s->streams[k])) != cudaSuccess) return cuda_fail(e, "stream synchronize");
     return SS_OK;
   }
-  // Geometric chunks (B/2, B/4, …, the last two equal): early chunks are big (full-speed chain scan, long compute
-  // that hides the previous chunk's D2H), the final chunk — whose D2H cannot be hidden — is small.
-  if (n_chunks > batch) n_chunks = (int32_t)batch;
-  std::vector<int64_t> sizes;
-  {
-    int64_t left = batch;
-    for (int c = 0; c < n_chunks && left > 0; ++c) {
-      const int64_t cb = (c == n_chunks - 1) ? left : std::max<int64_t>(1, (left + 1) / 2);
-      sizes.push_back(cb);
-      left -= cb;
-    }
-    n_chunks = (int32_t)sizes.size();
-  }
+  // Geometric batch chunks (plan_host_chunks, kind 0).
+  const std::vector<int64_t>& sizes = ks;
+  n_chunks = (int32_t)sizes.size();
   const int64_t cb_max = sizes[0];
   const size_t sweep_b = align256(sizeof(double) * s->P * cb_max);
   const size_t psi0_b = align256(sizeof(double) * 2 * D * cb_max);
@@ -734,6 +751,23 @@ int ss_evaluate_host(ss_sim* s, double t0, double t1, double dt_int, double dt_o
   }
   for (int k = 0; k < 2; ++k)
     if ((e = cudaStreamSynchronize(s->streams[k])) != cudaSuccess) return cuda_fail(e, "stream synchronize");
+  return SS_OK;
+}
+
+int ss_host_chunk_plan(const ss_sim* s, double t0, double t1, double dt_int, double dt_out, int64_t batch,
+                       int32_t n_chunks, int32_t* kind, int64_t* sizes, int32_t cap, int32_t* count) {
+  if (!s) return fail(SS_ERR_INVALID, "sim is NULL");
+  if (!kind || !count || (cap > 0 && !sizes)) return fail(SS_ERR_INVALID, "kind, count (and sizes) must be non-NULL");
+  int64_t K, L;
+  double dt;
+  int rc = plan_grid(t0, t1, dt_int, dt_out, &K, &L, &dt);
+  if (rc) return rc;
+  if (batch < 1) return fail(SS_ERR_INVALID, "batch must be >= 1");
+  std::vector<int64_t> ks;
+  plan_host_chunks(s, K, L, batch, n_chunks, kind, ks);
+  *count = (int32_t)ks.size();
+  if ((int64_t)ks.size() > (int64_t)cap) return fail(SS_ERR_INVALID, "cap (%d) < number of chunks (%d)", cap, *count);
+  for (size_t c = 0; c < ks.size(); ++c) sizes[c] = ks[c];
   return SS_OK;
 }
 

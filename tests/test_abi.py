@@ -153,3 +153,29 @@ def test_user_field_compiles_without_gpu(lib):
     d = _lib.ss_sim_desc(1, 0, 0, 24, 1, 0, 0)
     assert lib.ss_compile_user_field(ctypes.byref(d), b"__device__ void user_field( {", 1) == _lib.SS_ERR_INVALID
     assert b"compilation failed" in lib.ss_last_error()
+
+
+def test_host_chunk_plan(lib):
+    """ss_evaluate_host's pipeline plan (pure host logic; 148 SMs assumed without a GPU): sizes always partition the
+    batch or the K intervals; C3 takes the 40-chunk tent, C4 six time chunks, C2 the wave-aligned pair whose first
+    chunk is exactly two waves of interval threads (148 SMs × 4 blocks × 128 threads per wave, split S = 2), and an
+    explicit single chunk is honoured."""
+    import workloads as W
+    from paper_2204_05586_b200 import Simulator
+    cases = {"C3": (W.c3_batched(), 8192), "C4": (W.c4_long(), 1), "C2": (W.c2_neural(), 1),
+             "C5": (W.c5_matrix("lie_trotter", batch=100), 100), "small": (W.c3_batched(batch=5, duration=0.2e-3), 5)}
+    plans = {}
+    for name, (w, batch) in cases.items():
+        sim = Simulator(w.spin, w.method, w.expo, w.tau, w.frame, "fp64", w.field)
+        K = int(round((w.t1 - w.t0) / w.dt_out))
+        for n in (0, 1, 3, 6, 40):
+            kind, sizes = sim.host_chunk_plan(w.t0, w.t1, w.dt_int, w.dt_out, batch, n)
+            assert all(x >= 1 for x in sizes), (name, n, sizes)
+            assert sum(sizes) == (batch if kind == "batch" else K), (name, n, kind, sizes)
+            if n == 1:
+                assert (kind, sizes) == ("batch", [batch])
+        plans[name] = sim.host_chunk_plan(w.t0, w.t1, w.dt_int, w.dt_out, batch, 0)
+    assert plans["C3"][0] == "time" and len(plans["C3"][1]) == 40
+    assert plans["C4"][0] == "time" and len(plans["C4"][1]) == 6
+    assert plans["C2"] == ("wave_pair", [2 * 148 * 4 * 128 // 2, 100000 - 2 * 148 * 4 * 128 // 2])
+    assert plans["small"][0] == "batch"
