@@ -71,11 +71,13 @@ struct ss_sim {
   ssb::ExpoLaunchFn expo = nullptr;
   bool user = false;               // run-time compiled user field (ss_create_user)
   ssb::UserKernel user_kernel;
-  // ss_evaluate_host pipeline: streams[0] computes, streams[1] copies; two staging slots; events order them
-  cudaStream_t streams[2] = {nullptr, nullptr};
+  // ss_evaluate_host pipeline: streams[0] computes, streams[1] copies, streams[2] scans the time chunks (so chunk c's
+  // scan overlaps chunk c+1's interval kernel); three staging slots; events order them
+  cudaStream_t streams[3] = {nullptr, nullptr, nullptr};
   static constexpr int kSlots = 3;
   cudaEvent_t computed[kSlots] = {};   // slot's kernels done → its D2H may start
   cudaEvent_t drained[kSlots] = {};    // slot's D2H done → its buffers may be reused
+  cudaEvent_t stepped[kSlots] = {};    // slot's interval kernel done → its scan may start
   int device = -1;
   struct Slot {
     void* buf = nullptr;
@@ -314,6 +316,7 @@ void ss_destroy(ss_sim* s) {
   for (int k = 0; k < ss_sim::kSlots; ++k) {
     if (s->computed[k]) cudaEventDestroy(s->computed[k]);
     if (s->drained[k]) cudaEventDestroy(s->drained[k]);
+    if (s->stepped[k]) cudaEventDestroy(s->stepped[k]);
   }
   delete s;
 }
@@ -536,6 +539,9 @@ int ss_spin_projection(int32_t spin, int64_t n, const double* d_states, double* 
 // sweeps of small batches whose interval work spans ≥ 6 waves per chunk on average (one sweep of 1e6 intervals,
 // C4); there the single-sweep scan restarts from the carry each chunk, so states agree with ss_evaluate to
 // rounding (a different product order), not bit for bit.
+#ifndef SS_HOST_SCAN_STREAM
+#define SS_HOST_SCAN_STREAM 1   // 0: time chunks scan on the compute stream (comparison builds)
+#endif
 static int plan_host_chunks(const ss_sim* s, int64_t K, int64_t L, int64_t batch, int32_t n_chunks, int32_t* kind,
                      std::vector<int64_t>& ks) {
   ks.clear();
@@ -625,12 +631,14 @@ int ss_evaluate_host(ss_sim* s, double t0, double t1, double dt_int, double dt_o
     for (int k = 0; k < ss_sim::kSlots; ++k) {
       if (s->computed[k]) cudaEventDestroy(s->computed[k]), s->computed[k] = nullptr;
       if (s->drained[k]) cudaEventDestroy(s->drained[k]), s->drained[k] = nullptr;
+      if (s->stepped[k]) cudaEventDestroy(s->stepped[k]), s->stepped[k] = nullptr;
     }
     for (auto& st : s->streams)
       if ((e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)) != cudaSuccess) return cuda_fail(e, "stream create");
     for (int k = 0; k < ss_sim::kSlots; ++k)
       if ((e = cudaEventCreateWithFlags(&s->computed[k], cudaEventDisableTiming)) != cudaSuccess ||
-          (e = cudaEventCreateWithFlags(&s->drained[k], cudaEventDisableTiming)) != cudaSuccess)
+          (e = cudaEventCreateWithFlags(&s->drained[k], cudaEventDisableTiming)) != cudaSuccess ||
+          (e = cudaEventCreateWithFlags(&s->stepped[k], cudaEventDisableTiming)) != cudaSuccess)
         return cuda_fail(e, "event create");
     s->device = dev;
   }
@@ -645,9 +653,15 @@ int ss_evaluate_host(ss_sim* s, double t0, double t1, double dt_int, double dt_o
     return r;
   };
   cudaStream_t cs = s->streams[0], xs = s->streams[1];
+
   int32_t kind = 0;
   std::vector<int64_t> ks;
   plan_host_chunks(s, K, L, batch, n_chunks, &kind, ks);
+  // Scans on their own stream only for the tent over few sweeps (C4: the single-sweep scan of chunk c beside chunk
+  // c+1's interval kernel, e2e 0.957 → 0.970 of the device rate).  Measured worse elsewhere: the chain kernel of
+  // large batches (C3: 0.97 → 0.80) and the pair's cooperative scan (C2: 0.71 → 0.65) then wait for the next
+  // interval kernel's blocks to drain, which delays the copies.
+  cudaStream_t ss = (SS_HOST_SCAN_STREAM && kind == 1 && batch < ssb::chain_min_batch()) ? s->streams[2] : cs;
   if (kind != 0) {
     // Chunk the TIME axis, all sweeps per chunk (for large batches the per-sweep chain kernel stays at full width and
     // is sequential per sweep, so the states are bit-identical to one ss_evaluate).  Chunk c = intervals [k0, k0 + kc)
@@ -675,19 +689,24 @@ int ss_evaluate_host(ss_sim* s, double t0, double t1, double dt_int, double dt_o
       double* d_states = reinterpret_cast<double*>(base);
       double* d_U = reinterpret_cast<double*>(base + states_b);
       void* d_scan = base + states_b + U_b;
+      // [cs] interval kernel of chunk c (its slot's D2H, three chunks back, must have drained) → stepped[k];
+      // [ss] scan of chunk c from the running carry, carry ← its last states → computed[k] (the scans stay in chunk
+      // order on ss, so the carry chain is sequential; chunk c+1's interval kernel runs beside chunk c's scan).
       if (c >= (size_t)ss_sim::kSlots && (e = cudaStreamWaitEvent(cs, s->drained[k], 0)) != cudaSuccess)
         return cuda_fail(e, "event wait");
       const auto p = make_params(s, t0, dt_out, dt, L, (int64_t)k0, kc, batch, d_sweep, d_U, batch * K);
       if ((rc = launch_interval_checked(s, p, cs))) return rc;
+      if (ss != cs && ((e = cudaEventRecord(s->stepped[k], cs)) || (e = cudaStreamWaitEvent(ss, s->stepped[k], 0))))
+        return cuda_fail(e, "event record/wait");
       int n = 0;
-      if ((e = ssb::launch_scan(D, batch, kc, d_U, d_carry, d_states, d_scan, cs, &n)) != cudaSuccess)
+      if ((e = ssb::launch_scan(D, batch, kc, d_U, d_carry, d_states, d_scan, ss, &n)) != cudaSuccess)
         return cuda_fail(e, "scan launch");
       g_launches.fetch_add(n);
       // carry ← states[:, kc]
       if ((e = cudaMemcpy2DAsync(d_carry, row, d_states + (size_t)kc * 2 * D, row * (kc + 1), row, batch,
-                                 cudaMemcpyDeviceToDevice, cs)))
+                                 cudaMemcpyDeviceToDevice, ss)))
         return cuda_fail(e, "carry copy");
-      if ((e = cudaEventRecord(s->computed[k], cs)) || (e = cudaStreamWaitEvent(xs, s->computed[k], 0)))
+      if ((e = cudaEventRecord(s->computed[k], ss)) || (e = cudaStreamWaitEvent(xs, s->computed[k], 0)))
         return cuda_fail(e, "event record/wait");
       const size_t first = (c == 0) ? 0 : 1;                     // states[:, 0] of chunk c > 0 is the carry
       if ((e = cudaMemcpy2DAsync(h_states + (k0 + first) * 2 * D, row * (K + 1), d_states + first * 2 * D,
@@ -698,7 +717,7 @@ int ss_evaluate_host(ss_sim* s, double t0, double t1, double dt_int, double dt_o
         return cuda_fail(e, "D2H copy (unitaries)");
       if ((e = cudaEventRecord(s->drained[k], xs))) return cuda_fail(e, "event record");
     }
-    for (int k = 0; k < 2; ++k)
+    for (int k = 0; k < 3; ++k)
       if ((e = cudaStreamSynchronize(s->streams[k])) != cudaSuccess) return cuda_fail(e, "stream synchronize");
     return SS_OK;
   }

@@ -1,0 +1,11 @@
+# time-chunk scans on their own stream (overlap with the next chunk's interval kernel) vs the compute stream
+export PATH=/usr/local/cuda/bin:$PATH
+O=gpurun_out/s10_ss; mkdir -p $O
+timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -q -k "host_api" 2>&1 | tail -2 > $O/pytest_host.log
+for v in noscanstream "" noscanstream ""; do
+  export SPINSIM_LIB=$PWD/paper_2204_05586_b200/libspinsim_b200${v:+.$v}.so
+  for w in C2 C4 C3; do
+    timeout 600 python bench.py --workload $w --no-cpu-baseline --no-probe 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('${v:-scanstream}', '$w', d['value'], d['e2e']['value'], round(d['e2e']['value']/d['value'],4))" >> $O/ab.txt
+  done
+done
+cat $O/pytest_host.log $O/ab.txt
