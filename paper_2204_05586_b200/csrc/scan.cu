@@ -974,13 +974,19 @@ struct CoopArgs {
   double2* agg;            // [grid][D·D] CTA aggregates (workspace)
 };
 
-template <int D>
+// STAGED (one CTA per SM, the CTA's operators ≤ SS_COOP_STAGE_MAX bytes): the CTA's contiguous run of operators is
+// brought into shared memory by ONE bulk copy (cp.async.bulk, mbarrier completion) before pass 1, so the whole run is
+// in flight at once instead of each thread's dependent chain of 144-B loads (C2: 21 µs, long-scoreboard bound), and
+// pass 3 re-reads it from shared memory instead of L2.
+template <int D, bool STAGED>
 __global__ void __launch_bounds__(128) scan_coop_kernel(const CoopArgs a) {
   namespace cg = cooperative_groups;
   constexpr int NT = 128, NW = NT / 32;
   __shared__ double2 sWarpTot[NW][D * D];
   __shared__ double2 sPsiIn[D];
   __shared__ double2 sM[D * D];
+  __shared__ __align__(8) uint64_t sBar;
+  extern __shared__ __align__(128) double2 sRun[];
   const int c = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t K = a.k_count;
   const int64_t b = c / a.cps;
@@ -991,6 +997,22 @@ __global__ void __launch_bounds__(128) scan_coop_kernel(const CoopArgs a) {
   const int64_t m = (k1 - k0 + NT - 1) / NT;
   const int64_t t0 = min(k0 + (int64_t)tid * m, k1), t1 = min(t0 + m, k1);
   const double2* gU = a.U + (size_t)(has ? b : 0) * K * D * D;
+  if constexpr (STAGED) {
+    const unsigned bytes = (unsigned)((k1 - k0) * D * D * sizeof(double2));
+    if (bytes > 0) {
+      if (tid == 0) {
+        mbar_init(&sBar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      }
+      __syncthreads();
+      if (tid == 0) {
+        mbar_expect_tx(&sBar, bytes);
+        tma_load_1d(sRun, gU + (size_t)k0 * D * D, bytes, &sBar);
+      }
+      mbar_wait(&sBar, 0);
+    }
+    gU = sRun - (size_t)k0 * D * D;                          // operator k at gU + k·D² (shared memory)
+  }
   // 1. thread product and block exclusive scan
   CM<D> P;
   cm_eye(P);
@@ -1338,18 +1360,28 @@ size_t scan_workspace_bytes(int dim, int64_t batch, int64_t k_count) {
 }
 
 // Cooperative small-problem scan (scan_coop_kernel): returns cudaErrorNotSupported when the problem is not eligible.
+#ifndef SS_COOP_STAGE_MAX
+#define SS_COOP_STAGE_MAX (200 * 1024)   // bytes of operators one CTA stages in shared memory (0: never stage)
+#endif
 template <int D>
 static cudaError_t run_scan_coop(int64_t batch, int64_t k_count, const double* U, const double* psi0, double* states,
                                  double* spin, void* ws, cudaStream_t s, int* launches) {
-  static int max_grid = -1;
+  static int max_grid = -1, n_sms = 0;
   if (max_grid < 0) {
     int dev = 0, sms = 0, per_sm = 0, coop = 0;
     max_grid = 0;
     if (cudaGetDevice(&dev) == cudaSuccess &&
         cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev) == cudaSuccess && coop &&
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess &&
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scan_coop_kernel<D>, 128, 0) == cudaSuccess)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scan_coop_kernel<D, false>, 128, 0) == cudaSuccess)
       max_grid = std::min(kCoopMaxGrid, sms * std::max(per_sm, 0));
+    n_sms = sms;
+    if (SS_COOP_STAGE_MAX > 0 &&
+        cudaFuncSetAttribute(scan_coop_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             SS_COOP_STAGE_MAX) != cudaSuccess) {
+      (void)cudaGetLastError();
+      n_sms = 0;                                             // staging unavailable: the L2 path only
+    }
   }
   const double bytes = (double)batch * (double)k_count * D * D * sizeof(double2);
   if (SS_SCAN_COOP == 0 || max_grid < 2 || batch * 2 > max_grid || bytes > 64.0 * (1 << 20))
@@ -1362,8 +1394,14 @@ static cudaError_t run_scan_coop(int64_t batch, int64_t k_count, const double* U
   CoopArgs a{batch, k_count, cps, reinterpret_cast<const double2*>(U), reinterpret_cast<const double2*>(psi0),
              reinterpret_cast<double2*>(states), spin, static_cast<double2*>(ws)};
   void* args[] = {&a};
-  const cudaError_t e = cudaLaunchCooperativeKernel((const void*)scan_coop_kernel<D>, dim3((unsigned)(batch * cps)),
-                                                    dim3(128), args, 0, s);
+  // staged when every CTA has an SM of its own and its run of operators fits the shared-memory budget
+  const size_t run_bytes = (size_t)((k_count + cps - 1) / cps) * D * D * sizeof(double2);
+  const bool staged = n_sms > 0 && batch * cps <= n_sms && run_bytes <= (size_t)SS_COOP_STAGE_MAX;
+  const cudaError_t e =
+      staged ? cudaLaunchCooperativeKernel((const void*)scan_coop_kernel<D, true>, dim3((unsigned)(batch * cps)),
+                                           dim3(128), args, run_bytes, s)
+             : cudaLaunchCooperativeKernel((const void*)scan_coop_kernel<D, false>, dim3((unsigned)(batch * cps)),
+                                           dim3(128), args, 0, s);
   if (e == cudaErrorCooperativeLaunchTooLarge) {   // SMs taken by another context (MPS, green contexts): tile scan
     (void)cudaGetLastError();
     return cudaErrorNotSupported;
