@@ -218,6 +218,20 @@ def _fast_unitaries(B, K, d, seed):
     return u * np.exp(1j * rng.uniform(0, 2 * np.pi, (B, K, 1, 3)))
 
 
+@pytest.mark.parametrize("d,B,K", [(3, 1, 1422 * 128), (3, 1, 1422 * 128 + 1),   # 204 768 B per CTA: staged / not
+                                   (2, 1, 3200 * 128), (2, 1, 3200 * 128 + 1),   # 204 800 B per CTA: staged / not
+                                   (3, 1, 100000), (3, 2, 100000), (2, 1, 777)])  # C2 shape; 256 CTAs: L2 path
+def test_scan_coop_staging_boundary(ss, orc, d, B, K):
+    """The cooperative scan stages each CTA's run of operators in shared memory (one bulk copy) when every CTA has an
+    SM of its own and the run fits 200 KB, else it reads them through L2: both sides of each bound against the
+    oracle's sequential long-double chain."""
+    U = _fast_unitaries(B, K, d, seed=K + 7 * B)
+    psi0 = W.random_states(B, d, seed=35)
+    ref = orc.chain(U, psi0)
+    got = ss.scan_states(torch.from_numpy(U).cuda(), torch.from_numpy(psi0).cuda()).cpu().numpy()
+    assert np.abs(got - ref).max() < 1e-12 * max(1.0, np.sqrt(K) / 10)
+
+
 @pytest.mark.parametrize("d,B,K,spin", [(2, 1, 8192 * 600, False),      # tiles of 8192, all full (tensor TMA only)
                                         (2, 1, 1300001, True),          # nst = 4, ragged last tile
                                         (2, 7, 300000, False),          # several sweeps, j-major look-back
