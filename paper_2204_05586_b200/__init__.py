@@ -37,14 +37,29 @@ def _stream_ptr(stream=None):
     return ctypes.c_void_p(s.cuda_stream)
 
 
-def _dev_ptr(t: torch.Tensor, name: str, dtype=None):
+def _dev_ptr(t: torch.Tensor, name: str, dtype=None, shape=None):
+    """Device pointer of `t` after checking it: a contiguous CUDA tensor on the current device, of `dtype` and
+    `shape` when given (raises before any library call, so the kernels never see a short or foreign buffer)."""
     if not isinstance(t, torch.Tensor) or not t.is_cuda:
         raise TypeError(f"{name} must be a CUDA tensor (there is no CPU path)")
+    if t.device.index != torch.cuda.current_device():
+        raise ValueError(f"{name} is on {t.device}, but the current CUDA device is cuda:{torch.cuda.current_device()}")
     if dtype is not None and t.dtype != dtype:
         raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
     if not t.is_contiguous():
         raise ValueError(f"{name} must be contiguous")
     return ctypes.c_void_p(t.data_ptr())
+
+
+def _host_ptr(a: np.ndarray, name: str, dtype, shape):
+    """Pointer of a host array after checking dtype, shape and C-contiguity (ss_evaluate_host reads/writes it raw)."""
+    if not isinstance(a, np.ndarray) or a.dtype != dtype or tuple(a.shape) != tuple(shape) or not a.flags.c_contiguous:
+        raise ValueError(f"{name} must be a C-contiguous {np.dtype(dtype)} array of shape {tuple(shape)}")
+    if not a.flags.writeable and name.startswith("out"):
+        raise ValueError(f"{name} must be writeable")
+    return ctypes.c_void_p(a.ctypes.data)
 
 
 def kernel_launches() -> int:
@@ -134,14 +149,15 @@ class Simulator:
     def workspace_bytes(self, batch: int, K: int, unitaries_in_workspace: bool) -> int:
         return int(self._lib.ss_workspace_bytes(self._h, batch, K, int(unitaries_in_workspace)))
 
-    def _check_inputs(self, sweep, state_init):
-        B = sweep.shape[0]
-        if sweep.dim() != 2 or sweep.shape[1] != self.n_params:
+    def _check_sweep(self, sweep):
+        if not isinstance(sweep, torch.Tensor) or sweep.dim() != 2 or sweep.shape[1] != self.n_params:
             raise ValueError(f"sweep must be [batch][{self.n_params}] float64 for field {self.field!r}")
-        if tuple(state_init.shape) != (B, self.dim):
-            raise ValueError(f"state_init must be [batch={B}][{self.dim}] complex128")
         _dev_ptr(sweep, "sweep", torch.float64)
-        _dev_ptr(state_init, "state_init", torch.complex128)
+        return sweep.shape[0]
+
+    def _check_inputs(self, sweep, state_init):
+        B = self._check_sweep(sweep)
+        _dev_ptr(state_init, "state_init", torch.complex128, (B, self.dim))
         return B
 
     def evaluate(self, sweep, time_start, time_end, time_step_integration, time_step_output, state_init,
@@ -159,24 +175,26 @@ class Simulator:
             workspace = torch.empty(need, dtype=torch.uint8, device=dev)
         check(self._lib.ss_evaluate(self._h, time_start, time_end, time_step_integration, time_step_output, B,
                                     _dev_ptr(sweep, "sweep"), _dev_ptr(state_init, "state_init"),
-                                    _dev_ptr(states, "states", torch.complex128),
-                                    _dev_ptr(U, "unitaries", torch.complex128) if U is not None else None,
-                                    _dev_ptr(workspace, "workspace"), workspace.numel(), _stream_ptr(stream)),
+                                    _dev_ptr(states, "out_states", torch.complex128, (B, K + 1, self.dim)),
+                                    _dev_ptr(U, "out_unitaries", torch.complex128, (B, K, self.dim, self.dim))
+                                    if U is not None else None,
+                                    _dev_ptr(workspace, "workspace", torch.uint8), workspace.numel(),
+                                    _stream_ptr(stream)),
               "ss_evaluate")
         return Results(time_start, time_step_output, self.spin, states, U)
 
     def compute_unitaries(self, sweep, time_start, time_end, time_step_integration, time_step_output,
                           k_begin=0, k_count=None, out=None, stream=None) -> torch.Tensor:
         """Interval kernel only, for global intervals [k_begin, k_begin + k_count) → [B][k_count][dim][dim]."""
-        B = sweep.shape[0]
+        B = self._check_sweep(sweep)
         K, _, _ = plan(time_start, time_end, time_step_integration, time_step_output)
         if k_count is None:
             k_count = K - k_begin
-        _dev_ptr(sweep, "sweep", torch.float64)
         U = out if out is not None else torch.empty((B, k_count, self.dim, self.dim), dtype=torch.complex128, device=sweep.device)
         check(self._lib.ss_compute_unitaries(self._h, time_start, time_end, time_step_integration, time_step_output,
                                              k_begin, k_count, B, _dev_ptr(sweep, "sweep"),
-                                             _dev_ptr(U, "unitaries", torch.complex128), _stream_ptr(stream)),
+                                             _dev_ptr(U, "out", torch.complex128, (B, k_count, self.dim, self.dim)),
+                                             _stream_ptr(stream)),
               "ss_compute_unitaries")
         return U
 
@@ -188,9 +206,9 @@ class Simulator:
     def exponentiate(self, args: torch.Tensor, stream=None) -> torch.Tensor:
         """exp(−i(ax Jx + ay Jy + az Jz + aq Q [+ au1 U1 + au2 U2 + av1 V1 + av2 V2])) for args [n][4] (or [n][8] for
         lie_trotter_su3) float64 (device) → [n][dim][dim] complex128."""
-        args = args.contiguous()
-        if args.dim() != 2 or args.shape[1] != self.num_coefficients:
+        if not isinstance(args, torch.Tensor) or args.dim() != 2 or args.shape[1] != self.num_coefficients:
             raise ValueError(f"args must be [n][{self.num_coefficients}] for exponentiation {self.exponentiation!r}")
+        args = args.contiguous()
         out = torch.empty((args.shape[0], self.dim, self.dim), dtype=torch.complex128, device=args.device)
         check(self._lib.ss_exponentiate(self._h, args.shape[0], _dev_ptr(args, "args", torch.float64),
                                         _dev_ptr(out, "out"), _stream_ptr(stream)), "ss_exponentiate")
@@ -200,8 +218,7 @@ class Simulator:
                      stream=None) -> torch.Tensor:
         """Advisory Magnus-convergence diagnostic: per sweep, the largest Gauss–Legendre estimate of ∫‖H‖₂
         over one fine step (in the integration frame); the expansion converges where it is < SS_MAGNUS_XI."""
-        B = sweep.shape[0]
-        _dev_ptr(sweep, "sweep", torch.float64)
+        B = self._check_sweep(sweep)
         out = torch.empty(B, dtype=torch.float64, device=sweep.device)
         check(self._lib.ss_magnus_bound(self._h, time_start, time_end, time_step_integration, time_step_output, B,
                                         _dev_ptr(sweep, "sweep"), _dev_ptr(out, "out"), _stream_ptr(stream)),
@@ -216,13 +233,17 @@ class Simulator:
         K, _, _ = plan(time_start, time_end, time_step_integration, time_step_output)
         sweep = np.ascontiguousarray(sweep, dtype=np.float64)
         state_init = np.ascontiguousarray(state_init, dtype=np.complex128)
+        if sweep.ndim != 2 or sweep.shape[1] != self.n_params:
+            raise ValueError(f"sweep must be [batch][{self.n_params}] float64 for field {self.field!r}")
         B = sweep.shape[0]
         states = out_states if out_states is not None else np.empty((B, K + 1, self.dim), np.complex128)
         U = np.empty((B, K, self.dim, self.dim), np.complex128) if want_unitaries else None
-        vp = ctypes.c_void_p
         check(self._lib.ss_evaluate_host(self._h, time_start, time_end, time_step_integration, time_step_output, B,
-                                         vp(sweep.ctypes.data), vp(state_init.ctypes.data), vp(states.ctypes.data),
-                                         vp(U.ctypes.data) if U is not None else None, n_chunks), "ss_evaluate_host")
+                                         _host_ptr(sweep, "sweep", np.float64, (B, self.n_params)),
+                                         _host_ptr(state_init, "state_init", np.complex128, (B, self.dim)),
+                                         _host_ptr(states, "out_states", np.complex128, (B, K + 1, self.dim)),
+                                         _host_ptr(U, "out_unitaries", np.complex128, (B, K, self.dim, self.dim))
+                                         if U is not None else None, n_chunks), "ss_evaluate_host")
         return states, U
 
     def host_chunk_plan(self, time_start, time_end, time_step_integration, time_step_output, batch: int,
@@ -237,24 +258,34 @@ class Simulator:
         return {0: "batch", 1: "time", 2: "wave_pair"}[kind.value], [int(x) for x in sizes[:count.value]]
 
 
+def _unitaries_shape(unitaries):
+    if not isinstance(unitaries, torch.Tensor) or unitaries.dim() != 4 or unitaries.shape[2] != unitaries.shape[3] \
+            or unitaries.shape[2] not in (2, 3):
+        raise ValueError("unitaries must be [batch][K][dim][dim] complex128, dim 2 or 3")
+    B, K, dim, _ = unitaries.shape
+    return B, K, dim
+
+
 def scan_states(unitaries: torch.Tensor, state_init: torch.Tensor, out=None, workspace=None, stream=None) -> torch.Tensor:
     """ψ[b][0] = ψ0[b], ψ[b][k+1] = U[b][k] ψ[b][k] (decoupled look-back scan, row a9)."""
-    B, K, dim, _ = unitaries.shape
+    B, K, dim = _unitaries_shape(unitaries)
     lib = _lib.load()
     need = int(lib.ss_scan_workspace_bytes(dim, B, K))
     if workspace is None or workspace.numel() < need:
         workspace = torch.empty(need, dtype=torch.uint8, device=unitaries.device)
     states = out if out is not None else torch.empty((B, K + 1, dim), dtype=torch.complex128, device=unitaries.device)
     check(lib.ss_scan_states(dim, B, K, _dev_ptr(unitaries, "unitaries", torch.complex128),
-                             _dev_ptr(state_init, "state_init", torch.complex128), _dev_ptr(states, "states"),
-                             _dev_ptr(workspace, "workspace"), workspace.numel(), _stream_ptr(stream)), "ss_scan_states")
+                             _dev_ptr(state_init, "state_init", torch.complex128, (B, dim)),
+                             _dev_ptr(states, "out", torch.complex128, (B, K + 1, dim)),
+                             _dev_ptr(workspace, "workspace", torch.uint8), workspace.numel(), _stream_ptr(stream)),
+          "ss_scan_states")
     return states
 
 
 def scan_states_spin(unitaries: torch.Tensor, state_init: torch.Tensor, want_states: bool = True, workspace=None,
                      stream=None):
     """Row a9 with ⟨J⟩ fused into the write-out: returns (states [B][K+1][dim] or None, spin [B][K+1][3])."""
-    B, K, dim, _ = unitaries.shape
+    B, K, dim = _unitaries_shape(unitaries)
     lib = _lib.load()
     need = int(lib.ss_scan_workspace_bytes(dim, B, K))
     if workspace is None or workspace.numel() < need:
@@ -262,7 +293,7 @@ def scan_states_spin(unitaries: torch.Tensor, state_init: torch.Tensor, want_sta
     states = torch.empty((B, K + 1, dim), dtype=torch.complex128, device=unitaries.device) if want_states else None
     spin = torch.empty((B, K + 1, 3), dtype=torch.float64, device=unitaries.device)
     check(lib.ss_scan_states_spin(dim, B, K, _dev_ptr(unitaries, "unitaries", torch.complex128),
-                                  _dev_ptr(state_init, "state_init", torch.complex128),
+                                  _dev_ptr(state_init, "state_init", torch.complex128, (B, dim)),
                                   _dev_ptr(states, "states") if states is not None else None, _dev_ptr(spin, "spin"),
                                   _dev_ptr(workspace, "workspace"), workspace.numel(), _stream_ptr(stream)),
           "ss_scan_states_spin")
@@ -271,7 +302,7 @@ def scan_states_spin(unitaries: torch.Tensor, state_init: torch.Tensor, want_sta
 
 def chain_aggregate(unitaries: torch.Tensor, stream=None) -> torch.Tensor:
     """A[b] = U[b][K−1] ⋯ U[b][0] → [B][dim][dim]."""
-    B, K, dim, _ = unitaries.shape
+    B, K, dim = _unitaries_shape(unitaries)
     lib = _lib.load()
     need = int(lib.ss_aggregate_workspace_bytes(dim, B, K))
     ws = torch.empty(need, dtype=torch.uint8, device=unitaries.device)
@@ -283,10 +314,13 @@ def chain_aggregate(unitaries: torch.Tensor, stream=None) -> torch.Tensor:
 
 def compose_carry(aggregates: torch.Tensor, state_init: torch.Tensor, part: int, stream=None) -> torch.Tensor:
     """carry[b] = A_{part−1} ⋯ A_0 ψ0[b] from all-gathered aggregates [n_parts][B][dim][dim]."""
+    if aggregates.dim() != 4 or aggregates.shape[2] != aggregates.shape[3] or aggregates.shape[2] not in (2, 3):
+        raise ValueError("aggregates must be [n_parts][batch][dim][dim] complex128, dim 2 or 3")
     n_parts, B, dim, _ = aggregates.shape
     out = torch.empty((B, dim), dtype=torch.complex128, device=state_init.device)
     check(_lib.load().ss_compose_carry(dim, B, n_parts, part, _dev_ptr(aggregates, "aggregates", torch.complex128),
-                                       _dev_ptr(state_init, "state_init", torch.complex128), _dev_ptr(out, "carry"),
+                                       _dev_ptr(state_init, "state_init", torch.complex128, (B, dim)),
+                                       _dev_ptr(out, "carry"),
                                        _stream_ptr(stream)), "ss_compose_carry")
     return out
 
@@ -295,6 +329,8 @@ def spin_projection(spin: str, states: torch.Tensor, stream=None) -> torch.Tenso
     """⟨J⟩ for states [..., dim] complex128 → [..., 3] float64 (P:241-243)."""
     states = states.contiguous()
     dim = states.shape[-1]
+    if dim != (2 if spin == "half" else 3):
+        raise ValueError(f"states of spin {spin!r} must end in dim {2 if spin == 'half' else 3}, got {dim}")
     n = states.numel() // dim
     out = torch.empty(states.shape[:-1] + (3,), dtype=torch.float64, device=states.device)
     check(_lib.load().ss_spin_projection(SPIN[spin], n, _dev_ptr(states, "states", torch.complex128),

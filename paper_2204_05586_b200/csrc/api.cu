@@ -251,6 +251,12 @@ int ss_create(const ss_sim_desc* desc, ss_sim** out) {
   if (d.trotter_cutoff < 0 || d.trotter_cutoff > 60) return fail(SS_ERR_INVALID, "trotter_cutoff %d outside 0..60", d.trotter_cutoff);
   if (d.use_rotating_frame != 0 && d.use_rotating_frame != 1) return fail(SS_ERR_INVALID, "use_rotating_frame must be 0 or 1");
   if (d.precision != SS_FP64 && d.precision != SS_FP32) return fail(SS_ERR_INVALID, "precision %d unknown", d.precision);
+  // FP32 mode's 1e-4 bar (BASELINE north_star) holds in the rotating frame it is built for: in the lab
+  // frame every fine step rotates by |ω_z δt| ~ 1 rad and the FP32 rounding accumulates as ε₃₂·Σ|a| (4.5e-4 after
+  // 300 intervals) — so the combination is refused rather than run below its bar.
+  if (d.precision == SS_FP32 && !d.use_rotating_frame)
+    return fail(SS_ERR_UNSUPPORTED, "precision fp32 requires use_rotating_frame = 1: without the frame FP32 rounding "
+                                    "accumulates past the 1e-4 bar (DESIGN.md section 5); use fp64");
   if (field_params(d.field) < 0) return fail(SS_ERR_INVALID, "field %d unknown", d.field);
   ss_sim* s = new ss_sim;
   s->d = d;

@@ -102,6 +102,13 @@ def test_create_validation(lib):
         Simulator("half", "cf4", "lie_trotter_su3", 24, True, "fp64", "constant")
     assert e.value.code == SS_ERR_UNSUPPORTED
     assert Simulator("one").num_coefficients == 4
+    # FP32 needs the rotating frame: in the lab frame its rounding accumulates past the 1e-4 bar
+    for spin, expo in (("half", "analytic"), ("one", "lie_trotter"), ("one", "analytic"), ("one", "lie_trotter_su3")):
+        for method in ("cf4", "midpoint", "heun"):
+            with pytest.raises(SpinsimError) as e:
+                Simulator(spin, method, expo, 24, False, "fp32", "constant")
+            assert e.value.code == SS_ERR_UNSUPPORTED and "use_rotating_frame" in str(e.value)
+            Simulator(spin, method, expo, 24, False, "fp64", "constant")
 
 
 @pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU failure mode")
@@ -179,3 +186,24 @@ def test_host_chunk_plan(lib):
     assert plans["C4"][0] == "time" and len(plans["C4"][1]) == 6
     assert plans["C2"] == ("wave_pair", [2 * 148 * 4 * 128 // 2, 100000 - 2 * 148 * 4 * 128 // 2])
     assert plans["small"][0] == "batch"
+
+
+def test_wrappers_reject_bad_shapes_before_the_library(lib):
+    """The Python wrappers check shapes, dtypes and layout before any ctypes call (the library reads raw pointers)."""
+    from paper_2204_05586_b200 import Simulator
+    sim = Simulator("half", "cf4", "analytic", 24, True, "fp64", "rabi_circular")
+    sweep = np.zeros((2, 2))
+    psi0 = np.zeros((2, 2), np.complex128)
+    with pytest.raises(ValueError, match="sweep"):
+        sim.evaluate_host(np.zeros((2, 3)), 0.0, 1e-5, 1e-7, 1e-6, psi0)
+    with pytest.raises(ValueError, match="state_init"):
+        sim.evaluate_host(sweep, 0.0, 1e-5, 1e-7, 1e-6, np.zeros((3, 2), np.complex128))
+    with pytest.raises(ValueError, match="out_states"):
+        sim.evaluate_host(sweep, 0.0, 1e-5, 1e-7, 1e-6, psi0, out_states=np.zeros((2, 10, 2), np.complex128))
+    with pytest.raises(ValueError, match="out_states"):
+        sim.evaluate_host(sweep, 0.0, 1e-5, 1e-7, 1e-6, psi0, out_states=np.zeros((2, 11, 2), np.complex64))
+    with pytest.raises(ValueError, match="out_states"):
+        sim.evaluate_host(sweep, 0.0, 1e-5, 1e-7, 1e-6, psi0,
+                          out_states=np.zeros((2, 2, 11), np.complex128).transpose(0, 2, 1))
+    with pytest.raises((TypeError, ValueError)):
+        sim.evaluate(torch.zeros(2, 2, dtype=torch.float64), 0.0, 1e-5, 1e-7, 1e-6, torch.zeros(2, 2))
