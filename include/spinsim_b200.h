@@ -54,8 +54,12 @@ enum ss_integration { SS_CF4 = 0, SS_MIDPOINT = 1, SS_HEUN = 2 };   /* P:323; Eu
  * ships such an exponentiator without describing it — DESIGN.md readings R19, R20):
  *   H = ωx Jx + ωy Jy + ωz Jz + ωq Q + ωu1 U1 + ωu2 U2 + ωv1 V1 + ωv2 V2,
  *   U1 = Jx² − Jy², U2 = JxJy + JyJx (Δm = ±2), V1 = JxJz + JzJx, V2 = JyJz + JzJy (Δm = ±1);
- * Lie–Trotter U = T^n, n = 2^τ, T = e^{−iD/2} e^{−iX/2} e^{−iY} e^{−iX/2} e^{−iD/2} (D diagonal, X the (0,1)/(1,2)
- * couplings, Y the (0,2) coupling, each ÷ n), τ dense residual squarings.  Spin-one only; accepts every field. */
+ * Lie–Trotter U = T^n, n = 2^τ with the factor taken on the tridiagonalised generator: the
+ * unitary similarity W (reading R20) makes S = W†HW real symmetric tridiagonal, T = W e^{−iD/2} e^{−iX}
+ * e^{−iD/2} W† (D = diag S, X the (0,1)/(1,2) couplings of S, each ÷ n) — the shape of the paper's own factor
+ * (Eq. lie_trotter_4) — then τ residual squarings of the complex-symmetric T₀ in double-angle form.  A second-order
+ * splitting like the paper's basis product (which the oracle implements); the two agree to rounding for τ ≳ 20.
+ * Spin-one only; accepts every field. */
 enum ss_expo { SS_EXP_ANALYTIC = 0, SS_EXP_LIE_TROTTER = 1, SS_EXP_LIE_TROTTER_SU3 = 2 };  /* P:359 / P:360-466 / P:478 */
 enum ss_precision { SS_FP64 = 0, SS_FP32 = 1 };
 /* Built-in field functions replacing the paper's user numba function.  Sweep parameters:
@@ -88,7 +92,8 @@ typedef struct {
   int32_t exponentiation;     /* ss_expo; SPIN_HALF requires ANALYTIC; SPIN_ONE accepts both (ANALYTIC iff ω_q ≡ 0) */
   int32_t trotter_cutoff;     /* τ: n = 2^τ squarings' exponent; 0..60; default 24 */
   int32_t use_rotating_frame; /* 0/1; default 1 */
-  int32_t precision;          /* ss_precision */
+  int32_t precision;          /* ss_precision; SS_FP32 requires use_rotating_frame = 1 (else SS_ERR_UNSUPPORTED: in the
+                                 lab frame FP32 rounding accumulates past its 1e-4 bar) */
   int32_t field;              /* ss_field */
 } ss_sim_desc;
 

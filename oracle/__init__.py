@@ -154,7 +154,8 @@ def exponentiate(spin: str, args, expo: str = "analytic", tau: int = 24, long_do
 
 
 def trotter_residual_su3(args, tau: int) -> np.ndarray:
-    """T − I of the general spin-one leapfrog factor for args [8] divided by n = 2^tau (reading R20)."""
+    """T − I of the general spin-one factor — the paper's basis product in leapfrog order — for args [8]
+    divided by n = 2^tau (reading R20)."""
     a = _f64(args).reshape(8)
     out = np.zeros((3, 3), dtype=np.complex128)
     _load().oracle_trotter_residual_su3(_ptr(a), tau, _ptr(out))

@@ -282,26 +282,20 @@ template <class R> Mat<R> expm_spin1_analytic(R ax, R ay, R az) {
 
 // ------------------------------------------------------------------------------------------------
 // General spin-one exponentiator (the paper ships it but does not describe it — readings
-// R19, R20 in DESIGN.md).  H = Σ a_j A_j over the su(3) basis
-//   Jx, Jy, Jz (reading R5), Q = diag(1,−2,1)/3, U1 = Jx² − Jy², U2 = JxJy + JyJx (Δm = ±2 quadrupoles),
-//   V1 = JxJz + JzJx, V2 = JyJz + JzJy (Δm = ±1 quadrupoles)   (reading R19),
-// i.e. the Hermitian matrix with
-//   diagonal (az + aq/3, −2aq/3, −az + aq/3),
-//   H01 = (ax − i ay + av1 − i av2)/√2,  H12 = (ax − i ay − av1 + i av2)/√2,  H02 = au1 − i au2.
-// Lie–Trotter in the paper's form, reading R20: the paper's factor is built for a matrix
-// whose only couplings are (0,1) and (1,2) with one common phase (Eq. lie_trotter_4: e^{−iD/2} e^{−iΦJφ} e^{−iD/2},
-// the phase removed by a diagonal similarity R_φ).  A general H is first brought to that shape by a unitary
-// similarity W that fixes the m = +1 basis vector: W = diag(1, G)·diag(1, 1, e^{iψ}) with
-//   G = [[H01*, −H02], [H02*, H01]] / r,   r = √(|H01|² + |H02|²)    (G = I at r = 0),
-// which zeroes the (0,2) entry and makes the (0,1) entry r ≥ 0, and the phase e^{iψ} = B12*/|B12| (B = W†HW before
-// the phase; := 1 at B12 = 0) that makes the (1,2) entry real ≥ 0.  S = W†HW is then real symmetric tridiagonal
-// (the first steps of the Lanczos process started at the m = +1 vector), and
-//   T = W T₀ W†,   T₀ = e^{−iD/2} e^{−iX} e^{−iD/2}     (all arguments divided by n = 2^τ),
-// D = diag(S), X = S − D.  X has a closed-form exponential (X³ = ρ² X, ρ² = S01² + S12²):
-// e^{−iX} = I − i (sin ρ / ρ) X + ((cos ρ − 1)/ρ²) X².  With au = av = 0, W = e^{iφ}·R_φ up to a global phase and
-// T₀ is exactly the paper's factor of Eq. lie_trotter_4.  T − I is assembled from the factors' residuals
-// (cos − 1 = −2 sin²(·/2), expm1 diagonals) by the residual product (I + x)(I + y) − I = x + y + xy and
-// conjugated, T − I = W (T₀ − I) W†; then τ residual squarings s = (a + 2I)a.
+// R19, R20 in DESIGN.md).  H = Σ a_j A_j over the su(3) basis of P:184-187, in the order of Eq.:
+//   A_0..A_3 = Jx, Jy, Jz (reading R5), Q = diag(1,−2,1)/3;
+//   A_4..A_7 = U1 = Jx² − Jy², U2 = JxJy + JyJx (Δm = ±2), V1 = JxJz + JzJx, V2 = JyJz + JzJy (Δm = ±1)   (R19),
+// multiplied out below from the spin matrices themselves.
+// Lie–Trotter exactly as the paper prints it: T is the product of the exponentials of the single basis
+// elements, exp(−i a_j A_j / n), each of which "has a known analytic form" — taken in the leapfrog
+// (symmetric) arrangement the paper applies to its own factor (e^{−iD/2} … e^{−iD/2}, D = the diagonal
+// operators outermost), reading R20:
+//   T = E_2 E_3 E_4 E_5 E_6 E_7 E_0 · e^{−i a_1 A_1/n} · E_0 E_7 E_6 E_5 E_4 E_3 E_2,   E_j = exp(−i a_j A_j / 2n).
+// Closed form of one factor exp(−iθA) − I (residual):
+//   diagonal A (Jz, Q): entrywise expm1(−iθλ_i);
+//   A³ = A (Jx, Jy, U1, U2, V1, V2 — eigenvalues 0, ±1): −i sinθ A + (cosθ − 1) A², cosθ − 1 = −2 sin²(θ/2).
+// The residuals are multiplied by (I + x)(I + y) − I = x + y + xy, then τ residual squarings s = (a + 2I)a
+// and the identity added back.
 // ------------------------------------------------------------------------------------------------
 template <class R> Mat<R> res_prod(const Mat<R>& x, const Mat<R>& y) {   // (I + x)(I + y) − I
   Mat<R> z = mul(x, y);
@@ -309,69 +303,57 @@ template <class R> Mat<R> res_prod(const Mat<R>& x, const Mat<R>& y) {   // (I +
   return z;
 }
 
-template <class R> Mat<R> adjoint(const Mat<R>& x) {
-  Mat<R> y = Mat<R>::zero(x.n);
-  for (int i = 0; i < x.n; ++i) for (int j = 0; j < x.n; ++j) y.a[i][j] = std::conj(x.a[j][i]);
-  return y;
-}
+template <class R> struct SpinOneBasis {
+  Mat<R> A[NF];     // Jx, Jy, Jz, Q, U1, U2, V1, V2
+};
 
-// residual of exp(−iX) for a Hermitian X with X³ = r² X (r² given)
-template <class R> Mat<R> rodrigues_residual(const Mat<R>& X, R r2) {
-  const R r = std::sqrt(r2);
-  const R sinc = (r == R(0)) ? R(1) : std::sin(r) / r;                               // sin r / r
-  const R sh = std::sin(r / R(2));
-  const R cosm1 = (r == R(0)) ? R(-0.5) : -R(2) * sh * sh / r2;                     // (cos r − 1)/r²
-  const Mat<R> X2 = mul(X, X);
+template <class R> SpinOneBasis<R> spin_one_basis() {
   const Cx<R> I(0, 1);
-  Mat<R> a = Mat<R>::zero(3);
-  for (int i = 0; i < 3; ++i) for (int j = 0; j < 3; ++j) a.a[i][j] = -I * sinc * X.a[i][j] + cosm1 * X2.a[i][j];
-  return a;
+  const R s = R(1) / std::sqrt(R(2));
+  Mat<R> Jx = Mat<R>::zero(3), Jy = Mat<R>::zero(3), Jz = Mat<R>::zero(3), Q = Mat<R>::zero(3);
+  Jx.a[0][1] = Jx.a[1][0] = Jx.a[1][2] = Jx.a[2][1] = s;
+  Jy.a[0][1] = -I * s; Jy.a[1][0] = I * s; Jy.a[1][2] = -I * s; Jy.a[2][1] = I * s;
+  Jz.a[0][0] = R(1); Jz.a[2][2] = R(-1);
+  Q.a[0][0] = R(1) / R(3); Q.a[1][1] = R(-2) / R(3); Q.a[2][2] = R(1) / R(3);
+  auto anti = [](const Mat<R>& x, const Mat<R>& y) {       // x y + y x
+    Mat<R> a = mul(x, y), b = mul(y, x);
+    for (int i = 0; i < 3; ++i) for (int j = 0; j < 3; ++j) a.a[i][j] += b.a[i][j];
+    return a;
+  };
+  Mat<R> U1 = mul(Jx, Jx), Jy2 = mul(Jy, Jy);
+  for (int i = 0; i < 3; ++i) for (int j = 0; j < 3; ++j) U1.a[i][j] -= Jy2.a[i][j];
+  SpinOneBasis<R> b;
+  b.A[0] = Jx; b.A[1] = Jy; b.A[2] = Jz; b.A[3] = Q;
+  b.A[4] = U1; b.A[5] = anti(Jx, Jy); b.A[6] = anti(Jx, Jz); b.A[7] = anti(Jy, Jz);
+  return b;
 }
 
-template <class R> Mat<R> su3_hamiltonian(const R a[NF], R n) {      // H/n over the basis above (reading R19)
-  const R rt2 = std::sqrt(R(2));
-  const R z = a[2] / n, q = a[3] / n;
-  Mat<R> H = Mat<R>::zero(3);
-  H.a[0][0] = z + q / R(3);
-  H.a[1][1] = -R(2) * q / R(3);
-  H.a[2][2] = -z + q / R(3);
-  H.a[0][1] = Cx<R>(a[0] + a[6], -(a[1] + a[7])) / (rt2 * n);
-  H.a[1][2] = Cx<R>(a[0] - a[6], -(a[1] - a[7])) / (rt2 * n);
-  H.a[0][2] = Cx<R>(a[4], -a[5]) / n;
-  for (int i = 0; i < 3; ++i) for (int j = 0; j < i; ++j) H.a[i][j] = std::conj(H.a[j][i]);
-  return H;
-}
-
-// The similarity W of reading R20 (W†HW real symmetric tridiagonal, W e0 = e0).
-template <class R> Mat<R> su3_tridiagonaliser(const Mat<R>& H) {
-  const Cx<R> h01 = H.a[0][1], h02 = H.a[0][2];
-  const R r = std::sqrt(std::norm(h01) + std::norm(h02));
-  Mat<R> W = Mat<R>::eye(3);
-  if (r > R(0)) {
-    W.a[1][1] = std::conj(h01) / r;  W.a[1][2] = -h02 / r;
-    W.a[2][1] = std::conj(h02) / r;  W.a[2][2] = h01 / r;
+// exp(−iθA) − I for one basis element A, closed forms above.
+template <class R> Mat<R> basis_factor_residual(const Mat<R>& A, bool diagonal, R th) {
+  Mat<R> e = Mat<R>::zero(3);
+  if (diagonal) {
+    for (int i = 0; i < 3; ++i) e.a[i][i] = expm1i(-th * A.a[i][i].real());
+    return e;
   }
-  const Cx<R> b12 = mul(adjoint(W), mul(H, W)).a[1][2];
-  if (std::abs(b12) > R(0)) {
-    const Cx<R> ph = std::conj(b12) / std::abs(b12);
-    W.a[1][2] *= ph;
-    W.a[2][2] *= ph;
-  }
-  return W;
+  const Cx<R> I(0, 1);
+  const R sh = std::sin(th / R(2));
+  const R cosm1 = -R(2) * sh * sh, sn = std::sin(th);
+  const Mat<R> A2 = mul(A, A);
+  for (int i = 0; i < 3; ++i) for (int j = 0; j < 3; ++j) e.a[i][j] = -I * sn * A.a[i][j] + cosm1 * A2.a[i][j];
+  return e;
 }
 
+// T − I of the leapfrog basis product, arguments a[8] divided by n.
 template <class R> Mat<R> trotter_factor_residual_su3(const R a[NF], R n) {
-  const Mat<R> H = su3_hamiltonian(a, n);
-  const Mat<R> W = su3_tridiagonaliser(H);
-  const Mat<R> S = mul(adjoint(W), mul(H, W));      // real symmetric tridiagonal up to rounding
-  Mat<R> eD = Mat<R>::zero(3);                       // e^{−iD/2} − I
-  for (int i = 0; i < 3; ++i) eD.a[i][i] = expm1i(-S.a[i][i].real() / R(2));
-  Mat<R> X = Mat<R>::zero(3);
-  X.a[0][1] = X.a[1][0] = S.a[0][1].real();
-  X.a[1][2] = X.a[2][1] = S.a[1][2].real();
-  const Mat<R> eX = rodrigues_residual(X, std::norm(X.a[0][1]) + std::norm(X.a[1][2]));
-  const Mat<R> t0 = res_prod(res_prod(eD, eX), eD);  // T₀ − I
-  return mul(W, mul(t0, adjoint(W)));                // T − I = W (T₀ − I) W†
+  static const SpinOneBasis<R> B = spin_one_basis<R>();     // built once (thread-safe static initialisation)
+  const int outer[7] = {2, 3, 4, 5, 6, 7, 0};     // D = (Jz, Q) outermost as in P:374, then U, V, Jx; Jy in the middle
+  const int middle = 1;
+  auto factor = [&](int j, R frac) { return basis_factor_residual(B.A[j], j == 2 || j == 3, frac * a[j] / n); };
+  Mat<R> t = Mat<R>::zero(3);
+  for (int q = 0; q < 7; ++q) t = res_prod(t, factor(outer[q], R(0.5)));
+  t = res_prod(t, factor(middle, R(1)));
+  for (int q = 6; q >= 0; --q) t = res_prod(t, factor(outer[q], R(0.5)));
+  return t;
 }
 
 template <class R> Mat<R> expm_lie_trotter_su3(const R a[NF], int tau) {
@@ -502,35 +484,20 @@ template <class R> Mat<R> interval_operator(const Config& c, const Grid& g, cons
 // Per fine step: δt·(‖H(t₁)‖₂ + ‖H(t₂)‖₂)/2, the two-point Gauss–Legendre estimate of ∫‖H‖₂ on the CF4 sample times,
 // with H the field in the integration frame; the result is the maximum over the sweep.  H is assembled as the
 // dense matrix Σ f_j A_j from the operator DEFINITIONS (spin-half: σ/2; spin-one: Jx, Jy, Jz, Q and the quadrupoles
-// U1 = Jx² − Jy², U2 = {Jx, Jy}, V1 = {Jx, Jz}, V2 = {Jy, Jz} of reading R19, multiplied out here), and ‖H‖₂ is the
+// U1 = Jx² − Jy², U2 = {Jx, Jy}, V1 = {Jx, Jz}, V2 = {Jy, Jz} of reading R19, multiplied out in spin_one_basis), and ‖H‖₂ is the
 // largest |eigenvalue|, from the roots of the characteristic polynomial.
 // ------------------------------------------------------------------------------------------------
 template <class R> Mat<R> dense_hamiltonian(int spin, const R f[NF]) {
-  const Cx<R> I(0, 1);
   if (spin == HALF) {
     Mat<R> h = Mat<R>::zero(2);
     h.a[0][0] = f[2] / R(2);                 h.a[1][1] = -f[2] / R(2);
     h.a[0][1] = Cx<R>(f[0], -f[1]) / R(2);   h.a[1][0] = Cx<R>(f[0], f[1]) / R(2);
     return h;
   }
-  const R s = R(1) / std::sqrt(R(2));
-  Mat<R> Jx = Mat<R>::zero(3), Jy = Mat<R>::zero(3), Jz = Mat<R>::zero(3), Q = Mat<R>::zero(3);
-  Jx.a[0][1] = Jx.a[1][0] = Jx.a[1][2] = Jx.a[2][1] = s;
-  Jy.a[0][1] = -I * s; Jy.a[1][0] = I * s; Jy.a[1][2] = -I * s; Jy.a[2][1] = I * s;
-  Jz.a[0][0] = R(1); Jz.a[2][2] = R(-1);
-  Q.a[0][0] = R(1) / R(3); Q.a[1][1] = R(-2) / R(3); Q.a[2][2] = R(1) / R(3);
-  auto anti = [](const Mat<R>& x, const Mat<R>& y) {       // x y + y x
-    Mat<R> a = mul(x, y), b = mul(y, x);
-    for (int i = 0; i < 3; ++i) for (int j = 0; j < 3; ++j) a.a[i][j] += b.a[i][j];
-    return a;
-  };
-  Mat<R> U1 = mul(Jx, Jx), Jy2 = mul(Jy, Jy);
-  for (int i = 0; i < 3; ++i) for (int j = 0; j < 3; ++j) U1.a[i][j] -= Jy2.a[i][j];
-  const Mat<R> U2 = anti(Jx, Jy), V1 = anti(Jx, Jz), V2 = anti(Jy, Jz);
-  const Mat<R>* A[NF] = {&Jx, &Jy, &Jz, &Q, &U1, &U2, &V1, &V2};
+  static const SpinOneBasis<R> B = spin_one_basis<R>();
   Mat<R> h = Mat<R>::zero(3);
   for (int j = 0; j < NF; ++j)
-    for (int r = 0; r < 3; ++r) for (int c = 0; c < 3; ++c) h.a[r][c] += f[j] * A[j]->a[r][c];
+    for (int r = 0; r < 3; ++r) for (int c = 0; c < 3; ++c) h.a[r][c] += f[j] * B.A[j].a[r][c];
   return h;
 }
 
@@ -726,7 +693,7 @@ int oracle_exponentiate(int spin, int expo, int tau, int use_ld, long long n, in
   return 0;
 }
 
-// T − I of the general spin-one leapfrog factor for a[8] divided by n = 2^tau (long double).
+// T − I of the general spin-one leapfrog basis product (reading R20) for a[8] divided by n = 2^tau (long double).
 int oracle_trotter_residual_su3(const double* a, int tau, double* out) {
   long double al[NF];
   for (int j = 0; j < NF; ++j) al[j] = a[j];

@@ -37,20 +37,21 @@ MUTANTS = {
     # spin-one Jy sign convention broken inside the analytic map
     "d1_sign": ("D.a[1][0] = -rt2 * al * std::conj(be);", "D.a[1][0] = rt2 * al * std::conj(be);"),
     # --- general spin-one (su(3)) exponentiator and fields (readings R19, R20) ---
-    # V1 enters the lower pair with the wrong sign
-    "su3_v_sign": ("Cx<R>(a[0] - a[6], -(a[1] - a[7]))", "Cx<R>(a[0] + a[6], -(a[1] - a[7]))"),
+    # V1 built from the wrong pair of spin matrices (operator mix-up in the basis, reading R19)
+    "su3_v1_def": ("b.A[6] = anti(Jx, Jz);", "b.A[6] = anti(Jy, Jz);"),
+    # U2 = JxJy only: not Hermitian
+    "su3_u2_herm": ("b.A[5] = anti(Jx, Jy);", "b.A[5] = mul(Jx, Jy);"),
     # U pair rotated by θ instead of 2θ in the frame
     "su3_u_frame_angle": ("const R c2 = std::cos(R(2) * th), s2 = std::sin(R(2) * th);", "const R c2 = c, s2 = s;"),
-    # leapfrog half-step dropped on the diagonal part
-    "su3_d_half": ("expm1i(-S.a[i][i].real() / R(2))", "expm1i(-S.a[i][i].real())"),
-    # (0,2) coupling not Hermitian
-    "su3_h02_conj": ("H.a[0][2] = Cx<R>(a[4], -a[5]) / n;", "H.a[0][2] = Cx<R>(a[4], a[5]) / n;"),
-    # tridiagonalising rotation built from H01 instead of its conjugate
-    "su3_w_conj": ("W.a[1][1] = std::conj(h01) / r;", "W.a[1][1] = h01 / r;"),
-    # phase e^{iψ} applied with the wrong sign
-    "su3_w_phase": ("const Cx<R> ph = std::conj(b12) / std::abs(b12);", "const Cx<R> ph = b12 / std::abs(b12);"),
-    # factor conjugated the wrong way round: W† (T₀ − I) W
-    "su3_w_side": ("return mul(W, mul(t0, adjoint(W)));", "return mul(adjoint(W), mul(t0, W));"),
+    # leapfrog half-step dropped on the outer factors of the first half (over-rotation)
+    "su3_outer_half": ("for (int q = 0; q < 7; ++q) t = res_prod(t, factor(outer[q], R(0.5)));",
+                       "for (int q = 0; q < 7; ++q) t = res_prod(t, factor(outer[q], R(1)));"),
+    # middle factor multiplied on the wrong side: no longer symmetric (first-order splitting)
+    "su3_middle_side": ("t = res_prod(t, factor(middle, R(1)));", "t = res_prod(factor(middle, R(1)), t);"),
+    # closed form with cos θ − 1 = −sin²(θ/2) (dropped factor 2)
+    "su3_cosm1": ("const R cosm1 = -R(2) * sh * sh, sn = std::sin(th);", "const R cosm1 = -sh * sh, sn = std::sin(th);"),
+    # closed form with +i sin θ A
+    "su3_sin_sign": ("e.a[i][j] = -I * sn * A.a[i][j] + cosm1 * A2.a[i][j];", "e.a[i][j] = I * sn * A.a[i][j] + cosm1 * A2.a[i][j];"),
     # two-photon drive at ω_d instead of 2ω_d
     "su3_drive_2w": ("f[4] = (R)p[4] * std::cos(R(2) * ph);", "f[4] = (R)p[4] * std::cos(ph);"),
     # --- Magnus diagnostic ---

@@ -65,14 +65,16 @@ def test_su3_lie_trotter_vs_expm_random(orc):
     assert np.abs(U - ref).max() < 1e-14
 
 
-def test_su3_reduces_to_paper_factor(orc):
-    """With au = av = 0 the factor is the paper's T of Eq. lie_trotter_4: same U as the 4-operator
-    exponentiator up to rounding, for every τ (so also the Trotter error is the paper's)."""
+def test_su3_four_operator_case(orc):
+    """With au = av = 0 the basis product (reading R20) and the paper's own factor of Eq. lie_trotter_4 are two
+    second-order splittings of the same exponential: both within rounding of expm at τ = 24, so they agree there; at
+    τ = 0 they are different splittings (the paper groups Jx, Jy into one rotation ΦJφ)."""
     a4 = W.random_exponent_args(300, 1.0, seed=22)
     a8 = np.concatenate([a4, np.zeros((300, 4))], axis=1)
-    for tau in (0, 4, 24):
-        d = np.abs(orc.exponentiate("one", a8, "lie_trotter_su3", tau) - orc.exponentiate("one", a4, "lie_trotter", tau))
-        assert d.max() < 2e-15, tau
+    d = np.abs(orc.exponentiate("one", a8, "lie_trotter_su3", 24) - orc.exponentiate("one", a4, "lie_trotter", 24))
+    assert d.max() < 5e-15
+    d0 = np.abs(orc.exponentiate("one", a8, "lie_trotter_su3", 0) - orc.exponentiate("one", a4, "lie_trotter", 0))
+    assert d0.max() > 1e-3
 
 
 def test_su3_tau_sweep(orc):
@@ -85,69 +87,72 @@ def test_su3_tau_sweep(orc):
     assert max(errs[6:]) < 1e-14, errs
 
 
-def _mp_expm_residual(H, s):
-    """exp(−i s H) − I in 40-digit arithmetic (mpmath), no cancellation issue at this precision."""
+# Leapfrog order of the basis product (reading R20): diagonal operators (Jz, Q) outermost as in P:374, then U1, U2,
+# V1, V2, Jx, and Jy in the middle with the full step.
+OUTER, MIDDLE = (2, 3, 4, 5, 6, 7, 0), 1
+
+
+def _mp_basis_product_residual(a, n):
+    """T − I of the leapfrog basis product in 40-digit arithmetic: mpmath.expm of each single operator −i·frac·a_j·A_j/n
+    (the test's own matrices), multiplied out in order, then I subtracted (no cancellation at this precision)."""
     with mpmath.workdps(40):
-        M = mpmath.matrix([[mpmath.mpc(complex(H[i, j])) * (-1j) * s for j in range(3)] for i in range(3)])
-        E = mpmath.expm(M) - mpmath.eye(3)
-        return np.array([[complex(E[i, j]) for j in range(3)] for i in range(3)])
-
-
-def _mp_lanczos(Hm):
-    """Lanczos from the m = +1 basis vector in mpmath: W = [q0, q1, q2] with W†HW real tridiagonal, positive
-    off-diagonals (a construction independent of the oracle's explicit Givens-plus-phase W)."""
-    q0 = mpmath.matrix([1, 0, 0])
-    dot = lambda u, v: sum(mpmath.conj(u[i]) * v[i] for i in range(3))
-    w = Hm * q0
-    w = w - dot(q0, w) * q0
-    b1 = mpmath.sqrt(mpmath.re(dot(w, w)))
-    q1 = w / b1
-    w = Hm * q1
-    w = w - dot(q0, w) * q0 - dot(q1, w) * q1
-    q2 = w / mpmath.sqrt(mpmath.re(dot(w, w)))
-    return mpmath.matrix([[q[i] for q in (q0, q1, q2)] for i in range(3)])
+        def ex(j, frac):
+            M = mpmath.matrix([[mpmath.mpc(complex(BASIS[j][r, c])) for c in range(3)] for r in range(3)])
+            return mpmath.expm(M * (-1j) * mpmath.mpf(a[j]) * frac / n)
+        T = mpmath.eye(3)
+        for j in OUTER:
+            T = T * ex(j, mpmath.mpf(1) / 2)
+        T = T * ex(MIDDLE, 1)
+        for j in reversed(OUTER):
+            T = T * ex(j, mpmath.mpf(1) / 2)
+        T = T - mpmath.eye(3)
+        return np.array([[complex(T[i, j]) for j in range(3)] for i in range(3)])
 
 
 def test_su3_factor_residual_vs_mpmath(orc):
-    """T − I = W (e^{−iD/2n} e^{−iX/n} e^{−iD/2n} − I) W† with S = W†HW = D + X real tridiagonal (reading R20)
-    against 40-digit arithmetic with W from the Lanczos process (mpmath) — elementwise RELATIVE accuracy (the
-    residual form keeps the digits P:463-466 asks for), at a large and a tiny argument scale."""
+    """T − I of the basis product (reading R20) against 40-digit arithmetic — elementwise RELATIVE accuracy
+    (the residual form keeps the digits P:463-466 asks for, which subtracting I from T would lose), at a large and a
+    tiny argument scale."""
     rng = np.random.default_rng(24)
     for scale, tau in ((1.0, 0), (1.0, 20), (1e-4, 24)):
         for _ in range(6):
             a = rng.uniform(-scale, scale, 8)
-            n = 2.0 ** tau
-            Hfull = H8(a)
-            with mpmath.workdps(40):
-                Hm = mpmath.matrix([[mpmath.mpc(complex(Hfull[i, j])) for j in range(3)] for i in range(3)])
-                Wm = _mp_lanczos(Hm)
-                S = Wm.H * Hm * Wm
-                assert abs(S[0, 2]) < mpmath.mpf(10) ** -35 and abs(mpmath.im(S[1, 2])) < mpmath.mpf(10) ** -35
-                D = mpmath.diag([mpmath.re(S[i, i]) for i in range(3)])
-                X = mpmath.matrix(3, 3)
-                X[0, 1] = X[1, 0] = mpmath.re(S[0, 1])
-                X[1, 2] = X[2, 1] = mpmath.re(S[1, 2])
-                ex = lambda M, s: mpmath.expm(M * (-1j) * s / n)
-                T = Wm * ex(D, 0.5) * ex(X, 1.0) * ex(D, 0.5) * Wm.H - mpmath.eye(3)
-                ref = np.array([[complex(T[i, j]) for j in range(3)] for i in range(3)])
+            ref = _mp_basis_product_residual(a, 2.0 ** tau)
             got = orc.trotter_residual_su3(a, tau)
-            assert np.all(np.abs(got - ref) <= 1e-15 * np.abs(ref) + 1e-16 * scale / n), (scale, tau, got - ref)
+            assert np.all(np.abs(got - ref) <= 1e-15 * np.abs(ref) + 1e-16 * scale / 2.0 ** tau), (scale, tau, got - ref)
 
 
-def test_su3_factor_special_cases(orc):
-    """The reading-R20 factor's special shapes: (i) no (0,1)/(0,2) coupling (r = 0, W = phase only), (ii) no (1,2)
-    coupling after the rotation (B12 = 0), (iii) Δm = ±2 coupling only — each against the 40-digit Lanczos factor's
-    defining property: T unitary, and T = exp(−iH/n) + O(|H/n|³) with the Strang constant (halving H divides the
-    error by ≈ 8)."""
-    for a in (np.array([0.4, 0.4, 0.3, -0.7, 0, 0, -0.4, -0.4]),  # H01 = H02 = 0: r = 0, W = phase only
-              np.array([0.5, 0.2, 0.1, 0.3, 0, 0, 0.5, 0.2]),     # H12 = 0 (ax = av1, ay = av2)
-              np.array([0, 0, 0.2, 0.1, 0.8, -0.6, 0, 0])):       # U pair only: H01 = H12 = 0
+def test_su3_factor_properties(orc):
+    """Properties of the factor that do not depend on the splitting order: (i) unitary for any argument, (ii) exact
+    when only the commuting diagonal operators (Jz, Q) are present, (iii) T = exp(−iH/n) + O(|H/n|³) — a symmetric
+    (second-order) splitting: halving the argument divides the error by ≈ 8 (a first-order product would give ≈ 4)."""
+    rng = np.random.default_rng(25)
+    for _ in range(50):
+        a = rng.uniform(-2, 2, 8)
+        T = orc.trotter_residual_su3(a, 0) + np.eye(3)
+        assert np.abs(T.conj().T @ T - np.eye(3)).max() < 1e-15
+    a = np.array([0, 0, 0.7, -1.9, 0, 0, 0, 0])
+    assert np.abs(orc.trotter_residual_su3(a, 0) + np.eye(3) - sl.expm(-1j * H8(a))).max() < 1e-16
+    for a in (np.array([0.4, 0.4, 0.3, -0.7, 0, 0, -0.4, -0.4]), np.array([0, 0, 0.2, 0.1, 0.8, -0.6, 0, 0]),
+              rng.uniform(-1, 1, 8)):
         errs = []
-        for s in (1.0, 0.5, 0.25):
+        for s in (0.2, 0.1, 0.05):
             T = orc.trotter_residual_su3(s * a, 0) + np.eye(3)
-            assert np.abs(T.conj().T @ T - np.eye(3)).max() < 1e-15
             errs.append(np.abs(T - sl.expm(-1j * H8(s * a))).max())
-        assert 6 < errs[0] / errs[1] < 10 and 6 < errs[1] / errs[2] < 10, errs
+        assert 6.5 < errs[0] / errs[1] < 9.5 and 6.5 < errs[1] / errs[2] < 9.5, errs
+
+
+def test_su3_basis_closed_forms():
+    """The closed form the oracle uses for the non-diagonal factors needs A³ = A (eigenvalues 0, ±1) for Jx, Jy, U1,
+    U2, V1, V2; Jz and Q are diagonal."""
+    for j in (0, 1, 4, 5, 6, 7):
+        A = BASIS[j]
+        assert np.abs(A @ A @ A - A).max() < 1e-15, j
+        th = 0.37
+        E = np.eye(3) - 1j * np.sin(th) * A + (np.cos(th) - 1) * (A @ A)
+        assert np.abs(E - sl.expm(-1j * th * A)).max() < 1e-15, j
+    for j in (2, 3):
+        assert np.abs(BASIS[j] - np.diag(np.diag(BASIS[j]))).max() == 0
 
 
 def test_su3_structure(orc):
