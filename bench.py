@@ -7,8 +7,10 @@
 A "step" is one pass of the whole hot path (SURVEY §8(a) rows a1–a9: interval kernel + state scan) over one batch.
 Default workload: C3 (BASELINE configs[2]) — 8192 spin-one sweeps × 10 ms, δt = 100 ns, Δt = 1 µs, Lie–Trotter
 τ = 24, rotating frame — the batch-summed FP64 workload the metric is quoted on "at 1/2/4/8 B200".  Multi-GPU
-shards sweeps (no data-path collective); `--scaling weak` (default) keeps 8192 sweeps per rank, `--scaling strong`
-splits 8192 across ranks.  Timing: CUDA events on the launching stream, barrier + synchronize on both sides, max
+shards sweeps (no data-path collective); `--scaling strong` (default: BASELINE configs[2], "8192 … sharded across
+1/2/4/8 GPUs") splits the 8192 sweeps into contiguous blocks, one per rank; `--scaling weak` keeps 8192 sweeps per
+rank.  `--emulate-ranks N` (one GPU, no torchrun) times rank 0's shard of an N-rank strong-scaling run and adds the
+predicted N-GPU value (shard rate × N: sweep sharding has no exchange) — the per-rank shard shapes of the SCALE run.  Timing: CUDA events on the launching stream, barrier + synchronize on both sides, max
 over ranks (all_reduce MAX).  Working set (U 11.8 GB + states 3.9 GB per rank) ≫ L2 (126 MB), so no flush is needed.
 
 `--impl reference` times the CPU oracle (oracle/, the "reference arm" of this tier) on the host cores on a bounded
@@ -100,8 +102,15 @@ def hbm_peak_gbs():
     return 6650.0, "of fallback (B200_PROFILING.md: 6.65 TB/s)"
 
 
-def scan_bytes_per_interval(dim: int) -> int:
-    return (2 * dim * dim + 2 * dim) * 8       # read U_k, write ψ_{k+1}
+def scan_bytes_per_interval(dim: int, compact: bool = False) -> int:
+    """Algorithmic bytes of the state scan per interval: read U_k (dense dim×dim complex128, or the 32-B SU(2)
+    element the SU(2)-form paths hand over when U_k is not an output) + write ψ_{k+1}."""
+    return (2 * (2 if compact else dim * dim) + 2 * dim) * 8
+
+
+def su2_form(w) -> bool:
+    """spin-half and analytic spin-one accumulate in SU(2) (DESIGN.md §5 items 10-11): compact operators."""
+    return w.spin == "half" or w.expo == "analytic"
 
 
 def get_workload(name: str, batch: int, expo: str | None = None) -> W.Workload:
@@ -362,6 +371,20 @@ def reduce_max(vals, dev, world):
     return t.tolist()
 
 
+def shard_of(args, rank, world):
+    """This rank's contiguous block [lo, hi) of sweeps and the whole job's workload (shards are
+    contiguous blocks of B/G sweeps).  With --emulate-ranks N on one process: rank 0's block of an N-rank job."""
+    ranks = world
+    if world == 1 and args.emulate_ranks > 1:
+        ranks = args.emulate_ranks
+    if args.scaling == "weak":
+        full = get_workload(args.workload, args.batch * ranks, args.expo)
+        return rank * args.batch, (rank + 1) * args.batch, full
+    full = get_workload(args.workload, args.batch, args.expo)
+    per = (full.batch + ranks - 1) // ranks
+    return rank * per, min(full.batch, (rank + 1) * per), full
+
+
 def run_ours(args, rank, world, local):
     import torch
     import paper_2204_05586_b200 as ss
@@ -378,35 +401,31 @@ def run_ours(args, rank, world, local):
     if args.workload == "C4":
         return run_time_partition(args, rank, world, local, dev)
     # sweep shard of this rank
-    if args.scaling == "weak":
-        full = get_workload(args.workload, args.batch * world, args.expo)
-        lo, hi = rank * args.batch, (rank + 1) * args.batch
-    else:
-        full = get_workload(args.workload, args.batch, args.expo)
-        per = (full.batch + world - 1) // world
-        lo, hi = rank * per, min(full.batch, (rank + 1) * per)
+    lo, hi, full = shard_of(args, rank, world)
     w = full.with_(sweep=np.ascontiguousarray(full.sweep[lo:hi]), psi0=np.ascontiguousarray(full.psi0[lo:hi]))
     B, K, L, D = w.batch, w.K, w.L, w.dim
     sim = ss.Simulator(w.spin, w.method, w.expo, w.tau, w.frame, args.precision, w.field)
     sweep = torch.from_numpy(w.sweep).to(dev)
     psi0 = torch.from_numpy(w.psi0).to(dev)
     states = torch.empty((B, K + 1, D), dtype=torch.complex128, device=dev)
-    U = torch.empty((B, K, D, D), dtype=torch.complex128, device=dev)
-    scan_ws = torch.empty(int(ss._lib.load().ss_scan_workspace_bytes(D, B, K)), dtype=torch.uint8, device=dev)
+    ws = torch.empty(sim.workspace_bytes(B, K, True), dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
 
-    # Inputs validated once through the full public call (also a correctness warm-up of ss_evaluate).
-    sim.evaluate(sweep[: min(B, 4)], w.t0, min(w.t1, w.t0 + 20 * w.dt_out), w.dt_int, w.dt_out, psi0[: min(B, 4)])
+    # The step is the public ss_evaluate call (interval kernel + state scan; U_k not requested, so it stays in the
+    # workspace — compact SU(2) elements on the SU(2)-form paths).  Its synchronous input validation runs once here,
+    # on the full inputs, and is then switched off (ss_set_validation: a one-time check, not part of the path).
+    sim.evaluate(sweep, w.t0, w.t0 + w.dt_out, w.dt_int, w.dt_out, psi0, want_unitaries=False)
+    sim.set_validation(False)
 
     def step(ev=None):
         if ev is not None:
             ev[0].record(stream)
-        sim.compute_unitaries(sweep, w.t0, w.t1, w.dt_int, w.dt_out, out=U)
-        if ev is not None:
-            ev[1].record(stream)
-        ss.scan_states(U, psi0, out=states, workspace=scan_ws)
+            sim.set_split_event(ev[1])       # recorded inside ss_evaluate between the interval kernel and the scan
+        sim.evaluate(sweep, w.t0, w.t1, w.dt_int, w.dt_out, psi0, want_unitaries=False, workspace=ws,
+                     out_states=states)
         if ev is not None:
             ev[2].record(stream)
+            sim.set_split_event(None)
 
     def barrier():
         if world > 1:
@@ -422,13 +441,15 @@ def run_ours(args, rank, world, local):
     t_scan = float(np.mean([e[1].elapsed_time(e[2]) for e in evs]))
     elapsed_ms, t_interval, t_scan = reduce_max([elapsed_ms, t_interval, t_scan], dev, world)
     steps_per_rank = w.fine_steps
-    total_steps = steps_per_rank * world if args.scaling == "weak" else full.fine_steps
+    emulated = world == 1 and args.emulate_ranks > 1
+    total_steps = steps_per_rank * world if (args.scaling == "weak" or emulated) else full.fine_steps
     value = total_steps * args.steps / (elapsed_ms * 1e-3)
 
     # roofline of the dominant kernel (interval kernel): algorithmic flops per launch / average launch duration
     flops_launch = algorithmic_flops_per_fine_step(w.spin, w.expo, w.tau, w.method) * steps_per_rank
     achieved = flops_launch / (t_interval * 1e-3) / 1e12
-    scan_gbs = B * K * scan_bytes_per_interval(D) / (t_scan * 1e-3) / 1e9
+    scan_bpi = scan_bytes_per_interval(D, su2_form(w))
+    scan_gbs = B * K * scan_bpi / (t_scan * 1e-3) / 1e9
     peak = FP64_PEAK_TFLOPS if args.precision == "fp64" else FP32_PEAK_TFLOPS
     kernel_name = f"interval_kernel<spin-{w.spin},{w.expo},{w.method},{w.field},{args.precision}>"
 
@@ -486,10 +507,16 @@ def run_ours(args, rank, world, local):
                                                     if clocks.get("sm_mhz") else None)},
             "scan": {"bound": "hbm", "achieved": scan_gbs, "unit": "GB/s", "peak": hbm_peak_gbs()[0],
                      "frac": scan_gbs / hbm_peak_gbs()[0], "peak_basis": hbm_peak_gbs()[1], "ms_per_launch": t_scan,
-                     "bytes_per_launch": B * K * scan_bytes_per_interval(D)},
+                     "bytes_per_launch": B * K * scan_bpi,
+                     "operators": "SU(2) elements, 32 B" if su2_form(w) else f"dense {D}x{D} complex128"},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
             "fine_steps_per_step": total_steps,
         }
+        if emulated:
+            line["emulated"] = {"ranks": args.emulate_ranks, "rank": 0, "sweeps_per_rank": B,
+                                "predicted_value": value * args.emulate_ranks,
+                                "note": "one GPU timing rank 0's shard; value is that shard's rate, predicted_value "
+                                        "assumes the other ranks' identical shards run concurrently (no exchange)"}
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
@@ -593,7 +620,9 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=["C3", "C2", "C5", "C4", "G1"], default="C3")
     ap.add_argument("--batch", type=int, default=8192, help="sweeps per rank (weak) or in total (strong), C3")
-    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="strong")
+    ap.add_argument("--emulate-ranks", type=int, default=1,
+                    help="one GPU: time rank 0's shard of an N-rank strong-scaling job (per-rank shard shapes)")
     ap.add_argument("--precision", choices=["fp64", "fp32"], default="fp64")
     ap.add_argument("--expo", choices=["analytic", "lie_trotter"], default=None,
                     help="C5 only: the exponentiator column of the accuracy/throughput matrix (default lie_trotter)")

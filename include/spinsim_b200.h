@@ -140,7 +140,10 @@ size_t ss_workspace_bytes(const ss_sim* sim, int64_t batch, int64_t K, int32_t u
  *   d_states      device [batch][K+1][dim] complex128 (out)
  *   d_unitaries   device [batch][K][dim][dim] complex128 (out) or NULL (then kept in the workspace)
  *   d_workspace   device, >= ss_workspace_bytes(sim, batch, K, d_unitaries == NULL), 256-byte aligned
- * Validates sweep/state finiteness (and ω_q ≡ 0 for ANALYTIC spin-one) with a tiny device check that
+ * With d_unitaries == NULL on the SU(2)-form paths (spin-half; ANALYTIC spin-one) the interval operators reach the
+ * scan in the workspace as SU(2) elements (a, b) of U = [[a, b], [−b*, a*]] (32 B per interval instead of 64 / 144 B;
+ * D¹ of it for spin-one, reading R14) — the same operators, so the states agree with the dense path to
+ * rounding.  Validates sweep/state finiteness (and ω_q ≡ 0 for ANALYTIC spin-one) with a tiny device check that
  * synchronises the stream once, unless disabled by ss_set_validation(sim, 0). */
 int ss_evaluate(ss_sim* sim, double time_start, double time_end, double time_step_integration,
                 double time_step_output, int64_t batch, const double* d_sweep, const double* d_state_init,
@@ -149,6 +152,11 @@ int ss_evaluate(ss_sim* sim, double time_start, double time_end, double time_ste
 /* Enable (1, default) / disable (0) the synchronous input validation inside ss_evaluate (disable it to capture
  * ss_evaluate in a CUDA graph). */
 int ss_set_validation(ss_sim* sim, int32_t enabled);
+
+/* Profiling hook: `event` (a cudaEvent_t passed as void*, owned by the caller; NULL to clear) is recorded by every
+ * later ss_evaluate on its stream between the interval kernel and the state scan, so a caller can time the two
+ * phases of one call with its own events around it.  No other effect. */
+int ss_set_split_event(ss_sim* sim, void* event);
 
 /* Interval kernel only (rows a1–a8) for global interval indices k ∈ [k_begin, k_begin + k_count) of a grid of K
  * intervals: writes d_unitaries [batch][k_count][dim][dim].  The time grid uses the global k, so a time partition
@@ -171,6 +179,14 @@ int ss_scan_states(int32_t dim, int64_t batch, int64_t k_count, const double* d_
 int ss_scan_states_spin(int32_t dim, int64_t batch, int64_t k_count, const double* d_unitaries,
                         const double* d_state_init, double* d_states, double* d_spin, void* d_workspace,
                         size_t workspace_bytes, void* stream);
+
+/* Row a9 over compact SU(2) operators (the form the SU(2)-form interval kernels accumulate, DESIGN.md §5 items
+ * 10-11): d_ops device [batch][k_count][2] complex128 holds (a, b) of U_k = [[a, b], [−b*, a*]] (|a|² + |b|² = 1 is
+ * assumed, not checked); dim = 2 applies U_k, dim = 3 its spin-1 representation
+ * D¹(U) = [[a², √2ab, b²], [−√2ab*, |a|²−|b|², √2a*b], [b*², −√2a*b*, a*²]] (reading R14).  d_states and d_spin as in
+ * ss_scan_states_spin (either may be NULL, not both); workspace >= ss_scan_workspace_bytes(dim, batch, k_count). */
+int ss_scan_states_su2(int32_t dim, int64_t batch, int64_t k_count, const double* d_ops, const double* d_state_init,
+                       double* d_states, double* d_spin, void* d_workspace, size_t workspace_bytes, void* stream);
 
 /* Time-partition pieces (multi-GPU, one long simulation).  Aggregate of a partition:
  * d_aggregate[b] = U[b][k_count−1] ⋯ U[b][0]  ([batch][dim][dim] complex128).

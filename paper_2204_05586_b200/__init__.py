@@ -24,6 +24,7 @@ from . import _lib
 from ._lib import EXPONENTIATION, FIELD, INTEGRATION, PRECISION, SPIN, SpinsimError, check
 
 __all__ = ["Simulator", "Results", "SpinsimError", "plan", "num_sweep_params", "scan_states", "scan_states_spin",
+           "scan_states_su2",
            "chain_aggregate",
            "compose_carry", "spin_projection", "kernel_launches", "load"]
 
@@ -145,6 +146,15 @@ class Simulator:
 
     def set_validation(self, enabled: bool) -> None:
         check(self._lib.ss_set_validation(self._h, int(bool(enabled))), "ss_set_validation")
+
+    def set_split_event(self, event) -> None:
+        """Profiling hook: record `event` (a torch.cuda.Event, or None to clear) inside every later evaluate() between
+        the interval kernel and the state scan (ss_set_split_event)."""
+        if event is not None and not event.cuda_event:
+            event.record()                             # torch creates its CUDA events lazily, at the first record
+        self._split_event = event                      # keep the torch event alive while the library holds it
+        check(self._lib.ss_set_split_event(self._h, ctypes.c_void_p(event.cuda_event) if event is not None else None),
+              "ss_set_split_event")
 
     def workspace_bytes(self, batch: int, K: int, unitaries_in_workspace: bool) -> int:
         return int(self._lib.ss_workspace_bytes(self._h, batch, K, int(unitaries_in_workspace)))
@@ -297,6 +307,30 @@ def scan_states_spin(unitaries: torch.Tensor, state_init: torch.Tensor, want_sta
                                   _dev_ptr(states, "states") if states is not None else None, _dev_ptr(spin, "spin"),
                                   _dev_ptr(workspace, "workspace"), workspace.numel(), _stream_ptr(stream)),
           "ss_scan_states_spin")
+    return states, spin
+
+
+def scan_states_su2(ops: torch.Tensor, state_init: torch.Tensor, dim: int, want_states: bool = True,
+                    want_spin: bool = False, workspace=None, stream=None):
+    """Row a9 over compact SU(2) operators ops [B][K][2] complex128 = (a, b) of U = [[a, b], [−b*, a*]], applied
+    directly (dim 2) or through D¹ (dim 3).  Returns (states [B][K+1][dim] or None, spin [B][K+1][3] or None)."""
+    if not isinstance(ops, torch.Tensor) or ops.dim() != 3 or ops.shape[2] != 2 or dim not in (2, 3):
+        raise ValueError("ops must be [batch][K][2] complex128 and dim 2 or 3")
+    if not (want_states or want_spin):
+        raise ValueError("want_states or want_spin must be set")
+    B, K, _ = ops.shape
+    lib = _lib.load()
+    need = int(lib.ss_scan_workspace_bytes(dim, B, K))
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(need, dtype=torch.uint8, device=ops.device)
+    states = torch.empty((B, K + 1, dim), dtype=torch.complex128, device=ops.device) if want_states else None
+    spin = torch.empty((B, K + 1, 3), dtype=torch.float64, device=ops.device) if want_spin else None
+    check(lib.ss_scan_states_su2(dim, B, K, _dev_ptr(ops, "ops", torch.complex128, (B, K, 2)),
+                                 _dev_ptr(state_init, "state_init", torch.complex128, (B, dim)),
+                                 _dev_ptr(states, "states") if states is not None else None,
+                                 _dev_ptr(spin, "spin") if spin is not None else None,
+                                 _dev_ptr(workspace, "workspace", torch.uint8), workspace.numel(), _stream_ptr(stream)),
+          "ss_scan_states_su2")
     return states, spin
 
 

@@ -30,7 +30,8 @@ EXPORTS = [
     "ss_set_validation", "ss_compute_unitaries", "ss_scan_workspace_bytes", "ss_scan_states", "ss_scan_states_spin",
     "ss_aggregate_workspace_bytes", "ss_chain_aggregate", "ss_compose_carry", "ss_exponentiate",
     "ss_spin_projection", "ss_evaluate_host", "ss_kernel_launches", "ss_last_error", "ss_version",
-    "ss_num_coefficients", "ss_magnus_bound", "ss_host_chunk_plan",
+    "ss_num_coefficients", "ss_magnus_bound", "ss_host_chunk_plan", "ss_set_split_event",
+    "ss_scan_states_su2",
 ]
 
 
@@ -70,10 +71,12 @@ def load() -> ctypes.CDLL:
         "ss_workspace_bytes": (sz, [P, i64, i64, i32]),
         "ss_evaluate": (ctypes.c_int, [P, d, d, d, d, i64, P, P, P, P, P, sz, P]),
         "ss_set_validation": (ctypes.c_int, [P, i32]),
+        "ss_set_split_event": (ctypes.c_int, [P, P]),
         "ss_compute_unitaries": (ctypes.c_int, [P, d, d, d, d, i64, i64, i64, P, P, P]),
         "ss_scan_workspace_bytes": (sz, [i32, i64, i64]),
         "ss_scan_states": (ctypes.c_int, [i32, i64, i64, P, P, P, P, sz, P]),
         "ss_scan_states_spin": (ctypes.c_int, [i32, i64, i64, P, P, P, P, P, sz, P]),
+        "ss_scan_states_su2": (ctypes.c_int, [i32, i64, i64, P, P, P, P, P, sz, P]),
         "ss_aggregate_workspace_bytes": (sz, [i32, i64, i64]),
         "ss_chain_aggregate": (ctypes.c_int, [i32, i64, i64, P, P, P, sz, P]),
         "ss_compose_carry": (ctypes.c_int, [i32, i64, i32, i32, P, P, P, P]),

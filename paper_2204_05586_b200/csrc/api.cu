@@ -74,6 +74,7 @@ struct ss_sim {
   // ss_evaluate_host pipeline: streams[0] computes, streams[1] copies, streams[2] scans the time chunks (so chunk c's
   // scan overlaps chunk c+1's interval kernel); three staging slots; events order them
   cudaStream_t streams[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t split_event = nullptr;  // ss_set_split_event: recorded by ss_evaluate between interval kernel and scan
   static constexpr int kSlots = 3;
   cudaEvent_t computed[kSlots] = {};   // slot's kernels done → its D2H may start
   cudaEvent_t drained[kSlots] = {};    // slot's D2H done → its buffers may be reused
@@ -194,10 +195,15 @@ ssb::IntervalParams make_params(const ss_sim* s, double t0, double dt_out, doubl
   p.tau = s->d.trotter_cutoff;
   p.frame = s->d.use_rotating_frame;
   p.split = choose_split(s, n_total, L);
+  p.op_format = ssb::OP_DENSE;
   p.sweep = sweep;
   p.unitaries = U;
   return p;
 }
+
+// The SU(2)-form paths (spin-half; analytic spin-one accumulated in SU(2), DESIGN.md §5 items 10-11) can hand their
+// operators to the scan as SU(2) elements (32 B per interval instead of 64 / 144 B) when U_k is not an output.
+bool su2_form(const ss_sim* s) { return s->dim == 2 || s->d.exponentiation == SS_EXP_ANALYTIC; }
 
 int check_device_ptr(const void* p, const char* name) {
   if (!p) return fail(SS_ERR_INVALID, "%s is NULL", name);
@@ -223,7 +229,7 @@ int launch_interval_checked(ss_sim* s, const ssb::IntervalParams& p, cudaStream_
 
 extern "C" {
 
-int ss_version(void) { return 101; }
+int ss_version(void) { return 102; }
 
 int ss_num_coefficients(const ss_sim* s) {
   if (!s) return fail(SS_ERR_INVALID, "sim is NULL");
@@ -329,6 +335,12 @@ void ss_destroy(ss_sim* s) {
 
 int ss_dim(const ss_sim* s) { return s ? s->dim : fail(SS_ERR_INVALID, "sim is NULL"); }
 
+int ss_set_split_event(ss_sim* s, void* event) {
+  if (!s) return fail(SS_ERR_INVALID, "sim is NULL");
+  s->split_event = static_cast<cudaEvent_t>(event);
+  return SS_OK;
+}
+
 int ss_set_validation(ss_sim* s, int32_t enabled) {
   if (!s) return fail(SS_ERR_INVALID, "sim is NULL");
   s->validate = enabled ? 1 : 0;
@@ -431,6 +443,27 @@ int ss_scan_states_spin(int32_t dim, int64_t batch, int64_t k_count, const doubl
   return e == cudaSuccess ? SS_OK : cuda_fail(e, "scan launch");
 }
 
+int ss_scan_states_su2(int32_t dim, int64_t batch, int64_t k_count, const double* d_ops, const double* d_psi0,
+                       double* d_states, double* d_spin, void* d_ws, size_t ws_bytes, void* stream) {
+  if (dim != 2 && dim != 3) return fail(SS_ERR_INVALID, "dim must be 2 or 3");
+  if (batch < 1 || k_count < 1) return fail(SS_ERR_INVALID, "batch and k_count must be >= 1");
+  int rc;
+  if ((rc = check_device_ptr(d_ops, "d_ops")) || (rc = check_device_ptr(d_psi0, "d_state_init")) ||
+      (rc = check_device_ptr(d_ws, "d_workspace")))
+    return rc;
+  if (!d_states && !d_spin) return fail(SS_ERR_INVALID, "at least one of d_states, d_spin must be non-NULL");
+  if (d_states && (rc = check_device_ptr(d_states, "d_states"))) return rc;
+  if (d_spin && (reinterpret_cast<uintptr_t>(d_spin) & 7) != 0) return fail(SS_ERR_INVALID, "d_spin must be 8-byte aligned");
+  const size_t need = ssb::scan_workspace_bytes(dim, batch, k_count);
+  if (ws_bytes < need) return fail(SS_ERR_INVALID, "workspace_bytes %zu < required %zu", ws_bytes, need);
+  if ((rc = ensure_device())) return rc;
+  int n = 0;
+  const cudaError_t e = ssb::launch_scan(dim, batch, k_count, d_ops, d_psi0, d_states, d_ws,
+                                         static_cast<cudaStream_t>(stream), &n, d_spin, ssb::OP_SU2);
+  g_launches.fetch_add(n);
+  return e == cudaSuccess ? SS_OK : cuda_fail(e, "scan launch");
+}
+
 int ss_chain_aggregate(int32_t dim, int64_t batch, int64_t k_count, const double* d_U, double* d_agg, void* d_ws,
                        size_t ws_bytes, void* stream) {
   if (dim != 2 && dim != 3) return fail(SS_ERR_INVALID, "dim must be 2 or 3");
@@ -484,9 +517,18 @@ int ss_evaluate(ss_sim* s, double t0, double t1, double dt_int, double dt_out, i
   void* scan_ws = w + 256;
   double* U = d_U ? d_U : reinterpret_cast<double*>(w + 256 + align256(ssb::scan_workspace_bytes(s->dim, batch, K)));
   if (s->validate && (rc = validate_inputs(s, batch, d_sweep, d_psi0, reinterpret_cast<int*>(w), st))) return rc;
-  const auto p = make_params(s, t0, dt_out, dt, L, 0, K, batch, d_sweep, U, batch * K);
+  auto p = make_params(s, t0, dt_out, dt, L, 0, K, batch, d_sweep, U, batch * K);
+  // U_k only feeds the scan: SU(2)-form paths pass it compact (the workspace is sized for the dense layout)
+  if (!d_U && su2_form(s)) p.op_format = ssb::OP_SU2;
   if ((rc = launch_interval_checked(s, p, st))) return rc;
-  return ss_scan_states(s->dim, batch, K, U, d_psi0, d_states, scan_ws, need - 256, stream);
+  if (s->split_event) {
+    const cudaError_t e = cudaEventRecord(s->split_event, st);
+    if (e != cudaSuccess) return cuda_fail(e, "split event record");
+  }
+  int n = 0;
+  const cudaError_t e = ssb::launch_scan(s->dim, batch, K, U, d_psi0, d_states, scan_ws, st, &n, nullptr, p.op_format);
+  g_launches.fetch_add(n);
+  return e == cudaSuccess ? SS_OK : cuda_fail(e, "scan launch");
 }
 
 int ss_exponentiate(const ss_sim* s, int64_t n, const double* d_args, double* d_out, void* stream) {
@@ -700,12 +742,14 @@ int ss_evaluate_host(ss_sim* s, double t0, double t1, double dt_int, double dt_o
       // order on ss, so the carry chain is sequential; chunk c+1's interval kernel runs beside chunk c's scan).
       if (c >= (size_t)ss_sim::kSlots && (e = cudaStreamWaitEvent(cs, s->drained[k], 0)) != cudaSuccess)
         return cuda_fail(e, "event wait");
-      const auto p = make_params(s, t0, dt_out, dt, L, (int64_t)k0, kc, batch, d_sweep, d_U, batch * K);
+      auto p = make_params(s, t0, dt_out, dt, L, (int64_t)k0, kc, batch, d_sweep, d_U, batch * K);
+      if (!h_U && su2_form(s)) p.op_format = ssb::OP_SU2;
       if ((rc = launch_interval_checked(s, p, cs))) return rc;
       if (ss != cs && ((e = cudaEventRecord(s->stepped[k], cs)) || (e = cudaStreamWaitEvent(ss, s->stepped[k], 0))))
         return cuda_fail(e, "event record/wait");
       int n = 0;
-      if ((e = ssb::launch_scan(D, batch, kc, d_U, d_carry, d_states, d_scan, ss, &n)) != cudaSuccess)
+      if ((e = ssb::launch_scan(D, batch, kc, d_U, d_carry, d_states, d_scan, ss, &n, nullptr, p.op_format)) !=
+          cudaSuccess)
         return cuda_fail(e, "scan launch");
       g_launches.fetch_add(n);
       // carry ← states[:, kc]
@@ -757,10 +801,11 @@ int ss_evaluate_host(ss_sim* s, double t0, double t1, double dt_int, double dt_o
     if ((e = cudaMemcpyAsync(d_sweep, h_sweep + b0 * s->P, sizeof(double) * s->P * cb, cudaMemcpyHostToDevice, cs)) ||
         (e = cudaMemcpyAsync(d_psi0, h_psi0 + b0 * 2 * D, sizeof(double) * 2 * D * cb, cudaMemcpyHostToDevice, cs)))
       return cuda_fail(e, "H2D copy");
-    const auto p = make_params(s, t0, dt_out, dt, L, 0, K, cb, d_sweep, d_U, batch * K);   // S of the whole batch
+    auto p = make_params(s, t0, dt_out, dt, L, 0, K, cb, d_sweep, d_U, batch * K);   // S of the whole batch
+    if (!h_U && su2_form(s)) p.op_format = ssb::OP_SU2;
     if ((rc = launch_interval_checked(s, p, cs))) return rc;
     int n = 0;
-    if ((e = ssb::launch_scan(D, cb, K, d_U, d_psi0, d_states, d_scan, cs, &n)) != cudaSuccess)
+    if ((e = ssb::launch_scan(D, cb, K, d_U, d_psi0, d_states, d_scan, cs, &n, nullptr, p.op_format)) != cudaSuccess)
       return cuda_fail(e, "scan launch");
     g_launches.fetch_add(n);
     if ((e = cudaEventRecord(s->computed[k], cs)) || (e = cudaStreamWaitEvent(xs, s->computed[k], 0)))

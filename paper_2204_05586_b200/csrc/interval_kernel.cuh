@@ -29,8 +29,9 @@ struct IntervalParams {
   int32_t tau;
   int32_t frame;
   int32_t split;        // S: lanes per interval (power of two ≤ 32); lane p runs fine steps [p·L/S, (p+1)·L/S)
+  int32_t op_format;    // OP_DENSE, or OP_SU2 (SU(2)-form accumulators only): the layout of `unitaries`
   const double* sweep;  // [batch][P]
-  double* unitaries;    // [batch][k_count][D][D] complex128
+  double* unitaries;    // [batch][k_count][D][D] complex128 (OP_DENSE) or [batch][k_count][2] complex128 (OP_SU2)
 };
 
 #ifndef SS_INTERVAL_THREADS
@@ -252,6 +253,19 @@ __device__ __forceinline__ void interval_body(const IntervalParams& prm) {
   }
 
   // a8: U_k = R_{ω_r}(−Δt)(I + A) = diag(e^{−iω_r m Δt})(I + A); written as complex128.
+  if constexpr (DA == 2) {
+    if (prm.op_format == OP_SU2) {
+      // compact: the SU(2) element (a, b) = e^{−iω_rΔt/2}·(1 + δa, b) — R(−Δt) is diag(p, p*) with p = e^{−iω_rΔt/2}
+      // in SU(2), and D¹ of it for the analytic spin-one path (diag(p², 1, p*²), the phases below)
+      double s, c;
+      sincos(0.5 * omega_r * prm.dt_out, &s, &c);
+      const double ar = 1.0 + (double)A.ar, ai = (double)A.ai, br = (double)A.br, bi = (double)A.bi;
+      double2* o2 = reinterpret_cast<double2*>(prm.unitaries) + i * 2;
+      o2[0] = make_double2(c * ar + s * ai, c * ai - s * ar);     // (c − is)(ar + i ai)
+      o2[1] = make_double2(c * br + s * bi, c * bi - s * br);
+      return;
+    }
+  }
   double ph_re[D], ph_im[D];
   {
     double s, c;

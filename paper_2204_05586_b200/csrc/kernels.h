@@ -10,8 +10,10 @@ namespace ssb {
 size_t scan_workspace_bytes(int dim, int64_t batch, int64_t k_count);
 int64_t chain_min_batch();   // batches from this size take the per-sweep chain kernel (sequential, chunk-invariant)
 size_t aggregate_workspace_bytes(int dim, int64_t batch, int64_t k_count);
+// op_format: OP_DENSE (U as [batch][k_count][dim][dim] complex128) or OP_SU2 ([batch][k_count][2] complex128, the
+// SU(2) element (a, b) of U = [[a, b], [−b*, a*]], acting through D¹ when dim = 3).
 cudaError_t launch_scan(int dim, int64_t batch, int64_t k_count, const double* U, const double* psi0, double* states,
-                        void* ws, cudaStream_t s, int* launches, double* spin = nullptr);
+                        void* ws, cudaStream_t s, int* launches, double* spin = nullptr, int op_format = OP_DENSE);
 cudaError_t launch_aggregate(int dim, int64_t batch, int64_t k_count, const double* U, double* aggregate, void* ws,
                              cudaStream_t s, int* launches);
 cudaError_t launch_compose_carry(int dim, int64_t batch, int part, const double* aggs, const double* psi0,

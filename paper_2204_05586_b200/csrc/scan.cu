@@ -12,12 +12,17 @@
 //      PREFIX tile gives ψ_end(j′)), publishes its inclusive end state ψ_end = A·ψ_in (flag PREFIX),
 //   4. each thread applies its exclusive prefix to ψ_in and then its own operators in order, writing states through
 //      shared memory (coalesced).
-// HBM traffic per interval: read U_k (2·dim² doubles) + write ψ_{k+1} (2·dim doubles) — 192 B (spin-one) /
-// 96 B (spin-half): the kernel is HBM bound.
+// HBM traffic per interval: read U_k + write ψ_{k+1} (2·dim doubles).  U_k travels either as the dense dim×dim complex
+// matrix (the public layout: 144 / 64 B) or, for the SU(2)-form interval kernels (spin-half, analytic spin-one) when
+// U_k is not an output, as the SU(2) element (a, b) (32 B) the kernel accumulates: 192 / 96 B per interval dense,
+// 80 / 64 B compact.  Every scan is HBM bound.  The kernels are templated on the operator type M
+// (CM<D> dense, SU<D> compact acting on dim-D states), so each path exists for both formats.
 #include <cooperative_groups.h>
 #include <cuda/atomic>
 
 #include <algorithm>
+#include <atomic>
+#include <cstdlib>
 #include <cstring>
 
 #include <cuda.h>
@@ -25,6 +30,29 @@
 #include "kernels.h"
 
 namespace ssb {
+
+// Per-device host caches (function attributes, occupancy-derived grids, SM counts): cudaFuncSetAttribute applies to
+// the current device's context, so every value is keyed by the device ordinal; atomics make concurrent first calls
+// benign (both compute the same value).
+constexpr int kMaxDevices = 64;
+struct DeviceCache {
+  std::atomic<int> v[kMaxDevices] = {};
+  int get(int dev) const { return (dev >= 0 && dev < kMaxDevices) ? v[dev].load(std::memory_order_acquire) : 0; }
+  void set(int dev, int x) { if (dev >= 0 && dev < kMaxDevices) v[dev].store(x, std::memory_order_release); }
+};
+static int device_sms(int dev) {
+  static DeviceCache c;
+  int n = c.get(dev);
+  if (n == 0) {
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    c.set(dev, n);
+  }
+  return n;
+}
+static int current_device() {
+  int dev = 0;
+  return cudaGetDevice(&dev) == cudaSuccess ? dev : 0;
+}
 
 template <int D> struct ScanCfg;
 template <> struct ScanCfg<2> { static constexpr int kItems = 4; };
@@ -36,6 +64,7 @@ enum { FLAG_EMPTY = 0, FLAG_AGG = 1, FLAG_PREFIX = 2 };
 
 template <int D> struct CM {  // dense complex matrix in registers
   double re[D * D], im[D * D];
+  static constexpr int SD = D, W = D * D;   // state dimension, double2 per operator in memory
 };
 
 template <int D> __device__ __forceinline__ void cm_eye(CM<D>& m) {
@@ -104,6 +133,101 @@ template <int D> __device__ __forceinline__ CM<D> cm_shfl_up(const CM<D>& m, int
   return r;
 }
 
+template <int D> __device__ __forceinline__ CM<D> cm_shfl_down(const CM<D>& m, int delta) {
+  CM<D> r;
+#pragma unroll
+  for (int e = 0; e < D * D; ++e) {
+    r.re[e] = __shfl_down_sync(0xffffffffu, m.re[e], delta);
+    r.im[e] = __shfl_down_sync(0xffffffffu, m.im[e], delta);
+  }
+  return r;
+}
+template <int D> __device__ __forceinline__ CM<D> cm_shfl_idx(const CM<D>& m, int src) {
+  CM<D> r;
+#pragma unroll
+  for (int e = 0; e < D * D; ++e) {
+    r.re[e] = __shfl_sync(0xffffffffu, m.re[e], src);
+    r.im[e] = __shfl_sync(0xffffffffu, m.im[e], src);
+  }
+  return r;
+}
+
+// ---- compact SU(2) operators -------------------------------------------------------------------------------------
+// U = [[a, b], [−b*, a*]] held as (a, b): every operator of the spin-half path is in SU(2) (DESIGN.md §5 item 10),
+// and the analytic spin-one operator is D¹ of one (reading R14, §5 item 11), so the products of the scan stay in
+// SU(2) exactly (group law) and only the action on a state depends on D: directly for D = 2, through
+// D¹(U) = [[a², √2ab, b²], [−√2ab*, |a|²−|b|², √2a*b], [b*², −√2a*b*, a*²]] for D = 3.
+template <int D> struct SU {
+  double ar, ai, br, bi;
+  static constexpr int SD = D, W = 2;
+};
+template <int D> __device__ __forceinline__ void cm_eye(SU<D>& m) { m.ar = 1.0; m.ai = m.br = m.bi = 0.0; }
+// x·y = (x_a y_a − x_b y_b*, x_a y_b + x_b y_a*)
+template <int D> __device__ __forceinline__ SU<D> cm_mul(const SU<D>& x, const SU<D>& y) {
+  SU<D> c;
+  c.ar = fma(x.ar, y.ar, fma(-x.ai, y.ai, fma(-x.br, y.br, -(x.bi * y.bi))));
+  c.ai = fma(x.ar, y.ai, fma(x.ai, y.ar, fma(-x.bi, y.br, x.br * y.bi)));
+  c.br = fma(x.ar, y.br, fma(-x.ai, y.bi, fma(x.br, y.ar, x.bi * y.ai)));
+  c.bi = fma(x.ar, y.bi, fma(x.ai, y.br, fma(x.bi, y.ar, -(x.br * y.ai))));
+  return c;
+}
+template <int D> __device__ __forceinline__ void cm_apply(const SU<D>& u, const double xr[D], const double xi[D],
+                                                          double yr[D], double yi[D]) {
+  if constexpr (D == 2) {
+    // y0 = a x0 + b x1,  y1 = −b* x0 + a* x1
+    yr[0] = fma(u.ar, xr[0], fma(-u.ai, xi[0], fma(u.br, xr[1], -(u.bi * xi[1]))));
+    yi[0] = fma(u.ar, xi[0], fma(u.ai, xr[0], fma(u.br, xi[1], u.bi * xr[1])));
+    yr[1] = fma(-u.br, xr[0], fma(-u.bi, xi[0], fma(u.ar, xr[1], u.ai * xi[1])));
+    yi[1] = fma(-u.br, xi[0], fma(u.bi, xr[0], fma(u.ar, xi[1], -(u.ai * xr[1]))));
+  } else {
+    // D¹ entries from a, b (the map of the interval kernel's su2_to_spin1, full rather than residual form)
+    const double a2r = u.ar * u.ar - u.ai * u.ai, a2i = 2.0 * u.ar * u.ai;             // a²
+    const double b2r = u.br * u.br - u.bi * u.bi, b2i = 2.0 * u.br * u.bi;             // b²
+    const double abr = kSqrt2 * (u.ar * u.br - u.ai * u.bi), abi = kSqrt2 * (u.ar * u.bi + u.ai * u.br);   // √2ab
+    const double acr = kSqrt2 * (u.ar * u.br + u.ai * u.bi), aci = kSqrt2 * (u.ar * u.bi - u.ai * u.br);   // √2a*b
+    const double dd = (u.ar * u.ar + u.ai * u.ai) - (u.br * u.br + u.bi * u.bi);      // |a|² − |b|²
+    // row 0: a² x0 + √2ab x1 + b² x2
+    yr[0] = fma(a2r, xr[0], fma(-a2i, xi[0], fma(abr, xr[1], fma(-abi, xi[1], fma(b2r, xr[2], -(b2i * xi[2]))))));
+    yi[0] = fma(a2r, xi[0], fma(a2i, xr[0], fma(abr, xi[1], fma(abi, xr[1], fma(b2r, xi[2], b2i * xr[2])))));
+    // row 1: −√2ab* x0 + (|a|²−|b|²) x1 + √2a*b x2, with −√2ab* = −conj(√2a*b)
+    yr[1] = fma(-acr, xr[0], fma(-aci, xi[0], fma(dd, xr[1], fma(acr, xr[2], -(aci * xi[2])))));
+    yi[1] = fma(-acr, xi[0], fma(aci, xr[0], fma(dd, xi[1], fma(acr, xi[2], aci * xr[2]))));
+    // row 2: b*² x0 − √2a*b* x1 + a*² x2, with √2a*b* = conj(√2ab)
+    yr[2] = fma(b2r, xr[0], fma(b2i, xi[0], fma(-abr, xr[1], fma(-abi, xi[1], fma(a2r, xr[2], a2i * xi[2])))));
+    yi[2] = fma(b2r, xi[0], fma(-b2i, xr[0], fma(-abr, xi[1], fma(abi, xr[1], fma(a2r, xi[2], -(a2i * xr[2]))))));
+  }
+}
+template <int D> __device__ __forceinline__ void cm_load(const double2* src, SU<D>& m) {
+  const double2 a = src[0], b = src[1];
+  m.ar = a.x; m.ai = a.y; m.br = b.x; m.bi = b.y;
+}
+template <int D> __device__ __forceinline__ void cm_load_cg(const double2* src, SU<D>& m) {
+  const double2 a = __ldcg(src), b = __ldcg(src + 1);
+  m.ar = a.x; m.ai = a.y; m.br = b.x; m.bi = b.y;
+}
+template <int D> __device__ __forceinline__ void cm_store(double2* dst, const SU<D>& m) {
+  dst[0] = make_double2(m.ar, m.ai);
+  dst[1] = make_double2(m.br, m.bi);
+}
+template <int D> __device__ __forceinline__ SU<D> cm_shfl_up(const SU<D>& m, int delta) {
+  SU<D> r;
+  r.ar = __shfl_up_sync(0xffffffffu, m.ar, delta); r.ai = __shfl_up_sync(0xffffffffu, m.ai, delta);
+  r.br = __shfl_up_sync(0xffffffffu, m.br, delta); r.bi = __shfl_up_sync(0xffffffffu, m.bi, delta);
+  return r;
+}
+template <int D> __device__ __forceinline__ SU<D> cm_shfl_down(const SU<D>& m, int delta) {
+  SU<D> r;
+  r.ar = __shfl_down_sync(0xffffffffu, m.ar, delta); r.ai = __shfl_down_sync(0xffffffffu, m.ai, delta);
+  r.br = __shfl_down_sync(0xffffffffu, m.br, delta); r.bi = __shfl_down_sync(0xffffffffu, m.bi, delta);
+  return r;
+}
+template <int D> __device__ __forceinline__ SU<D> cm_shfl_idx(const SU<D>& m, int src) {
+  SU<D> r;
+  r.ar = __shfl_sync(0xffffffffu, m.ar, src); r.ai = __shfl_sync(0xffffffffu, m.ai, src);
+  r.br = __shfl_sync(0xffffffffu, m.br, src); r.bi = __shfl_sync(0xffffffffu, m.bi, src);
+  return r;
+}
+
 // ⟨J⟩ = (Re ψ†Jxψ, Re ψ†Jyψ, ψ†Jzψ), closed forms of the textbook matrices (reading R5).
 template <int D> __device__ __forceinline__ void spin_of(const double pr[D], const double pi[D], double j[3]) {
   if (D == 2) {
@@ -119,8 +243,8 @@ template <int D> __device__ __forceinline__ void spin_of(const double pr[D], con
   }
 }
 
-// Workspace layout (all offsets 256-byte aligned): [ticket u64][flags int32 × ntiles][agg dim² c128 × ntiles]
-// [psi_end dim c128 × ntiles].
+// Workspace layouts (all offsets 256-byte aligned): [ticket u64][flags int32 × ntiles][agg op × ntiles]
+// [psi_end dim c128 × ntiles]; the v1 layout below also sizes the per-tile totals of ss_chain_aggregate.
 static inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 template <int D> struct ScanLayout {
@@ -136,48 +260,35 @@ template <int D> struct ScanLayout {
   }
 };
 
-template <int D> struct Scan2Layout;   // defined after the v2 kernel configuration
 
 struct ScanArgs {
   int64_t batch, k_count, tiles_per_sweep;
   const double2* U;          // [batch][k_count][D][D]
-  const double2* psi0;       // [batch][D]
-  double2* states;           // [batch][k_count+1][D]  (SCAN mode)
-  double2* aggregate_out;    // [ntiles][D][D]          (AGGREGATE mode: per-tile totals)
-  unsigned long long* ticket;
-  int* flags;
-  double2* agg;
-  double2* psi_end;
+  double2* aggregate_out;    // [ntiles][D][D] per-tile totals
 };
 
-template <int D, bool SCAN>
-__global__ void __launch_bounds__(kScanThreads) scan_kernel(const ScanArgs a) {
+// Per-tile aggregates for the time partition (ss_chain_aggregate): a block stages one tile of kTile consecutive
+// operators of one sweep in shared memory, each thread multiplies its kItems consecutive operators, a warp shuffle
+// tree and one pass over the warp totals give the tile total T = U_{last} ⋯ U_{first}; combine_tiles_kernel then
+// multiplies the tiles of each sweep in order.  No look-back: the result is the same fixed association on every rank.
+template <int D>
+__global__ void __launch_bounds__(kScanThreads) aggregate_kernel(const ScanArgs a) {
   constexpr int C = ScanCfg<D>::kItems;
   constexpr int TILE = kScanThreads * C;
   constexpr int NW = kScanThreads / 32;
-  extern __shared__ double2 smem[];          // [TILE·D·D] operators, then [TILE·D] states (SCAN)
+  extern __shared__ double2 smem[];          // [TILE·D·D] operators
   double2* sU = smem;
-  double2* sPsi = smem + TILE * D * D;
   __shared__ double2 sWarpTot[NW][D * D];
-  __shared__ double2 sPsiIn[D];
-  __shared__ long long sTicket;
-
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) sTicket = (long long)atomicAdd(a.ticket, 1ull);
-  __syncthreads();
-  const long long ticket = sTicket;
+  const long long ticket = blockIdx.x;
   const long long b = ticket / a.tiles_per_sweep;
   const long long j = ticket - b * a.tiles_per_sweep;
   const long long k0 = j * TILE;
   const int n_items = (int)min((long long)TILE, a.k_count - k0);
-
-  // 1. stage U (coalesced 16-byte loads, streaming)
   const double2* gU = a.U + ((size_t)b * a.k_count + k0) * D * D;
   for (int e = tid; e < n_items * D * D; e += kScanThreads) sU[e] = __ldcs(gU + e);
   __syncthreads();
-
-  // 2. thread aggregate over its C consecutive items: P = U_{c+C−1} ⋯ U_c
-  CM<D> P;
+  CM<D> P;                                   // thread product U_{c+C−1} ⋯ U_c
   cm_eye(P);
 #pragma unroll
   for (int c = 0; c < C; ++c) {
@@ -188,97 +299,19 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(const ScanArgs a) {
       P = cm_mul(u, P);
     }
   }
-  // warp inclusive scan (later·earlier)
 #pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const CM<D> q = cm_shfl_up(P, off);
-    if (lane >= off) P = cm_mul(P, q);
+  for (int off = 1; off < 32; off <<= 1) {   // warp total, later·earlier
+    const CM<D> q = cm_shfl_down(P, off);
+    if ((lane & (2 * off - 1)) == 0) P = cm_mul(q, P);
   }
-  CM<D> E = cm_shfl_up(P, 1);  // exclusive within the warp
-  if (lane == 0) cm_eye(E);
-  if (lane == 31) cm_store(sWarpTot[warp], P);
+  if (lane == 0) cm_store(sWarpTot[warp], P);
   __syncthreads();
-  // prefix of earlier warps W = T_{w−1} ⋯ T_0 ; thread exclusive X = E · W
-  CM<D> W;
-  cm_eye(W);
-  for (int w = 0; w < warp; ++w) {
-    CM<D> t;
-    cm_load(sWarpTot[w], t);
-    W = cm_mul(t, W);
-  }
-  const CM<D> X = cm_mul(E, W);
-
   if (tid == 0) {
-    CM<D> tot;  // block aggregate T_{NW−1} ⋯ T_0
+    CM<D> tot, t;
     cm_eye(tot);
-    for (int w = 0; w < NW; ++w) {
-      CM<D> t;
-      cm_load(sWarpTot[w], t);
-      tot = cm_mul(t, tot);
-    }
-    if (!SCAN) {
-      cm_store(a.aggregate_out + (size_t)ticket * D * D, tot);
-    } else {
-      cuda::atomic_ref<int, cuda::thread_scope_device> my_flag(a.flags[ticket]);
-      double pr[D], pi[D];
-      if (j == 0) {
-        for (int d = 0; d < D; ++d) { const double2 v = a.psi0[b * D + d]; pr[d] = v.x; pi[d] = v.y; }
-      } else {
-        // 3a. publish the aggregate
-        cm_store(a.agg + (size_t)ticket * D * D, tot);
-        my_flag.store(FLAG_AGG, cuda::memory_order_release);
-        // 3b. look back
-        CM<D> M;
-        cm_eye(M);
-        long long jj = ticket - 1;
-        for (;;) {
-          cuda::atomic_ref<int, cuda::thread_scope_device> f(a.flags[jj]);
-          int fv;
-          while ((fv = f.load(cuda::memory_order_acquire)) == FLAG_EMPTY) __nanosleep(20);
-          if (fv == FLAG_PREFIX) {
-            double er[D], ei[D];
-            for (int d = 0; d < D; ++d) { const double2 v = __ldcg(a.psi_end + jj * D + d); er[d] = v.x; ei[d] = v.y; }
-            cm_apply(M, er, ei, pr, pi);
-            break;
-          }
-          CM<D> A;
-          cm_load_cg(a.agg + (size_t)jj * D * D, A);
-          M = cm_mul(M, A);
-          --jj;
-        }
-      }
-      // 3c. publish the inclusive end state ψ_end = tot·ψ_in
-      double er[D], ei[D];
-      cm_apply(tot, pr, pi, er, ei);
-      for (int d = 0; d < D; ++d) a.psi_end[ticket * D + d] = make_double2(er[d], ei[d]);
-      my_flag.store(FLAG_PREFIX, cuda::memory_order_release);
-      for (int d = 0; d < D; ++d) sPsiIn[d] = make_double2(pr[d], pi[d]);
-      if (j == 0)
-        for (int d = 0; d < D; ++d) a.states[(size_t)b * (a.k_count + 1) * D + d] = make_double2(pr[d], pi[d]);
-    }
+    for (int w = 0; w < NW; ++w) { cm_load(sWarpTot[w], t); tot = cm_mul(t, tot); }
+    cm_store(a.aggregate_out + (size_t)ticket * D * D, tot);
   }
-  if (!SCAN) return;
-  __syncthreads();
-
-  // 4. apply: ψ = X·ψ_in, then the thread's own operators in order
-  double xr[D], xi[D], yr[D], yi[D];
-#pragma unroll
-  for (int d = 0; d < D; ++d) { xr[d] = sPsiIn[d].x; xi[d] = sPsiIn[d].y; }
-  cm_apply(X, xr, xi, yr, yi);
-#pragma unroll
-  for (int c = 0; c < C; ++c) {
-    const int it = tid * C + c;
-    if (it < n_items) {
-      CM<D> u;
-      cm_load(sU + it * D * D, u);
-      cm_apply(u, yr, yi, xr, xi);
-#pragma unroll
-      for (int d = 0; d < D; ++d) { yr[d] = xr[d]; yi[d] = xi[d]; sPsi[it * D + d] = make_double2(xr[d], xi[d]); }
-    }
-  }
-  __syncthreads();
-  double2* gS = a.states + ((size_t)b * (a.k_count + 1) + k0 + 1) * D;
-  for (int e = tid; e < n_items * D; e += kScanThreads) __stcs(gS + e, sPsi[e]);
 }
 
 // ---- state scan v2: persistent CTAs, TMA bulk-copy double buffering, j-major tiles, warp-parallel look-back ----
@@ -292,36 +325,37 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(const ScanArgs a) {
 #ifndef SS_SCAN2_NT
 #define SS_SCAN2_NT 128
 #endif
-template <int D> struct Scan2Cfg;
 #ifndef SS_SCAN2_TILE3
 #define SS_SCAN2_TILE3 512
 #endif
 #ifndef SS_SCAN2_TILE2
 #define SS_SCAN2_TILE2 1024
 #endif
-template <> struct Scan2Cfg<2> { static constexpr int NT = SS_SCAN2_NT, C = SS_SCAN2_TILE2 / SS_SCAN2_NT; };
-template <> struct Scan2Cfg<3> { static constexpr int NT = SS_SCAN2_NT, C = SS_SCAN2_TILE3 / SS_SCAN2_NT; };
-template <int D> constexpr int scan2_tile() { return Scan2Cfg<D>::NT * Scan2Cfg<D>::C; }
+// tile: 1024 intervals of dim-2 states, 512 of dim-3 (either operator format)
+template <class M> struct Scan2Cfg {
+  static constexpr int NT = SS_SCAN2_NT, C = (M::SD == 2 ? SS_SCAN2_TILE2 : SS_SCAN2_TILE3) / SS_SCAN2_NT;
+};
+template <class M> constexpr int scan2_tile() { return Scan2Cfg<M>::NT * Scan2Cfg<M>::C; }
 // Per-thread shared-memory slots (a thread's C operators / C states), strides padded to an odd number of 16-byte
 // words so the warp's LDS.128/STS.128 at equal offsets of 32 slots are bank-conflict free.
-template <int D> __host__ __device__ constexpr int scan2_u_stride() { return (Scan2Cfg<D>::C * D * D) | 1; }
-template <int D> __host__ __device__ constexpr int scan2_s_stride() { return (Scan2Cfg<D>::C * D) | 1; }
-template <int D> __host__ __device__ constexpr int scan2_j_stride() { return (Scan2Cfg<D>::C * 3) | 1; }  // doubles
-template <int D> constexpr size_t scan2_smem() {
-  return sizeof(double2) * (size_t)Scan2Cfg<D>::NT * (2 * scan2_u_stride<D>() + scan2_s_stride<D>()) +
-         sizeof(double) * (size_t)Scan2Cfg<D>::NT * scan2_j_stride<D>() + 64;
+template <class M> __host__ __device__ constexpr int scan2_u_stride() { return (Scan2Cfg<M>::C * M::W) | 1; }
+template <class M> __host__ __device__ constexpr int scan2_s_stride() { return (Scan2Cfg<M>::C * M::SD) | 1; }
+template <class M> __host__ __device__ constexpr int scan2_j_stride() { return (Scan2Cfg<M>::C * 3) | 1; }  // doubles
+template <class M> constexpr size_t scan2_smem() {
+  return sizeof(double2) * (size_t)Scan2Cfg<M>::NT * (2 * scan2_u_stride<M>() + scan2_s_stride<M>()) +
+         sizeof(double) * (size_t)Scan2Cfg<M>::NT * scan2_j_stride<M>() + 64;
 }
 
-template <int D> struct Scan2Layout {
+template <class M> struct Scan2Layout {
   int64_t tiles_per_sweep, ntiles;
   size_t off_flags, off_agg, off_psi, total;
   Scan2Layout(int64_t batch, int64_t k_count) {
-    tiles_per_sweep = (k_count + scan2_tile<D>() - 1) / scan2_tile<D>();
+    tiles_per_sweep = (k_count + scan2_tile<M>() - 1) / scan2_tile<M>();
     ntiles = batch * tiles_per_sweep;
     off_flags = 256;
     off_agg = align256(off_flags + sizeof(int) * (size_t)ntiles);
-    off_psi = align256(off_agg + sizeof(double2) * D * D * (size_t)ntiles);
-    total = align256(off_psi + sizeof(double2) * D * (size_t)ntiles);
+    off_psi = align256(off_agg + sizeof(double2) * M::W * (size_t)ntiles);
+    total = align256(off_psi + sizeof(double2) * M::SD * (size_t)ntiles);
   }
 };
 
@@ -359,28 +393,19 @@ struct Scan2Args {
   double2* psi_end;
 };
 
-template <int D> __device__ __forceinline__ CM<D> cm_shfl_down(const CM<D>& m, int delta) {
-  CM<D> r;
-#pragma unroll
-  for (int e = 0; e < D * D; ++e) {
-    r.re[e] = __shfl_down_sync(0xffffffffu, m.re[e], delta);
-    r.im[e] = __shfl_down_sync(0xffffffffu, m.im[e], delta);
-  }
-  return r;
-}
-
-template <int D>
-__global__ void __launch_bounds__(Scan2Cfg<D>::NT) scan2_kernel(const Scan2Args a) {
-  constexpr int NT = Scan2Cfg<D>::NT, C = Scan2Cfg<D>::C, TILE = NT * C, NW = NT / 32;
-  constexpr int SU = scan2_u_stride<D>(), SS = scan2_s_stride<D>();
+template <class M>
+__global__ void __launch_bounds__(Scan2Cfg<M>::NT) scan2_kernel(const Scan2Args a) {
+  constexpr int D = M::SD, W = M::W;
+  constexpr int NT = Scan2Cfg<M>::NT, C = Scan2Cfg<M>::C, TILE = NT * C, NW = NT / 32;
+  constexpr int SU = scan2_u_stride<M>(), SS = scan2_s_stride<M>();
   extern __shared__ __align__(128) double2 smem2[];
   double2* sU[2] = {smem2, smem2 + NT * SU};                // [stage][thread][SU]
   double2* sPsi = smem2 + 2 * NT * SU;                      // [thread][SS]
-  constexpr int SJ = scan2_j_stride<D>();
+  constexpr int SJ = scan2_j_stride<M>();
   double* sJ = reinterpret_cast<double*>(sPsi + NT * SS);   // [thread][SJ]
   __shared__ __align__(8) uint64_t sBar[2];
-  __shared__ double2 sWarpTot[NW][D * D];
-  __shared__ double2 sWarpPre[NW][D * D];
+  __shared__ double2 sWarpTot[NW][W];
+  __shared__ double2 sWarpPre[NW][W];
   __shared__ double2 sPsiIn[D];
   __shared__ long long sNext;
 
@@ -393,9 +418,9 @@ __global__ void __launch_bounds__(Scan2Cfg<D>::NT) scan2_kernel(const Scan2Args 
     const long long k0 = j * TILE + (long long)tid * C;
     const int n = (int)max(0LL, min((long long)C, a.k_count - k0));
     if (n > 0) {
-      const unsigned bytes = (unsigned)(n * D * D * sizeof(double2));
+      const unsigned bytes = (unsigned)(n * W * sizeof(double2));
       mbar_expect_tx(&sBar[stage], bytes);
-      tma_load_1d(sU[stage] + tid * SU, a.U + ((size_t)b * a.k_count + k0) * D * D, bytes, &sBar[stage]);
+      tma_load_1d(sU[stage] + tid * SU, a.U + ((size_t)b * a.k_count + k0) * W, bytes, &sBar[stage]);
     } else {
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&sBar[stage])) : "memory");
     }
@@ -432,46 +457,41 @@ __global__ void __launch_bounds__(Scan2Cfg<D>::NT) scan2_kernel(const Scan2Args 
     const double2* U = sU[stage] + tid * SU;                // this thread's C operators
 
     // thread aggregate, warp inclusive scan, warp totals
-    CM<D> P;
+    M P;
     cm_eye(P);
 #pragma unroll
     for (int c = 0; c < C; ++c) {
       const int it = tid * C + c;
       if (it < n_items) {
-        CM<D> u;
-        cm_load(U + c * D * D, u);
+        M u;
+        cm_load(U + c * W, u);
         P = cm_mul(u, P);
       }
     }
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
-      const CM<D> q = cm_shfl_up(P, off);
+      const M q = cm_shfl_up(P, off);
       if (lane >= off) P = cm_mul(P, q);
     }
-    CM<D> E = cm_shfl_up(P, 1);
+    M E = cm_shfl_up(P, 1);
     if (lane == 0) cm_eye(E);
     if (lane == 31) cm_store(sWarpTot[warp], P);
     __syncthreads();
 
     if (warp == 0) {
       // scan of the warp totals (lanes < NW), exclusive prefixes to shared memory, block total in lane NW−1
-      CM<D> T;
+      M T;
       if (lane < NW) cm_load(sWarpTot[lane], T); else cm_eye(T);
 #pragma unroll
       for (int off = 1; off < NW; off <<= 1) {
-        const CM<D> q = cm_shfl_up(T, off);
+        const M q = cm_shfl_up(T, off);
         if (lane >= off) T = cm_mul(T, q);
       }
-      CM<D> Wx = cm_shfl_up(T, 1);
+      M Wx = cm_shfl_up(T, 1);
       if (lane == 0) cm_eye(Wx);
       if (lane < NW) cm_store(sWarpPre[lane], Wx);
       // block total to every lane
-      CM<D> tot;
-#pragma unroll
-      for (int e = 0; e < D * D; ++e) {
-        tot.re[e] = __shfl_sync(0xffffffffu, T.re[e], NW - 1);
-        tot.im[e] = __shfl_sync(0xffffffffu, T.im[e], NW - 1);
-      }
+      const M tot = cm_shfl_idx(T, NW - 1);
       cuda::atomic_ref<int, cuda::thread_scope_device> my_flag(a.flags[t]);
       double pr[D], pi[D];
       if (j == 0) {
@@ -479,12 +499,12 @@ __global__ void __launch_bounds__(Scan2Cfg<D>::NT) scan2_kernel(const Scan2Args 
         for (int d = 0; d < D; ++d) { const double2 v = a.psi0[b * D + d]; pr[d] = v.x; pi[d] = v.y; }
       } else {
         if (lane == 0) {
-          cm_store(a.agg + (size_t)t * D * D, tot);
+          cm_store(a.agg + (size_t)t * W, tot);
           my_flag.store(FLAG_AGG, cuda::memory_order_release);
         }
         // warp-parallel look-back: lane ℓ inspects predecessor j − 1 − ℓ − 32r
-        CM<D> M;
-        cm_eye(M);
+        M Mlb;
+        cm_eye(Mlb);
         long long jb = j - 1;
         for (;;) {
           const long long jq = jb - lane;
@@ -497,14 +517,14 @@ __global__ void __launch_bounds__(Scan2Cfg<D>::NT) scan2_kernel(const Scan2Args 
           const unsigned pm = __ballot_sync(0xffffffffu, fv == FLAG_PREFIX);
           const int first = pm ? __ffs(pm) - 1 : 32;
           if (first > 0) {                            // product of aggregates of lanes < first (nearest first)
-            CM<D> A;
-            if (lane < first) cm_load_cg(a.agg + (size_t)q * D * D, A); else cm_eye(A);
+            M A;
+            if (lane < first) cm_load_cg(a.agg + (size_t)q * W, A); else cm_eye(A);
 #pragma unroll
             for (int off = 1; off < 32; off <<= 1) {
-              const CM<D> o = cm_shfl_down(A, off);
+              const M o = cm_shfl_down(A, off);
               if ((lane & (2 * off - 1)) == 0) A = cm_mul(A, o);
             }
-            M = cm_mul(M, A);                         // meaningful in lane 0
+            Mlb = cm_mul(Mlb, A);                     // meaningful in lane 0
           }
           if (first < 32) {
             double er[D], ei[D];
@@ -515,7 +535,7 @@ __global__ void __launch_bounds__(Scan2Cfg<D>::NT) scan2_kernel(const Scan2Args 
               er[d] = __shfl_sync(0xffffffffu, er[d], first);
               ei[d] = __shfl_sync(0xffffffffu, ei[d], first);
             }
-            cm_apply(M, er, ei, pr, pi);              // valid in lane 0
+            cm_apply(Mlb, er, ei, pr, pi);            // valid in lane 0
             break;
           }
           jb -= 32;
@@ -546,9 +566,9 @@ __global__ void __launch_bounds__(Scan2Cfg<D>::NT) scan2_kernel(const Scan2Args 
     __syncthreads();
 
     // apply: ψ = (E·W_w)·ψ_in, then the thread's own operators
-    CM<D> Wp;
+    M Wp;
     cm_load(sWarpPre[warp], Wp);
-    const CM<D> X = cm_mul(E, Wp);
+    const M X = cm_mul(E, Wp);
     double xr[D], xi[D], yr[D], yi[D];
 #pragma unroll
     for (int d = 0; d < D; ++d) { xr[d] = sPsiIn[d].x; xi[d] = sPsiIn[d].y; }
@@ -557,8 +577,8 @@ __global__ void __launch_bounds__(Scan2Cfg<D>::NT) scan2_kernel(const Scan2Args 
     for (int c = 0; c < C; ++c) {
       const int it = tid * C + c;
       if (it < n_items) {
-        CM<D> u;
-        cm_load(U + c * D * D, u);
+        M u;
+        cm_load(U + c * W, u);
         cm_apply(u, yr, yi, xr, xi);
 #pragma unroll
         for (int d = 0; d < D; ++d) { yr[d] = xr[d]; yi[d] = xi[d]; sPsi[tid * SS + c * D + d] = make_double2(xr[d], xi[d]); }
@@ -601,25 +621,29 @@ __global__ void __launch_bounds__(Scan2Cfg<D>::NT) scan2_kernel(const Scan2Args 
 #ifndef SS_SCAN3_NSTAGE
 #define SS_SCAN3_NSTAGE 5   // TMA ring depth; shallower rings fit 2 CTAs per SM (tuning knob)
 #endif
-template <int D> struct Scan3Cfg {
-  static constexpr int NT = 128, NW = NT / 32, C = (D == 2) ? 4 : 2, NSTAGE = SS_SCAN3_NSTAGE, MAXST = SS_SCAN3_MAXST;
-  static constexpr int SU = C * D * D + 1;   // slot pitch in double2: odd → conflict-free per-thread reads
+// C intervals per thread and stage: ≈ 256 B of operators per row (dense: 4 × 64 B, 2 × 144 B); compact SU(2)
+// operators (32 B) take C = 4 and a deeper ring (8 stages) so that as many bytes are in flight.
+template <class M> struct Scan3Cfg {
+  static constexpr int D = M::SD, W = M::W;
+  static constexpr int NT = 128, NW = NT / 32, C = (W == 9) ? 2 : 4;
+  static constexpr int NSTAGE = (W == 2) ? 8 : SS_SCAN3_NSTAGE, MAXST = SS_SCAN3_MAXST;
+  static constexpr int SU = C * W + 1;       // slot pitch in double2: odd → conflict-free per-thread reads
   static constexpr int SS = C * D + 1;       // state staging pitch in double2
 };
-template <int D> constexpr size_t scan3_smem() {
-  return sizeof(double2) * (size_t)Scan3Cfg<D>::NT * (Scan3Cfg<D>::NSTAGE * Scan3Cfg<D>::SU + 2 * Scan3Cfg<D>::SS);
+template <class M> constexpr size_t scan3_smem() {
+  return sizeof(double2) * (size_t)Scan3Cfg<M>::NT * (Scan3Cfg<M>::NSTAGE * Scan3Cfg<M>::SU + 2 * Scan3Cfg<M>::SS);
 }
-template <int D> struct Scan3Layout {
+template <class M> struct Scan3Layout {
   int64_t tile, tiles_per_sweep, ntiles;
   size_t off_flags, off_agg, off_psi, total;
   Scan3Layout(int64_t batch, int64_t k_count, int nst) {
-    tile = (int64_t)Scan3Cfg<D>::NT * Scan3Cfg<D>::C * nst;
+    tile = (int64_t)Scan3Cfg<M>::NT * Scan3Cfg<M>::C * nst;
     tiles_per_sweep = (k_count + tile - 1) / tile;
     ntiles = batch * tiles_per_sweep;
     off_flags = 256;
     off_agg = align256(off_flags + sizeof(int) * (size_t)ntiles);
-    off_psi = align256(off_agg + sizeof(double2) * D * D * (size_t)ntiles);
-    total = align256(off_psi + sizeof(double2) * D * (size_t)ntiles);
+    off_psi = align256(off_agg + sizeof(double2) * M::W * (size_t)ntiles);
+    total = align256(off_psi + sizeof(double2) * M::SD * (size_t)ntiles);
   }
 };
 struct Scan3Args {
@@ -672,12 +696,13 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-template <int D>
-__global__ void __launch_bounds__(Scan3Cfg<D>::NT, 1)
+template <class M>
+__global__ void __launch_bounds__(Scan3Cfg<M>::NT, 1)
     scan3_kernel(const __grid_constant__ Scan3Args A3, const __grid_constant__ CUtensorMap tmU,
                  const __grid_constant__ CUtensorMap tmS) {
-  constexpr int NT = Scan3Cfg<D>::NT, NW = Scan3Cfg<D>::NW, C = Scan3Cfg<D>::C, NSTAGE = Scan3Cfg<D>::NSTAGE;
-  constexpr int SU = Scan3Cfg<D>::SU, SS = Scan3Cfg<D>::SS;
+  constexpr int D = M::SD, W = M::W;
+  constexpr int NT = Scan3Cfg<M>::NT, NW = Scan3Cfg<M>::NW, C = Scan3Cfg<M>::C, NSTAGE = Scan3Cfg<M>::NSTAGE;
+  constexpr int SU = Scan3Cfg<M>::SU, SS = Scan3Cfg<M>::SS;
   const Scan2Args& a = A3.s;
   const int nst = A3.nst, IPT = nst * C, LPT = 2 * nst;   // stages per pass, intervals per thread, loads per tile
   const long long TILE = (long long)NT * IPT;
@@ -685,12 +710,12 @@ __global__ void __launch_bounds__(Scan3Cfg<D>::NT, 1)
   double2* const sStage = smem5 + NSTAGE * NT * SU;         // [2][NT][SS] state staging
   __shared__ __align__(8) uint64_t sFull[NSTAGE];
   __shared__ __align__(8) uint64_t sEmpty[NSTAGE];
-  __shared__ double2 sWarpTot[NW][D * D];
+  __shared__ double2 sWarpTot[NW][W];
   __shared__ double2 sPsiIn[D];
   __shared__ double2 sPsiEnd[D];
-  __shared__ double2 sTot[D * D];
-  __shared__ double2 sM[D * D];
-  __shared__ double2 sWarpAgg[NW][D * D];
+  __shared__ double2 sTot[W];
+  __shared__ double2 sM[W];
+  __shared__ double2 sWarpAgg[NW][W];
   __shared__ unsigned sBal[NW];
   __shared__ long long sNext;
 
@@ -729,10 +754,10 @@ __global__ void __launch_bounds__(Scan3Cfg<D>::NT, 1)
       const long long k0 = j * TILE + (long long)tid * IPT + (long long)s * C;
       const int nit = (int)max(0LL, min((long long)C, a.k_count - k0));
       if (nit > 0) {
-        const unsigned bytes = (unsigned)(nit * D * D * sizeof(double2));
+        const unsigned bytes = (unsigned)(nit * W * sizeof(double2));
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx(&sFull[x], bytes);
-        tma_load_1d(smem5 + (x * NT + tid) * SU, a.U + ((size_t)b * a.k_count + k0) * D * D, bytes, &sFull[x]);
+        tma_load_1d(smem5 + (x * NT + tid) * SU, a.U + ((size_t)b * a.k_count + k0) * W, bytes, &sFull[x]);
       } else {
         mbar_arrive(&sFull[x]);
       }
@@ -786,7 +811,7 @@ __global__ void __launch_bounds__(Scan3Cfg<D>::NT, 1)
     const long long kt = j * TILE + (long long)tid * IPT;     // this thread's first interval
     const bool full = fc;
     // ---- pass A: P_i = U_{last} ⋯ U_{first} over this thread's intervals (HBM stream)
-    CM<D> P;
+    M P;
     cm_eye(P);
     for (int s = 0; s < nst; ++s) {
       const double2* U = consume();
@@ -794,8 +819,8 @@ __global__ void __launch_bounds__(Scan3Cfg<D>::NT, 1)
 #pragma unroll
       for (int c = 0; c < C; ++c) {
         if (k0 + c < a.k_count) {
-          CM<D> u;
-          cm_load(U + c * D * D, u);
+          M u;
+          cm_load(U + c * W, u);
           P = cm_mul(u, P);
         }
       }
@@ -805,29 +830,29 @@ __global__ void __launch_bounds__(Scan3Cfg<D>::NT, 1)
     // ---- block exclusive scan of the P_i: X_i = (P_{i-1} ⋯ P_0); tile aggregate G
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
-      const CM<D> o = cm_shfl_up(P, off);
+      const M o = cm_shfl_up(P, off);
       if (lane >= off) P = cm_mul(P, o);
     }
-    CM<D> X = cm_shfl_up(P, 1);
+    M X = cm_shfl_up(P, 1);
     if (lane == 0) cm_eye(X);
     if (lane == 31) cm_store(sWarpTot[warp], P);
     __syncthreads();
     {
-      CM<D> W, T;
-      cm_eye(W);
-      for (int w = 0; w < warp; ++w) { cm_load(sWarpTot[w], T); W = cm_mul(T, W); }
-      X = cm_mul(X, W);
+      M Wpre, T;
+      cm_eye(Wpre);
+      for (int w = 0; w < warp; ++w) { cm_load(sWarpTot[w], T); Wpre = cm_mul(T, Wpre); }
+      X = cm_mul(X, Wpre);
     }
     // ---- publish AGG, then a block-wide decoupled look-back: 128 predecessors per round (one round covers a wave)
     if (tid == 0) {
-      CM<D> tot, T;
+      M tot, T;
       cm_eye(tot);
       for (int w = 0; w < NW; ++w) { cm_load(sWarpTot[w], T); tot = cm_mul(T, tot); }
       cm_store(sTot, tot);
       if (j > 0) {
-        cm_store(a.agg + (size_t)tcur * D * D, tot);
+        cm_store(a.agg + (size_t)tcur * W, tot);
         cuda::atomic_ref<int, cuda::thread_scope_device>(a.flags[tcur]).store(FLAG_AGG, cuda::memory_order_release);
-        cm_store(sM, [] { CM<D> e; cm_eye(e); return e; }());
+        cm_store(sM, [] { M e; cm_eye(e); return e; }());
       } else {
         for (int d = 0; d < D; ++d) sPsiIn[d] = a.psi0[b * D + d];
       }
@@ -848,11 +873,11 @@ __global__ void __launch_bounds__(Scan3Cfg<D>::NT, 1)
         for (int w = NW - 1; w >= 0; --w)
           if (sBal[w]) first = w * 32 + __ffs(sBal[w]) - 1;
         if (first > 0) {                                       // product of the AGGs before the first PREFIX
-          CM<D> Ag;
-          if (tid < first) cm_load_cg(a.agg + (size_t)tq * D * D, Ag); else cm_eye(Ag);
+          M Ag;
+          if (tid < first) cm_load_cg(a.agg + (size_t)tq * W, Ag); else cm_eye(Ag);
 #pragma unroll
           for (int off = 1; off < 32; off <<= 1) {
-            const CM<D> o = cm_shfl_down(Ag, off);
+            const M o = cm_shfl_down(Ag, off);
             if ((lane & (2 * off - 1)) == 0) Ag = cm_mul(Ag, o);
           }
           if (lane == 0) cm_store(sWarpAgg[warp], Ag);
@@ -860,24 +885,24 @@ __global__ void __launch_bounds__(Scan3Cfg<D>::NT, 1)
         if (tid == first) for (int d = 0; d < D; ++d) sPsiEnd[d] = __ldcg(a.psi_end + tq * D + d);
         __syncthreads();
         if (tid == 0) {
-          CM<D> M, T;
-          cm_load(sM, M);
+          M Mlb, T;
+          cm_load(sM, Mlb);
           if (first > 0)
-            for (int w = 0; w < NW; ++w) { cm_load(sWarpAgg[w], T); M = cm_mul(M, T); }
+            for (int w = 0; w < NW; ++w) { cm_load(sWarpAgg[w], T); Mlb = cm_mul(Mlb, T); }
           if (first < NT) {
             double er[D], ei[D], pr[D], pi[D];
             for (int d = 0; d < D; ++d) { er[d] = sPsiEnd[d].x; ei[d] = sPsiEnd[d].y; }
-            cm_apply(M, er, ei, pr, pi);
+            cm_apply(Mlb, er, ei, pr, pi);
             for (int d = 0; d < D; ++d) sPsiIn[d] = make_double2(pr[d], pi[d]);
           } else {
-            cm_store(sM, M);
+            cm_store(sM, Mlb);
           }
         }
         if (first < NT) break;
       }
     }
     if (tid == 0) {                                            // publish PREFIX: ψ at the end of this tile
-      CM<D> tot;
+      M tot;
       cm_load(sTot, tot);
       double pr[D], pi[D], er[D], ei[D];
       for (int d = 0; d < D; ++d) { pr[d] = sPsiIn[d].x; pi[d] = sPsiIn[d].y; }
@@ -911,8 +936,8 @@ __global__ void __launch_bounds__(Scan3Cfg<D>::NT, 1)
 #pragma unroll
       for (int c = 0; c < C; ++c) {
         if (c < nit) {
-          CM<D> u;
-          cm_load(U + c * D * D, u);
+          M u;
+          cm_load(U + c * W, u);
           double zr[D], zi[D];
           cm_apply(u, yr, yi, zr, zi);
 #pragma unroll
@@ -953,6 +978,198 @@ __global__ void __launch_bounds__(Scan3Cfg<D>::NT, 1)
   bulk_wait_all();
 }
 
+// ---- state scan v4: register-resident tiles, many short-lived CTAs, warp-parallel decoupled look-back ------------
+//
+// A CTA takes the next ticket t (j-major: tile j of sweep b, t = j·batch + b) and holds its tile — NT·C consecutive
+// operators, thread i owning the C at [i·C, (i+1)·C) — in REGISTERS: loaded once from HBM (all C·W 16-byte loads of a
+// thread in flight at once), multiplied into the thread product, scanned (warp Kogge–Stone + warp totals), and after
+// the look-back applied again from the same registers to write the states.  No shared-memory ring, no second pass
+// over memory: the bytes moved are the algorithmic ones.  Latency is hidden across CTAs instead of inside one — several
+// CTAs per SM, each short-lived, so while one waits on its predecessor's flag the others stream.  C = 8 compact SU(2)
+// operators (32 registers), 4 dense 2×2 or 2 dense 3×3 per thread.
+template <class M> struct Scan4Cfg {
+  static constexpr int NT = 128, NW = NT / 32;
+  static constexpr int C = (M::W == 2) ? 8 : (M::W == 4 ? 4 : 2);
+  static constexpr int TILE = NT * C;
+};
+template <class M> struct Scan4Layout {
+  int64_t tiles_per_sweep, ntiles;
+  size_t off_flags, off_agg, off_psi, total;
+  Scan4Layout(int64_t batch, int64_t k_count) {
+    tiles_per_sweep = (k_count + Scan4Cfg<M>::TILE - 1) / Scan4Cfg<M>::TILE;
+    ntiles = batch * tiles_per_sweep;
+    off_flags = 256;
+    off_agg = align256(off_flags + sizeof(int) * (size_t)ntiles);
+    off_psi = align256(off_agg + sizeof(double2) * M::W * (size_t)ntiles);
+    total = align256(off_psi + sizeof(double2) * M::SD * (size_t)ntiles);
+  }
+};
+
+template <class M>
+__global__ void __launch_bounds__(Scan4Cfg<M>::NT) scan4_kernel(const Scan2Args a) {
+  constexpr int D = M::SD, W = M::W;
+  constexpr int NT = Scan4Cfg<M>::NT, NW = Scan4Cfg<M>::NW, C = Scan4Cfg<M>::C, TILE = Scan4Cfg<M>::TILE;
+  __shared__ double2 sWarpTot[NW][W];
+  __shared__ double2 sWarpPre[NW][W];
+  __shared__ double2 sPsiIn[D];
+  __shared__ long long sTicket;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) sTicket = (long long)atomicAdd(a.ticket, 1ull);
+  __syncthreads();
+  const long long t = sTicket;
+  const long long j = t / a.batch, b = t - j * a.batch;
+  const long long k0 = j * TILE + (long long)tid * C;           // this thread's first interval
+  const int n = (int)max(0LL, min((long long)C, a.k_count - k0));
+
+  // 1. the thread's C operators into registers (streaming loads, all in flight), thread product P = U_{C−1} ⋯ U_0
+  M u[C];
+  const double2* gU = a.U + ((size_t)b * a.k_count + k0) * W;
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    if (c < n) {
+      if constexpr (W == 2) {
+        const double2 x = __ldcs(gU + 2 * c), y = __ldcs(gU + 2 * c + 1);
+        u[c].ar = x.x; u[c].ai = x.y; u[c].br = y.x; u[c].bi = y.y;
+      } else {
+#pragma unroll
+        for (int e = 0; e < W; ++e) { const double2 x = __ldcs(gU + c * W + e); u[c].re[e] = x.x; u[c].im[e] = x.y; }
+      }
+    } else {
+      cm_eye(u[c]);
+    }
+  }
+  M P = u[0];
+#pragma unroll
+  for (int c = 1; c < C; ++c) P = cm_mul(u[c], P);
+
+  // 2. warp inclusive scan (later·earlier) → exclusive X; warp totals → exclusive warp prefixes + tile total
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const M q = cm_shfl_up(P, off);
+    if (lane >= off) P = cm_mul(P, q);
+  }
+  M X = cm_shfl_up(P, 1);
+  if (lane == 0) cm_eye(X);
+  if (lane == 31) cm_store(sWarpTot[warp], P);
+  __syncthreads();
+
+  if (warp == 0) {
+    M T;
+    if (lane < NW) cm_load(sWarpTot[lane], T); else cm_eye(T);
+#pragma unroll
+    for (int off = 1; off < NW; off <<= 1) {
+      const M q = cm_shfl_up(T, off);
+      if (lane >= off) T = cm_mul(T, q);
+    }
+    M Wx = cm_shfl_up(T, 1);
+    if (lane == 0) cm_eye(Wx);
+    if (lane < NW) cm_store(sWarpPre[lane], Wx);
+    const M tot = cm_shfl_idx(T, NW - 1);
+    // 3. publish AGG, warp-parallel look-back (lane ℓ inspects predecessor j − 1 − ℓ − 32r), publish PREFIX
+    double pr[D], pi[D];
+    if (j == 0) {
+#pragma unroll
+      for (int d = 0; d < D; ++d) { const double2 v = a.psi0[b * D + d]; pr[d] = v.x; pi[d] = v.y; }
+    } else {
+      if (lane == 0) {
+        cm_store(a.agg + (size_t)t * W, tot);
+        cuda::atomic_ref<int, cuda::thread_scope_device>(a.flags[t]).store(FLAG_AGG, cuda::memory_order_release);
+      }
+      M Mlb;
+      cm_eye(Mlb);
+      for (long long jb = j - 1;; jb -= 32) {
+        const long long jq = jb - lane;
+        const long long q = jq * a.batch + b;
+        int fv = FLAG_PREFIX;                       // lanes before tile 0 never matter (tile 0 is PREFIX)
+        if (jq >= 0) {
+          cuda::atomic_ref<int, cuda::thread_scope_device> f(a.flags[q]);
+          while ((fv = f.load(cuda::memory_order_acquire)) == FLAG_EMPTY) __nanosleep(32);
+        }
+        const unsigned pm = __ballot_sync(0xffffffffu, fv == FLAG_PREFIX);
+        const int first = pm ? __ffs(pm) - 1 : 32;
+        if (first > 0) {                            // product of the aggregates of lanes < first (nearest first)
+          M A;
+          if (lane < first) cm_load_cg(a.agg + (size_t)q * W, A); else cm_eye(A);
+#pragma unroll
+          for (int off = 1; off < 32; off <<= 1) {
+            const M o = cm_shfl_down(A, off);
+            if ((lane & (2 * off - 1)) == 0) A = cm_mul(A, o);
+          }
+          Mlb = cm_mul(Mlb, A);                     // meaningful in lane 0
+        }
+        if (first < 32) {
+          double er[D], ei[D];
+          if (lane == first)
+            for (int d = 0; d < D; ++d) { const double2 v = __ldcg(a.psi_end + q * D + d); er[d] = v.x; ei[d] = v.y; }
+#pragma unroll
+          for (int d = 0; d < D; ++d) {
+            er[d] = __shfl_sync(0xffffffffu, er[d], first);
+            ei[d] = __shfl_sync(0xffffffffu, ei[d], first);
+          }
+          cm_apply(Mlb, er, ei, pr, pi);            // valid in lane 0
+          break;
+        }
+      }
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        pr[d] = __shfl_sync(0xffffffffu, pr[d], 0);
+        pi[d] = __shfl_sync(0xffffffffu, pi[d], 0);
+      }
+    }
+    if (lane == 0) {
+      double er[D], ei[D];
+      cm_apply(tot, pr, pi, er, ei);
+      for (int d = 0; d < D; ++d) a.psi_end[t * D + d] = make_double2(er[d], ei[d]);
+      cuda::atomic_ref<int, cuda::thread_scope_device>(a.flags[t]).store(FLAG_PREFIX, cuda::memory_order_release);
+      for (int d = 0; d < D; ++d) sPsiIn[d] = make_double2(pr[d], pi[d]);
+      if (j == 0) {
+        if (a.states)
+          for (int d = 0; d < D; ++d) a.states[(size_t)b * (a.k_count + 1) * D + d] = make_double2(pr[d], pi[d]);
+        if (a.spin) {
+          double jj3[3];
+          spin_of<D>(pr, pi, jj3);
+          for (int e = 0; e < 3; ++e) a.spin[(size_t)b * (a.k_count + 1) * 3 + e] = jj3[e];
+        }
+      }
+    }
+  }
+  __syncthreads();
+
+  // 4. y = (X·W_w)·ψ_in, then the thread's operators again from registers; states written straight out
+  {
+    M Wp;
+    cm_load(sWarpPre[warp], Wp);
+    X = cm_mul(X, Wp);
+  }
+  double yr[D], yi[D];
+  {
+    double xr[D], xi[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) { xr[d] = sPsiIn[d].x; xi[d] = sPsiIn[d].y; }
+    cm_apply(X, xr, xi, yr, yi);
+  }
+  double2* gS = a.states ? a.states + ((size_t)b * (a.k_count + 1) + k0 + 1) * D : nullptr;
+  double* gJ = a.spin ? a.spin + ((size_t)b * (a.k_count + 1) + k0 + 1) * 3 : nullptr;
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    if (c < n) {
+      double zr[D], zi[D];
+      cm_apply(u[c], yr, yi, zr, zi);
+#pragma unroll
+      for (int d = 0; d < D; ++d) { yr[d] = zr[d]; yi[d] = zi[d]; }
+      if (gS)
+#pragma unroll
+        for (int d = 0; d < D; ++d) __stcs(gS + c * D + d, make_double2(zr[d], zi[d]));
+      if (gJ) {
+        double jj3[3];
+        spin_of<D>(zr, zi, jj3);
+#pragma unroll
+        for (int e = 0; e < 3; ++e) __stcs(gJ + c * 3 + e, jj3[e]);
+      }
+    }
+  }
+}
+
 // ---- small problems: one cooperative wave with two grid-wide barriers instead of look-back -------------------------
 //
 // For problems whose operators fit in L2 (B·K·dim²·16 B ≤ 64 MB) and with few sweeps (C1, C2, C4's 1e6-interval
@@ -978,13 +1195,14 @@ struct CoopArgs {
 // brought into shared memory by ONE bulk copy (cp.async.bulk, mbarrier completion) before pass 1, so the whole run is
 // in flight at once instead of each thread's dependent chain of 144-B loads (C2: 21 µs, long-scoreboard bound), and
 // pass 3 re-reads it from shared memory instead of L2.
-template <int D, bool STAGED>
+template <class M, bool STAGED>
 __global__ void __launch_bounds__(128) scan_coop_kernel(const CoopArgs a) {
   namespace cg = cooperative_groups;
+  constexpr int D = M::SD, W = M::W;
   constexpr int NT = 128, NW = NT / 32;
-  __shared__ double2 sWarpTot[NW][D * D];
+  __shared__ double2 sWarpTot[NW][W];
   __shared__ double2 sPsiIn[D];
-  __shared__ double2 sM[D * D];
+  __shared__ double2 sM[W];
   __shared__ __align__(8) uint64_t sBar;
   extern __shared__ __align__(128) double2 sRun[];
   const int c = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -996,9 +1214,9 @@ __global__ void __launch_bounds__(128) scan_coop_kernel(const CoopArgs a) {
   const int64_t k0 = has ? min((int64_t)part * per, K) : 0, k1 = has ? min(k0 + per, K) : 0;
   const int64_t m = (k1 - k0 + NT - 1) / NT;
   const int64_t t0 = min(k0 + (int64_t)tid * m, k1), t1 = min(t0 + m, k1);
-  const double2* gU = a.U + (size_t)(has ? b : 0) * K * D * D;
+  const double2* gU = a.U + (size_t)(has ? b : 0) * K * W;
   if constexpr (STAGED) {
-    const unsigned bytes = (unsigned)((k1 - k0) * D * D * sizeof(double2));
+    const unsigned bytes = (unsigned)((k1 - k0) * W * sizeof(double2));
     if (bytes > 0) {
       if (tid == 0) {
         mbar_init(&sBar, 1);
@@ -1007,41 +1225,41 @@ __global__ void __launch_bounds__(128) scan_coop_kernel(const CoopArgs a) {
       __syncthreads();
       if (tid == 0) {
         mbar_expect_tx(&sBar, bytes);
-        tma_load_1d(sRun, gU + (size_t)k0 * D * D, bytes, &sBar);
+        tma_load_1d(sRun, gU + (size_t)k0 * W, bytes, &sBar);
       }
       mbar_wait(&sBar, 0);
     }
-    gU = sRun - (size_t)k0 * D * D;                          // operator k at gU + k·D² (shared memory)
+    gU = sRun - (size_t)k0 * W;                          // operator k at gU + k·W (shared memory)
   }
   // 1. thread product and block exclusive scan
-  CM<D> P;
+  M P;
   cm_eye(P);
   // unrolled so several operators' loads are in flight per thread (the products are a dependent chain)
 #pragma unroll 4
   for (int64_t k = t0; k < t1; ++k) {
-    CM<D> u;
-    cm_load(gU + (size_t)k * D * D, u);
+    M u;
+    cm_load(gU + (size_t)k * W, u);
     P = cm_mul(u, P);
   }
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
-    const CM<D> o = cm_shfl_up(P, off);
+    const M o = cm_shfl_up(P, off);
     if (lane >= off) P = cm_mul(P, o);
   }
-  CM<D> X = cm_shfl_up(P, 1);
+  M X = cm_shfl_up(P, 1);
   if (lane == 0) cm_eye(X);
   if (lane == 31) cm_store(sWarpTot[warp], P);
   __syncthreads();
   {
-    CM<D> W, T;
-    cm_eye(W);
-    for (int w = 0; w < warp; ++w) { cm_load(sWarpTot[w], T); W = cm_mul(T, W); }
-    X = cm_mul(X, W);
+    M Wpre, T;
+    cm_eye(Wpre);
+    for (int w = 0; w < warp; ++w) { cm_load(sWarpTot[w], T); Wpre = cm_mul(T, Wpre); }
+    X = cm_mul(X, Wpre);
     if (tid == 0) {
-      CM<D> tot;
+      M tot;
       cm_eye(tot);
       for (int w = 0; w < NW; ++w) { cm_load(sWarpTot[w], T); tot = cm_mul(T, tot); }
-      cm_store(a.agg + (size_t)c * D * D, tot);
+      cm_store(a.agg + (size_t)c * W, tot);
       cm_eye(tot);
       cm_store(sM, tot);
     }
@@ -1050,30 +1268,30 @@ __global__ void __launch_bounds__(128) scan_coop_kernel(const CoopArgs a) {
   // 2. ψ_in: ordered product of the predecessors' aggregates (latest first), NT per round
   for (int q0 = part - 1; q0 >= 0; q0 -= NT) {
     const int q = q0 - tid;                                  // thread t holds G_{q0 − t} (later on the left)
-    CM<D> Ag;
-    if (q >= 0) cm_load_cg(a.agg + (size_t)(c - part + q) * D * D, Ag); else cm_eye(Ag);
+    M Ag;
+    if (q >= 0) cm_load_cg(a.agg + (size_t)(c - part + q) * W, Ag); else cm_eye(Ag);
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
-      const CM<D> o = cm_shfl_down(Ag, off);
+      const M o = cm_shfl_down(Ag, off);
       if ((lane & (2 * off - 1)) == 0) Ag = cm_mul(Ag, o);
     }
     __syncthreads();                                         // sWarpTot reuse
     if (lane == 0) cm_store(sWarpTot[warp], Ag);
     __syncthreads();
     if (tid == 0) {
-      CM<D> M, T;
-      cm_load(sM, M);
-      for (int w = 0; w < NW; ++w) { cm_load(sWarpTot[w], T); M = cm_mul(M, T); }
-      cm_store(sM, M);
+      M Mlb, T;
+      cm_load(sM, Mlb);
+      for (int w = 0; w < NW; ++w) { cm_load(sWarpTot[w], T); Mlb = cm_mul(Mlb, T); }
+      cm_store(sM, Mlb);
     }
   }
   __syncthreads();
   if (tid == 0 && has) {
-    CM<D> M;
-    cm_load(sM, M);
+    M Mlb;
+    cm_load(sM, Mlb);
     double xr[D], xi[D], yr[D], yi[D];
     for (int d = 0; d < D; ++d) { xr[d] = a.psi0[b * D + d].x; xi[d] = a.psi0[b * D + d].y; }
-    cm_apply(M, xr, xi, yr, yi);
+    cm_apply(Mlb, xr, xi, yr, yi);
     for (int d = 0; d < D; ++d) sPsiIn[d] = make_double2(yr[d], yi[d]);
     if (part == 0) {
       if (a.states)
@@ -1099,8 +1317,8 @@ __global__ void __launch_bounds__(128) scan_coop_kernel(const CoopArgs a) {
   double* gJ = a.spin ? a.spin + (size_t)b * (K + 1) * 3 : nullptr;
 #pragma unroll 4
   for (int64_t k = t0; k < t1; ++k) {
-    CM<D> u;
-    cm_load(gU + (size_t)k * D * D, u);
+    M u;
+    cm_load(gU + (size_t)k * W, u);
     double zr[D], zi[D];
     cm_apply(u, yr, yi, zr, zi);
 #pragma unroll
@@ -1126,24 +1344,19 @@ __global__ void __launch_bounds__(128) scan_coop_kernel(const CoopArgs a) {
 #define SS_CHAIN_THREADS 64
 #endif
 constexpr int kChainThreads = SS_CHAIN_THREADS;
-#ifndef SS_SCAN_COOP
-#define SS_SCAN_COOP 1         // 0: small problems keep the round-1 tile scan (comparison builds)
-#endif
 #ifndef SS_COOP_MAXCPS
 #define SS_COOP_MAXCPS 128     // CTAs per sweep of the cooperative scan (one predecessor round)
-#endif
-#ifndef SS_CHAIN_FULL_CTAS
-#define SS_CHAIN_FULL_CTAS 0   // 1: the round-1 launch (kChainThreads sweeps per CTA), for comparison
 #endif
 constexpr int64_t kChainMinBatch = 4096;
 #ifndef SS_CHAIN_CH
 #define SS_CHAIN_CH 12   // operators per bulk copy: 4 / 8 / 12 → 2.9 / 5.2 / 5.4 TB/s on C3 (14 exceeds shared memory)
 #endif
-template <int D> struct ChainCfg { static constexpr int CH = SS_CHAIN_CH; };
+// compact SU(2) operators (32 B) are copied 48 at a time: ≈ 1.5 KB per copy like 12 dense spin-one operators
+template <class M> struct ChainCfg { static constexpr int CH = M::W == 2 ? 4 * SS_CHAIN_CH : SS_CHAIN_CH; };
 // Per-lane slot: 2 stages of CH operators, stride padded to an odd number of 16-byte words so the 32 lanes' LDS.128
 // at the same offset hit distinct banks (an unpadded stride is a multiple of 128 B: a 32-way conflict).
-template <int D> __host__ __device__ constexpr int chain_slot_stride() { return (2 * ChainCfg<D>::CH * D * D) | 1; }
-template <int D> constexpr size_t chain_smem() { return sizeof(double2) * (size_t)kChainThreads * chain_slot_stride<D>(); }
+template <class M> __host__ __device__ constexpr int chain_slot_stride() { return (2 * ChainCfg<M>::CH * M::W) | 1; }
+template <class M> constexpr size_t chain_smem() { return sizeof(double2) * (size_t)kChainThreads * chain_slot_stride<M>(); }
 
 struct ChainArgs {
   int64_t batch, k_count;
@@ -1154,15 +1367,16 @@ struct ChainArgs {
   int spc;           // sweeps per CTA (≤ kChainThreads): spreads the batch over every SM
 };
 
-template <int D>
+template <class M>
 __global__ void __launch_bounds__(kChainThreads) chain_kernel(const ChainArgs a) {
-  constexpr int CH = ChainCfg<D>::CH;
+  constexpr int D = M::SD, W = M::W;
+  constexpr int CH = ChainCfg<M>::CH;
   extern __shared__ __align__(128) double2 smem3[];
   __shared__ __align__(8) uint64_t sBar[kChainThreads / 32][2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t b = (int64_t)blockIdx.x * a.spc + tid;
   const bool valid = tid < a.spc && b < a.batch;
-  double2* slot[2] = {smem3 + (size_t)tid * chain_slot_stride<D>(), smem3 + (size_t)tid * chain_slot_stride<D>() + CH * D * D};
+  double2* slot[2] = {smem3 + (size_t)tid * chain_slot_stride<M>(), smem3 + (size_t)tid * chain_slot_stride<M>() + CH * W};
   if (lane == 0) {
     mbar_init(&sBar[warp][0], 32);
     mbar_init(&sBar[warp][1], 32);
@@ -1170,14 +1384,14 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(const ChainArgs a)
   }
   __syncwarp();
   const int64_t nchunks = (a.k_count + CH - 1) / CH;
-  const double2* gU = a.U + (size_t)(valid ? b : 0) * a.k_count * D * D;
+  const double2* gU = a.U + (size_t)(valid ? b : 0) * a.k_count * W;
   auto issue = [&](int64_t c, int st) {
     const int64_t k0 = c * CH;
     const int n = valid ? (int)min((int64_t)CH, a.k_count - k0) : 0;
-    const unsigned bytes = (unsigned)(n * D * D * sizeof(double2));
+    const unsigned bytes = (unsigned)(n * W * sizeof(double2));
     if (bytes) {
       mbar_expect_tx(&sBar[warp][st], bytes);
-      tma_load_1d(slot[st], gU + (size_t)k0 * D * D, bytes, &sBar[warp][st]);
+      tma_load_1d(slot[st], gU + (size_t)k0 * W, bytes, &sBar[warp][st]);
     } else {
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&sBar[warp][st])) : "memory");
     }
@@ -1213,19 +1427,9 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(const ChainArgs a)
       const size_t kout = (size_t)(c * CH + 1);
       for (int i = 0; i < n; ++i) {
         double yr[D], yi[D];
-#pragma unroll
-        for (int r = 0; r < D; ++r) {
-          double sr = 0.0, si = 0.0;
-#pragma unroll
-          for (int k = 0; k < D; ++k) {
-            const double2 m = u[(i * D + r) * D + k];
-            sr = fma(m.x, pr[k], sr);
-            sr = fma(-m.y, pi[k], sr);
-            si = fma(m.x, pi[k], si);
-            si = fma(m.y, pr[k], si);
-          }
-          yr[r] = sr; yi[r] = si;
-        }
+        M m;
+        cm_load(u + i * W, m);
+        cm_apply(m, pr, pi, yr, yi);
 #pragma unroll
         for (int d = 0; d < D; ++d) { pr[d] = yr[d]; pi[d] = yi[d]; }
         if (gS)
@@ -1241,31 +1445,27 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(const ChainArgs a)
   }
 }
 
-template <int D>
+template <class M>
 static cudaError_t run_chain(int64_t batch, int64_t k_count, const double* U, const double* psi0, double* states,
                              double* spin, cudaStream_t s, int* launches) {
-  constexpr size_t smem = chain_smem<D>();
-  static bool attr = false;
-  if (!attr) {
-    const cudaError_t e = cudaFuncSetAttribute(chain_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  constexpr size_t smem = chain_smem<M>();
+  static DeviceCache attr;   // per device: the shared-memory opt-in applies to the current device's context
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (!attr.get(dev)) {
+    e = cudaFuncSetAttribute(chain_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr.set(dev, 1);
   }
   // Sweeps per CTA: at most kChainThreads, and few enough that the CTAs cover every SM (8192 sweeps: 56 per CTA on
   // 147 CTAs instead of 64 on 128 — the per-SM TMA/L1 path, not HBM, limited the 128-CTA launch).
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) !=
-                                                   cudaSuccess || sms <= 0)
-      sms = 148;
-  }
+  const int sms = device_sms(dev);
   int spc = (int)std::min<int64_t>(kChainThreads, (batch + sms - 1) / sms);
-  if (SS_CHAIN_FULL_CTAS) spc = kChainThreads;
   if (spc < 1) spc = 1;
   ChainArgs a{batch, k_count, reinterpret_cast<const double2*>(U), reinterpret_cast<const double2*>(psi0),
               reinterpret_cast<double2*>(states), spin, spc};
-  chain_kernel<D><<<(unsigned)((batch + spc - 1) / spc), kChainThreads, smem, s>>>(a);
+  chain_kernel<M><<<(unsigned)((batch + spc - 1) / spc), kChainThreads, smem, s>>>(a);
   ++*launches;
   return cudaGetLastError();
 }
@@ -1353,39 +1553,44 @@ template <int D> size_t scan_ws_bytes(int64_t batch, int64_t k_count) { return S
 int64_t chain_min_batch() { return kChainMinBatch; }
 
 constexpr int kCoopMaxGrid = 1024;
+// Sized for the dense operators of this dim (the compact ones need less).
+template <class M> static size_t tile_ws_bytes(int64_t batch, int64_t k_count) {
+  return std::max({Scan2Layout<M>(batch, k_count).total, Scan3Layout<M>(batch, k_count, 1).total,
+                   Scan4Layout<M>(batch, k_count).total});
+}
 size_t scan_workspace_bytes(int dim, int64_t batch, int64_t k_count) {
   const size_t coop = sizeof(double2) * (size_t)dim * dim * kCoopMaxGrid;
-  return std::max(coop, dim == 2 ? std::max(Scan2Layout<2>(batch, k_count).total, Scan3Layout<2>(batch, k_count, 1).total)
-                                 : std::max(Scan2Layout<3>(batch, k_count).total, Scan3Layout<3>(batch, k_count, 1).total));
+  return std::max(coop, dim == 2 ? std::max(tile_ws_bytes<CM<2>>(batch, k_count), tile_ws_bytes<SU<2>>(batch, k_count))
+                                 : std::max(tile_ws_bytes<CM<3>>(batch, k_count), tile_ws_bytes<SU<3>>(batch, k_count)));
 }
 
 // Cooperative small-problem scan (scan_coop_kernel): returns cudaErrorNotSupported when the problem is not eligible.
 #ifndef SS_COOP_STAGE_MAX
 #define SS_COOP_STAGE_MAX (200 * 1024)   // bytes of operators one CTA stages in shared memory (0: never stage)
 #endif
-template <int D>
+template <class M>
 static cudaError_t run_scan_coop(int64_t batch, int64_t k_count, const double* U, const double* psi0, double* states,
                                  double* spin, void* ws, cudaStream_t s, int* launches) {
-  static int max_grid = -1, n_sms = 0;
-  if (max_grid < 0) {
-    int dev = 0, sms = 0, per_sm = 0, coop = 0;
-    max_grid = 0;
-    if (cudaGetDevice(&dev) == cudaSuccess &&
-        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev) == cudaSuccess && coop &&
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess &&
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scan_coop_kernel<D, false>, 128, 0) == cudaSuccess)
-      max_grid = std::min(kCoopMaxGrid, sms * std::max(per_sm, 0));
-    n_sms = sms;
-    if (SS_COOP_STAGE_MAX > 0 &&
-        cudaFuncSetAttribute(scan_coop_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             SS_COOP_STAGE_MAX) != cudaSuccess) {
-      (void)cudaGetLastError();
-      n_sms = 0;                                             // staging unavailable: the L2 path only
-    }
+  constexpr int W = M::W;
+  static DeviceCache c_grid, c_stage;   // max co-resident grid + 1 (0: unset); staging available + 1
+  const int dev = current_device();
+  if (c_grid.get(dev) == 0) {
+    int coop = 0, per_sm = 0, max_grid = 0;
+    if (cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev) == cudaSuccess && coop &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scan_coop_kernel<M, false>, 128, 0) == cudaSuccess)
+      max_grid = std::min(kCoopMaxGrid, device_sms(dev) * std::max(per_sm, 0));
+    (void)cudaGetLastError();
+    bool stage = SS_COOP_STAGE_MAX > 0 &&
+                 cudaFuncSetAttribute(scan_coop_kernel<M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      SS_COOP_STAGE_MAX) == cudaSuccess;
+    if (!stage) (void)cudaGetLastError();                     // staging unavailable: the L2 path only
+    c_stage.set(dev, stage ? 2 : 1);
+    c_grid.set(dev, max_grid + 1);
   }
-  const double bytes = (double)batch * (double)k_count * D * D * sizeof(double2);
-  if (SS_SCAN_COOP == 0 || max_grid < 2 || batch * 2 > max_grid || bytes > 64.0 * (1 << 20))
-    return cudaErrorNotSupported;
+  const int max_grid = c_grid.get(dev) - 1;
+  const int n_sms = c_stage.get(dev) == 2 ? device_sms(dev) : 0;
+  const double bytes = (double)batch * (double)k_count * W * sizeof(double2);
+  if (max_grid < 2 || batch * 2 > max_grid || bytes > 64.0 * (1 << 20)) return cudaErrorNotSupported;
   // CTAs per sweep: fill the resident grid, but keep ≥ 256 intervals per CTA
   // (measured: C2's 1e5 intervals prefer 128 CTAs — one predecessor round — C4's 1e6 prefer 256: shorter thread chains)
   const int64_t cap = (k_count > (int64_t)SS_COOP_MAXCPS * 4096) ? 2 * SS_COOP_MAXCPS : SS_COOP_MAXCPS;
@@ -1395,12 +1600,12 @@ static cudaError_t run_scan_coop(int64_t batch, int64_t k_count, const double* U
              reinterpret_cast<double2*>(states), spin, static_cast<double2*>(ws)};
   void* args[] = {&a};
   // staged when every CTA has an SM of its own and its run of operators fits the shared-memory budget
-  const size_t run_bytes = (size_t)((k_count + cps - 1) / cps) * D * D * sizeof(double2);
+  const size_t run_bytes = (size_t)((k_count + cps - 1) / cps) * W * sizeof(double2);
   const bool staged = n_sms > 0 && batch * cps <= n_sms && run_bytes <= (size_t)SS_COOP_STAGE_MAX;
   const cudaError_t e =
-      staged ? cudaLaunchCooperativeKernel((const void*)scan_coop_kernel<D, true>, dim3((unsigned)(batch * cps)),
+      staged ? cudaLaunchCooperativeKernel((const void*)scan_coop_kernel<M, true>, dim3((unsigned)(batch * cps)),
                                            dim3(128), args, run_bytes, s)
-             : cudaLaunchCooperativeKernel((const void*)scan_coop_kernel<D, false>, dim3((unsigned)(batch * cps)),
+             : cudaLaunchCooperativeKernel((const void*)scan_coop_kernel<M, false>, dim3((unsigned)(batch * cps)),
                                            dim3(128), args, 0, s);
   if (e == cudaErrorCooperativeLaunchTooLarge) {   // SMs taken by another context (MPS, green contexts): tile scan
     (void)cudaGetLastError();
@@ -1411,52 +1616,43 @@ static cudaError_t run_scan_coop(int64_t batch, int64_t k_count, const double* U
 }
 
 size_t aggregate_workspace_bytes(int dim, int64_t batch, int64_t k_count) {
-  // v1 tiling; per-tile totals live in the agg region
+  // v1 tiling; per-tile totals live in the workspace, then one combine per sweep
   return dim == 2 ? scan_ws_bytes<2>(batch, k_count) : scan_ws_bytes<3>(batch, k_count);
 }
 
-template <int D, bool SCAN>
-static cudaError_t run_scan(int64_t batch, int64_t k_count, const double* U, const double* psi0, double* states,
-                            double* aggregate, void* ws, cudaStream_t s, int* launches) {
+template <int D>
+static cudaError_t run_aggregate(int64_t batch, int64_t k_count, const double* U, double* aggregate, void* ws,
+                                 cudaStream_t s, int* launches) {
   ScanLayout<D> L(batch, k_count);
-  char* w = static_cast<char*>(ws);
   ScanArgs a;
   a.batch = batch;
   a.k_count = k_count;
   a.tiles_per_sweep = L.tiles_per_sweep;
   a.U = reinterpret_cast<const double2*>(U);
-  a.psi0 = reinterpret_cast<const double2*>(psi0);
-  a.states = reinterpret_cast<double2*>(states);
-  a.ticket = reinterpret_cast<unsigned long long*>(w);
-  a.flags = reinterpret_cast<int*>(w + L.off_flags);
-  a.agg = reinterpret_cast<double2*>(w + L.off_agg);
-  a.psi_end = reinterpret_cast<double2*>(w + L.off_psi);
-  a.aggregate_out = a.agg;
-  cudaError_t e = cudaMemsetAsync(w, 0, L.off_agg, s);   // ticket + flags
-  if (e != cudaSuccess) return e;
+  a.aggregate_out = reinterpret_cast<double2*>(static_cast<char*>(ws) + L.off_agg);
   if (L.ntiles > 0x7fffffffLL) return cudaErrorInvalidValue;
-  constexpr int TILE = tile_size<D>();
-  constexpr size_t smem = sizeof(double2) * (size_t)TILE * D * (D + (SCAN ? 1 : 0));
-  static bool attr_set = false;
-  if (!attr_set) {
-    e = cudaFuncSetAttribute(scan_kernel<D, SCAN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  constexpr size_t smem = sizeof(double2) * (size_t)tile_size<D>() * D * D;
+  static DeviceCache attr;
+  const int dev = current_device();
+  if (!attr.get(dev)) {
+    const cudaError_t e = cudaFuncSetAttribute(aggregate_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr.set(dev, 1);
   }
-  scan_kernel<D, SCAN><<<(unsigned)L.ntiles, kScanThreads, smem, s>>>(a);
+  aggregate_kernel<D><<<(unsigned)L.ntiles, kScanThreads, smem, s>>>(a);
   ++*launches;
-  e = cudaGetLastError();
-  if (e != cudaSuccess || SCAN) return e;
-  combine_tiles_kernel<D><<<(unsigned)batch, 256, 0, s>>>(L.tiles_per_sweep, a.agg,
-                                                                          reinterpret_cast<double2*>(aggregate));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  combine_tiles_kernel<D><<<(unsigned)batch, 256, 0, s>>>(L.tiles_per_sweep, a.aggregate_out,
+                                                          reinterpret_cast<double2*>(aggregate));
   ++*launches;
   return cudaGetLastError();
 }
 
-template <int D>
+template <class M>
 static cudaError_t run_scan2(int64_t batch, int64_t k_count, const double* U, const double* psi0, double* states,
                              double* spin, void* ws, cudaStream_t s, int* launches) {
-  Scan2Layout<D> L(batch, k_count);
+  Scan2Layout<M> L(batch, k_count);
   char* w = static_cast<char*>(ws);
   Scan2Args a;
   a.batch = batch;
@@ -1473,27 +1669,28 @@ static cudaError_t run_scan2(int64_t batch, int64_t k_count, const double* U, co
   a.psi_end = reinterpret_cast<double2*>(w + L.off_psi);
   cudaError_t e = cudaMemsetAsync(w, 0, L.off_agg, s);   // ticket + flags
   if (e != cudaSuccess) return e;
-  constexpr size_t smem = scan2_smem<D>();
-  static int grid = 0;
+  constexpr size_t smem = scan2_smem<M>();
+  static DeviceCache c_grid;
+  const int dev = current_device();
+  int grid = c_grid.get(dev);
   if (grid == 0) {
-    e = cudaFuncSetAttribute(scan2_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = cudaFuncSetAttribute(scan2_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scan2_kernel<D>, Scan2Cfg<D>::NT, smem);
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scan2_kernel<M>, Scan2Cfg<M>::NT, smem);
     if (e != cudaSuccess) return e;
-    grid = sms * (per_sm > 0 ? per_sm : 1);   // persistent: every CTA resident (look-back forward progress)
+    grid = device_sms(dev) * (per_sm > 0 ? per_sm : 1);   // persistent: every CTA resident (look-back forward progress)
+    c_grid.set(dev, grid);
   }
   const int g = (int)std::min<int64_t>(grid, L.ntiles);
-  scan2_kernel<D><<<g, Scan2Cfg<D>::NT, smem, s>>>(a);
+  scan2_kernel<M><<<g, Scan2Cfg<M>::NT, smem, s>>>(a);
   ++*launches;
   return cudaGetLastError();
 }
 
-template <int D> static int scan3_nst(int64_t batch, int64_t k_count, int grid) {
-  int nst = Scan3Cfg<D>::MAXST;   // largest tile that still leaves ≥ 4 tiles per CTA
-  while (nst > 1 && Scan3Layout<D>(batch, k_count, nst).ntiles < 4LL * grid) nst >>= 1;
+template <class M> static int scan3_nst(int64_t batch, int64_t k_count, int grid) {
+  int nst = Scan3Cfg<M>::MAXST;   // largest tile that still leaves ≥ 4 tiles per CTA
+  while (nst > 1 && Scan3Layout<M>(batch, k_count, nst).ntiles < 4LL * grid) nst >>= 1;
   return nst;
 }
 
@@ -1501,57 +1698,61 @@ using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, 
                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-// 4-D view of a [B][rows·IPT + …][w] complex128 array (w = D² for U, D for states) for scan3's stage boxes:
-// dim0 = the C·w·2 doubles of one stage of one row, dim1 = stage s, dim2 = row (IPT intervals), dim3 = sweep.  The box
-// is one double2 wider than dim0: the out-of-bounds element is zero-filled on loads and dropped on stores, and gives the
-// shared-memory rows an odd 16-B pitch.
+// 4-D view of a [B][rows·IPT + …][w] complex128 array (w = W double2 per operator, D per state) for scan3's stage
+// boxes: dim0 = the C·w·2 doubles of one stage of one row, dim1 = stage s, dim2 = row (IPT intervals), dim3 = sweep.
+// The box is one double2 wider than dim0: the out-of-bounds element is zero-filled on loads and dropped on stores,
+// and gives the shared-memory rows an odd 16-B pitch.
 static cudaError_t encode_stage_map(CUtensorMap* tm, const void* base, int w, int C, int nst, int64_t rows,
                                     int64_t sweep_stride_items, int64_t batch, int box_rows) {
-  static EncodeTiled encode = nullptr;
-  if (!encode) {
+  static std::atomic<EncodeTiled> encode{nullptr};
+  EncodeTiled fn = encode.load();
+  if (!fn) {
     cudaDriverEntryPointQueryResult qr;
-    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&encode, cudaEnableDefault, &qr);
-    if (e != cudaSuccess || qr != cudaDriverEntryPointSuccess || !encode) return cudaErrorSymbolNotFound;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&fn, cudaEnableDefault, &qr);
+    if (e != cudaSuccess || qr != cudaDriverEntryPointSuccess || !fn) return cudaErrorSymbolNotFound;
+    encode.store(fn);
   }
   const cuuint64_t item = (cuuint64_t)w * sizeof(double2);
   const cuuint64_t dims[4] = {(cuuint64_t)C * w * 2, (cuuint64_t)nst, (cuuint64_t)rows, (cuuint64_t)batch};
   const cuuint64_t strides[3] = {C * item, (cuuint64_t)nst * C * item, (cuuint64_t)sweep_stride_items * item};
   const cuuint32_t box[4] = {(cuuint32_t)(C * w * 2 + 2), 1u, (cuuint32_t)box_rows, 1u};
   const cuuint32_t estr[4] = {1u, 1u, 1u, 1u};
-  const CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<void*>(base), dims, strides, box, estr,
-                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  const CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<void*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-// persistent grid of scan3: every CTA resident (look-back forward progress); 0 on error
-template <int D> static int scan3_grid() {
-  static int grid = 0;
+// persistent grid of scan3 on the current device: every CTA resident (look-back forward progress); 0 on error
+template <class M> static int scan3_grid() {
+  static DeviceCache c_grid;
+  const int dev = current_device();
+  int grid = c_grid.get(dev);
   if (grid == 0) {
-    if (cudaFuncSetAttribute(scan3_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan3_smem<D>()) !=
+    if (cudaFuncSetAttribute(scan3_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan3_smem<M>()) !=
         cudaSuccess)
       return 0;
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scan3_kernel<D>, Scan3Cfg<D>::NT, scan3_smem<D>()) !=
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scan3_kernel<M>, Scan3Cfg<M>::NT, scan3_smem<M>()) !=
         cudaSuccess)
       return 0;
-    grid = sms * (per_sm > 0 ? per_sm : 1);
+    grid = device_sms(dev) * (per_sm > 0 ? per_sm : 1);
+    c_grid.set(dev, grid);
   }
   return grid;
 }
 
-template <int D>
+template <class M>
 static cudaError_t run_scan3(int64_t batch, int64_t k_count, const double* U, const double* psi0, double* states,
                              double* spin, void* ws, cudaStream_t s, int* launches) {
-  using Cfg = Scan3Cfg<D>;
-  constexpr size_t smem = scan3_smem<D>();
-  const int grid = scan3_grid<D>();
+  using Cfg = Scan3Cfg<M>;
+  constexpr int D = M::SD;
+  constexpr size_t smem = scan3_smem<M>();
+  const int grid = scan3_grid<M>();
   if (grid == 0) return cudaErrorInvalidConfiguration;
   cudaError_t e;
-  const int nst = scan3_nst<D>(batch, k_count, grid);
-  Scan3Layout<D> L(batch, k_count, nst);
+  const int nst = scan3_nst<M>(batch, k_count, grid);
+  Scan3Layout<M> L(batch, k_count, nst);
   char* w = static_cast<char*>(ws);
   Scan3Args A3;
   Scan2Args& a = A3.s;
@@ -1575,7 +1776,7 @@ static cudaError_t run_scan3(int64_t batch, int64_t k_count, const double* U, co
   A3.tensor_u = k_count >= L.tile;             // some tile is full
   A3.tensor_s = A3.tensor_u && states != nullptr;
   if (A3.tensor_u) {
-    e = encode_stage_map(&tmU, U, D * D, Cfg::C, nst, rows, k_count, batch, Cfg::NT);
+    e = encode_stage_map(&tmU, U, M::W, Cfg::C, nst, rows, k_count, batch, Cfg::NT);
     if (e != cudaSuccess) return e;
   }
   if (A3.tensor_s) {   // states[b][k + 1] for interval k: base at state 1, sweep stride K + 1
@@ -1585,38 +1786,90 @@ static cudaError_t run_scan3(int64_t batch, int64_t k_count, const double* U, co
   e = cudaMemsetAsync(w, 0, L.off_agg, s);   // ticket + flags
   if (e != cudaSuccess) return e;
   const int g = (int)std::min<int64_t>(grid, L.ntiles);
-  scan3_kernel<D><<<g, Cfg::NT, smem, s>>>(A3, tmU, tmS);
+  scan3_kernel<M><<<g, Cfg::NT, smem, s>>>(A3, tmU, tmS);
   ++*launches;
   return cudaGetLastError();
 }
 
-#ifndef SS_SCAN_VERSION
-#define SS_SCAN_VERSION 3
-#endif
+template <class M>
+static cudaError_t run_scan4(int64_t batch, int64_t k_count, const double* U, const double* psi0, double* states,
+                             double* spin, void* ws, cudaStream_t s, int* launches) {
+  Scan4Layout<M> L(batch, k_count);
+  if (L.ntiles > 0x7fffffffLL) return cudaErrorInvalidValue;
+  char* w = static_cast<char*>(ws);
+  Scan2Args a;
+  a.batch = batch;
+  a.k_count = k_count;
+  a.tiles_per_sweep = L.tiles_per_sweep;
+  a.ntiles = L.ntiles;
+  a.U = reinterpret_cast<const double2*>(U);
+  a.psi0 = reinterpret_cast<const double2*>(psi0);
+  a.states = reinterpret_cast<double2*>(states);
+  a.spin = spin;
+  a.ticket = reinterpret_cast<unsigned long long*>(w);
+  a.flags = reinterpret_cast<int*>(w + L.off_flags);
+  a.agg = reinterpret_cast<double2*>(w + L.off_agg);
+  a.psi_end = reinterpret_cast<double2*>(w + L.off_psi);
+  cudaError_t e = cudaMemsetAsync(w, 0, L.off_agg, s);   // ticket + flags
+  if (e != cudaSuccess) return e;
+  // one CTA per tile; a CTA's ticket is taken when it starts, so every tile it waits on is running or done
+  scan4_kernel<M><<<(unsigned)L.ntiles, Scan4Cfg<M>::NT, 0, s>>>(a);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+// Path override for tests and measurement tools: SPINSIM_SCAN_PATH = coop | chain | scan2 | scan3 | scan4 forces
+// that kernel (coop and chain only where they apply: coop needs an L2-sized problem); unset = the heuristic below.
+// Read on every call (one getenv per scan launch), so a test can switch paths within one process.
+static int forced_scan_path() {
+  const char* p = std::getenv("SPINSIM_SCAN_PATH");
+  if (!p) return 0;
+  const char* names[] = {"", "coop", "chain", "scan2", "scan3", "scan4"};
+  for (int i = 1; i < 6; ++i)
+    if (!std::strcmp(p, names[i])) return i;
+  return 0;
+}
+
+// Path choice: the cooperative single-wave scan for L2-sized problems; the per-sweep chain for ≥ kChainMinBatch
+// sweeps; otherwise compact SU(2) operators take the register-resident tile scan (scan4), dense ones scan3 where its
+// tiles get ≥ 4 stages (long sweeps, moderate batch) and scan2 for the rest.
+template <class M>
+static cudaError_t run_state_scan(int64_t batch, int64_t k_count, const double* U, const double* psi0, double* states,
+                                  void* ws, cudaStream_t s, int* launches, double* spin) {
+  switch (forced_scan_path()) {
+    case 1: {
+      const cudaError_t e = run_scan_coop<M>(batch, k_count, U, psi0, states, spin, ws, s, launches);
+      if (e != cudaErrorNotSupported) return e;
+      break;
+    }
+    case 2: return run_chain<M>(batch, k_count, U, psi0, states, spin, s, launches);
+    case 3: return run_scan2<M>(batch, k_count, U, psi0, states, spin, ws, s, launches);
+    case 4: return run_scan3<M>(batch, k_count, U, psi0, states, spin, ws, s, launches);
+    case 5: return run_scan4<M>(batch, k_count, U, psi0, states, spin, ws, s, launches);
+  }
+  const cudaError_t e = run_scan_coop<M>(batch, k_count, U, psi0, states, spin, ws, s, launches);
+  if (e != cudaErrorNotSupported) return e;
+  if (batch >= kChainMinBatch) return run_chain<M>(batch, k_count, U, psi0, states, spin, s, launches);
+  if (M::W == 2) return run_scan4<M>(batch, k_count, U, psi0, states, spin, ws, s, launches);
+  // scan3 amortises its look-back over big tiles; below ~4 stages per tile (small problems) scan2's single pass wins
+  if (scan3_nst<M>(batch, k_count, scan3_grid<M>()) >= 4)
+    return run_scan3<M>(batch, k_count, U, psi0, states, spin, ws, s, launches);
+  return run_scan2<M>(batch, k_count, U, psi0, states, spin, ws, s, launches);
+}
 
 cudaError_t launch_scan(int dim, int64_t batch, int64_t k_count, const double* U, const double* psi0, double* states,
-                        void* ws, cudaStream_t s, int* launches, double* spin) {
-  {
-    const cudaError_t e = dim == 2 ? run_scan_coop<2>(batch, k_count, U, psi0, states, spin, ws, s, launches)
-                                   : run_scan_coop<3>(batch, k_count, U, psi0, states, spin, ws, s, launches);
-    if (e != cudaErrorNotSupported) return e;
-  }
-  // scan3 amortises its look-back over big tiles; below ~4 stages per tile (small problems) scan2's single pass wins
-  if (SS_SCAN_VERSION == 3 && batch < kChainMinBatch &&
-      (dim == 2 ? scan3_nst<2>(batch, k_count, scan3_grid<2>()) : scan3_nst<3>(batch, k_count, scan3_grid<3>())) >= 4)
-    return dim == 2 ? run_scan3<2>(batch, k_count, U, psi0, states, spin, ws, s, launches)
-                    : run_scan3<3>(batch, k_count, U, psi0, states, spin, ws, s, launches);
-  if (batch >= kChainMinBatch)   // enough sweeps to saturate HBM with one sequential chain per thread
-    return dim == 2 ? run_chain<2>(batch, k_count, U, psi0, states, spin, s, launches)
-                    : run_chain<3>(batch, k_count, U, psi0, states, spin, s, launches);
-  return dim == 2 ? run_scan2<2>(batch, k_count, U, psi0, states, spin, ws, s, launches)
-                  : run_scan2<3>(batch, k_count, U, psi0, states, spin, ws, s, launches);
+                        void* ws, cudaStream_t s, int* launches, double* spin, int op_format) {
+  if (op_format == OP_SU2)
+    return dim == 2 ? run_state_scan<SU<2>>(batch, k_count, U, psi0, states, ws, s, launches, spin)
+                    : run_state_scan<SU<3>>(batch, k_count, U, psi0, states, ws, s, launches, spin);
+  return dim == 2 ? run_state_scan<CM<2>>(batch, k_count, U, psi0, states, ws, s, launches, spin)
+                  : run_state_scan<CM<3>>(batch, k_count, U, psi0, states, ws, s, launches, spin);
 }
 
 cudaError_t launch_aggregate(int dim, int64_t batch, int64_t k_count, const double* U, double* aggregate, void* ws,
                              cudaStream_t s, int* launches) {
-  return dim == 2 ? run_scan<2, false>(batch, k_count, U, nullptr, nullptr, aggregate, ws, s, launches)
-                  : run_scan<3, false>(batch, k_count, U, nullptr, nullptr, aggregate, ws, s, launches);
+  return dim == 2 ? run_aggregate<2>(batch, k_count, U, aggregate, ws, s, launches)
+                  : run_aggregate<3>(batch, k_count, U, aggregate, ws, s, launches);
 }
 
 cudaError_t launch_compose_carry(int dim, int64_t batch, int part, const double* aggs, const double* psi0,

@@ -44,6 +44,11 @@ constexpr double kRsqrt2 = 0x1.6a09e667f3bcdp-1;   // 1/√2
 constexpr double kSqrt2 = 0x1.6a09e667f3bcdp+0;
 constexpr double kThird = 0x1.5555555555555p-2;
 
+// Format of the interval operators handed from the interval kernel to the state scan: the dense dim×dim complex
+// matrix (the public U_k layout), or — for the SU(2)-form paths when U_k is not an output — the SU(2) element (a, b)
+// of U = [[a, b], [−b*, a*]] (2 complex128 per interval; D¹ of it for the analytic spin-one path, reading R14).
+enum { OP_DENSE = 0, OP_SU2 = 1 };
+
 template <int SPIN> struct SpinDim { static constexpr int D = (SPIN == SPIN_HALF) ? 2 : 3; };
 template <int F> struct FieldParams;
 template <> struct FieldParams<FIELD_CONSTANT> { static constexpr int P = 4; };
@@ -524,46 +529,6 @@ template <typename T> struct Sym3 {   // unique entries of a complex symmetric 3
   T r00, i00, r01, i01, r02, i02, r11, i11, r12, i12, r22, i22;
 };
 
-// s = (a + 2I)a for symmetric a (so s is symmetric):
-//   s00 = (a00+2)a00 + a01² + a02²   s01 = a01(a00 + a11 + 2) + a02 a12   s02 = a02(a00 + a22 + 2) + a01 a12
-//   s11 = (a11+2)a11 + a01² + a12²   s12 = a12(a11 + a22 + 2) + a01 a02   s22 = (a22+2)a22 + a02² + a12²
-template <typename T> __device__ __forceinline__ void sym_square(Sym3<T>& a) {
-  // complex squares of the off-diagonal entries
-  const T q01r = fmaT(a.r01, a.r01, -a.i01 * a.i01), q01i = fmaT(a.r01, a.i01, a.r01 * a.i01);
-  const T q02r = fmaT(a.r02, a.r02, -a.i02 * a.i02), q02i = fmaT(a.r02, a.i02, a.r02 * a.i02);
-  const T q12r = fmaT(a.r12, a.r12, -a.i12 * a.i12), q12i = fmaT(a.r12, a.i12, a.r12 * a.i12);
-  const T two = splat<T>(2.0);
-  const T d0 = a.r00 + two, d1 = a.r11 + two, d2 = a.r22 + two;
-  Sym3<T> s;
-  // diagonal
-  s.r00 = fmaT(d0, a.r00, fmaT(-a.i00, a.i00, q01r + q02r));
-  s.i00 = fmaT(d0, a.i00, fmaT(a.i00, a.r00, q01i + q02i));
-  s.r11 = fmaT(d1, a.r11, fmaT(-a.i11, a.i11, q01r + q12r));
-  s.i11 = fmaT(d1, a.i11, fmaT(a.i11, a.r11, q01i + q12i));
-  s.r22 = fmaT(d2, a.r22, fmaT(-a.i22, a.i22, q02r + q12r));
-  s.i22 = fmaT(d2, a.i22, fmaT(a.i22, a.r22, q02i + q12i));
-  // off-diagonal: x·c + y·w with c = a_ii + a_jj + 2
-  {
-    const T cr = d0 + a.r11, ci = a.i00 + a.i11;
-    const T pr = fmaT(a.r02, a.r12, -a.i02 * a.i12), pi = fmaT(a.r02, a.i12, a.i02 * a.r12);
-    s.r01 = fmaT(a.r01, cr, fmaT(-a.i01, ci, pr));
-    s.i01 = fmaT(a.r01, ci, fmaT(a.i01, cr, pi));
-  }
-  {
-    const T cr = d0 + a.r22, ci = a.i00 + a.i22;
-    const T pr = fmaT(a.r01, a.r12, -a.i01 * a.i12), pi = fmaT(a.r01, a.i12, a.i01 * a.r12);
-    s.r02 = fmaT(a.r02, cr, fmaT(-a.i02, ci, pr));
-    s.i02 = fmaT(a.r02, ci, fmaT(a.i02, cr, pi));
-  }
-  {
-    const T cr = d1 + a.r22, ci = a.i11 + a.i22;
-    const T pr = fmaT(a.r01, a.r02, -a.i01 * a.i02), pi = fmaT(a.r01, a.i02, a.i01 * a.r02);
-    s.r12 = fmaT(a.r12, cr, fmaT(-a.i12, ci, pr));
-    s.i12 = fmaT(a.r12, ci, fmaT(a.i12, cr, pi));
-  }
-  a = s;
-}
-
 // Below this bound on the entries of A = H/n (Σ|a_j|/n), the leapfrog factor's residual equals its second-order
 // Taylor polynomial to within rounding: a palindromic product of exponentials is exp(−iA + O(A³)) (symmetric
 // splitting), so T − I = −iA − A²/2 + O(A³), and the dropped terms are ≤ |A|²/6 ≈ 2^-56 (FP64) / 2^-26 (FP32)
@@ -573,35 +538,13 @@ template <typename T> __device__ __forceinline__ T taylor_bound();
 template <> __device__ __forceinline__ double taylor_bound<double>() { return 7.450580596923828e-09; }   // 2^-27
 template <> __device__ __forceinline__ float taylor_bound<float>() { return 2.44140625e-04f; }           // 2^-12
 
-// The same squaring in double-angle form.  T₀ is complex symmetric AND unitary, so with T₀ = X + iY (X, Y real
-// symmetric) unitarity T₀T₀* = I reads X² + Y² = I and XY = YX; every power keeps both properties.  Then
-//   T₀² = X² − Y² + 2iXY = (I − 2Y²) + 2i XY,
-// i.e. for the residual a = x + iy (x = X − I, y = Y):  x' = −2y²,  y' = 2y + 2xy  — the double-angle formulas
-// cos 2Θ = 1 − 2 sin²Θ, sin 2Θ = 2 sin Θ cos Θ of T₀ = e^{iΘ}.  Exactly the residual squaring s = (a + 2I)a of
-// P:456-462 for a unitary symmetric T₀ (the dropped term x² + 2x + y² is T₀'s unitarity defect, zero up to rounding):
-// two real symmetric products instead of a complex one, 48 FP64 instructions instead of 63 (DESIGN.md §5 item 13).
-template <typename T> __device__ __forceinline__ void sym_square_u(Sym3<T>& a) {
-  const T m2 = splat<T>(-2.0), p2 = splat<T>(2.0);
-  // w = −2y, u = 2x
-  const T w00 = m2 * a.i00, w01 = m2 * a.i01, w02 = m2 * a.i02, w11 = m2 * a.i11, w12 = m2 * a.i12, w22 = m2 * a.i22;
-  const T u00 = p2 * a.r00, u01 = p2 * a.r01, u02 = p2 * a.r02, u11 = p2 * a.r11, u12 = p2 * a.r12, u22 = p2 * a.r22;
-  const T y00 = a.i00, y01 = a.i01, y02 = a.i02, y11 = a.i11, y12 = a.i12, y22 = a.i22;
-  // x' = w·y (symmetric: w and y commute up to rounding)
-  a.r00 = fmaT(w00, y00, fmaT(w01, y01, w02 * y02));
-  a.r01 = fmaT(w00, y01, fmaT(w01, y11, w02 * y12));
-  a.r02 = fmaT(w00, y02, fmaT(w01, y12, w02 * y22));
-  a.r11 = fmaT(w01, y01, fmaT(w11, y11, w12 * y12));
-  a.r12 = fmaT(w01, y02, fmaT(w11, y12, w12 * y22));
-  a.r22 = fmaT(w02, y02, fmaT(w12, y12, w22 * y22));
-  // y' = 2y + u·y = u·y − w
-  a.i00 = fmaT(u00, y00, fmaT(u01, y01, fmaT(u02, y02, -w00)));
-  a.i01 = fmaT(u00, y01, fmaT(u01, y11, fmaT(u02, y12, -w01)));
-  a.i02 = fmaT(u00, y02, fmaT(u01, y12, fmaT(u02, y22, -w02)));
-  a.i11 = fmaT(u01, y01, fmaT(u11, y11, fmaT(u12, y12, -w11)));
-  a.i12 = fmaT(u01, y02, fmaT(u11, y12, fmaT(u12, y22, -w12)));
-  a.i22 = fmaT(u02, y02, fmaT(u12, y12, fmaT(u22, y22, -w22)));
-}
-
+// The residual squaring s = (a + 2I)a of P:456-462 in double-angle form.  T₀ is complex symmetric AND unitary, so
+// with T₀ = X + iY (X, Y real symmetric) unitarity T₀T₀* = I reads X² + Y² = I and XY = YX; every power keeps both
+// properties.  Then T₀² = X² − Y² + 2iXY = (I − 2Y²) + 2i XY, i.e. for the residual a = x + iy (x = X − I, y = Y):
+// x' = −2y², y' = 2y + 2xy — the double-angle formulas cos 2Θ = 1 − 2 sin²Θ, sin 2Θ = 2 sin Θ cos Θ of T₀ = e^{iΘ}.
+// Exactly (a + 2I)a for a unitary symmetric T₀ (the dropped term x² + 2x + y² is T₀'s unitarity defect, zero up to
+// rounding): two real symmetric products instead of a complex one (DESIGN.md §5 item 13; the complex form took 63 FP64
+// instructions, the unscaled double-angle one 48).
 // Scaled double-angle form: carrying x̃ = 2x and ỹ = −2y (exact rescalings by powers of two) the doubling becomes
 //   x̃' = −ỹ²,  ỹ' = (x̃ + 2I)·ỹ
 // (x̃' = 2x' = −4y² = −ỹ²;  ỹ' = −2y' = −4y − 4xy = (2x + 2I)(−2y)) — two symmetric products and a diagonal shift:
@@ -627,15 +570,8 @@ template <typename T> __device__ __forceinline__ void sym_square_s(Sym3<T>& a) {
   a.i22 = fmaT(x02, y02, fmaT(x12, y12, d2 * y22));
 }
 
-#ifndef SS_SQUARE_FORM
-#define SS_SQUARE_FORM 2    // 0: complex form (sym_square); 1: double-angle (sym_square_u); 2: scaled double-angle
-#endif
-constexpr bool kLtScaled = SS_SQUARE_FORM == 2;   // Sym3 between trotter_init and trotter_expand holds (2x, −2y)
-template <typename T> __device__ __forceinline__ void lt_square(Sym3<T>& a) {
-  if constexpr (SS_SQUARE_FORM == 2) sym_square_s<T>(a);
-  else if constexpr (SS_SQUARE_FORM == 1) sym_square_u<T>(a);
-  else sym_square<T>(a);
-}
+// The Sym3 between trotter_init and trotter_expand holds the scaled pair (x̃, ỹ) = (2x, −2y).
+template <typename T> __device__ __forceinline__ void lt_square(Sym3<T>& a) { sym_square_s<T>(a); }
 
 // Two FP32 symmetric residuals packed one per float2 lane (FP32 mode squares both exponentials of a CF4 step in
 // lockstep with packed FFMA2).
@@ -677,23 +613,14 @@ __device__ __forceinline__ void trotter_init(const T a[4], int tau, Sym3<T>& m, 
     // x = Φ/√2 on (0,1), (1,2).  A₀² = [[d0² + x², x(d0 + d1), x²], [·, d1² + 2x², x(d1 + d2)], [·, ·, d2² + x²]].
     const T d0 = z + q * T(kThird), d1 = T(-2) * q * T(kThird), d2 = q * T(kThird) - z;
     const T x = Phi * T(kRsqrt2), x2 = x * x;
-    if constexpr (kLtScaled) {     // (2x, −2y) = (−A₀², 2A₀)
-      const T x_2 = x + x;
-      m.r00 = -fmaT(d0, d0, x2);          m.i00 = d0 + d0;
-      m.r11 = -fmaT(d1, d1, x2 + x2);     m.i11 = d1 + d1;
-      m.r22 = -fmaT(d2, d2, x2);          m.i22 = d2 + d2;
-      m.r01 = -(x * (d0 + d1));           m.i01 = x_2;
-      m.r12 = -(x * (d1 + d2));           m.i12 = x_2;
-      m.r02 = -x2;                        m.i02 = T(0);
-      return;
-    }
-    const T mh = T(-0.5);
-    m.r00 = mh * fmaT(d0, d0, x2);        m.i00 = -d0;
-    m.r11 = mh * fmaT(d1, d1, x2 + x2);   m.i11 = -d1;
-    m.r22 = mh * fmaT(d2, d2, x2);        m.i22 = -d2;
-    m.r01 = mh * x * (d0 + d1);           m.i01 = -x;
-    m.r12 = mh * x * (d1 + d2);           m.i12 = -x;
-    m.r02 = mh * x2;                      m.i02 = T(0);
+    // scaled pair (2x, −2y) = (−A₀², 2A₀)
+    const T x_2 = x + x;
+    m.r00 = -fmaT(d0, d0, x2);          m.i00 = d0 + d0;
+    m.r11 = -fmaT(d1, d1, x2 + x2);     m.i11 = d1 + d1;
+    m.r22 = -fmaT(d2, d2, x2);          m.i22 = d2 + d2;
+    m.r01 = -(x * (d0 + d1));           m.i01 = x_2;
+    m.r12 = -(x * (d1 + d2));           m.i12 = x_2;
+    m.r02 = -x2;                        m.i02 = T(0);
     return;
   }
   const T th1 = z + q * T(kThird), th2 = T(2) * q * T(kThird), th3 = z - q * T(kThird);
@@ -733,7 +660,7 @@ __device__ __forceinline__ void trotter_init(const T a[4], int tau, Sym3<T>& m, 
     m.r11 = v2 - T(2) * ss * (T(1) + v2);      m.i11 = sin2 - T(2) * ss * sin2;    // expm1(iθ2) − 2s² e^{iθ2}
     m.r22 = v3 - ss * (T(1) + v3);             m.i22 = sin3 - ss * sin3;           // expm1(iθ3) − s² e^{iθ3}
   }
-  if constexpr (kLtScaled) {
+  {                                                   // to the scaled pair (2x, −2y)
     const T p2 = T(2), m2 = T(-2);
     m.r00 *= p2; m.r01 *= p2; m.r02 *= p2; m.r11 *= p2; m.r12 *= p2; m.r22 *= p2;
     m.i00 *= m2; m.i01 *= m2; m.i02 *= m2; m.i11 *= m2; m.i12 *= m2; m.i22 *= m2;
@@ -744,7 +671,7 @@ __device__ __forceinline__ void trotter_init(const T a[4], int tau, Sym3<T>& m, 
 template <typename T>
 __device__ __forceinline__ void trotter_expand(const Sym3<T>& m0, T cphi, T sphi, Res<3, T>& e) {
   Sym3<T> m = m0;
-  if constexpr (kLtScaled) {     // back from (2x, −2y): the ½ folds into the phase factors, the diagonal costs 6 DMUL
+  {                              // back from (2x, −2y): the ½ folds into the phase factors, the diagonal costs 6 DMUL
     const T h = T(0.5), mh = T(-0.5);
     m.r00 = h * m0.r00; m.r11 = h * m0.r11; m.r22 = h * m0.r22;
     m.i00 = mh * m0.i00; m.i11 = mh * m0.i11; m.i22 = mh * m0.i22;
@@ -752,8 +679,8 @@ __device__ __forceinline__ void trotter_expand(const Sym3<T>& m0, T cphi, T sphi
     cphi = h * cphi;
     sphi = h * sphi;
   }
-  const T c2phi = (kLtScaled ? T(2) : T(1)) * (cphi * cphi - sphi * sphi);
-  const T s2phi = (kLtScaled ? T(4) : T(2)) * cphi * sphi;
+  const T c2phi = T(2) * (cphi * cphi - sphi * sphi);
+  const T s2phi = T(4) * cphi * sphi;
   e.re[0] = m.r00;  e.im[0] = m.i00;
   e.re[4] = m.r11;  e.im[4] = m.i11;
   e.re[8] = m.r22;  e.im[8] = m.i22;

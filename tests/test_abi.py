@@ -56,7 +56,7 @@ def test_library_is_sm100a_only(lib):
 
 
 def test_version_and_params(lib):
-    assert lib.ss_version() == 101
+    assert lib.ss_version() == 102
     from paper_2204_05586_b200 import num_sweep_params
     assert [num_sweep_params(f) for f in ("constant", "rabi_linear", "rabi_circular", "neural", "gradient",
                                           "su3_constant", "su3_drive")] == [4, 2, 2, 7, 2, 8, 6]
