@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -192,6 +193,9 @@ ssb::IntervalParams make_params(const ss_sim* s, double t0, double dt_out, doubl
   p.k_count = k_count;
   p.batch = batch;
   p.n_threads = batch * k_count;
+  p.k_stride = k_count;
+  p.ipt = 1;
+  p.run_agg = nullptr;
   p.tau = s->d.trotter_cutoff;
   p.frame = s->d.use_rotating_frame;
   p.split = choose_split(s, n_total, L);
@@ -223,6 +227,75 @@ int launch_interval_checked(ss_sim* s, const ssb::IntervalParams& p, cudaStream_
   if (e != cudaSuccess) return cuda_fail(e, "interval kernel launch");
   g_launches.fetch_add(1);
   return SS_OK;
+}
+
+// Fused run aggregates (DESIGN.md §5 item 16): for long problems (S = 1, ≥ 16 waves of interval threads even at 4
+// intervals per thread) each interval-kernel thread computes ipt consecutive intervals and multiplies their U_k into
+// a run aggregate; a coarse scan over the aggregates gives every run's start state and one chain lane per run
+// writes the states — U_k is read once, by a plain streaming pass, instead of through a look-back tile scan.  ipt is
+// the largest of 32, 16, 8, 4 that divides K, fits the operator type (ssb::fused_max_ipt: a warp's 32 runs in shared
+// memory) and keeps ≥ 16 waves.  Below the chain kernel's batch size only (it streams U once
+// already); the workspace holds ≤ ⌈K/4⌉ run aggregates + ⌈K/4⌉ + 1 run states per sweep.
+// SPINSIM_FUSED=0 turns it off, SPINSIM_FUSED_IPT=n forces ipt (comparison runs; read on every call).
+constexpr int64_t kFusedMinIpt = 4;
+constexpr double kFusedMinWaves = 16.0;
+bool fused_batch(int64_t batch) { return batch < ssb::chain_min_batch(); }
+size_t fused_bytes(int dim, int64_t batch, int64_t K) {
+  if (!fused_batch(batch)) return 0;
+  const size_t nseg = (size_t)((K + kFusedMinIpt - 1) / kFusedMinIpt);
+  return align256(sizeof(double) * 2 * dim * dim * (size_t)batch * nseg) +
+         align256(sizeof(double) * 2 * dim * (size_t)batch * (nseg + 1));
+}
+// ipt of the fused path for this launch, 0 = unfused
+int64_t fused_ipt(const ss_sim* s, int64_t batch, int64_t K, int S, int op_format) {
+  const char* env = std::getenv("SPINSIM_FUSED");
+  if ((env && env[0] == '0') || !fused_batch(batch) || S != 1) return 0;
+  const int64_t max_ipt = ssb::fused_max_ipt(s->dim, op_format);
+  const char* fi = std::getenv("SPINSIM_FUSED_IPT");
+  if (fi) {
+    const int64_t v = std::atoll(fi);
+    return (v >= kFusedMinIpt && v <= max_ipt && (v & (v - 1)) == 0 && K % v == 0 && K >= 2 * v) ? v : 0;
+  }
+  const double R = resident_threads(s);
+  for (int64_t ipt = max_ipt; ipt >= kFusedMinIpt; ipt /= 2)
+    if (K % ipt == 0 && (double)batch * (double)(K / ipt) >= kFusedMinWaves * R) return ipt;
+  return 0;
+}
+// Sets up the interval launch for the fused path: one thread slot per ipt intervals, run aggregates at `agg`.
+void enable_fused(ssb::IntervalParams& p, int64_t ipt, double* agg) {
+  p.ipt = ipt;
+  p.k_stride = (p.k_count + ipt - 1) / ipt;
+  p.n_threads = p.batch * p.k_stride;
+  p.run_agg = agg;
+}
+// Where the fused path's run aggregates and run states live inside the ss_evaluate workspace region `fw`.
+double* fused_phi(char* fw, int dim, int64_t batch, int64_t K) {
+  return reinterpret_cast<double*>(
+      fw + align256(sizeof(double) * 2 * dim * dim * (size_t)batch * (size_t)((K + kFusedMinIpt - 1) / kFusedMinIpt)));
+}
+
+// Interval kernel for p, then the state propagation from d_psi0 into d_states (row a9): fused (run aggregates +
+// coarse scan + run chain) where fused_ipt allows it and the caller has a fused region `fused_ws`, else the state-scan
+// heuristic in scan_ws.  The scan runs on `scan_st`; when that is not `cs`, `stepped` orders it after the interval
+// kernel.  `split_event` (profiling) is recorded between the two.
+int launch_path(ss_sim* s, ssb::IntervalParams& p, const double* d_psi0, double* d_states, void* scan_ws,
+                char* fused_ws, cudaStream_t cs, cudaStream_t scan_st, cudaEvent_t stepped) {
+  const int64_t ipt = fused_ws ? fused_ipt(s, p.batch, p.k_count, p.split, p.op_format) : 0;
+  if (ipt) enable_fused(p, ipt, reinterpret_cast<double*>(fused_ws));
+  int rc = launch_interval_checked(s, p, cs);
+  if (rc) return rc;
+  cudaError_t e;
+  if (s->split_event && (e = cudaEventRecord(s->split_event, cs)) != cudaSuccess) return cuda_fail(e, "split event record");
+  if (scan_st != cs && ((e = cudaEventRecord(stepped, cs)) || (e = cudaStreamWaitEvent(scan_st, stepped, 0))))
+    return cuda_fail(e, "event record/wait");
+  int n = 0;
+  e = ipt ? ssb::launch_fused_scan(s->dim, p.batch, p.k_count, ipt, p.unitaries, p.run_agg, d_psi0,
+                                   fused_phi(fused_ws, s->dim, p.batch, p.k_count), d_states, scan_ws, scan_st, &n,
+                                   nullptr, p.op_format)
+          : ssb::launch_scan(s->dim, p.batch, p.k_count, p.unitaries, d_psi0, d_states, scan_ws, scan_st, &n, nullptr,
+                             p.op_format);
+  g_launches.fetch_add(n);
+  return e == cudaSuccess ? SS_OK : cuda_fail(e, "scan launch");
 }
 
 }  // namespace
@@ -362,10 +435,11 @@ size_t ss_aggregate_workspace_bytes(int32_t dim, int64_t batch, int64_t k_count)
   return ssb::aggregate_workspace_bytes(dim, batch, k_count);
 }
 
-// Layout: [0, 256) control (validation flag) | scan workspace | U (optional).
+// Layout: [0, 256) control (validation flag) | scan workspace | fused-path run aggregates + run states (batches below
+// the chain kernel's) | U (optional).
 size_t ss_workspace_bytes(const ss_sim* s, int64_t batch, int64_t K, int32_t unitaries_in_workspace) {
   if (!s || batch < 0 || K < 0) return 0;
-  size_t n = 256 + align256(ssb::scan_workspace_bytes(s->dim, batch, K));
+  size_t n = 256 + align256(ssb::scan_workspace_bytes(s->dim, batch, K)) + fused_bytes(s->dim, batch, K);
   if (unitaries_in_workspace) n += align256(sizeof(double) * 2 * s->dim * s->dim * (size_t)batch * (size_t)K);
   return n;
 }
@@ -515,20 +589,15 @@ int ss_evaluate(ss_sim* s, double t0, double t1, double dt_int, double dt_out, i
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   char* w = static_cast<char*>(d_ws);
   void* scan_ws = w + 256;
-  double* U = d_U ? d_U : reinterpret_cast<double*>(w + 256 + align256(ssb::scan_workspace_bytes(s->dim, batch, K)));
+  double* U = d_U ? d_U
+                  : reinterpret_cast<double*>(w + 256 + align256(ssb::scan_workspace_bytes(s->dim, batch, K)) +
+                                              fused_bytes(s->dim, batch, K));
   if (s->validate && (rc = validate_inputs(s, batch, d_sweep, d_psi0, reinterpret_cast<int*>(w), st))) return rc;
   auto p = make_params(s, t0, dt_out, dt, L, 0, K, batch, d_sweep, U, batch * K);
   // U_k only feeds the scan: SU(2)-form paths pass it compact (the workspace is sized for the dense layout)
   if (!d_U && su2_form(s)) p.op_format = ssb::OP_SU2;
-  if ((rc = launch_interval_checked(s, p, st))) return rc;
-  if (s->split_event) {
-    const cudaError_t e = cudaEventRecord(s->split_event, st);
-    if (e != cudaSuccess) return cuda_fail(e, "split event record");
-  }
-  int n = 0;
-  const cudaError_t e = ssb::launch_scan(s->dim, batch, K, U, d_psi0, d_states, scan_ws, st, &n, nullptr, p.op_format);
-  g_launches.fetch_add(n);
-  return e == cudaSuccess ? SS_OK : cuda_fail(e, "scan launch");
+  char* fw = w + 256 + align256(ssb::scan_workspace_bytes(s->dim, batch, K));   // fused region
+  return launch_path(s, p, d_psi0, d_states, scan_ws, fused_batch(batch) ? fw : nullptr, st, st, nullptr);
 }
 
 int ss_exponentiate(const ss_sim* s, int64_t n, const double* d_args, double* d_out, void* stream) {
@@ -720,9 +789,10 @@ int ss_evaluate_host(ss_sim* s, double t0, double t1, double dt_int, double dt_o
     const size_t states_b = align256(sizeof(double) * 2 * D * (size_t)batch * (kc_max + 1));
     const size_t U_b = align256(sizeof(double) * 2 * D * D * (size_t)batch * kc_max);
     const size_t scan_b = align256(ssb::scan_workspace_bytes(D, batch, kc_max));
+    const size_t fused_b = fused_bytes(D, batch, kc_max);
     if ((e = ensure(s->aux, sweep_b + carry_b)) != cudaSuccess) return cuda_fail(e, "cudaMalloc (host-API staging)");
     for (int k = 0; k < ss_sim::kSlots; ++k)
-      if ((e = ensure(s->slots[k], states_b + U_b + scan_b)) != cudaSuccess)
+      if ((e = ensure(s->slots[k], states_b + U_b + scan_b + fused_b)) != cudaSuccess)
         return cuda_fail(e, "cudaMalloc (host-API staging)");
     double* d_sweep = static_cast<double*>(s->aux.buf);
     double* d_carry = reinterpret_cast<double*>(static_cast<char*>(s->aux.buf) + sweep_b);
@@ -744,14 +814,9 @@ int ss_evaluate_host(ss_sim* s, double t0, double t1, double dt_int, double dt_o
         return cuda_fail(e, "event wait");
       auto p = make_params(s, t0, dt_out, dt, L, (int64_t)k0, kc, batch, d_sweep, d_U, batch * K);
       if (!h_U && su2_form(s)) p.op_format = ssb::OP_SU2;
-      if ((rc = launch_interval_checked(s, p, cs))) return rc;
-      if (ss != cs && ((e = cudaEventRecord(s->stepped[k], cs)) || (e = cudaStreamWaitEvent(ss, s->stepped[k], 0))))
-        return cuda_fail(e, "event record/wait");
-      int n = 0;
-      if ((e = ssb::launch_scan(D, batch, kc, d_U, d_carry, d_states, d_scan, ss, &n, nullptr, p.op_format)) !=
-          cudaSuccess)
-        return cuda_fail(e, "scan launch");
-      g_launches.fetch_add(n);
+      if ((rc = launch_path(s, p, d_carry, d_states, d_scan, fused_b ? base + states_b + U_b + scan_b : nullptr, cs, ss,
+                            s->stepped[k])))
+        return rc;
       // carry ← states[:, kc]
       if ((e = cudaMemcpy2DAsync(d_carry, row, d_states + (size_t)kc * 2 * D, row * (kc + 1), row, batch,
                                  cudaMemcpyDeviceToDevice, ss)))
@@ -780,7 +845,8 @@ int ss_evaluate_host(ss_sim* s, double t0, double t1, double dt_int, double dt_o
   const size_t states_b = align256(sizeof(double) * 2 * D * (size_t)cb_max * (K + 1));
   const size_t U_b = align256(sizeof(double) * 2 * D * D * (size_t)cb_max * K);
   const size_t scan_b = align256(ssb::scan_workspace_bytes(D, cb_max, K));
-  const size_t slot_bytes = sweep_b + psi0_b + states_b + U_b + scan_b;
+  const size_t fused_b = fused_bytes(D, cb_max, K);   // a chunk has ≤ cb_max sweeps: fused_bytes(D, cb, K) ≤ fused_b
+  const size_t slot_bytes = sweep_b + psi0_b + states_b + U_b + scan_b + fused_b;
   const int nslots = n_chunks > 1 ? 2 : 1;
   for (int k = 0; k < nslots; ++k)
     if ((e = ensure(s->slots[k], slot_bytes)) != cudaSuccess) return cuda_fail(e, "cudaMalloc (host-API staging)");
@@ -803,11 +869,10 @@ int ss_evaluate_host(ss_sim* s, double t0, double t1, double dt_int, double dt_o
       return cuda_fail(e, "H2D copy");
     auto p = make_params(s, t0, dt_out, dt, L, 0, K, cb, d_sweep, d_U, batch * K);   // S of the whole batch
     if (!h_U && su2_form(s)) p.op_format = ssb::OP_SU2;
-    if ((rc = launch_interval_checked(s, p, cs))) return rc;
-    int n = 0;
-    if ((e = ssb::launch_scan(D, cb, K, d_U, d_psi0, d_states, d_scan, cs, &n, nullptr, p.op_format)) != cudaSuccess)
-      return cuda_fail(e, "scan launch");
-    g_launches.fetch_add(n);
+    char* d_fused = static_cast<char*>(d_scan) + scan_b;
+    if ((rc = launch_path(s, p, d_psi0, d_states, d_scan, fused_b && fused_batch(cb) ? d_fused : nullptr, cs, cs,
+                          nullptr)))
+      return rc;
     if ((e = cudaEventRecord(s->computed[k], cs)) || (e = cudaStreamWaitEvent(xs, s->computed[k], 0)))
       return cuda_fail(e, "event record/wait");
     if ((e = cudaMemcpyAsync(h_states + b0 * 2 * D * (K + 1), d_states, sizeof(double) * 2 * D * cb * (K + 1),

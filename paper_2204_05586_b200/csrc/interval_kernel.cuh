@@ -11,6 +11,7 @@
 // occupancy with full ILP (18 independent accumulation chains per squaring) rather than for memory.
 #pragma once
 
+#include "ops.cuh"
 #include "spinsim_device.cuh"
 
 namespace ssb {
@@ -25,13 +26,16 @@ struct IntervalParams {
   double wpd, wmd;    // fl(w±·δt): the CF4 weights with δt folded in (read from the parameter bank, no UMOV)
   int64_t L;
   int64_t k_begin, k_count, batch;
-  int64_t n_threads;  // batch·k_count
+  int64_t n_threads;  // batch·k_stride: interval slots of the launch
+  int64_t k_stride;   // thread slots per sweep: k_count, or ⌈k_count/ipt⌉ when run aggregates are written
+  int64_t ipt;        // intervals per thread: 1, or the run length of the fused path (S = 1)
   int32_t tau;
   int32_t frame;
   int32_t split;        // S: lanes per interval (power of two ≤ 32); lane p runs fine steps [p·L/S, (p+1)·L/S)
   int32_t op_format;    // OP_DENSE, or OP_SU2 (SU(2)-form accumulators only): the layout of `unitaries`
   const double* sweep;  // [batch][P]
   double* unitaries;    // [batch][k_count][D][D] complex128 (OP_DENSE) or [batch][k_count][2] complex128 (OP_SU2)
+  double* run_agg;      // NULL, or [batch][k_stride] operators (op_format): the product of each thread's ipt intervals
 };
 
 #ifndef SS_INTERVAL_THREADS
@@ -67,20 +71,18 @@ __device__ __forceinline__ void sample_in_frame(const Field<F>& fld, double off,
   if (frame) to_rotating_frame<NC>(f, off, omega_r);
 }
 
+// Rows a1–a7 for interval k of sweep b: A = U_r − I in the rotating frame at ω_r (residual form, reading R9).  With
+// the sub-interval split (S > 1) the S lanes of an interval each run L/S fine steps and the shuffle tree leaves the
+// whole product in the lane with part = 0 (every lane of the warp must call this; `active` = false lanes idle).
 template <int SPIN, int EXPO, int METHOD, int FIELD, typename T>
-__device__ __forceinline__ void interval_body(const IntervalParams& prm) {
+__device__ __forceinline__ void interval_residual(const IntervalParams& prm, int64_t b, int64_t k, int part,
+                                                  bool active, Res<AccDim<SPIN, EXPO>::D, T>& A_out,
+                                                  double& omega_r_out) {
   constexpr int D = SpinDim<SPIN>::D;
   constexpr int P = FieldParams<FIELD>::P;
   constexpr int NC = NumCoeffs<EXPO>::N;             // 4, or 8 for the general spin-one exponentiator
-  const int64_t gt = (int64_t)blockIdx.x * kIntervalThreads + threadIdx.x;
   const int S = prm.split;
-  const int64_t i = gt / S;                          // interval index (sweep-major)
-  const int part = (int)(gt - i * S);
-  const bool active = i < prm.n_threads;
-  if (S == 1 && !active) return;                     // with S > 1 every lane must reach the shuffles below
-  const int64_t ic = active ? i : 0;
-  const int64_t b = ic / prm.k_count;
-  const int64_t k = prm.k_begin + (ic - b * prm.k_count);
+  (void)D;
 
   double p[P];
 #pragma unroll
@@ -249,23 +251,14 @@ __device__ __forceinline__ void interval_body(const IntervalParams& prm) {
         A = C;
       }
     }
-    if (part != 0 || !active) return;
   }
+  A_out = A;
+  omega_r_out = omega_r;
+}
 
-  // a8: U_k = R_{ω_r}(−Δt)(I + A) = diag(e^{−iω_r m Δt})(I + A); written as complex128.
-  if constexpr (DA == 2) {
-    if (prm.op_format == OP_SU2) {
-      // compact: the SU(2) element (a, b) = e^{−iω_rΔt/2}·(1 + δa, b) — R(−Δt) is diag(p, p*) with p = e^{−iω_rΔt/2}
-      // in SU(2), and D¹ of it for the analytic spin-one path (diag(p², 1, p*²), the phases below)
-      double s, c;
-      sincos(0.5 * omega_r * prm.dt_out, &s, &c);
-      const double ar = 1.0 + (double)A.ar, ai = (double)A.ai, br = (double)A.br, bi = (double)A.bi;
-      double2* o2 = reinterpret_cast<double2*>(prm.unitaries) + i * 2;
-      o2[0] = make_double2(c * ar + s * ai, c * ai - s * ar);     // (c − is)(ar + i ai)
-      o2[1] = make_double2(c * br + s * bi, c * bi - s * br);
-      return;
-    }
-  }
+// a8: U_k = R_{ω_r}(−Δt)(I + A) = diag(e^{−iω_r m Δt})(I + A), as the dense D×D complex matrix ...
+template <int D, int DA, typename T>
+__device__ __forceinline__ void make_op(const Res<DA, T>& A, double omega_r, const IntervalParams& prm, CM<D>& m) {
   double ph_re[D], ph_im[D];
   {
     double s, c;
@@ -277,29 +270,122 @@ __device__ __forceinline__ void interval_body(const IntervalParams& prm) {
   }
   Res<D, T> Ad;                                      // D¹ map of the SU(2) accumulator (analytic spin-one)
   acc_to_dim<T>(A, Ad);
-  double2* out = reinterpret_cast<double2*>(prm.unitaries) + i * (D * D);
 #pragma unroll
   for (int r = 0; r < D; ++r)
 #pragma unroll
     for (int cc = 0; cc < D; ++cc) {
       const double mr = (double)res_re(Ad, r, cc) + (r == cc ? 1.0 : 0.0);
       const double mi = (double)res_im(Ad, r, cc);
-      out[r * D + cc] = make_double2(ph_re[r] * mr - ph_im[r] * mi, ph_re[r] * mi + ph_im[r] * mr);
+      m.re[r * D + cc] = ph_re[r] * mr - ph_im[r] * mi;
+      m.im[r * D + cc] = ph_re[r] * mi + ph_im[r] * mr;
     }
 }
+// ... or (SU(2)-form accumulators) compact: the SU(2) element (a, b) = e^{−iω_rΔt/2}·(1 + δa, b) — R(−Δt) is
+// diag(p, p*) with p = e^{−iω_rΔt/2} in SU(2), and D¹ of it for the analytic spin-one path (diag(p², 1, p*²)).
+template <int D, typename T>
+__device__ __forceinline__ void make_op(const Res<2, T>& A, double omega_r, const IntervalParams& prm, SU<D>& u) {
+  double s, c;
+  sincos(0.5 * omega_r * prm.dt_out, &s, &c);
+  const double ar = 1.0 + (double)A.ar, ai = (double)A.ai, br = (double)A.br, bi = (double)A.bi;
+  u.ar = c * ar + s * ai; u.ai = c * ai - s * ar;     // (c − is)(ar + i ai)
+  u.br = c * br + s * bi; u.bi = c * bi - s * br;
+}
 
-template <int SPIN, int EXPO, int METHOD, int FIELD, typename T>
+// Fused path (DESIGN.md §5 item 16; SURVEY §8(a) a9 "Fusion"): this thread owns the n ≤ ipt consecutive intervals
+// [k_lo, k_lo + n) of sweep b, writes each U_k and folds it into the run product G ← U_k·G (later·earlier),
+// held in shared memory (the kernels sit at their register budget), then writes G to run_agg[slot].
+template <class M, int SPIN, int EXPO, int METHOD, int FIELD, typename T>
+__device__ __forceinline__ void interval_run(const IntervalParams& prm, int64_t b, int64_t k_lo, int64_t n,
+                                             int64_t slot) {
+  extern __shared__ __align__(16) double2 ss_run_smem[];
+  double2* acc = ss_run_smem + threadIdx.x * M::W;
+  {
+    M e;
+    cm_eye(e);
+    cm_store(acc, e);
+  }
+  double2* U = reinterpret_cast<double2*>(prm.unitaries);
+#pragma unroll 1
+  for (int64_t j = 0; j < n; ++j) {
+    Res<AccDim<SPIN, EXPO>::D, T> A;
+    double omega_r;
+    interval_residual<SPIN, EXPO, METHOD, FIELD, T>(prm, b, prm.k_begin + k_lo + j, 0, true, A, omega_r);
+    M op, g;
+    make_op(A, omega_r, prm, op);
+    cm_store(U + (b * prm.k_count + k_lo + j) * M::W, op);
+    cm_load(acc, g);
+    cm_store(acc, cm_mul(op, g));
+  }
+  M g;
+  cm_load(acc, g);
+  cm_store(reinterpret_cast<double2*>(prm.run_agg) + slot * M::W, g);
+}
+
+// FUSED (a separate instance, so the unfused kernel's code is untouched): prm.run_agg is set, S = 1, and thread slot
+// gt of sweep b owns ipt intervals.
+template <int SPIN, int EXPO, int METHOD, int FIELD, typename T, bool FUSED>
+__device__ __forceinline__ void interval_body(const IntervalParams& prm) {
+  constexpr int D = SpinDim<SPIN>::D;
+  constexpr int DA = AccDim<SPIN, EXPO>::D;
+  const int64_t gt = (int64_t)blockIdx.x * kIntervalThreads + threadIdx.x;
+  if constexpr (FUSED) {
+    const int64_t b = gt / prm.k_stride, t = gt - b * prm.k_stride;
+    if (b >= prm.batch) return;
+    const int64_t k_lo = t * prm.ipt, n = min(prm.ipt, prm.k_count - k_lo);
+    if constexpr (DA == 2) {
+      if (prm.op_format == OP_SU2) {
+        interval_run<SU<D>, SPIN, EXPO, METHOD, FIELD, T>(prm, b, k_lo, n, gt);
+        return;
+      }
+    }
+    interval_run<CM<D>, SPIN, EXPO, METHOD, FIELD, T>(prm, b, k_lo, n, gt);
+    return;
+  }
+  const int S = prm.split;
+  const int64_t i = gt / S;                          // interval index (sweep-major)
+  const int part = (int)(gt - i * S);
+  const bool active = i < prm.n_threads;
+  if (S == 1 && !active) return;                     // with S > 1 every lane must reach the shuffles
+  const int64_t ic = active ? i : 0;
+  const int64_t b = ic / prm.k_count;
+  const int64_t k = prm.k_begin + (ic - b * prm.k_count);
+  Res<DA, T> A;
+  double omega_r;
+  interval_residual<SPIN, EXPO, METHOD, FIELD, T>(prm, b, k, part, active, A, omega_r);
+  if (part != 0 || !active) return;
+  if constexpr (DA == 2) {
+    if (prm.op_format == OP_SU2) {
+      SU<D> u;
+      make_op(A, omega_r, prm, u);
+      cm_store(reinterpret_cast<double2*>(prm.unitaries) + i * 2, u);
+      return;
+    }
+  }
+  CM<D> m;
+  make_op(A, omega_r, prm, m);
+  cm_store(reinterpret_cast<double2*>(prm.unitaries) + i * (D * D), m);
+}
+
+template <int SPIN, int EXPO, int METHOD, int FIELD, typename T, bool FUSED>
 __global__ void __launch_bounds__(kIntervalThreads, kIntervalMinBlocks<SPIN, EXPO, T>())
 interval_kernel(const IntervalParams prm) {
-  interval_body<SPIN, EXPO, METHOD, FIELD, T>(prm);
+  interval_body<SPIN, EXPO, METHOD, FIELD, T, FUSED>(prm);
 }
 
 #ifndef __CUDACC_RTC__
+// Dynamic shared memory of an interval launch: the fused path's per-thread run product (≤ 9 complex128).
+inline size_t interval_smem(const IntervalParams& prm) {
+  return prm.run_agg ? (size_t)kIntervalThreads * 9 * 16 : 0;
+}
+
 template <int SPIN, int EXPO, int METHOD, int FIELD, typename T>
 cudaError_t launch_interval(const IntervalParams& prm, cudaStream_t stream) {
   const int64_t blocks = (prm.n_threads * prm.split + kIntervalThreads - 1) / kIntervalThreads;
   if (blocks <= 0) return cudaSuccess;
-  interval_kernel<SPIN, EXPO, METHOD, FIELD, T><<<(unsigned)blocks, kIntervalThreads, 0, stream>>>(prm);
+  if (prm.run_agg)
+    interval_kernel<SPIN, EXPO, METHOD, FIELD, T, true><<<(unsigned)blocks, kIntervalThreads, interval_smem(prm), stream>>>(prm);
+  else
+    interval_kernel<SPIN, EXPO, METHOD, FIELD, T, false><<<(unsigned)blocks, kIntervalThreads, 0, stream>>>(prm);
   return cudaGetLastError();
 }
 #endif  // !__CUDACC_RTC__

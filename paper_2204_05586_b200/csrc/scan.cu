@@ -28,6 +28,7 @@
 #include <cuda.h>
 
 #include "kernels.h"
+#include "ops.cuh"
 
 namespace ssb {
 
@@ -62,186 +63,7 @@ template <int D> constexpr int tile_size() { return kScanThreads * ScanCfg<D>::k
 
 enum { FLAG_EMPTY = 0, FLAG_AGG = 1, FLAG_PREFIX = 2 };
 
-template <int D> struct CM {  // dense complex matrix in registers
-  double re[D * D], im[D * D];
-  static constexpr int SD = D, W = D * D;   // state dimension, double2 per operator in memory
-};
-
-template <int D> __device__ __forceinline__ void cm_eye(CM<D>& m) {
-#pragma unroll
-  for (int e = 0; e < D * D; ++e) { m.re[e] = (e % (D + 1) == 0) ? 1.0 : 0.0; m.im[e] = 0.0; }
-}
-
-// c = a·b
-template <int D> __device__ __forceinline__ CM<D> cm_mul(const CM<D>& a, const CM<D>& b) {
-  CM<D> c;
-#pragma unroll
-  for (int i = 0; i < D; ++i)
-#pragma unroll
-    for (int j = 0; j < D; ++j) {
-      double r = 0.0, m = 0.0;
-#pragma unroll
-      for (int k = 0; k < D; ++k) {
-        r = fma(a.re[i * D + k], b.re[k * D + j], r);
-        r = fma(-a.im[i * D + k], b.im[k * D + j], r);
-        m = fma(a.re[i * D + k], b.im[k * D + j], m);
-        m = fma(a.im[i * D + k], b.re[k * D + j], m);
-      }
-      c.re[i * D + j] = r;
-      c.im[i * D + j] = m;
-    }
-  return c;
-}
-
-// y = a·x
-template <int D> __device__ __forceinline__ void cm_apply(const CM<D>& a, const double xr[D], const double xi[D],
-                                                          double yr[D], double yi[D]) {
-#pragma unroll
-  for (int i = 0; i < D; ++i) {
-    double r = 0.0, m = 0.0;
-#pragma unroll
-    for (int k = 0; k < D; ++k) {
-      r = fma(a.re[i * D + k], xr[k], r);
-      r = fma(-a.im[i * D + k], xi[k], r);
-      m = fma(a.re[i * D + k], xi[k], m);
-      m = fma(a.im[i * D + k], xr[k], m);
-    }
-    yr[i] = r;
-    yi[i] = m;
-  }
-}
-
-template <int D> __device__ __forceinline__ void cm_load(const double2* src, CM<D>& m) {
-#pragma unroll
-  for (int e = 0; e < D * D; ++e) { const double2 v = src[e]; m.re[e] = v.x; m.im[e] = v.y; }
-}
-template <int D> __device__ __forceinline__ void cm_load_cg(const double2* src, CM<D>& m) {
-#pragma unroll
-  for (int e = 0; e < D * D; ++e) { const double2 v = __ldcg(src + e); m.re[e] = v.x; m.im[e] = v.y; }
-}
-template <int D> __device__ __forceinline__ void cm_store(double2* dst, const CM<D>& m) {
-#pragma unroll
-  for (int e = 0; e < D * D; ++e) dst[e] = make_double2(m.re[e], m.im[e]);
-}
-template <int D> __device__ __forceinline__ CM<D> cm_shfl_up(const CM<D>& m, int delta) {
-  CM<D> r;
-#pragma unroll
-  for (int e = 0; e < D * D; ++e) {
-    r.re[e] = __shfl_up_sync(0xffffffffu, m.re[e], delta);
-    r.im[e] = __shfl_up_sync(0xffffffffu, m.im[e], delta);
-  }
-  return r;
-}
-
-template <int D> __device__ __forceinline__ CM<D> cm_shfl_down(const CM<D>& m, int delta) {
-  CM<D> r;
-#pragma unroll
-  for (int e = 0; e < D * D; ++e) {
-    r.re[e] = __shfl_down_sync(0xffffffffu, m.re[e], delta);
-    r.im[e] = __shfl_down_sync(0xffffffffu, m.im[e], delta);
-  }
-  return r;
-}
-template <int D> __device__ __forceinline__ CM<D> cm_shfl_idx(const CM<D>& m, int src) {
-  CM<D> r;
-#pragma unroll
-  for (int e = 0; e < D * D; ++e) {
-    r.re[e] = __shfl_sync(0xffffffffu, m.re[e], src);
-    r.im[e] = __shfl_sync(0xffffffffu, m.im[e], src);
-  }
-  return r;
-}
-
-// ---- compact SU(2) operators -------------------------------------------------------------------------------------
-// U = [[a, b], [−b*, a*]] held as (a, b): every operator of the spin-half path is in SU(2) (DESIGN.md §5 item 10),
-// and the analytic spin-one operator is D¹ of one (reading R14, §5 item 11), so the products of the scan stay in
-// SU(2) exactly (group law) and only the action on a state depends on D: directly for D = 2, through
-// D¹(U) = [[a², √2ab, b²], [−√2ab*, |a|²−|b|², √2a*b], [b*², −√2a*b*, a*²]] for D = 3.
-template <int D> struct SU {
-  double ar, ai, br, bi;
-  static constexpr int SD = D, W = 2;
-};
-template <int D> __device__ __forceinline__ void cm_eye(SU<D>& m) { m.ar = 1.0; m.ai = m.br = m.bi = 0.0; }
-// x·y = (x_a y_a − x_b y_b*, x_a y_b + x_b y_a*)
-template <int D> __device__ __forceinline__ SU<D> cm_mul(const SU<D>& x, const SU<D>& y) {
-  SU<D> c;
-  c.ar = fma(x.ar, y.ar, fma(-x.ai, y.ai, fma(-x.br, y.br, -(x.bi * y.bi))));
-  c.ai = fma(x.ar, y.ai, fma(x.ai, y.ar, fma(-x.bi, y.br, x.br * y.bi)));
-  c.br = fma(x.ar, y.br, fma(-x.ai, y.bi, fma(x.br, y.ar, x.bi * y.ai)));
-  c.bi = fma(x.ar, y.bi, fma(x.ai, y.br, fma(x.bi, y.ar, -(x.br * y.ai))));
-  return c;
-}
-template <int D> __device__ __forceinline__ void cm_apply(const SU<D>& u, const double xr[D], const double xi[D],
-                                                          double yr[D], double yi[D]) {
-  if constexpr (D == 2) {
-    // y0 = a x0 + b x1,  y1 = −b* x0 + a* x1
-    yr[0] = fma(u.ar, xr[0], fma(-u.ai, xi[0], fma(u.br, xr[1], -(u.bi * xi[1]))));
-    yi[0] = fma(u.ar, xi[0], fma(u.ai, xr[0], fma(u.br, xi[1], u.bi * xr[1])));
-    yr[1] = fma(-u.br, xr[0], fma(-u.bi, xi[0], fma(u.ar, xr[1], u.ai * xi[1])));
-    yi[1] = fma(-u.br, xi[0], fma(u.bi, xr[0], fma(u.ar, xi[1], -(u.ai * xr[1]))));
-  } else {
-    // D¹ entries from a, b (the map of the interval kernel's su2_to_spin1, full rather than residual form)
-    const double a2r = u.ar * u.ar - u.ai * u.ai, a2i = 2.0 * u.ar * u.ai;             // a²
-    const double b2r = u.br * u.br - u.bi * u.bi, b2i = 2.0 * u.br * u.bi;             // b²
-    const double abr = kSqrt2 * (u.ar * u.br - u.ai * u.bi), abi = kSqrt2 * (u.ar * u.bi + u.ai * u.br);   // √2ab
-    const double acr = kSqrt2 * (u.ar * u.br + u.ai * u.bi), aci = kSqrt2 * (u.ar * u.bi - u.ai * u.br);   // √2a*b
-    const double dd = (u.ar * u.ar + u.ai * u.ai) - (u.br * u.br + u.bi * u.bi);      // |a|² − |b|²
-    // row 0: a² x0 + √2ab x1 + b² x2
-    yr[0] = fma(a2r, xr[0], fma(-a2i, xi[0], fma(abr, xr[1], fma(-abi, xi[1], fma(b2r, xr[2], -(b2i * xi[2]))))));
-    yi[0] = fma(a2r, xi[0], fma(a2i, xr[0], fma(abr, xi[1], fma(abi, xr[1], fma(b2r, xi[2], b2i * xr[2])))));
-    // row 1: −√2ab* x0 + (|a|²−|b|²) x1 + √2a*b x2, with −√2ab* = −conj(√2a*b)
-    yr[1] = fma(-acr, xr[0], fma(-aci, xi[0], fma(dd, xr[1], fma(acr, xr[2], -(aci * xi[2])))));
-    yi[1] = fma(-acr, xi[0], fma(aci, xr[0], fma(dd, xi[1], fma(acr, xi[2], aci * xr[2]))));
-    // row 2: b*² x0 − √2a*b* x1 + a*² x2, with √2a*b* = conj(√2ab)
-    yr[2] = fma(b2r, xr[0], fma(b2i, xi[0], fma(-abr, xr[1], fma(-abi, xi[1], fma(a2r, xr[2], a2i * xi[2])))));
-    yi[2] = fma(b2r, xi[0], fma(-b2i, xr[0], fma(-abr, xi[1], fma(abi, xr[1], fma(a2r, xi[2], -(a2i * xr[2]))))));
-  }
-}
-template <int D> __device__ __forceinline__ void cm_load(const double2* src, SU<D>& m) {
-  const double2 a = src[0], b = src[1];
-  m.ar = a.x; m.ai = a.y; m.br = b.x; m.bi = b.y;
-}
-template <int D> __device__ __forceinline__ void cm_load_cg(const double2* src, SU<D>& m) {
-  const double2 a = __ldcg(src), b = __ldcg(src + 1);
-  m.ar = a.x; m.ai = a.y; m.br = b.x; m.bi = b.y;
-}
-template <int D> __device__ __forceinline__ void cm_store(double2* dst, const SU<D>& m) {
-  dst[0] = make_double2(m.ar, m.ai);
-  dst[1] = make_double2(m.br, m.bi);
-}
-template <int D> __device__ __forceinline__ SU<D> cm_shfl_up(const SU<D>& m, int delta) {
-  SU<D> r;
-  r.ar = __shfl_up_sync(0xffffffffu, m.ar, delta); r.ai = __shfl_up_sync(0xffffffffu, m.ai, delta);
-  r.br = __shfl_up_sync(0xffffffffu, m.br, delta); r.bi = __shfl_up_sync(0xffffffffu, m.bi, delta);
-  return r;
-}
-template <int D> __device__ __forceinline__ SU<D> cm_shfl_down(const SU<D>& m, int delta) {
-  SU<D> r;
-  r.ar = __shfl_down_sync(0xffffffffu, m.ar, delta); r.ai = __shfl_down_sync(0xffffffffu, m.ai, delta);
-  r.br = __shfl_down_sync(0xffffffffu, m.br, delta); r.bi = __shfl_down_sync(0xffffffffu, m.bi, delta);
-  return r;
-}
-template <int D> __device__ __forceinline__ SU<D> cm_shfl_idx(const SU<D>& m, int src) {
-  SU<D> r;
-  r.ar = __shfl_sync(0xffffffffu, m.ar, src); r.ai = __shfl_sync(0xffffffffu, m.ai, src);
-  r.br = __shfl_sync(0xffffffffu, m.br, src); r.bi = __shfl_sync(0xffffffffu, m.bi, src);
-  return r;
-}
-
-// ⟨J⟩ = (Re ψ†Jxψ, Re ψ†Jyψ, ψ†Jzψ), closed forms of the textbook matrices (reading R5).
-template <int D> __device__ __forceinline__ void spin_of(const double pr[D], const double pi[D], double j[3]) {
-  if (D == 2) {
-    // Jx = σx/2: Re(ψ0*ψ1); Jy = σy/2: Im(ψ0*ψ1); Jz = (|ψ0|² − |ψ1|²)/2
-    j[0] = pr[0] * pr[1] + pi[0] * pi[1];
-    j[1] = pr[0] * pi[1] - pi[0] * pr[1];
-    j[2] = 0.5 * ((pr[0] * pr[0] + pi[0] * pi[0]) - (pr[1] * pr[1] + pi[1] * pi[1]));
-  } else {
-    // Jx = (1/√2)·tridiag(1): √2 Re(ψ0*ψ1 + ψ1*ψ2); Jy: √2 Im(ψ0*ψ1 + ψ1*ψ2); Jz = |ψ0|² − |ψ2|²
-    j[0] = kSqrt2 * (pr[0] * pr[1] + pi[0] * pi[1] + pr[1] * pr[D - 1] + pi[1] * pi[D - 1]);
-    j[1] = kSqrt2 * (pr[0] * pi[1] - pi[0] * pr[1] + pr[1] * pi[D - 1] - pi[1] * pr[D - 1]);
-    j[2] = (pr[0] * pr[0] + pi[0] * pi[0]) - (pr[D - 1] * pr[D - 1] + pi[D - 1] * pi[D - 1]);
-  }
-}
+// Operator types (CM<D>, SU<D>), their products, loads, shuffles and ⟨J⟩: ops.cuh.
 
 // Workspace layouts (all offsets 256-byte aligned): [ticket u64][flags int32 × ntiles][agg op × ntiles]
 // [psi_end dim c128 × ntiles]; the v1 layout below also sizes the per-tile totals of ss_chain_aggregate.
@@ -1470,6 +1292,140 @@ static cudaError_t run_chain(int64_t batch, int64_t k_count, const double* U, co
   return cudaGetLastError();
 }
 
+// ---- run chain of the fused path: one lane per run of SEG intervals, a warp per 32 consecutive runs ----------------
+//
+// The fused path picks SEG | K, so run g of the flat [batch][K] operator array covers operators [g·SEG, (g+1)·SEG)
+// and a warp's 32 runs are ONE contiguous range of 32·SEG operators: the warp copies it into shared memory with
+// coalesced 16-byte cp.async (LDGSTS, all in flight at once, no registers held), each run landing in its own slot at
+// an odd 16-byte pitch (conflict-free per-lane reads).  Every lane then applies its run's operators from its start
+// state phi[b][r] (the coarse scan's), writing state i over the slot's front while the operators sit at its back
+// (state i never reaches an operator not yet read), and the warp streams each run's SEG contiguous states out with
+// coalesced stores.  One-warp CTAs: the shared-memory footprint sets how many are resident per SM, each with its
+// whole range in flight.
+struct RunChainArgs {
+  int64_t batch, k_count, nseg;   // nseg = K / SEG runs per sweep
+  const double2* U;
+  const double2* phi;             // [batch][nseg + 1][D]
+  double2* states;                // [batch][K+1][D] or NULL
+  double* spin;                   // [batch][K+1][3] or NULL
+};
+template <class M> __host__ __device__ constexpr int run_width() { return M::W > M::SD ? M::W : M::SD; }   // double2 per interval slot
+template <class M, int SEG> __host__ __device__ constexpr int run_slot_stride() { return (SEG * run_width<M>()) | 1; }
+template <class M, int SEG> constexpr size_t run_chain_smem() {
+  return sizeof(double2) * 32 * (size_t)run_slot_stride<M, SEG>();
+}
+
+template <class M, int SEG>
+__global__ void __launch_bounds__(32) run_chain_kernel(const RunChainArgs a) {
+  constexpr int D = M::SD, W = M::W, STR = run_slot_stride<M, SEG>();
+  constexpr int OFF = SEG * (run_width<M>() - W);            // operators at the back of the slot
+  extern __shared__ __align__(128) double2 smem_rc[];
+  const int lane = threadIdx.x;
+  const int64_t nruns = a.batch * a.nseg;
+  const int64_t g0 = (int64_t)blockIdx.x * 32;
+  const int nw = (int)min((int64_t)32, nruns - g0);          // runs of this warp
+  const double2* src = a.U + (size_t)g0 * SEG * W;
+  const int nchunks = nw * SEG * W;                          // 16-byte chunks of the warp's range
+#pragma unroll 4
+  for (int c = lane; c < nchunks; c += 32) {
+    const int j = c / (SEG * W), o = c - j * (SEG * W);     // run j of the warp, chunk o of it
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_rc + j * STR + OFF + o)),
+                 "l"(src + c)
+                 : "memory");
+  }
+  asm volatile("cp.async.commit_group;\n cp.async.wait_group 0;" ::: "memory");
+  __syncwarp();
+  const int64_t g = g0 + (lane < nw ? lane : 0), b = g / a.nseg, r = g - b * a.nseg;
+  const size_t row = (size_t)(b * (a.k_count + 1) + r * SEG);   // state index of this run's start
+  double2* slot = smem_rc + lane * STR;
+  if (lane < nw) {
+    double pr[D], pi[D];
+    const double2* start = a.phi + (size_t)(b * (a.nseg + 1) + r) * D;
+#pragma unroll
+    for (int d = 0; d < D; ++d) { const double2 v = start[d]; pr[d] = v.x; pi[d] = v.y; }
+    double* gJ = a.spin ? a.spin + row * 3 : nullptr;
+    if (r == 0) {                                            // ψ_0; a later run's first state is its predecessor's last
+      if (a.states)
+#pragma unroll
+        for (int d = 0; d < D; ++d) __stcs(a.states + row * D + d, make_double2(pr[d], pi[d]));
+      if (gJ) {
+        double j[3];
+        spin_of<D>(pr, pi, j);
+        for (int q = 0; q < 3; ++q) __stcs(gJ + q, j[q]);
+      }
+    }
+#pragma unroll 4
+    for (int i = 0; i < SEG; ++i) {
+      double yr[D], yi[D];
+      M m;
+      cm_load(slot + OFF + i * W, m);
+      cm_apply(m, pr, pi, yr, yi);
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        pr[d] = yr[d]; pi[d] = yi[d];
+        slot[i * D + d] = make_double2(yr[d], yi[d]);
+      }
+      if (gJ) {
+        double j[3];
+        spin_of<D>(pr, pi, j);
+        for (int q = 0; q < 3; ++q) __stcs(gJ + (1 + i) * 3 + q, j[q]);
+      }
+    }
+  }
+  __syncwarp();
+  if (!a.states) return;
+  // run j's states ψ[row_j + 1 .. row_j + SEG] are contiguous: one coalesced pass per run
+  for (int j = 0; j < nw; ++j) {
+    const size_t rj = (size_t)__shfl_sync(0xffffffffu, (long long)row, j);
+    double2* dst = a.states + (rj + 1) * D;
+    const double2* sj = smem_rc + j * STR;
+#pragma unroll
+    for (int c = lane; c < SEG * D; c += 32) __stcs(dst + c, sj[c]);
+  }
+}
+
+template <class M, int SEG>
+static cudaError_t launch_run_chain(const RunChainArgs& a, cudaStream_t s, int* launches) {
+  constexpr size_t smem = run_chain_smem<M, SEG>();
+  if constexpr (smem > 48 * 1024) {
+    static DeviceCache attr;
+    const int dev = current_device();
+    if (!attr.get(dev)) {
+      const cudaError_t e = cudaFuncSetAttribute(run_chain_kernel<M, SEG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)smem);
+      if (e != cudaSuccess) return e;
+      attr.set(dev, 1);
+    }
+  }
+  const int64_t nruns = a.batch * a.nseg;
+  run_chain_kernel<M, SEG><<<(unsigned)((nruns + 31) / 32), 32, smem, s>>>(a);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+// Largest run length the fused path may use with this operator type: a warp's 32 runs fit in shared memory.
+template <class M> constexpr int run_max_seg() { return M::W == 2 ? 32 : (M::W == 4 ? 16 : 8); }
+
+template <class M>
+static cudaError_t run_segment_chain(int64_t batch, int64_t k_count, int64_t seg, const double* U, const double* phi,
+                                     double* states, double* spin, cudaStream_t s, int* launches) {
+  if (seg > run_max_seg<M>() || k_count % seg != 0) return cudaErrorInvalidValue;
+  const RunChainArgs a{batch, k_count, k_count / seg, reinterpret_cast<const double2*>(U),
+                       reinterpret_cast<const double2*>(phi), reinterpret_cast<double2*>(states), spin};
+  switch (seg) {
+    case 4: return launch_run_chain<M, 4>(a, s, launches);
+    case 8: return launch_run_chain<M, 8>(a, s, launches);
+    case 16: if constexpr (run_max_seg<M>() >= 16) return launch_run_chain<M, 16>(a, s, launches); break;
+    case 32: if constexpr (run_max_seg<M>() >= 32) return launch_run_chain<M, 32>(a, s, launches); break;
+  }
+  return cudaErrorInvalidValue;
+}
+
+int fused_max_ipt(int dim, int op_format) {
+  if (op_format == OP_SU2) return run_max_seg<SU<2>>();
+  return dim == 2 ? run_max_seg<CM<2>>() : run_max_seg<CM<3>>();
+}
+
 // Per-sweep product of the tile aggregates, in order: A[b] = T_{n−1} ⋯ T_0.
 template <int D>
 __global__ void __launch_bounds__(256) combine_tiles_kernel(int64_t tiles_per_sweep, const double2* tiles,
@@ -1864,6 +1820,30 @@ cudaError_t launch_scan(int dim, int64_t batch, int64_t k_count, const double* U
                     : run_state_scan<SU<3>>(batch, k_count, U, psi0, states, ws, s, launches, spin);
   return dim == 2 ? run_state_scan<CM<2>>(batch, k_count, U, psi0, states, ws, s, launches, spin)
                   : run_state_scan<CM<3>>(batch, k_count, U, psi0, states, ws, s, launches, spin);
+}
+
+// Fused path (the interval kernel wrote run aggregates G[b][r] = U_{(r+1)seg−1} ⋯ U_{r·seg}): the coarse scan turns
+// them into the run start states phi[b][r] = G[b][r−1] ⋯ G[b][0] ψ0[b] (any state-scan path, on 1/seg of the data),
+// then one chain thread per run applies the run's own operators from phi[b][r] — every run independent, so the
+// states pass is a plain stream over U (read once) and ψ (written once).
+template <class M>
+static cudaError_t run_fused(int64_t batch, int64_t k_count, int64_t seg, const double* U, const double* run_agg,
+                             const double* psi0, double* phi, double* states, void* ws, cudaStream_t s, int* launches,
+                             double* spin) {
+  const int64_t nseg = (k_count + seg - 1) / seg;
+  cudaError_t e = run_state_scan<M>(batch, nseg, run_agg, psi0, phi, ws, s, launches, nullptr);
+  if (e != cudaSuccess) return e;
+  return run_segment_chain<M>(batch, k_count, seg, U, phi, states, spin, s, launches);
+}
+
+cudaError_t launch_fused_scan(int dim, int64_t batch, int64_t k_count, int64_t seg, const double* U,
+                              const double* run_agg, const double* psi0, double* phi, double* states, void* ws,
+                              cudaStream_t s, int* launches, double* spin, int op_format) {
+  if (op_format == OP_SU2)
+    return dim == 2 ? run_fused<SU<2>>(batch, k_count, seg, U, run_agg, psi0, phi, states, ws, s, launches, spin)
+                    : run_fused<SU<3>>(batch, k_count, seg, U, run_agg, psi0, phi, states, ws, s, launches, spin);
+  return dim == 2 ? run_fused<CM<2>>(batch, k_count, seg, U, run_agg, psi0, phi, states, ws, s, launches, spin)
+                  : run_fused<CM<3>>(batch, k_count, seg, U, run_agg, psi0, phi, states, ws, s, launches, spin);
 }
 
 cudaError_t launch_aggregate(int dim, int64_t batch, int64_t k_count, const double* U, double* aggregate, void* ws,

@@ -2,8 +2,9 @@
 intervals, L = 10.  Times, with CUDA events:
   (a) the public two-call path — interval kernel writing dense U_k (64 B), then the single-sweep scan (scan3) over
       them: 96 B per interval (read U_k 64 B + write ψ 32 B);
-  (b) ss_evaluate without U — the interval kernel hands the scan compact SU(2) elements (32 B): 64 B per interval;
-      the split between the two kernels comes from the ss_set_split_event hook.
+  (b) ss_evaluate without U — the interval kernel hands the state pass compact SU(2) elements (32 B) and, fused, the
+      run aggregates of its warps: 64 B per interval (read U 32 B + write ψ 32 B); (c) the same unfused; (d) dense U_k
+      requested as an output (96 B per interval), fused.
 
     python tools/scan_stress.py > profiles/r02/<tag>/scan_stress.txt
 """
@@ -43,22 +44,30 @@ def main():
           f"{t_scan:.3f} ms for {nbytes / 1e9:.1f} GB = {nbytes / (t_scan * 1e-3) / 1e9:.0f} GB/s "
           f"({nbytes / (t_scan * 1e-3) / HBM:.2f} of 6534.8 GB/s); step {t_int + t_scan:.2f} ms")
     del U, ws
-    # (b) ss_evaluate, compact operators
+    # (b)–(d) ss_evaluate: compact operators with the fused run aggregates (default), compact unfused
+    # (SPINSIM_FUSED=0), dense U_k as an output with the fused path; the split between the interval kernel and the
+    # state pass comes from the ss_set_split_event hook
     wsb = torch.empty(sim.workspace_bytes(1, w.K, True), dtype=torch.uint8, device="cuda")
+    Ud = torch.empty((1, w.K, 2, 2), dtype=torch.complex128, device="cuda")
     sim.evaluate(sweep, w.t0, w.t0 + w.dt_out, w.dt_int, w.dt_out, psi0, want_unitaries=False)
     sim.set_validation(False)
-    for rep in range(3):
-        ev[0].record()
-        sim.set_split_event(ev[1])
-        sim.evaluate(sweep, w.t0, w.t1, w.dt_int, w.dt_out, psi0, want_unitaries=False, workspace=wsb, out_states=st)
-        ev[2].record()
-        torch.cuda.synchronize()
-    sim.set_split_event(None)
-    t_int, t_scan = ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2])
-    nbytes = w.K * 64
-    print(f"(b) compact:   interval kernel {t_int:.2f} ms; scan {t_scan:.3f} ms for {nbytes / 1e9:.1f} GB = "
-          f"{nbytes / (t_scan * 1e-3) / 1e9:.0f} GB/s ({nbytes / (t_scan * 1e-3) / HBM:.2f} of 6534.8 GB/s); "
-          f"step {t_int + t_scan:.2f} ms = {w.fine_steps / ((t_int + t_scan) * 1e-3):.3e} fine steps/s")
+    for tag, fused, dense in (("(b) compact, fused", "1", False), ("(c) compact, unfused", "0", False),
+                              ("(d) dense U out, fused", "1", True)):
+        os.environ["SPINSIM_FUSED"] = fused
+        for rep in range(3):
+            ev[0].record()
+            sim.set_split_event(ev[1])
+            sim.evaluate(sweep, w.t0, w.t1, w.dt_int, w.dt_out, psi0, want_unitaries=dense, workspace=wsb,
+                         out_states=st, out_unitaries=Ud if dense else None)
+            ev[2].record()
+            torch.cuda.synchronize()
+        sim.set_split_event(None)
+        t_int, t_scan = ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2])
+        nbytes = w.K * (96 if dense else 64)
+        print(f"{tag}: interval kernel {t_int:.2f} ms; states {t_scan:.3f} ms for {nbytes / 1e9:.1f} GB = "
+              f"{nbytes / (t_scan * 1e-3) / 1e9:.0f} GB/s ({nbytes / (t_scan * 1e-3) / HBM:.2f} of 6534.8 GB/s); "
+              f"step {t_int + t_scan:.2f} ms = {w.fine_steps / ((t_int + t_scan) * 1e-3):.3e} fine steps/s")
+    os.environ.pop("SPINSIM_FUSED", None)
     print(f"final state norm − 1: {abs(torch.linalg.vector_norm(st[0, -1]).item() - 1):.2e}")
 
 
