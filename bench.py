@@ -89,6 +89,24 @@ def ncu_traffic(kernel: str, workload: str, full_size: bool):
     return e["bytes"] if e else None
 
 
+def executed_flops(kernel: str, workload: str):
+    """FP64 flops one fine step EXECUTES (ncu SASS op counts: 2·DFMA + DMUL + DADD per fine step) for this kernel on
+    this workload, from the committed capture (profiles/executed_flops.json), or None."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "executed_flops.json")))
+    except (OSError, ValueError):
+        return None
+    return d.get(f"{kernel}@{workload}")
+
+
+def executed_of(kernel: str, workload: str, fine_steps: int, ms: float, peak: float):
+    e = executed_flops(kernel, workload)
+    if not e:
+        return None
+    tf = e["flops_per_fine_step"] * fine_steps / (ms * 1e-3) / 1e12
+    return {"flops_per_fine_step": e["flops_per_fine_step"], "achieved": tf, "frac": tf / peak, "source": e["source"]}
+
+
 def hbm_peak_gbs():
     """HBM roofline denominator: MEASURED_PEAKS.json's STREAM-style copy (driver-written), else the profiling guide's
     fallback 6.65 TB/s (B200_PROFILING.md) — returned with which one it is."""
@@ -395,6 +413,7 @@ def run_ours(args, rank, world, local):
     if world > 1:
         import torch.distributed as dist
         if args.dist_backend == "nccl":
+            os.environ.setdefault("NCCL_DEBUG", "INFO")   # the init log names the communicator (comm_nranks)
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group("gloo")
@@ -503,6 +522,12 @@ def run_ours(args, rank, world, local):
                                         if args.precision == "fp64" else
                                         "nominal FP32: 148 SM x 128 FFMA/clk x 2 x 1.965 GHz (DESIGN.md §6)"),
                          "measured_dfma_peak_tflops": measured_peak,
+                         # the same achieved rate against the DFMA microbenchmark's sustainable peak, and the rate of
+                         # the flops the kernel actually executes (ncu SASS counts) against the nominal peak
+                         "frac_of_measured_dfma_peak": (achieved / measured_peak
+                                                        if isinstance(measured_peak, float) and measured_peak > 0
+                                                        else None),
+                         "executed": executed_of(kernel_name, w.name, steps_per_rank, t_interval, peak),
                          "frac_at_observed_clock": (achieved / (peak * clocks["sm_mhz"] / SM_MAX_MHZ)
                                                     if clocks.get("sm_mhz") else None)},
             "scan": {"bound": "hbm", "achieved": scan_gbs, "unit": "GB/s", "peak": hbm_peak_gbs()[0],
@@ -603,7 +628,9 @@ def run_time_partition(args, rank, world, local, dev):
                          "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
                          "kernel": f"interval_kernel<spin-half,analytic,cf4,neural,{args.precision}>",
                          "flops_per_launch": flops_launch, "ms_per_launch": t_interval,
-                         "peak_basis": "nominal FP64: 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (DESIGN.md §6)"},
+                         "peak_basis": "nominal FP64: 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (DESIGN.md §6)",
+                         "executed": executed_of(f"interval_kernel<spin-half,analytic,cf4,neural,{args.precision}>",
+                                                 "C4", kc * L, t_interval, FP64_PEAK_TFLOPS)},
             "interval_ms_per_launch": t_interval, "exchange_and_scan_ms": t_rest, "e2e": e2e,
             "gpu_launches": int(launches), "clocks": clocks,
         }

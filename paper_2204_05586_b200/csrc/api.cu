@@ -37,6 +37,31 @@ int cuda_fail(cudaError_t e, const char* where) {
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
+// cudaMemcpy2DAsync rejects pitches above the device's cudaDevAttrMaxPitch (≈ 2^31 B: spin-one states of one sweep
+// past ≈ 45M intervals); beyond it the rows go as one cudaMemcpyAsync each.
+cudaError_t copy_rows(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height,
+                      cudaMemcpyKind kind, cudaStream_t st) {
+  static std::atomic<long long> max_pitch{0};
+  long long mp = max_pitch.load(std::memory_order_relaxed);
+  if (mp == 0) {
+    int dev = 0, v = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&v, cudaDevAttrMaxPitch, dev) == cudaSuccess && v > 0)
+      mp = v;
+    else
+      mp = 1LL << 31;
+    max_pitch.store(mp, std::memory_order_relaxed);
+  }
+  if (height == 1 || ((long long)dpitch <= mp && (long long)spitch <= mp))
+    return height == 1 ? cudaMemcpyAsync(dst, src, width, kind, st)
+                       : cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, kind, st);
+  for (size_t r = 0; r < height; ++r) {
+    const cudaError_t e = cudaMemcpyAsync(static_cast<char*>(dst) + r * dpitch,
+                                          static_cast<const char*>(src) + r * spitch, width, kind, st);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 int field_params(int field) {
   switch (field) {
     case SS_FIELD_CONSTANT: return 4;
@@ -150,13 +175,20 @@ int plan_grid(double t0, double t1, double dt_int, double dt_out, int64_t* K, in
 #define SS_FORCE_SPLIT 0    // tuning experiments only: a fixed S (must divide L)
 #endif
 // Interval-kernel threads resident on the device at once (one wave).
+// SM counts are cached per device ordinal (a process may drive several GPUs); 148 when no device answers
+// (host-only planning, e.g. ss_host_chunk_plan on a machine without a GPU).
 double resident_threads(const ss_sim* s) {
-  static int sms = 0;
+  static std::atomic<int> sms_of[64];
+  int dev = -1, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = -1;
+  if (dev >= 0) sms = sms_of[dev].load(std::memory_order_relaxed);
   if (sms == 0) {
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) !=
-                                                   cudaSuccess || sms <= 0)
+    if (dev >= 0 && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && sms > 0) {
+      sms_of[dev].store(sms, std::memory_order_relaxed);
+    } else {
       sms = 148;
+      (void)cudaGetLastError();
+    }
   }
   const bool su3 = s->d.exponentiation == SS_EXP_LIE_TROTTER_SU3;
   return (double)sms * (su3 ? SS_INTERVAL_MINBLOCKS_SU3 : SS_INTERVAL_MINBLOCKS) * ssb::kIntervalThreads;
@@ -760,6 +792,15 @@ int ss_evaluate_host(ss_sim* s, double t0, double t1, double dt_int, double dt_o
     s->device = dev;
   }
   const int D = s->dim;
+  // Synchronous call: on every return — including an error after work was enqueued — all three streams are drained
+  // first, so no copy into the caller's host buffers or scan over the carry is still in flight.
+  struct DrainOnExit {
+    cudaStream_t* st;
+    ~DrainOnExit() {
+      for (int k = 0; k < 3; ++k)
+        if (st[k]) (void)cudaStreamSynchronize(st[k]);
+    }
+  } drain{s->streams};
   auto ensure = [&](ss_sim::Slot& sl, size_t bytes) -> cudaError_t {
     if (sl.cap >= bytes) return cudaSuccess;
     if (sl.buf) cudaFree(sl.buf);
@@ -818,16 +859,16 @@ int ss_evaluate_host(ss_sim* s, double t0, double t1, double dt_int, double dt_o
                             s->stepped[k])))
         return rc;
       // carry ← states[:, kc]
-      if ((e = cudaMemcpy2DAsync(d_carry, row, d_states + (size_t)kc * 2 * D, row * (kc + 1), row, batch,
+      if ((e = copy_rows(d_carry, row, d_states + (size_t)kc * 2 * D, row * (kc + 1), row, batch,
                                  cudaMemcpyDeviceToDevice, ss)))
         return cuda_fail(e, "carry copy");
       if ((e = cudaEventRecord(s->computed[k], ss)) || (e = cudaStreamWaitEvent(xs, s->computed[k], 0)))
         return cuda_fail(e, "event record/wait");
       const size_t first = (c == 0) ? 0 : 1;                     // states[:, 0] of chunk c > 0 is the carry
-      if ((e = cudaMemcpy2DAsync(h_states + (k0 + first) * 2 * D, row * (K + 1), d_states + first * 2 * D,
+      if ((e = copy_rows(h_states + (k0 + first) * 2 * D, row * (K + 1), d_states + first * 2 * D,
                                  row * (kc + 1), row * (kc + 1 - first), batch, cudaMemcpyDeviceToHost, xs)))
         return cuda_fail(e, "D2H copy (states)");
-      if (h_U && (e = cudaMemcpy2DAsync(h_U + k0 * 2 * D * D, row * D * K, d_U, row * D * kc, row * D * kc, batch,
+      if (h_U && (e = copy_rows(h_U + k0 * 2 * D * D, row * D * K, d_U, row * D * kc, row * D * kc, batch,
                                         cudaMemcpyDeviceToHost, xs)))
         return cuda_fail(e, "D2H copy (unitaries)");
       if ((e = cudaEventRecord(s->drained[k], xs))) return cuda_fail(e, "event record");

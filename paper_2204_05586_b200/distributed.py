@@ -3,7 +3,9 @@
 Two ways the path shards:
 
 * **Sweep sharding** (C3): independent sweeps are split into contiguous blocks, one per rank; no data-path
-  collective.  Per-sweep results are bitwise identical to a single-GPU run (same kernels, same per-sweep work).
+  collective.  Per-sweep results are bitwise identical to a single-GPU run when the rank's shard takes the same
+  state-scan kernel and sub-interval split as the whole batch (C3: the per-sweep chain kernel from 4096 sweeps per
+  rank), and otherwise equal to rounding (≲ 1e-13): a smaller shard may take another scan association.
 * **Time partitioning** (C4, one long simulation): rank g owns intervals [k_g, k_{g+1}) of the global grid.
   Each rank computes its U_k with the *global* k (bit-identical operators to the one-GPU run), reduces them to its
   aggregate A_g = U_{k_{g+1}−1} ⋯ U_{k_g}, and the aggregates are all-gathered (dim² complex128 per sweep per rank —
