@@ -71,17 +71,16 @@ __device__ __forceinline__ void sample_in_frame(const Field<F>& fld, double off,
   if (frame) to_rotating_frame<NC>(f, off, omega_r);
 }
 
-// Rows a1–a7 for interval k of sweep b: A = U_r − I in the rotating frame at ω_r (residual form, reading R9).  With
-// the sub-interval split (S > 1) the S lanes of an interval each run L/S fine steps and the shuffle tree leaves the
-// whole product in the lane with part = 0 (every lane of the warp must call this; `active` = false lanes idle).
+// Rows a1–a7 for fine steps [l_begin, l_end) of interval k of sweep b: A = the product of those steps' exponentials
+// minus I, in the rotating frame at ω_r (residual form, reading R9) — the whole interval's U_r − I when the range is
+// [0, L), else a piece that the caller multiplies with its neighbours' (same samples, same frame).
 template <int SPIN, int EXPO, int METHOD, int FIELD, typename T>
-__device__ __forceinline__ void interval_residual(const IntervalParams& prm, int64_t b, int64_t k, int part,
-                                                  bool active, Res<AccDim<SPIN, EXPO>::D, T>& A_out,
+__device__ __forceinline__ void interval_residual(const IntervalParams& prm, int64_t b, int64_t k, int64_t l_begin,
+                                                  int64_t l_end, Res<AccDim<SPIN, EXPO>::D, T>& A_out,
                                                   double& omega_r_out) {
   constexpr int D = SpinDim<SPIN>::D;
   constexpr int P = FieldParams<FIELD>::P;
   constexpr int NC = NumCoeffs<EXPO>::N;             // 4, or 8 for the general spin-one exponentiator
-  const int S = prm.split;
   (void)D;
 
   double p[P];
@@ -115,7 +114,6 @@ __device__ __forceinline__ void interval_residual(const IntervalParams& prm, int
   Res<DA, T> A;   // U_r − I, U_r initialised to the identity
   res_zero(A);
 
-  const int64_t l_begin = (prm.L * part) / S, l_end = active ? (prm.L * (part + 1)) / S : l_begin;
   // One fine step.  ANCHOR (exact sincos of the phase steppers, every kAnchor-th step) and PULSE (this interval can
   // meet the neural field's pulse window) are compile-time, so the step body carries no per-step branches for them.
   auto step = [&](int64_t l, auto anchor_c, auto pulse_c, auto short_c) {
@@ -240,18 +238,6 @@ __device__ __forceinline__ void interval_residual(const IntervalParams& prm, int
       step(l, RtBool{((l - l_begin) % kAnchor) == 0}, BoolC<true>{}, BoolC<false>{});
   }
 
-  // Sub-interval split: lane p holds the partial product of its fine steps; combine later·earlier in a shuffle tree
-  // (U_r = P_{S−1} ⋯ P_0, same samples, only the association of the product differs).
-  if (S > 1) {
-    for (int off = 1; off < S; off <<= 1) {
-      const Res<DA, T> B = res_shfl_down(A, off);
-      if ((part & (2 * off - 1)) == 0) {
-        Res<DA, T> C;
-        res_mul(B, A, C);
-        A = C;
-      }
-    }
-  }
   A_out = A;
   omega_r_out = omega_r;
 }
@@ -309,7 +295,7 @@ __device__ __forceinline__ void interval_run(const IntervalParams& prm, int64_t 
   for (int64_t j = 0; j < n; ++j) {
     Res<AccDim<SPIN, EXPO>::D, T> A;
     double omega_r;
-    interval_residual<SPIN, EXPO, METHOD, FIELD, T>(prm, b, prm.k_begin + k_lo + j, 0, true, A, omega_r);
+    interval_residual<SPIN, EXPO, METHOD, FIELD, T>(prm, b, prm.k_begin + k_lo + j, 0, prm.L, A, omega_r);
     M op, g;
     make_op(A, omega_r, prm, op);
     cm_store(U + (b * prm.k_count + k_lo + j) * M::W, op);
@@ -321,38 +307,10 @@ __device__ __forceinline__ void interval_run(const IntervalParams& prm, int64_t 
   cm_store(reinterpret_cast<double2*>(prm.run_agg) + slot * M::W, g);
 }
 
-// FUSED (a separate instance, so the unfused kernel's code is untouched): prm.run_agg is set, S = 1, and thread slot
-// gt of sweep b owns ipt intervals.
-template <int SPIN, int EXPO, int METHOD, int FIELD, typename T, bool FUSED>
-__device__ __forceinline__ void interval_body(const IntervalParams& prm) {
-  constexpr int D = SpinDim<SPIN>::D;
-  constexpr int DA = AccDim<SPIN, EXPO>::D;
-  const int64_t gt = (int64_t)blockIdx.x * kIntervalThreads + threadIdx.x;
-  if constexpr (FUSED) {
-    const int64_t b = gt / prm.k_stride, t = gt - b * prm.k_stride;
-    if (b >= prm.batch) return;
-    const int64_t k_lo = t * prm.ipt, n = min(prm.ipt, prm.k_count - k_lo);
-    if constexpr (DA == 2) {
-      if (prm.op_format == OP_SU2) {
-        interval_run<SU<D>, SPIN, EXPO, METHOD, FIELD, T>(prm, b, k_lo, n, gt);
-        return;
-      }
-    }
-    interval_run<CM<D>, SPIN, EXPO, METHOD, FIELD, T>(prm, b, k_lo, n, gt);
-    return;
-  }
-  const int S = prm.split;
-  const int64_t i = gt / S;                          // interval index (sweep-major)
-  const int part = (int)(gt - i * S);
-  const bool active = i < prm.n_threads;
-  if (S == 1 && !active) return;                     // with S > 1 every lane must reach the shuffles
-  const int64_t ic = active ? i : 0;
-  const int64_t b = ic / prm.k_count;
-  const int64_t k = prm.k_begin + (ic - b * prm.k_count);
-  Res<DA, T> A;
-  double omega_r;
-  interval_residual<SPIN, EXPO, METHOD, FIELD, T>(prm, b, k, part, active, A, omega_r);
-  if (part != 0 || !active) return;
+// U_k of the launch's flat interval index i (sweep-major) from the residual A of the whole interval, in the output
+// format: dense D×D, or compact SU(2) for the SU(2)-form accumulators.
+template <int D, int DA, typename T>
+__device__ __forceinline__ void store_op(const IntervalParams& prm, const Res<DA, T>& A, double omega_r, int64_t i) {
   if constexpr (DA == 2) {
     if (prm.op_format == OP_SU2) {
       SU<D> u;
@@ -366,10 +324,62 @@ __device__ __forceinline__ void interval_body(const IntervalParams& prm) {
   cm_store(reinterpret_cast<double2*>(prm.unitaries) + i * (D * D), m);
 }
 
-template <int SPIN, int EXPO, int METHOD, int FIELD, typename T, bool FUSED>
+// Kernel modes (separate instances, so each one's code is untouched by the other):
+//   MODE_SPLIT: one interval per S lanes (S = 1: per thread; S > 1: the sub-interval split, DESIGN.md §5 item 8);
+//   MODE_FUSED: prm.run_agg is set, S = 1, thread slot gt of sweep b owns ipt intervals (§5 item 16).
+enum { MODE_SPLIT = 0, MODE_FUSED = 1 };
+
+template <int SPIN, int EXPO, int METHOD, int FIELD, typename T, int MODE>
+__device__ __forceinline__ void interval_body(const IntervalParams& prm) {
+  constexpr int D = SpinDim<SPIN>::D;
+  constexpr int DA = AccDim<SPIN, EXPO>::D;
+  const int64_t gt = (int64_t)blockIdx.x * kIntervalThreads + threadIdx.x;
+  if constexpr (MODE == MODE_FUSED) {
+    const int64_t b = gt / prm.k_stride, t = gt - b * prm.k_stride;
+    if (b >= prm.batch) return;
+    const int64_t k_lo = t * prm.ipt, n = min(prm.ipt, prm.k_count - k_lo);
+    if constexpr (DA == 2) {
+      if (prm.op_format == OP_SU2) {
+        interval_run<SU<D>, SPIN, EXPO, METHOD, FIELD, T>(prm, b, k_lo, n, gt);
+        return;
+      }
+    }
+    interval_run<CM<D>, SPIN, EXPO, METHOD, FIELD, T>(prm, b, k_lo, n, gt);
+    return;
+  } else {
+    const int S = prm.split;
+    const int64_t i = gt / S;                        // interval index (sweep-major)
+    const int part = (int)(gt - i * S);
+    const bool active = i < prm.n_threads;
+    if (S == 1 && !active) return;                   // with S > 1 every lane must reach the shuffles
+    const int64_t ic = active ? i : 0;
+    const int64_t b = ic / prm.k_count;
+    const int64_t k = prm.k_begin + (ic - b * prm.k_count);
+    const int64_t l_begin = (prm.L * part) / S, l_end = active ? (prm.L * (part + 1)) / S : l_begin;
+    Res<DA, T> A;
+    double omega_r;
+    interval_residual<SPIN, EXPO, METHOD, FIELD, T>(prm, b, k, l_begin, l_end, A, omega_r);
+    // Sub-interval split: lane p holds the partial product of its fine steps; combine later·earlier in a shuffle tree
+    // (U_r = P_{S−1} ⋯ P_0, same samples, only the association of the product differs).
+    if (S > 1) {
+      for (int off = 1; off < S; off <<= 1) {
+        const Res<DA, T> B = res_shfl_down(A, off);
+        if ((part & (2 * off - 1)) == 0) {
+          Res<DA, T> C;
+          res_mul(B, A, C);
+          A = C;
+        }
+      }
+    }
+    if (part != 0 || !active) return;
+    store_op<D>(prm, A, omega_r, i);
+  }
+}
+
+template <int SPIN, int EXPO, int METHOD, int FIELD, typename T, int MODE>
 __global__ void __launch_bounds__(kIntervalThreads, kIntervalMinBlocks<SPIN, EXPO, T>())
 interval_kernel(const IntervalParams prm) {
-  interval_body<SPIN, EXPO, METHOD, FIELD, T, FUSED>(prm);
+  interval_body<SPIN, EXPO, METHOD, FIELD, T, MODE>(prm);
 }
 
 #ifndef __CUDACC_RTC__
@@ -378,14 +388,19 @@ inline size_t interval_smem(const IntervalParams& prm) {
   return prm.run_agg ? (size_t)kIntervalThreads * 9 * 16 : 0;
 }
 
+// Blocks of an interval launch: one lane per interval slot (S lanes per interval with the split).
+inline int64_t interval_blocks(const IntervalParams& prm) {
+  return (prm.n_threads * prm.split + kIntervalThreads - 1) / kIntervalThreads;
+}
+
 template <int SPIN, int EXPO, int METHOD, int FIELD, typename T>
 cudaError_t launch_interval(const IntervalParams& prm, cudaStream_t stream) {
-  const int64_t blocks = (prm.n_threads * prm.split + kIntervalThreads - 1) / kIntervalThreads;
+  const int64_t blocks = interval_blocks(prm);
   if (blocks <= 0) return cudaSuccess;
   if (prm.run_agg)
-    interval_kernel<SPIN, EXPO, METHOD, FIELD, T, true><<<(unsigned)blocks, kIntervalThreads, interval_smem(prm), stream>>>(prm);
+    interval_kernel<SPIN, EXPO, METHOD, FIELD, T, MODE_FUSED><<<(unsigned)blocks, kIntervalThreads, interval_smem(prm), stream>>>(prm);
   else
-    interval_kernel<SPIN, EXPO, METHOD, FIELD, T, false><<<(unsigned)blocks, kIntervalThreads, 0, stream>>>(prm);
+    interval_kernel<SPIN, EXPO, METHOD, FIELD, T, MODE_SPLIT><<<(unsigned)blocks, kIntervalThreads, 0, stream>>>(prm);
   return cudaGetLastError();
 }
 #endif  // !__CUDACC_RTC__

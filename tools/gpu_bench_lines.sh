@@ -14,9 +14,14 @@ $B --workload C2 --steps 20 > "$O/bench_c2.jsonl" 2> "$O/bench_c2.err"
 $B --workload C5 --expo analytic --steps 10 > "$O/bench_c5an.jsonl" 2> "$O/bench_c5an.err"
 $B --workload C5 --steps 10 > "$O/bench_c5lt.jsonl" 2> "$O/bench_c5lt.err"
 $B --workload C4 --steps 10 > "$O/bench_c4.jsonl" 2> "$O/bench_c4.err"
+$B --workload C5 --precision fp32 --steps 10 > "$O/bench_c5lt_fp32.jsonl" 2> "$O/bench_c5lt_fp32.err"
+$B --workload C5 --expo analytic --precision fp32 --steps 10 > "$O/bench_c5an_fp32.jsonl" 2> "$O/bench_c5an_fp32.err"
+$B --workload G1 > "$O/bench_g1.jsonl" 2> "$O/bench_g1.err"
 for n in 2 4 8; do
   $B --emulate-ranks $n --no-e2e > "$O/bench_c3_rankof$n.jsonl" 2> "$O/bench_c3_rankof$n.err" || true
+  $B --workload C4 --steps 10 --emulate-ranks $n --no-e2e > "$O/bench_c4_rankof$n.jsonl" 2> "$O/bench_c4_rankof$n.err" || true
 done
+timeout 300 python tools/c2_dt_sweep.py > "$O/c2_dt_sweep.txt" 2>&1
 timeout 300 python tools/scan_stress.py > "$O/scan_stress.txt" 2>&1
 for f in "$O"/bench_*.jsonl; do
   python - "$f" <<'EOF'
@@ -29,7 +34,7 @@ for l in open(sys.argv[1]):
     r = d.get("roofline", {}); s = d.get("scan", {}) or {}; e = d.get("e2e") or {}
     print(sys.argv[1].split("/")[-1], f"{d['value']:.4g}", f"ms/step {d['ms_per_step']:.4g}", f"frac {r.get('frac', 0):.3f}",
           f"int_ms {r.get('ms_per_launch', 0):.4g}", f"scan_ms {s.get('ms_per_launch', 0) or 0:.4g}",
-          f"e2e {e.get('value', 0) or 0:.4g}")
+          f"e2e {e.get('value', 0) or 0:.4g}", f"pred {(d.get('emulated') or {}).get('predicted_value', 0):.4g}")
 EOF
 done
-cat "$O/scan_stress.txt"
+cat "$O/scan_stress.txt" "$O/c2_dt_sweep.txt"
