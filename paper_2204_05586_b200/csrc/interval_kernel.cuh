@@ -71,13 +71,60 @@ __device__ __forceinline__ void sample_in_frame(const Field<F>& fld, double off,
   if (frame) to_rotating_frame<NC>(f, off, omega_r);
 }
 
+#ifndef SS_WARP_TRIG
+#define SS_WARP_TRIG 1        // warp-shared per-interval sincos (warp_trig); 0: every lane evaluates its own
+#endif
+#ifndef SS_WARP_TRIG_EXIT
+#define SS_WARP_TRIG_EXIT 1   // include a8's exit angle (held through the step loop) in the shared set
+#endif
+// The frame exit's sincos (a8), when warp_trig supplied it.
+struct ExitTrig {
+  bool pre;
+  double s, c;
+};
+
+// Per-interval trigonometry shared across a warp.  An interval's prologue takes seven sincos whose arguments depend
+// only on the sweep and on ω_r — the field's RF rotations ω·g1δt, ω·g2δt, ω·δt (init_cf4), the frame's ω_r·g1δt,
+// ω_r·g2δt, ω_r·δt and the exit angle of a8 — and ω_r is the same for every interval outside a pulse window.  When
+// all 32 lanes hold the same sweep and ω_r (a warp-uniform test), lane j evaluates the j-th of them and the warp
+// exchanges the results by shuffles: one sincos latency per warp instead of seven in a row (the ncu source view put
+// these calls at ≈ 10 % of the C3 kernel's warp samples).  Same expressions, same library sincos: bit-identical values.
+template <class FLD>
+__device__ __forceinline__ bool warp_trig(const FLD& fld, int64_t b, double omega_r, double exit_angle,
+                                          const IntervalParams& prm, double tr[14]) {
+  if (__activemask() != 0xffffffffu) return false;
+  const long long b0 = __shfl_sync(0xffffffffu, (long long)b, 0);
+  const double w0 = __shfl_sync(0xffffffffu, omega_r, 0);
+  if (!__all_sync(0xffffffffu, (long long)b == b0 && omega_r == w0)) return false;
+  const int lane = threadIdx.x & 31;
+  const double W = fld.rf();
+  double x = 0.0;
+  switch (lane) {
+    case 0: x = W * prm.g1dt; break;
+    case 1: x = W * prm.g2dt; break;
+    case 2: x = W * prm.dt; break;
+    case 3: x = omega_r * prm.g1dt; break;
+    case 4: x = omega_r * prm.g2dt; break;
+    case 5: x = omega_r * prm.dt; break;
+    case 6: x = exit_angle; break;
+  }
+  double sn, cs;
+  sincos(x, &sn, &cs);
+#pragma unroll
+  for (int j = 0; j < 7; ++j) {
+    tr[2 * j] = __shfl_sync(0xffffffffu, sn, j);
+    tr[2 * j + 1] = __shfl_sync(0xffffffffu, cs, j);
+  }
+  return true;
+}
+
 // Rows a1–a7 for fine steps [l_begin, l_end) of interval k of sweep b: A = the product of those steps' exponentials
 // minus I, in the rotating frame at ω_r (residual form, reading R9) — the whole interval's U_r − I when the range is
 // [0, L), else a piece that the caller multiplies with its neighbours' (same samples, same frame).
 template <int SPIN, int EXPO, int METHOD, int FIELD, typename T>
 __device__ __forceinline__ void interval_residual(const IntervalParams& prm, int64_t b, int64_t k, int64_t l_begin,
                                                   int64_t l_end, Res<AccDim<SPIN, EXPO>::D, T>& A_out,
-                                                  double& omega_r_out) {
+                                                  double& omega_r_out, ExitTrig& ex) {
   constexpr int D = SpinDim<SPIN>::D;
   constexpr int P = FieldParams<FIELD>::P;
   constexpr int NC = NumCoeffs<EXPO>::N;             // 4, or 8 for the general spin-one exponentiator
@@ -99,9 +146,23 @@ __device__ __forceinline__ void interval_residual(const IntervalParams& prm, int
   }
 
   FrameCF4 frame2;
+  ex.pre = false;
   if (METHOD == CF4) {
-    fld.init_cf4(prm.g1dt, prm.g2dt, prm.dt);
-    frame2.init(omega_r, prm.g1dt, prm.g2dt, prm.dt);
+    // a8's angle: ω_rΔt/2 for the SU(2) forms (spin-half, compact operators), ω_rΔt for dense spin-one (make_op)
+    const double exit_angle = (D == 2 || prm.op_format == OP_SU2) ? 0.5 * omega_r * prm.dt_out : omega_r * prm.dt_out;
+    double tr[14];
+    if (SS_WARP_TRIG && warp_trig(fld, b, omega_r, exit_angle, prm, tr)) {
+      fld.init_cf4_pre(tr);
+      frame2.init_pre(omega_r, tr + 6);
+      if (SS_WARP_TRIG_EXIT) {
+        ex.pre = true;
+        ex.s = tr[12];
+        ex.c = tr[13];
+      }
+    } else {
+      fld.init_cf4(prm.g1dt, prm.g2dt, prm.dt);
+      frame2.init(omega_r, prm.g1dt, prm.g2dt, prm.dt);
+    }
   }
 
   constexpr int DA = AccDim<SPIN, EXPO>::D;         // accumulated residual: SU(2) form (2) or dense 3×3
@@ -244,11 +305,13 @@ __device__ __forceinline__ void interval_residual(const IntervalParams& prm, int
 
 // a8: U_k = R_{ω_r}(−Δt)(I + A) = diag(e^{−iω_r m Δt})(I + A), as the dense D×D complex matrix ...
 template <int D, int DA, typename T>
-__device__ __forceinline__ void make_op(const Res<DA, T>& A, double omega_r, const IntervalParams& prm, CM<D>& m) {
+__device__ __forceinline__ void make_op(const Res<DA, T>& A, double omega_r, const ExitTrig& ex,
+                                        const IntervalParams& prm, CM<D>& m) {
   double ph_re[D], ph_im[D];
   {
     double s, c;
-    if (D == 2) sincos(0.5 * omega_r * prm.dt_out, &s, &c);
+    if (ex.pre) { s = ex.s; c = ex.c; }
+    else if (D == 2) sincos(0.5 * omega_r * prm.dt_out, &s, &c);
     else sincos(omega_r * prm.dt_out, &s, &c);
     ph_re[0] = c; ph_im[0] = -s;                      // m = +1 (or +½)
     ph_re[D - 1] = c; ph_im[D - 1] = s;               // m = −1 (or −½)
@@ -269,9 +332,11 @@ __device__ __forceinline__ void make_op(const Res<DA, T>& A, double omega_r, con
 // ... or (SU(2)-form accumulators) compact: the SU(2) element (a, b) = e^{−iω_rΔt/2}·(1 + δa, b) — R(−Δt) is
 // diag(p, p*) with p = e^{−iω_rΔt/2} in SU(2), and D¹ of it for the analytic spin-one path (diag(p², 1, p*²)).
 template <int D, typename T>
-__device__ __forceinline__ void make_op(const Res<2, T>& A, double omega_r, const IntervalParams& prm, SU<D>& u) {
+__device__ __forceinline__ void make_op(const Res<2, T>& A, double omega_r, const ExitTrig& ex,
+                                        const IntervalParams& prm, SU<D>& u) {
   double s, c;
-  sincos(0.5 * omega_r * prm.dt_out, &s, &c);
+  if (ex.pre) { s = ex.s; c = ex.c; }
+  else sincos(0.5 * omega_r * prm.dt_out, &s, &c);
   const double ar = 1.0 + (double)A.ar, ai = (double)A.ai, br = (double)A.br, bi = (double)A.bi;
   u.ar = c * ar + s * ai; u.ai = c * ai - s * ar;     // (c − is)(ar + i ai)
   u.br = c * br + s * bi; u.bi = c * bi - s * br;
@@ -295,9 +360,10 @@ __device__ __forceinline__ void interval_run(const IntervalParams& prm, int64_t 
   for (int64_t j = 0; j < n; ++j) {
     Res<AccDim<SPIN, EXPO>::D, T> A;
     double omega_r;
-    interval_residual<SPIN, EXPO, METHOD, FIELD, T>(prm, b, prm.k_begin + k_lo + j, 0, prm.L, A, omega_r);
+    ExitTrig ex;
+    interval_residual<SPIN, EXPO, METHOD, FIELD, T>(prm, b, prm.k_begin + k_lo + j, 0, prm.L, A, omega_r, ex);
     M op, g;
-    make_op(A, omega_r, prm, op);
+    make_op(A, omega_r, ex, prm, op);
     cm_store(U + (b * prm.k_count + k_lo + j) * M::W, op);
     cm_load(acc, g);
     cm_store(acc, cm_mul(op, g));
@@ -310,17 +376,18 @@ __device__ __forceinline__ void interval_run(const IntervalParams& prm, int64_t 
 // U_k of the launch's flat interval index i (sweep-major) from the residual A of the whole interval, in the output
 // format: dense D×D, or compact SU(2) for the SU(2)-form accumulators.
 template <int D, int DA, typename T>
-__device__ __forceinline__ void store_op(const IntervalParams& prm, const Res<DA, T>& A, double omega_r, int64_t i) {
+__device__ __forceinline__ void store_op(const IntervalParams& prm, const Res<DA, T>& A, double omega_r,
+                                         const ExitTrig& ex, int64_t i) {
   if constexpr (DA == 2) {
     if (prm.op_format == OP_SU2) {
       SU<D> u;
-      make_op(A, omega_r, prm, u);
+      make_op(A, omega_r, ex, prm, u);
       cm_store(reinterpret_cast<double2*>(prm.unitaries) + i * 2, u);
       return;
     }
   }
   CM<D> m;
-  make_op(A, omega_r, prm, m);
+  make_op(A, omega_r, ex, prm, m);
   cm_store(reinterpret_cast<double2*>(prm.unitaries) + i * (D * D), m);
 }
 
@@ -358,7 +425,8 @@ __device__ __forceinline__ void interval_body(const IntervalParams& prm) {
     const int64_t l_begin = (prm.L * part) / S, l_end = active ? (prm.L * (part + 1)) / S : l_begin;
     Res<DA, T> A;
     double omega_r;
-    interval_residual<SPIN, EXPO, METHOD, FIELD, T>(prm, b, k, l_begin, l_end, A, omega_r);
+    ExitTrig ex;
+    interval_residual<SPIN, EXPO, METHOD, FIELD, T>(prm, b, k, l_begin, l_end, A, omega_r, ex);
     // Sub-interval split: lane p holds the partial product of its fine steps; combine later·earlier in a shuffle tree
     // (U_r = P_{S−1} ⋯ P_0, same samples, only the association of the product differs).
     if (S > 1) {
@@ -372,7 +440,7 @@ __device__ __forceinline__ void interval_body(const IntervalParams& prm) {
       }
     }
     if (part != 0 || !active) return;
-    store_op<D>(prm, A, omega_r, i);
+    store_op<D>(prm, A, omega_r, ex, i);
   }
 }
 

@@ -123,6 +123,10 @@ struct PhaseStepper {
     w = w_; ph0 = ph0_;
     sincos(w * dt, &sd, &cd);
   }
+  // the same with sincos(w·δt) supplied (computed once per warp, warp_trig in interval_kernel.cuh)
+  __device__ __forceinline__ void init_pre(double w_, double ph0_, double sd_, double cd_) {
+    w = w_; ph0 = ph0_; sd = sd_; cd = cd_;
+  }
   __device__ __forceinline__ void next(double base, bool anchor) {
     if (anchor) {
       sincos(fma(w, base, ph0), &s, &c);
@@ -155,6 +159,9 @@ template <> struct Field<FIELD_CONSTANT> {
   __device__ __forceinline__ double mag_bound(double wr) const { return fabs(f0) + fabs(f1) + fabs(f2 - wr); }
   __device__ __forceinline__ void sample(double, double f[4]) const { f[0] = f0; f[1] = f1; f[2] = f2; f[3] = f3; }
   __device__ __forceinline__ void init_cf4(double, double, double) {}
+  static constexpr bool kRF = false;
+  __device__ __forceinline__ double rf() const { return 0.0; }
+  __device__ __forceinline__ void init_cf4_pre(const double*) {}
   __device__ __forceinline__ void sample_cf4(double, bool, bool, double o1, double o2, double g1[4], double g2[4]) {
     sample(o1, g1); sample(o2, g2);
   }
@@ -173,6 +180,13 @@ template <> struct Field<FIELD_RABI_LINEAR> {        // ω0 Jz + 2Ω cos(ω0 t) 
   __device__ __forceinline__ void init_cf4(double g1dt, double g2dt, double dt) {
     sincos(w0 * g1dt, &s1, &c1); sincos(w0 * g2dt, &s2, &c2);
     ps.init(w0, ph0, dt);
+  }
+  // RF phase stepper: init_cf4 with its three sincos — of ω·g1δt, ω·g2δt, ω·δt — supplied in t[0..5] as (s, c)
+  static constexpr bool kRF = true;
+  __device__ __forceinline__ double rf() const { return w0; }
+  __device__ __forceinline__ void init_cf4_pre(const double* t) {
+    s1 = t[0]; c1 = t[1]; s2 = t[2]; c2 = t[3];
+    ps.init_pre(w0, ph0, t[4], t[5]);
   }
   __device__ __forceinline__ void sample_cf4(double base, bool anchor, bool, double, double, double g1[4], double g2[4]) {
     ps.next(base, anchor);
@@ -197,6 +211,13 @@ template <> struct Field<FIELD_RABI_CIRCULAR> {      // ω0 Jz + Ω(cos(ω0 t) J
   __device__ __forceinline__ void init_cf4(double g1dt, double g2dt, double dt) {
     sincos(w0 * g1dt, &s1, &c1); sincos(w0 * g2dt, &s2, &c2);
     ps.init(w0, ph0, dt);
+  }
+  // RF phase stepper: init_cf4 with its three sincos — of ω·g1δt, ω·g2δt, ω·δt — supplied in t[0..5] as (s, c)
+  static constexpr bool kRF = true;
+  __device__ __forceinline__ double rf() const { return w0; }
+  __device__ __forceinline__ void init_cf4_pre(const double* t) {
+    s1 = t[0]; c1 = t[1]; s2 = t[2]; c2 = t[3];
+    ps.init_pre(w0, ph0, t[4], t[5]);
   }
   __device__ __forceinline__ void sample_cf4(double base, bool anchor, bool, double, double, double g1[4], double g2[4]) {
     ps.next(base, anchor);
@@ -240,6 +261,13 @@ template <> struct Field<FIELD_NEURAL> {
     sincos(wrf * g1dt, &s1, &c1); sincos(wrf * g2dt, &s2, &c2);
     ps.init(wrf, ph0, dt);
   }
+  // RF phase stepper: init_cf4 with its three sincos — of ω·g1δt, ω·g2δt, ω·δt — supplied in t[0..5] as (s, c)
+  static constexpr bool kRF = true;
+  __device__ __forceinline__ double rf() const { return wrf; }
+  __device__ __forceinline__ void init_cf4_pre(const double* t) {
+    s1 = t[0]; c1 = t[1]; s2 = t[2]; c2 = t[3];
+    ps.init_pre(wrf, ph0, t[4], t[5]);
+  }
   __device__ __forceinline__ void sample_cf4(double base, bool anchor, bool pulse, double o1, double o2, double g1[4], double g2[4]) {
     ps.next(base, anchor);                         // e^{i ω_rf (t_k + base)}, reduced
     const double sb = ps.s, cb = ps.c;
@@ -256,6 +284,9 @@ template <> struct Field<FIELD_GRADIENT> {          // ω_z = x − 2y
   __device__ __forceinline__ double mag_bound(double wr) const { return fabs(wz - wr); }
   __device__ __forceinline__ void sample(double, double f[4]) const { f[0] = 0.0; f[1] = 0.0; f[2] = wz; f[3] = 0.0; }
   __device__ __forceinline__ void init_cf4(double, double, double) {}
+  static constexpr bool kRF = false;
+  __device__ __forceinline__ double rf() const { return 0.0; }
+  __device__ __forceinline__ void init_cf4_pre(const double*) {}
   __device__ __forceinline__ void sample_cf4(double, bool, bool, double o1, double o2, double g1[4], double g2[4]) {
     sample(o1, g1); sample(o2, g2);
   }
@@ -273,6 +304,9 @@ template <> struct Field<FIELD_SU3_CONSTANT> {      // p = all 8 coefficients
     for (int j = 0; j < 8; ++j) f[j] = c[j];
   }
   __device__ __forceinline__ void init_cf4(double, double, double) {}
+  static constexpr bool kRF = false;
+  __device__ __forceinline__ double rf() const { return 0.0; }
+  __device__ __forceinline__ void init_cf4_pre(const double*) {}
   __device__ __forceinline__ void sample_cf4(double, bool, bool, double o1, double o2, double g1[8], double g2[8]) {
     sample(o1, g1); sample(o2, g2);
   }
@@ -300,6 +334,13 @@ template <> struct Field<FIELD_SU3_DRIVE> {
   __device__ __forceinline__ void init_cf4(double g1dt, double g2dt, double dt) {
     sincos(wd * g1dt, &s1, &c1); sincos(wd * g2dt, &s2, &c2);
     ps.init(wd, ph0, dt);
+  }
+  // RF phase stepper: init_cf4 with its three sincos — of ω·g1δt, ω·g2δt, ω·δt — supplied in t[0..5] as (s, c)
+  static constexpr bool kRF = true;
+  __device__ __forceinline__ double rf() const { return wd; }
+  __device__ __forceinline__ void init_cf4_pre(const double* t) {
+    s1 = t[0]; c1 = t[1]; s2 = t[2]; c2 = t[3];
+    ps.init_pre(wd, ph0, t[4], t[5]);
   }
   __device__ __forceinline__ void sample_cf4(double base, bool anchor, bool, double, double, double g1[8], double g2[8]) {
     ps.next(base, anchor);
@@ -353,6 +394,12 @@ struct FrameCF4 {
     sincos(omega_r * g1dt, &s1, &c1);
     sincos(omega_r * g2dt, &s2, &c2);
     ps.init(omega_r, 0.0, dt);
+  }
+  // the same with the three (s, c) supplied in t[0..5] (warp_trig)
+  __device__ __forceinline__ void init_pre(double omega_r, const double* t) {
+    wr = omega_r;
+    s1 = t[0]; c1 = t[1]; s2 = t[2]; c2 = t[3];
+    ps.init_pre(omega_r, 0.0, t[4], t[5]);
   }
   template <int NC = 4, bool ZERO_Y = false>
   __device__ __forceinline__ void apply(double base, bool anchor, double* f1, double* f2) {
