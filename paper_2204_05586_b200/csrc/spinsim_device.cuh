@@ -115,8 +115,14 @@ template <int F> struct Field;
 
 // e^{i(ph0 + w·base_l)} along the fine steps of one interval: an exact sincos on anchor steps (every kAnchor-th step
 // of a lane, and its first), otherwise advanced by the per-interval rotation e^{iwδt} (error ≲ kAnchor·2 ulp of a
-// unit vector; the grid's base_l = fl(l·δt) differs from l·δt by < 1 ulp, i.e. ≲ 1e-15 rad at |w δt| ≤ 5).
-constexpr int kAnchor = 8;
+// unit vector, ≲ 7e-15 rad at kAnchor = 32; the grid's base_l = fl(l·δt) differs from l·δt by < 1 ulp, i.e.
+// ≲ 1e-15 rad at |w δt| ≤ 5).  Anchors every 8 / 16 / 32 / 64 steps (profiles/r02/s13_anchor/): C4 1.50 / 1.57 / 1.61 /
+// 1.63e11 fine steps/s, C5 analytic 1.248 / 1.187 / 1.188 ms, the 3×3 paths unchanged (their L = 10 intervals anchor
+// once); parity unchanged (the C4 every-state check passes at 64).
+#ifndef SS_ANCHOR
+#define SS_ANCHOR 32
+#endif
+constexpr int kAnchor = SS_ANCHOR;
 struct PhaseStepper {
   double w, ph0, cd, sd, c, s;
   __device__ __forceinline__ void init(double w_, double ph0_, double dt) {
