@@ -167,10 +167,11 @@ __device__ __forceinline__ void interval_residual(const IntervalParams& prm, int
 
   constexpr int DA = AccDim<SPIN, EXPO>::D;         // accumulated residual: SU(2) form (2) or dense 3×3
   // SU(2) closed form: |a| ≤ (|w+| + |w−|)·|f| (CF4) or δt·|f| ≤ 2^-13 on every step of this interval ⇒ short series
-  bool su2_short = false;
+  int su2_ser = 0;
   if constexpr (DA == 2 && sizeof(T) == 8) {
     const double rb = (METHOD == CF4 ? fabs(prm.wpd) + fabs(prm.wmd) : prm.dt) * field_bound(fld, omega_r, 0);
-    su2_short = rb * 1.01 <= 1.220703125e-04;        // 2^-13 with a margin for the rounding of a and of the bound
+    // 2^-13 / 2^-7 with a margin for the rounding of a and of the bound (expo_su2's short / medium series)
+    su2_ser = rb * 1.01 <= 1.220703125e-04 ? 2 : (rb * 1.01 <= 0.0078125 ? 1 : 0);
   }
   Res<DA, T> A;   // U_r − I, U_r initialised to the identity
   res_zero(A);
@@ -179,7 +180,7 @@ __device__ __forceinline__ void interval_residual(const IntervalParams& prm, int
   // meet the neural field's pulse window) are compile-time, so the step body carries no per-step branches for them.
   auto step = [&](int64_t l, auto anchor_c, auto pulse_c, auto short_c) {
     const bool ANCHOR = anchor_c.value, PULSE = pulse_c.value;   // compile-time for BoolC, run-time for RtBool
-    const bool SHORT = short_c.value;
+    const int SER = short_c.value;
     const double base = __dmul_rn((double)l, prm.dt);
     Res<DA, T> u;
     if (METHOD == CF4) {
@@ -236,12 +237,12 @@ __device__ __forceinline__ void interval_residual(const IntervalParams& prm, int
       // one exponential is live in registers (occupancy).  Residual form: A ← e + A + e·A.
       {
         Res<DA, T> e;
-        Expo<SPIN, EXPO, T>::run(a1, prm.tau, e, SHORT);
+        Expo<SPIN, EXPO, T>::run(a1, prm.tau, e, SER);
         res_mul(e, A, u);
       }
       {
         Res<DA, T> e;
-        Expo<SPIN, EXPO, T>::run(a2, prm.tau, e, SHORT);
+        Expo<SPIN, EXPO, T>::run(a2, prm.tau, e, SER);
         res_mul(e, u, A);
       }
       return;
@@ -263,7 +264,7 @@ __device__ __forceinline__ void interval_residual(const IntervalParams& prm, int
       T a[NC];
 #pragma unroll
       for (int j = 0; j < NC; ++j) a[j] = (T)(f[j] * prm.dt);
-      Expo<SPIN, EXPO, T>::run(a, prm.tau, u, SHORT);
+      Expo<SPIN, EXPO, T>::run(a, prm.tau, u, SER);
     }
     // a7: U_r ← u·U_r, residual form: A ← u + A + u·A.
     Res<DA, T> An;
@@ -284,10 +285,11 @@ __device__ __forceinline__ void interval_residual(const IntervalParams& prm, int
     // the short-series choice too (SS_SU2_SHORT_BODIES)
     auto with_pulse = [&](auto pulse_c) {
       if constexpr (SS_SU2_SHORT_BODIES && sizeof(T) == 8) {
-        if (su2_short) run_steps(pulse_c, BoolC<true>{});
-        else run_steps(pulse_c, BoolC<false>{});
+        if (su2_ser == 2) run_steps(pulse_c, IntC<2>{});
+        else if (su2_ser == 1) run_steps(pulse_c, IntC<1>{});
+        else run_steps(pulse_c, IntC<0>{});
       } else {
-        run_steps(pulse_c, RtBool{su2_short});
+        run_steps(pulse_c, RtInt{su2_ser});
       }
     };
     if (field_pulse_possible(fld, prm.dt_out, 0)) with_pulse(BoolC<true>{});
@@ -296,7 +298,7 @@ __device__ __forceinline__ void interval_residual(const IntervalParams& prm, int
     // 3×3 paths: one body with a run-time anchor test (four specialised copies spill more: C3 −2.5 %, measured)
 #pragma unroll 1
     for (int64_t l = l_begin; l < l_end; ++l)
-      step(l, RtBool{((l - l_begin) % kAnchor) == 0}, BoolC<true>{}, BoolC<false>{});
+      step(l, RtBool{((l - l_begin) % kAnchor) == 0}, BoolC<true>{}, IntC<0>{});
   }
 
   A_out = A;
@@ -345,32 +347,55 @@ __device__ __forceinline__ void make_op(const Res<2, T>& A, double omega_r, cons
 // Fused path (DESIGN.md §5 item 16; SURVEY §8(a) a9 "Fusion"): this thread owns the n ≤ ipt consecutive intervals
 // [k_lo, k_lo + n) of sweep b, writes each U_k and folds it into the run product G ← U_k·G (later·earlier),
 // held in shared memory (the kernels sit at their register budget), then writes G to run_agg[slot].
-template <class M, int SPIN, int EXPO, int METHOD, int FIELD, typename T>
+template <class M>
+__device__ __forceinline__ void run_fold(double2* acc, const M& op, double2* dst) {
+  M g;
+  cm_load(acc, g);
+  cm_store(acc, cm_mul(op, g));
+  cm_store(dst, op);
+}
+template <int SPIN, int EXPO, int METHOD, int FIELD, typename T>
 __device__ __forceinline__ void interval_run(const IntervalParams& prm, int64_t b, int64_t k_lo, int64_t n,
                                              int64_t slot) {
+  constexpr int D = SpinDim<SPIN>::D, DA = AccDim<SPIN, EXPO>::D;
+  // the operator format is a run-time choice, but the step loop (interval_residual) appears once in the code: only
+  // the small per-interval fold is specialised per format (two inlined copies of the loop bodies defeated inlining)
+  [[maybe_unused]] const bool su = DA == 2 && prm.op_format == OP_SU2;
   extern __shared__ __align__(16) double2 ss_run_smem[];
-  double2* acc = ss_run_smem + threadIdx.x * M::W;
-  {
-    M e;
-    cm_eye(e);
-    cm_store(acc, e);
-  }
+  double2* acc = ss_run_smem + threadIdx.x * (D * D);
+  if (DA == 2 && su) { SU<D> e; cm_eye(e); cm_store(acc, e); }
+  else { CM<D> e; cm_eye(e); cm_store(acc, e); }
   double2* U = reinterpret_cast<double2*>(prm.unitaries);
 #pragma unroll 1
   for (int64_t j = 0; j < n; ++j) {
-    Res<AccDim<SPIN, EXPO>::D, T> A;
+    Res<DA, T> A;
     double omega_r;
     ExitTrig ex;
     interval_residual<SPIN, EXPO, METHOD, FIELD, T>(prm, b, prm.k_begin + k_lo + j, 0, prm.L, A, omega_r, ex);
-    M op, g;
+    const int64_t i = b * prm.k_count + k_lo + j;
+    if constexpr (DA == 2) {
+      if (su) {
+        SU<D> op;
+        make_op(A, omega_r, ex, prm, op);
+        run_fold(acc, op, U + i * 2);
+        continue;
+      }
+    }
+    CM<D> op;
     make_op(A, omega_r, ex, prm, op);
-    cm_store(U + (b * prm.k_count + k_lo + j) * M::W, op);
-    cm_load(acc, g);
-    cm_store(acc, cm_mul(op, g));
+    run_fold(acc, op, U + i * (D * D));
   }
-  M g;
+  if constexpr (DA == 2) {
+    if (su) {
+      SU<D> g;
+      cm_load(acc, g);
+      cm_store(reinterpret_cast<double2*>(prm.run_agg) + slot * 2, g);
+      return;
+    }
+  }
+  CM<D> g;
   cm_load(acc, g);
-  cm_store(reinterpret_cast<double2*>(prm.run_agg) + slot * M::W, g);
+  cm_store(reinterpret_cast<double2*>(prm.run_agg) + slot * (D * D), g);
 }
 
 // U_k of the launch's flat interval index i (sweep-major) from the residual A of the whole interval, in the output
@@ -405,13 +430,7 @@ __device__ __forceinline__ void interval_body(const IntervalParams& prm) {
     const int64_t b = gt / prm.k_stride, t = gt - b * prm.k_stride;
     if (b >= prm.batch) return;
     const int64_t k_lo = t * prm.ipt, n = min(prm.ipt, prm.k_count - k_lo);
-    if constexpr (DA == 2) {
-      if (prm.op_format == OP_SU2) {
-        interval_run<SU<D>, SPIN, EXPO, METHOD, FIELD, T>(prm, b, k_lo, n, gt);
-        return;
-      }
-    }
-    interval_run<CM<D>, SPIN, EXPO, METHOD, FIELD, T>(prm, b, k_lo, n, gt);
+    interval_run<SPIN, EXPO, METHOD, FIELD, T>(prm, b, k_lo, n, gt);
     return;
   } else {
     const int S = prm.split;

@@ -378,6 +378,8 @@ template <class F> __device__ __forceinline__ bool field_pulse_possible(const F&
 // Compile-time booleans for the interval kernel's specialised step bodies (no <type_traits> under NVRTC).
 template <bool B> struct BoolC { static constexpr bool value = B; };
 struct RtBool { bool value; };
+template <int N> struct IntC { static constexpr int value = N; };
+struct RtInt { int value; };
 
 // Rotating frame (reading R6): rotate (ωx, ωy) by θ = ω_r·t_local, shift ωz by −ω_r; ωq unchanged.
 template <int NC = 4> __device__ __forceinline__ void to_rotating_frame(double* f, double t_local, double omega_r) {
@@ -526,17 +528,24 @@ template <typename T> __device__ __forceinline__ Res<3, T> res_shfl_down(const R
 // ---- exponentiators: residual of exp(−i(ax Jx + ay Jy + az Jz + aq Q)) -----------------------------------------
 
 // Spin-half closed form: exp(−i a·σ/2) = cos(r/2) I − i (sin(r/2)/r) a·σ.  cos(r/2) − 1 = −2 sin²(r/4).
+// series (FP64): 2 = the caller guarantees r ≤ 2^-13, 1 = r ≤ 2^-7, 0 = no bound (interval_residual bounds |a| once per
+// interval from the field's magnitude bound).  The short series keeps two terms of each function (the dropped r⁶/46080
+// and r⁴/3840 are < 1.2e-19 relative), the medium one three (dropped r⁸/10321920 and r⁶/645120: < 7e-19 relative at
+// r = 2^-7), the full one five below r = 2^-4 and the library sincos above.  Former description of the short case:
 // short_series: the caller guarantees r ≤ 2^-13 for this argument (interval_body bounds |a| once per interval from
 // the field's magnitude bound, field_bound): then two series terms each suffice — the dropped r⁶/46080 and r⁴/3840
 // are < 1.2e-19 relative (DESIGN.md §5 item 15).  A per-step test instead costs an FP64 compare per exponential and,
 // where lanes straddle the bound (C5's 100 ns steps), both series.
 template <typename T>
-__device__ __forceinline__ void expo_su2(const T a[4], Res<2, T>& e, bool short_series = false) {
+__device__ __forceinline__ void expo_su2(const T a[4], Res<2, T>& e, int series = 0) {
   const T r2 = a[0] * a[0] + a[1] * a[1] + a[2] * a[2];
   T cm1, s;
-  if (sizeof(T) == 8 && short_series) {
+  if (sizeof(T) == 8 && series == 2) {
     cm1 = r2 * fmaT(r2, T(kSu2Series[3]), T(kSu2Series[4]));
     s = fmaT(r2, T(kSu2Series[8]), T(kSu2Series[9]));
+  } else if (sizeof(T) == 8 && series == 1) {
+    cm1 = r2 * fmaT(r2, fmaT(r2, T(kSu2Series[2]), T(kSu2Series[3])), T(kSu2Series[4]));
+    s = fmaT(r2, fmaT(r2, T(kSu2Series[7]), T(kSu2Series[8])), T(kSu2Series[9]));
   } else if (r2 <= T(0.00390625)) {
     // r ≤ 2^-4 (every fine step of the configs): both functions are even, so series in r² need no sqrt, sincos
     // or division.  cos(r/2) − 1 = −r²/8 + r⁴/384 − r⁶/46080 + r⁸/10321920 − r¹⁰/3715891200,
@@ -1010,18 +1019,18 @@ template <typename T> __device__ __forceinline__ void trotter_residual_su3(const
 }
 
 template <int SPIN, int EXPO, typename T> struct Expo;
-// run(a, τ, e, short_series): short_series (the caller's per-interval bound r ≤ 2^-13) only matters for the SU(2)
-// closed form.
+// run(a, τ, e, series): the series choice (the caller's per-interval bound on r, see expo_su2) only matters for the
+// SU(2) closed form.
 template <int EXPO, typename T> struct Expo<SPIN_HALF, EXPO, T> {
-  __device__ __forceinline__ static void run(const T a[4], int, Res<2, T>& e, bool sh = false) { expo_su2<T>(a, e, sh); }
+  __device__ __forceinline__ static void run(const T a[4], int, Res<2, T>& e, int ser = 0) { expo_su2<T>(a, e, ser); }
 };
 template <typename T> struct Expo<SPIN_ONE, EXP_LIE_TROTTER, T> {
-  __device__ __forceinline__ static void run(const T a[4], int tau, Res<3, T>& e, bool = false) {
+  __device__ __forceinline__ static void run(const T a[4], int tau, Res<3, T>& e, int = 0) {
     trotter_residual<T>(a, tau, e);
   }
 };
 template <typename T> struct Expo<SPIN_ONE, EXP_LIE_TROTTER_SU3, T> {
-  __device__ __forceinline__ static void run(const T* a, int tau, Res<3, T>& e, bool = false) {
+  __device__ __forceinline__ static void run(const T* a, int tau, Res<3, T>& e, int = 0) {
     trotter_residual_su3<T>(a, tau, e);
   }
 };
@@ -1033,7 +1042,7 @@ template <typename T> __device__ __forceinline__ void expo_spin1_analytic(const 
 // The analytic spin-one path accumulates in SU(2) and maps once: D¹ is a homomorphism, so D¹(u_L)⋯D¹(u_1) =
 // D¹(u_L⋯u_1) — the same interval operator, exactly (DESIGN.md §5 item 11).  Expo returns the SU(2) residual.
 template <typename T> struct Expo<SPIN_ONE, EXP_ANALYTIC, T> {
-  __device__ __forceinline__ static void run(const T a[4], int, Res<2, T>& e, bool sh = false) { expo_su2<T>(a, e, sh); }
+  __device__ __forceinline__ static void run(const T a[4], int, Res<2, T>& e, int ser = 0) { expo_su2<T>(a, e, ser); }
 };
 
 // Dimension of the residual the interval kernel accumulates: 2 (SU(2) form) for spin-half and for the analytic
