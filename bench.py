@@ -403,6 +403,45 @@ def shard_of(args, rank, world):
     return rank * per, min(full.batch, (rank + 1) * per), full
 
 
+def paper_benchmark(args, dev, steps: int = 20):
+    """The paper's own benchmark (C2: one spin-one Eq. neural_pulse simulation, 100 ms at δt = 100 ns, P:866-870;
+    SURVEY §8(d) reports it beside C3) timed after the headline line's timed region, so the default run shows it:
+    device fine steps/s and the interval kernel's counted-flop fraction of the FP64 peak."""
+    import torch
+    import paper_2204_05586_b200 as ss
+    w = get_workload("C2", 1)
+    sim = ss.Simulator(w.spin, w.method, w.expo, w.tau, w.frame, args.precision, w.field)
+    sweep, psi0 = torch.from_numpy(w.sweep).to(dev), torch.from_numpy(w.psi0).to(dev)
+    states = torch.empty((1, w.K + 1, w.dim), dtype=torch.complex128, device=dev)
+    ws = torch.empty(sim.workspace_bytes(1, w.K, True), dtype=torch.uint8, device=dev)
+    sim.evaluate(sweep, w.t0, w.t0 + w.dt_out, w.dt_int, w.dt_out, psi0, want_unitaries=False)
+    sim.set_validation(False)
+    stream = torch.cuda.current_stream()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    t_int = []
+    for i in range(3 + steps):
+        if i == 3:
+            torch.cuda.synchronize()
+            ev[0].record(stream)
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        e[0].record(stream)
+        sim.set_split_event(e[1])
+        sim.evaluate(sweep, w.t0, w.t1, w.dt_int, w.dt_out, psi0, want_unitaries=False, workspace=ws, out_states=states)
+        sim.set_split_event(None)
+        e[2].record(stream)
+        if i >= 3:
+            t_int.append(e)
+    ev[1].record(stream)
+    torch.cuda.synchronize()
+    ms = ev[0].elapsed_time(ev[1]) / steps
+    ms_int = float(np.mean([e[0].elapsed_time(e[1]) for e in t_int]))
+    flops = algorithmic_flops_per_fine_step(w.spin, w.expo, w.tau, w.method) * w.fine_steps
+    return {"workload": "C2", "value": w.fine_steps / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "steps": steps,
+            "interval_ms": ms_int, "roofline_frac": flops / (ms_int * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
+            "note": "one simulation of 1e5 intervals x 10 steps (2.6 waves of interval threads); timed after the "
+                    "headline's timed region"}
+
+
 def run_ours(args, rank, world, local):
     import torch
     import paper_2204_05586_b200 as ss
@@ -537,6 +576,8 @@ def run_ours(args, rank, world, local):
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
             "fine_steps_per_step": total_steps,
         }
+        if world == 1 and args.workload == "C3" and not emulated and not args.no_secondary:
+            line["paper_benchmark"] = paper_benchmark(args, dev)
         if emulated:
             line["emulated"] = {"ranks": args.emulate_ranks, "rank": 0, "sweeps_per_rank": B,
                                 "predicted_value": value * args.emulate_ranks,
@@ -671,6 +712,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-probe", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the paper-benchmark (C2) side measurement")
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
                     help="gloo only to exercise the multi-rank code path where NCCL cannot run (e.g. ranks sharing a GPU)")
     ap.add_argument("--share-gpu", action="store_true", help="map every rank to cuda:0 (code-path test, not timing)")

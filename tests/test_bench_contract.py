@@ -48,6 +48,8 @@ def test_device_arm_contract():
     # waves at 4 intervals per thread, DESIGN.md §5 item 16)
     assert d["gpu_launches"] in (2 * d["steps"], 3 * d["steps"])
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
+    pb = d["paper_benchmark"]                      # the paper's own benchmark (C2) beside the headline
+    assert pb["workload"] == "C2" and pb["value"] > 0 and 0 < pb["roofline_frac"] < 1.0
 
 
 def test_flop_model():
