@@ -135,3 +135,47 @@ def test_fused_host_pipeline(ss, monkeypatch, name):
         st_h, _ = sim.evaluate_host(w.sweep, w.t0, w.t1, w.dt_int, w.dt_out, w.psi0, want_unitaries=False,
                                     n_chunks=chunks)
         assert np.abs(st_h - st0).max() <= 1e-12, chunks
+
+
+NEURAL_USER_SRC = r"""
+__device__ void user_field(double t_k, double off, const double* p, double f[4]) {
+  const double t = t_k + off;
+  f[0] = 2.0 * p[2] * cos(p[1] * t);
+  const double x = p[4] * ((t_k - p[5]) + off);
+  f[2] = p[0] + ((x >= 0.0 && x <= 6.283185307179586) ? p[3] * sin(x) : 0.0);
+  f[3] = p[6];
+}
+"""
+
+
+@pytest.mark.parametrize("spin", ["half", "one"])
+def test_fused_user_field(ss, orc, monkeypatch, spin):
+    """The run-time compiled (NVRTC) interval kernel takes the fused mode too (its dynamic shared memory and mode
+    branch): a user copy of Eq. neural_pulse against the oracle's built-in field, ipt forced."""
+    w = _shape("half" if spin == "half" else "one_lt")
+    monkeypatch.setenv("SPINSIM_FUSED", "1")
+    monkeypatch.setenv("SPINSIM_FUSED_IPT", "8")
+    sim = ss.Simulator(w.spin, w.method, w.expo, w.tau, w.frame, "fp64", "user", field_source=NEURAL_USER_SRC,
+                       n_params=7)
+    n0 = ss.kernel_launches()
+    for want_unitaries in (False, True):
+        res = sim.evaluate(torch.from_numpy(w.sweep).cuda(), w.t0, w.t1, w.dt_int, w.dt_out,
+                           torch.from_numpy(w.psi0).cuda(), want_unitaries=want_unitaries)
+        assert np.abs(res.state.cpu().numpy() - _oracle(orc, w)[0]).max() <= 1e-10
+    assert ss.kernel_launches() - n0 >= 2 * 4                # validation, interval, coarse scan, run chain (each call)
+
+
+@pytest.mark.parametrize("expo", ["lie_trotter", "analytic"])
+def test_fused_fp32(ss, orc, monkeypatch, expo):
+    """FP32 mode through the fused path (the FP64 run products and run chain over the FP32 kernel's operators)
+    against the oracle at the FP32 bar, and against the unfused FP32 path to rounding."""
+    w = _shape("one_lt" if expo == "lie_trotter" else "one_an")
+    monkeypatch.setenv("SPINSIM_FUSED_IPT", "8")
+    sim32 = ss.Simulator(w.spin, w.method, w.expo, w.tau, w.frame, "fp32", w.field)
+    sweep, psi0 = torch.from_numpy(w.sweep).cuda(), torch.from_numpy(w.psi0).cuda()
+    monkeypatch.setenv("SPINSIM_FUSED", "1")
+    st32 = sim32.evaluate(sweep, w.t0, w.t1, w.dt_int, w.dt_out, psi0, want_unitaries=False).state.cpu().numpy()
+    monkeypatch.setenv("SPINSIM_FUSED", "0")
+    st32u = sim32.evaluate(sweep, w.t0, w.t1, w.dt_int, w.dt_out, psi0, want_unitaries=False).state.cpu().numpy()
+    assert np.abs(st32 - _oracle(orc, w)[0]).max() <= 1e-4
+    assert np.abs(st32 - st32u).max() <= 1e-12            # same FP32 operators, two FP64 product associations
