@@ -131,7 +131,8 @@ int ss_plan(double time_start, double time_end, double time_step_integration, do
             int64_t* K, int64_t* L, double* dt_fine);
 
 /* Device workspace needed by ss_evaluate for `batch` sweeps of K intervals; includes room for the interval
- * unitaries when the caller passes d_unitaries = NULL. */
+ * unitaries when the caller passes d_unitaries = NULL, and — below the chain kernel's 4096 sweeps — for the fused
+ * path's run aggregates and run start states (at most ⌈K/4⌉ + ⌈K/4⌉ + 1 per sweep). */
 size_t ss_workspace_bytes(const ss_sim* sim, int64_t batch, int64_t K, int32_t unitaries_in_workspace);
 
 /* Whole hot path on device buffers: interval kernel (§8(a) rows a1–a8) then the state scan (a9).
@@ -143,8 +144,13 @@ size_t ss_workspace_bytes(const ss_sim* sim, int64_t batch, int64_t K, int32_t u
  * With d_unitaries == NULL on the SU(2)-form paths (spin-half; ANALYTIC spin-one) the interval operators reach the
  * scan in the workspace as SU(2) elements (a, b) of U = [[a, b], [−b*, a*]] (32 B per interval instead of 64 / 144 B;
  * D¹ of it for spin-one, reading R14) — the same operators, so the states agree with the dense path to
- * rounding.  Validates sweep/state finiteness (and ω_q ≡ 0 for ANALYTIC spin-one) with a tiny device check that
- * synchronises the stream once, unless disabled by ss_set_validation(sim, 0). */
+ * rounding.  Long problems below 4096 sweeps (≥ 16 waves of interval threads at 4 intervals per thread, K divisible
+ * by the run length) take the fused path (DESIGN.md §5 item 16): each interval-kernel thread computes ipt ∈ {4, 8,
+ * 16, 32} consecutive U_k and their run product, a coarse scan over the run products gives the run start states, and
+ * a run chain writes the states — U_k bit for bit as on the unfused path, states equal to rounding (a different
+ * product association; the scan's association is never part of the contract).  Validates sweep/state finiteness
+ * (and ω_q ≡ 0 for ANALYTIC spin-one) with a tiny device check that synchronises the stream once, unless disabled by
+ * ss_set_validation(sim, 0). */
 int ss_evaluate(ss_sim* sim, double time_start, double time_end, double time_step_integration,
                 double time_step_output, int64_t batch, const double* d_sweep, const double* d_state_init,
                 double* d_states, double* d_unitaries, void* d_workspace, size_t workspace_bytes, void* stream);
@@ -154,8 +160,8 @@ int ss_evaluate(ss_sim* sim, double time_start, double time_end, double time_ste
 int ss_set_validation(ss_sim* sim, int32_t enabled);
 
 /* Profiling hook: `event` (a cudaEvent_t passed as void*, owned by the caller; NULL to clear) is recorded by every
- * later ss_evaluate on its stream between the interval kernel and the state scan, so a caller can time the two
- * phases of one call with its own events around it.  No other effect. */
+ * later ss_evaluate (and every chunk of ss_evaluate_host) on its stream between the interval kernel and the state
+ * scan, so a caller can time the two phases of one call with its own events around it.  No other effect. */
 int ss_set_split_event(ss_sim* sim, void* event);
 
 /* Interval kernel only (rows a1–a8) for global interval indices k ∈ [k_begin, k_begin + k_count) of a grid of K
