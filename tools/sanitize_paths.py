@@ -1,0 +1,62 @@
+"""Small end-to-end calls through every round-2 kernel path, for compute-sanitizer (memcheck / racecheck / synccheck /
+initcheck): the fused interval kernel (compact and dense operators, both spins, every exponentiator, FP32), the coarse
+scans, the warp-cooperative run chain (cp.async staging, in-place states), warp-shared trigonometry (full and partial
+warps), and the NVRTC user-field kernel in fused mode.
+
+    compute-sanitizer --tool memcheck python tools/sanitize_paths.py
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2204_05586_b200 as ss  # noqa: E402
+import workloads as W  # noqa: E402
+
+USER = r"""
+__device__ void user_field(double t_k, double off, const double* p, double f[4]) {
+  f[0] = 2.0 * p[2] * cos(p[1] * (t_k + off)); f[2] = p[0]; f[3] = p[6];
+}
+"""
+
+
+def run(w, precision="fp64", want_unitaries=False, field=None, **env):
+    for k, v in env.items():
+        os.environ[k] = str(v)
+    if field == "user":
+        sim = ss.Simulator(w.spin, w.method, w.expo, w.tau, w.frame, precision, "user", field_source=USER, n_params=7)
+    else:
+        sim = ss.Simulator(w.spin, w.method, w.expo, w.tau, w.frame, precision, w.field)
+    res = sim.evaluate(torch.from_numpy(w.sweep).cuda(), w.t0, w.t1, w.dt_int, w.dt_out,
+                       torch.from_numpy(w.psi0).cuda(), want_unitaries=want_unitaries)
+    torch.cuda.synchronize()
+    for k in env:
+        del os.environ[k]
+    return float(np.abs(res.state.cpu().numpy()).sum())
+
+
+def main():
+    half = W.c4_long(duration=256e-6, dt_int=200e-9).with_(
+        sweep=np.repeat(W.c4_long().sweep, 3, 0), psi0=W.random_states(3, 2, 1))
+    one_lt = W.c5_matrix("lie_trotter", batch=2).with_(t1=96e-6, dt_int=200e-9, psi0=W.random_states(2, 3, 2))
+    one_an = W.c5_matrix("analytic", batch=3).with_(t1=160e-6, dt_int=200e-9, psi0=W.random_states(3, 3, 3))
+    su3 = W.g1_su3(batch=2, duration=64e-6).with_(dt_int=200e-9, psi0=W.random_states(2, 3, 4))
+    for w in (half, one_lt, one_an, su3):
+        for wu in (False, True):
+            for ipt in (4, 8, 32):
+                run(w, want_unitaries=wu, SPINSIM_FUSED_IPT=ipt)
+        run(w, SPINSIM_FUSED=0)
+        for path in ("coop", "scan2", "scan3", "scan4", "chain"):
+            run(w, SPINSIM_FUSED_IPT=8, SPINSIM_SCAN_PATH=path)
+    run(one_lt, precision="fp32", SPINSIM_FUSED_IPT=8)
+    run(one_an, precision="fp32", SPINSIM_FUSED_IPT=8)
+    run(one_lt, field="user", SPINSIM_FUSED_IPT=8)
+    # a partial last warp (K·batch not a multiple of 32) and sweeps straddling warps: warp_trig's fallback
+    run(W.c5_matrix("lie_trotter", batch=3).with_(t1=37e-6, psi0=W.random_states(3, 3, 5)))
+    print("ok")
+
+
+if __name__ == "__main__":
+    main()
