@@ -48,7 +48,7 @@ def main():
         res[f"{kernel}@{tag}"] = {
             "flops_per_fine_step": 2 * dfma + dmul + dadd, "dfma": dfma, "dmul": dmul, "dadd": dadd,
             "fp64_pipe_pct": m["sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"],
-            "source": f"profiles/r02/flops/flops_{tag}.csv"}
+            "source": f"profiles/r02/{os.path.basename(os.path.normpath(out))}/flops_{tag}.csv"}
         print(tag, json.dumps(res[f"{kernel}@{tag}"]))
     json.dump(res, open(os.path.join(out, "executed_flops.json"), "w"), indent=1)
 
