@@ -800,198 +800,6 @@ __global__ void __launch_bounds__(Scan3Cfg<M>::NT, 1)
   bulk_wait_all();
 }
 
-// ---- state scan v4: register-resident tiles, many short-lived CTAs, warp-parallel decoupled look-back ------------
-//
-// A CTA takes the next ticket t (j-major: tile j of sweep b, t = j·batch + b) and holds its tile — NT·C consecutive
-// operators, thread i owning the C at [i·C, (i+1)·C) — in REGISTERS: loaded once from HBM (all C·W 16-byte loads of a
-// thread in flight at once), multiplied into the thread product, scanned (warp Kogge–Stone + warp totals), and after
-// the look-back applied again from the same registers to write the states.  No shared-memory ring, no second pass
-// over memory: the bytes moved are the algorithmic ones.  Latency is hidden across CTAs instead of inside one — several
-// CTAs per SM, each short-lived, so while one waits on its predecessor's flag the others stream.  C = 8 compact SU(2)
-// operators (32 registers), 4 dense 2×2 or 2 dense 3×3 per thread.
-template <class M> struct Scan4Cfg {
-  static constexpr int NT = 128, NW = NT / 32;
-  static constexpr int C = (M::W == 2) ? 8 : (M::W == 4 ? 4 : 2);
-  static constexpr int TILE = NT * C;
-};
-template <class M> struct Scan4Layout {
-  int64_t tiles_per_sweep, ntiles;
-  size_t off_flags, off_agg, off_psi, total;
-  Scan4Layout(int64_t batch, int64_t k_count) {
-    tiles_per_sweep = (k_count + Scan4Cfg<M>::TILE - 1) / Scan4Cfg<M>::TILE;
-    ntiles = batch * tiles_per_sweep;
-    off_flags = 256;
-    off_agg = align256(off_flags + sizeof(int) * (size_t)ntiles);
-    off_psi = align256(off_agg + sizeof(double2) * M::W * (size_t)ntiles);
-    total = align256(off_psi + sizeof(double2) * M::SD * (size_t)ntiles);
-  }
-};
-
-template <class M>
-__global__ void __launch_bounds__(Scan4Cfg<M>::NT) scan4_kernel(const Scan2Args a) {
-  constexpr int D = M::SD, W = M::W;
-  constexpr int NT = Scan4Cfg<M>::NT, NW = Scan4Cfg<M>::NW, C = Scan4Cfg<M>::C, TILE = Scan4Cfg<M>::TILE;
-  __shared__ double2 sWarpTot[NW][W];
-  __shared__ double2 sWarpPre[NW][W];
-  __shared__ double2 sPsiIn[D];
-  __shared__ long long sTicket;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) sTicket = (long long)atomicAdd(a.ticket, 1ull);
-  __syncthreads();
-  const long long t = sTicket;
-  const long long j = t / a.batch, b = t - j * a.batch;
-  const long long k0 = j * TILE + (long long)tid * C;           // this thread's first interval
-  const int n = (int)max(0LL, min((long long)C, a.k_count - k0));
-
-  // 1. the thread's C operators into registers (streaming loads, all in flight), thread product P = U_{C−1} ⋯ U_0
-  M u[C];
-  const double2* gU = a.U + ((size_t)b * a.k_count + k0) * W;
-#pragma unroll
-  for (int c = 0; c < C; ++c) {
-    if (c < n) {
-      if constexpr (W == 2) {
-        const double2 x = __ldcs(gU + 2 * c), y = __ldcs(gU + 2 * c + 1);
-        u[c].ar = x.x; u[c].ai = x.y; u[c].br = y.x; u[c].bi = y.y;
-      } else {
-#pragma unroll
-        for (int e = 0; e < W; ++e) { const double2 x = __ldcs(gU + c * W + e); u[c].re[e] = x.x; u[c].im[e] = x.y; }
-      }
-    } else {
-      cm_eye(u[c]);
-    }
-  }
-  M P = u[0];
-#pragma unroll
-  for (int c = 1; c < C; ++c) P = cm_mul(u[c], P);
-
-  // 2. warp inclusive scan (later·earlier) → exclusive X; warp totals → exclusive warp prefixes + tile total
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const M q = cm_shfl_up(P, off);
-    if (lane >= off) P = cm_mul(P, q);
-  }
-  M X = cm_shfl_up(P, 1);
-  if (lane == 0) cm_eye(X);
-  if (lane == 31) cm_store(sWarpTot[warp], P);
-  __syncthreads();
-
-  if (warp == 0) {
-    M T;
-    if (lane < NW) cm_load(sWarpTot[lane], T); else cm_eye(T);
-#pragma unroll
-    for (int off = 1; off < NW; off <<= 1) {
-      const M q = cm_shfl_up(T, off);
-      if (lane >= off) T = cm_mul(T, q);
-    }
-    M Wx = cm_shfl_up(T, 1);
-    if (lane == 0) cm_eye(Wx);
-    if (lane < NW) cm_store(sWarpPre[lane], Wx);
-    const M tot = cm_shfl_idx(T, NW - 1);
-    // 3. publish AGG, warp-parallel look-back (lane ℓ inspects predecessor j − 1 − ℓ − 32r), publish PREFIX
-    double pr[D], pi[D];
-    if (j == 0) {
-#pragma unroll
-      for (int d = 0; d < D; ++d) { const double2 v = a.psi0[b * D + d]; pr[d] = v.x; pi[d] = v.y; }
-    } else {
-      if (lane == 0) {
-        cm_store(a.agg + (size_t)t * W, tot);
-        cuda::atomic_ref<int, cuda::thread_scope_device>(a.flags[t]).store(FLAG_AGG, cuda::memory_order_release);
-      }
-      M Mlb;
-      cm_eye(Mlb);
-      for (long long jb = j - 1;; jb -= 32) {
-        const long long jq = jb - lane;
-        const long long q = jq * a.batch + b;
-        int fv = FLAG_PREFIX;                       // lanes before tile 0 never matter (tile 0 is PREFIX)
-        if (jq >= 0) {
-          cuda::atomic_ref<int, cuda::thread_scope_device> f(a.flags[q]);
-          while ((fv = f.load(cuda::memory_order_acquire)) == FLAG_EMPTY) __nanosleep(32);
-        }
-        const unsigned pm = __ballot_sync(0xffffffffu, fv == FLAG_PREFIX);
-        const int first = pm ? __ffs(pm) - 1 : 32;
-        if (first > 0) {                            // product of the aggregates of lanes < first (nearest first)
-          M A;
-          if (lane < first) cm_load_cg(a.agg + (size_t)q * W, A); else cm_eye(A);
-#pragma unroll
-          for (int off = 1; off < 32; off <<= 1) {
-            const M o = cm_shfl_down(A, off);
-            if ((lane & (2 * off - 1)) == 0) A = cm_mul(A, o);
-          }
-          Mlb = cm_mul(Mlb, A);                     // meaningful in lane 0
-        }
-        if (first < 32) {
-          double er[D], ei[D];
-          if (lane == first)
-            for (int d = 0; d < D; ++d) { const double2 v = __ldcg(a.psi_end + q * D + d); er[d] = v.x; ei[d] = v.y; }
-#pragma unroll
-          for (int d = 0; d < D; ++d) {
-            er[d] = __shfl_sync(0xffffffffu, er[d], first);
-            ei[d] = __shfl_sync(0xffffffffu, ei[d], first);
-          }
-          cm_apply(Mlb, er, ei, pr, pi);            // valid in lane 0
-          break;
-        }
-      }
-#pragma unroll
-      for (int d = 0; d < D; ++d) {
-        pr[d] = __shfl_sync(0xffffffffu, pr[d], 0);
-        pi[d] = __shfl_sync(0xffffffffu, pi[d], 0);
-      }
-    }
-    if (lane == 0) {
-      double er[D], ei[D];
-      cm_apply(tot, pr, pi, er, ei);
-      for (int d = 0; d < D; ++d) a.psi_end[t * D + d] = make_double2(er[d], ei[d]);
-      cuda::atomic_ref<int, cuda::thread_scope_device>(a.flags[t]).store(FLAG_PREFIX, cuda::memory_order_release);
-      for (int d = 0; d < D; ++d) sPsiIn[d] = make_double2(pr[d], pi[d]);
-      if (j == 0) {
-        if (a.states)
-          for (int d = 0; d < D; ++d) a.states[(size_t)b * (a.k_count + 1) * D + d] = make_double2(pr[d], pi[d]);
-        if (a.spin) {
-          double jj3[3];
-          spin_of<D>(pr, pi, jj3);
-          for (int e = 0; e < 3; ++e) a.spin[(size_t)b * (a.k_count + 1) * 3 + e] = jj3[e];
-        }
-      }
-    }
-  }
-  __syncthreads();
-
-  // 4. y = (X·W_w)·ψ_in, then the thread's operators again from registers; states written straight out
-  {
-    M Wp;
-    cm_load(sWarpPre[warp], Wp);
-    X = cm_mul(X, Wp);
-  }
-  double yr[D], yi[D];
-  {
-    double xr[D], xi[D];
-#pragma unroll
-    for (int d = 0; d < D; ++d) { xr[d] = sPsiIn[d].x; xi[d] = sPsiIn[d].y; }
-    cm_apply(X, xr, xi, yr, yi);
-  }
-  double2* gS = a.states ? a.states + ((size_t)b * (a.k_count + 1) + k0 + 1) * D : nullptr;
-  double* gJ = a.spin ? a.spin + ((size_t)b * (a.k_count + 1) + k0 + 1) * 3 : nullptr;
-#pragma unroll
-  for (int c = 0; c < C; ++c) {
-    if (c < n) {
-      double zr[D], zi[D];
-      cm_apply(u[c], yr, yi, zr, zi);
-#pragma unroll
-      for (int d = 0; d < D; ++d) { yr[d] = zr[d]; yi[d] = zi[d]; }
-      if (gS)
-#pragma unroll
-        for (int d = 0; d < D; ++d) __stcs(gS + c * D + d, make_double2(zr[d], zi[d]));
-      if (gJ) {
-        double jj3[3];
-        spin_of<D>(zr, zi, jj3);
-#pragma unroll
-        for (int e = 0; e < 3; ++e) __stcs(gJ + c * 3 + e, jj3[e]);
-      }
-    }
-  }
-}
-
 // ---- small problems: one cooperative wave with two grid-wide barriers instead of look-back -------------------------
 //
 // For problems whose operators fit in L2 (B·K·dim²·16 B ≤ 64 MB) and with few sweeps (C1, C2, C4's 1e6-interval
@@ -1308,6 +1116,7 @@ struct RunChainArgs {
   const double2* phi;             // [batch][nseg + 1][D]
   double2* states;                // [batch][K+1][D] or NULL
   double* spin;                   // [batch][K+1][3] or NULL
+  double2* agg;                   // AGG mode: [batch][nseg] run products (W double2 each)
 };
 template <class M> __host__ __device__ constexpr int run_width() { return M::W > M::SD ? M::W : M::SD; }   // double2 per interval slot
 template <class M, int SEG> __host__ __device__ constexpr int run_slot_stride() { return (SEG * run_width<M>()) | 1; }
@@ -1315,7 +1124,9 @@ template <class M, int SEG> constexpr size_t run_chain_smem() {
   return sizeof(double2) * 32 * (size_t)run_slot_stride<M, SEG>();
 }
 
-template <class M, int SEG>
+// AGG = true: the same staging, but each lane writes its run's product G = U_last ⋯ U_first (the reduce pass of the
+// standalone two-pass scan, run_two_pass) instead of chaining states.
+template <class M, int SEG, bool AGG = false>
 __global__ void __launch_bounds__(32) run_chain_kernel(const RunChainArgs a) {
   constexpr int D = M::SD, W = M::W, STR = run_slot_stride<M, SEG>();
   constexpr int OFF = SEG * (run_width<M>() - W);            // operators at the back of the slot
@@ -1335,6 +1146,20 @@ __global__ void __launch_bounds__(32) run_chain_kernel(const RunChainArgs a) {
   }
   asm volatile("cp.async.commit_group;\n cp.async.wait_group 0;" ::: "memory");
   __syncwarp();
+  if constexpr (AGG) {
+    if (lane < nw) {
+      const double2* u = smem_rc + lane * STR + OFF;
+      M G, m;
+      cm_load(u, G);
+#pragma unroll 4
+      for (int i = 1; i < SEG; ++i) {
+        cm_load(u + i * W, m);
+        G = cm_mul(m, G);
+      }
+      cm_store(a.agg + (size_t)(g0 + lane) * W, G);
+    }
+    return;
+  }
   const int64_t g = g0 + (lane < nw ? lane : 0), b = g / a.nseg, r = g - b * a.nseg;
   const size_t row = (size_t)(b * (a.k_count + 1) + r * SEG);   // state index of this run's start
   double2* slot = smem_rc + lane * STR;
@@ -1384,21 +1209,21 @@ __global__ void __launch_bounds__(32) run_chain_kernel(const RunChainArgs a) {
   }
 }
 
-template <class M, int SEG>
+template <class M, int SEG, bool AGG = false>
 static cudaError_t launch_run_chain(const RunChainArgs& a, cudaStream_t s, int* launches) {
   constexpr size_t smem = run_chain_smem<M, SEG>();
   if constexpr (smem > 48 * 1024) {
     static DeviceCache attr;
     const int dev = current_device();
     if (!attr.get(dev)) {
-      const cudaError_t e = cudaFuncSetAttribute(run_chain_kernel<M, SEG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)smem);
+      const cudaError_t e = cudaFuncSetAttribute(run_chain_kernel<M, SEG, AGG>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
       attr.set(dev, 1);
     }
   }
   const int64_t nruns = a.batch * a.nseg;
-  run_chain_kernel<M, SEG><<<(unsigned)((nruns + 31) / 32), 32, smem, s>>>(a);
+  run_chain_kernel<M, SEG, AGG><<<(unsigned)((nruns + 31) / 32), 32, smem, s>>>(a);
   ++*launches;
   return cudaGetLastError();
 }
@@ -1411,7 +1236,7 @@ static cudaError_t run_segment_chain(int64_t batch, int64_t k_count, int64_t seg
                                      double* states, double* spin, cudaStream_t s, int* launches) {
   if (seg > run_max_seg<M>() || k_count % seg != 0) return cudaErrorInvalidValue;
   const RunChainArgs a{batch, k_count, k_count / seg, reinterpret_cast<const double2*>(U),
-                       reinterpret_cast<const double2*>(phi), reinterpret_cast<double2*>(states), spin};
+                       reinterpret_cast<const double2*>(phi), reinterpret_cast<double2*>(states), spin, nullptr};
   switch (seg) {
     case 4: return launch_run_chain<M, 4>(a, s, launches);
     case 8: return launch_run_chain<M, 8>(a, s, launches);
@@ -1419,6 +1244,29 @@ static cudaError_t run_segment_chain(int64_t batch, int64_t k_count, int64_t seg
     case 32: if constexpr (run_max_seg<M>() >= 32) return launch_run_chain<M, 32>(a, s, launches); break;
   }
   return cudaErrorInvalidValue;
+}
+
+template <class M>
+static cudaError_t run_segment_aggregate(int64_t batch, int64_t k_count, int64_t seg, const double* U, double* agg,
+                                         cudaStream_t s, int* launches) {
+  if (seg > run_max_seg<M>() || k_count % seg != 0) return cudaErrorInvalidValue;
+  const RunChainArgs a{batch, k_count, k_count / seg, reinterpret_cast<const double2*>(U), nullptr, nullptr, nullptr,
+                       reinterpret_cast<double2*>(agg)};
+  switch (seg) {
+    case 4: return launch_run_chain<M, 4, true>(a, s, launches);
+    case 8: return launch_run_chain<M, 8, true>(a, s, launches);
+    case 16: if constexpr (run_max_seg<M>() >= 16) return launch_run_chain<M, 16, true>(a, s, launches); break;
+    case 32: if constexpr (run_max_seg<M>() >= 32) return launch_run_chain<M, 32, true>(a, s, launches); break;
+  }
+  return cudaErrorInvalidValue;
+}
+
+// Run length of the standalone two-pass scan for K intervals (the largest of 32, 16, 8, 4 dividing K with ≥ 2 runs),
+// 0 when none applies.
+template <class M> static int64_t two_pass_seg(int64_t k_count) {
+  for (int64_t c = run_max_seg<M>(); c >= 4; c /= 2)
+    if (k_count % c == 0 && k_count >= 2 * c) return c;
+  return 0;
 }
 
 int fused_max_ipt(int dim, int op_format) {
@@ -1511,13 +1359,24 @@ int64_t chain_min_batch() { return kChainMinBatch; }
 constexpr int kCoopMaxGrid = 1024;
 // Sized for the dense operators of this dim (the compact ones need less).
 template <class M> static size_t tile_ws_bytes(int64_t batch, int64_t k_count) {
-  return std::max({Scan2Layout<M>(batch, k_count).total, Scan3Layout<M>(batch, k_count, 1).total,
-                   Scan4Layout<M>(batch, k_count).total});
+  return std::max(Scan2Layout<M>(batch, k_count).total, Scan3Layout<M>(batch, k_count, 1).total);
+}
+// Two-pass (compact operators): [run products: batch·nseg operators][run start states: batch·(nseg + 1)][the coarse
+// scan's own workspace for (batch, nseg)].  Sized for the shortest run (4 intervals) whatever K's divisors, so the
+// total is monotone in K (the fused path's coarse scan, over K/ipt ≤ K/4 runs, fits the workspace sized for K); only
+// below the chain kernel's batch size, the only place the path is taken.
+template <class M> static size_t two_pass_ws_bytes(int64_t batch, int64_t k_count) {
+  if (batch >= kChainMinBatch || k_count < 8) return 0;
+  const int64_t nseg = (k_count + 3) / 4;
+  return align256(sizeof(double2) * M::W * (size_t)batch * nseg) +
+         align256(sizeof(double2) * M::SD * (size_t)batch * (nseg + 1)) + scan_workspace_bytes(M::SD, batch, nseg);
 }
 size_t scan_workspace_bytes(int dim, int64_t batch, int64_t k_count) {
   const size_t coop = sizeof(double2) * (size_t)dim * dim * kCoopMaxGrid;
-  return std::max(coop, dim == 2 ? std::max(tile_ws_bytes<CM<2>>(batch, k_count), tile_ws_bytes<SU<2>>(batch, k_count))
-                                 : std::max(tile_ws_bytes<CM<3>>(batch, k_count), tile_ws_bytes<SU<3>>(batch, k_count)));
+  return std::max({coop,
+                   dim == 2 ? std::max(tile_ws_bytes<CM<2>>(batch, k_count), tile_ws_bytes<SU<2>>(batch, k_count))
+                            : std::max(tile_ws_bytes<CM<3>>(batch, k_count), tile_ws_bytes<SU<3>>(batch, k_count)),
+                   dim == 2 ? two_pass_ws_bytes<SU<2>>(batch, k_count) : two_pass_ws_bytes<SU<3>>(batch, k_count)});
 }
 
 // Cooperative small-problem scan (scan_coop_kernel): returns cudaErrorNotSupported when the problem is not eligible.
@@ -1748,47 +1607,47 @@ static cudaError_t run_scan3(int64_t batch, int64_t k_count, const double* U, co
 }
 
 template <class M>
-static cudaError_t run_scan4(int64_t batch, int64_t k_count, const double* U, const double* psi0, double* states,
-                             double* spin, void* ws, cudaStream_t s, int* launches) {
-  Scan4Layout<M> L(batch, k_count);
-  if (L.ntiles > 0x7fffffffLL) return cudaErrorInvalidValue;
+static cudaError_t run_state_scan(int64_t batch, int64_t k_count, const double* U, const double* psi0, double* states,
+                                  void* ws, cudaStream_t s, int* launches, double* spin);
+
+// Standalone two-pass scan for compact SU(2) operators (reduce-then-scan, the fused path's structure with its first
+// pass as a kernel of its own): run products of `seg` consecutive operators (run_chain_kernel, AGG), a coarse scan of
+// them into the run start states, then the run chain — U read twice, each time by a plain coalesced stream, instead
+// of through a look-back tile scan.  cudaErrorNotSupported when no run length divides K.
+template <class M>
+static cudaError_t run_two_pass(int64_t batch, int64_t k_count, const double* U, const double* psi0, double* states,
+                                double* spin, void* ws, cudaStream_t s, int* launches) {
+  const int64_t seg = two_pass_seg<M>(k_count);
+  if (!seg) return cudaErrorNotSupported;
+  const int64_t nseg = k_count / seg;
   char* w = static_cast<char*>(ws);
-  Scan2Args a;
-  a.batch = batch;
-  a.k_count = k_count;
-  a.tiles_per_sweep = L.tiles_per_sweep;
-  a.ntiles = L.ntiles;
-  a.U = reinterpret_cast<const double2*>(U);
-  a.psi0 = reinterpret_cast<const double2*>(psi0);
-  a.states = reinterpret_cast<double2*>(states);
-  a.spin = spin;
-  a.ticket = reinterpret_cast<unsigned long long*>(w);
-  a.flags = reinterpret_cast<int*>(w + L.off_flags);
-  a.agg = reinterpret_cast<double2*>(w + L.off_agg);
-  a.psi_end = reinterpret_cast<double2*>(w + L.off_psi);
-  cudaError_t e = cudaMemsetAsync(w, 0, L.off_agg, s);   // ticket + flags
+  double* agg = reinterpret_cast<double*>(w);
+  w += align256(sizeof(double2) * M::W * (size_t)batch * nseg);
+  double* phi = reinterpret_cast<double*>(w);
+  w += align256(sizeof(double2) * M::SD * (size_t)batch * (nseg + 1));
+  cudaError_t e = run_segment_aggregate<M>(batch, k_count, seg, U, agg, s, launches);
   if (e != cudaSuccess) return e;
-  // one CTA per tile; a CTA's ticket is taken when it starts, so every tile it waits on is running or done
-  scan4_kernel<M><<<(unsigned)L.ntiles, Scan4Cfg<M>::NT, 0, s>>>(a);
-  ++*launches;
-  return cudaGetLastError();
+  e = run_state_scan<M>(batch, nseg, agg, psi0, phi, w, s, launches, nullptr);
+  if (e != cudaSuccess) return e;
+  return run_segment_chain<M>(batch, k_count, seg, U, phi, states, spin, s, launches);
 }
 
-// Path override for tests and measurement tools: SPINSIM_SCAN_PATH = coop | chain | scan2 | scan3 | scan4 forces
-// that kernel (coop and chain only where they apply: coop needs an L2-sized problem); unset = the heuristic below.
-// Read on every call (one getenv per scan launch), so a test can switch paths within one process.
+// Path override for tests and measurement tools: SPINSIM_SCAN_PATH = coop | chain | scan2 | scan3 | twopass forces
+// that kernel (coop and chain only where they apply: coop needs an L2-sized problem; twopass compact operators and a
+// run length dividing K); unset = the heuristic below.  Read on every call (one getenv per scan launch), so a test
+// can switch paths within one process.
 static int forced_scan_path() {
   const char* p = std::getenv("SPINSIM_SCAN_PATH");
   if (!p) return 0;
-  const char* names[] = {"", "coop", "chain", "scan2", "scan3", "scan4"};
+  const char* names[] = {"", "coop", "chain", "scan2", "scan3", "twopass"};
   for (int i = 1; i < 6; ++i)
     if (!std::strcmp(p, names[i])) return i;
   return 0;
 }
 
 // Path choice: the cooperative single-wave scan for L2-sized problems; the per-sweep chain for ≥ kChainMinBatch
-// sweeps; otherwise compact SU(2) operators take the register-resident tile scan (scan4), dense ones scan3 where its
-// tiles get ≥ 4 stages (long sweeps, moderate batch) and scan2 for the rest.
+// sweeps; otherwise compact SU(2) operators take the two-pass scan where a run length divides K, dense ones scan3
+// where its tiles get ≥ 4 stages (long sweeps, moderate batch) and scan2 for the rest.
 template <class M>
 static cudaError_t run_state_scan(int64_t batch, int64_t k_count, const double* U, const double* psi0, double* states,
                                   void* ws, cudaStream_t s, int* launches, double* spin) {
@@ -1801,12 +1660,20 @@ static cudaError_t run_state_scan(int64_t batch, int64_t k_count, const double* 
     case 2: return run_chain<M>(batch, k_count, U, psi0, states, spin, s, launches);
     case 3: return run_scan2<M>(batch, k_count, U, psi0, states, spin, ws, s, launches);
     case 4: return run_scan3<M>(batch, k_count, U, psi0, states, spin, ws, s, launches);
-    case 5: return run_scan4<M>(batch, k_count, U, psi0, states, spin, ws, s, launches);
+    case 5:
+      if constexpr (M::W == 2) {
+        const cudaError_t e = run_two_pass<M>(batch, k_count, U, psi0, states, spin, ws, s, launches);
+        if (e != cudaErrorNotSupported) return e;
+      }
+      break;
   }
   const cudaError_t e = run_scan_coop<M>(batch, k_count, U, psi0, states, spin, ws, s, launches);
   if (e != cudaErrorNotSupported) return e;
   if (batch >= kChainMinBatch) return run_chain<M>(batch, k_count, U, psi0, states, spin, s, launches);
-  if (M::W == 2) return run_scan4<M>(batch, k_count, U, psi0, states, spin, ws, s, launches);
+  if constexpr (M::W == 2) {
+    const cudaError_t e2 = run_two_pass<M>(batch, k_count, U, psi0, states, spin, ws, s, launches);
+    if (e2 != cudaErrorNotSupported) return e2;
+  }
   // scan3 amortises its look-back over big tiles; below ~4 stages per tile (small problems) scan2's single pass wins
   if (scan3_nst<M>(batch, k_count, scan3_grid<M>()) >= 4)
     return run_scan3<M>(batch, k_count, U, psi0, states, spin, ws, s, launches);

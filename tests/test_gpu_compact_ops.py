@@ -125,7 +125,7 @@ def test_host_api_compact_matches_device(ss):
         assert U_h is None and np.abs(st_h - st_d).max() <= 1e-12
 
 
-@pytest.mark.parametrize("path", ["coop", "scan2", "scan3", "scan4", "chain"])
+@pytest.mark.parametrize("path", ["coop", "scan2", "scan3", "twopass", "chain"])
 @pytest.mark.parametrize("d,compact", [(2, True), (3, True), (2, False), (3, False)])
 def test_every_scan_path_forced(ss, orc, monkeypatch, path, d, compact):
     """SPINSIM_SCAN_PATH forces each scan kernel (the heuristic picks one per shape): every kernel, for both operator
@@ -148,3 +148,26 @@ def test_every_scan_path_forced(ss, orc, monkeypatch, path, d, compact):
         st, J = ss.scan_states_spin(torch.from_numpy(dense).cuda(), pg, want_states=True)
     assert np.abs(st.cpu().numpy() - ref).max() < 1e-12
     assert np.abs(J.cpu().numpy() - refJ).max() < 2e-12
+
+
+@pytest.mark.parametrize("d", [2, 3])
+@pytest.mark.parametrize("B,K,forced", [(3, 9000 + 36, True),         # runs of 4 (K = 4·2259)
+                                        (2, 8192 + 64, True),         # runs of 32, several warps per sweep
+                                        (3, 800_000, False)])         # 77 MB of operators: the heuristic's choice
+def test_two_pass_compact_scan(ss, orc, monkeypatch, d, B, K, forced):
+    """The standalone two-pass scan of compact operators (run products, coarse scan, run chain) against the oracle's
+    sequential chain, with the fused ⟨J⟩; forced, or chosen by the heuristic for a problem beyond the L2 bound."""
+    if forced:
+        monkeypatch.setenv("SPINSIM_SCAN_PATH", "twopass")
+    else:
+        monkeypatch.delenv("SPINSIM_SCAN_PATH", raising=False)
+    ops = random_su2(B, K, seed=61 + K)
+    psi0 = W.random_states(B, d, seed=62)
+    ref = orc.chain(dense_of(ops, d), psi0)
+    refJ = orc.spin_projection("half" if d == 2 else "one", ref)
+    n0 = ss.kernel_launches()
+    st, J = ss.scan_states_su2(torch.from_numpy(ops).cuda(), torch.from_numpy(psi0).cuda(), d, want_spin=True)
+    assert ss.kernel_launches() - n0 >= 3                   # run products, coarse scan, run chain
+    tol = 1e-12 * max(1.0, np.sqrt(K) / 10)
+    assert np.abs(st.cpu().numpy() - ref).max() < tol
+    assert np.abs(J.cpu().numpy() - refJ).max() < 2 * tol

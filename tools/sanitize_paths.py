@@ -48,7 +48,7 @@ def main():
             for ipt in (4, 8, 32):
                 run(w, want_unitaries=wu, SPINSIM_FUSED_IPT=ipt)
         run(w, SPINSIM_FUSED=0)
-        for path in ("coop", "scan2", "scan3", "scan4", "chain"):
+        for path in ("coop", "scan2", "scan3", "twopass", "chain"):
             run(w, SPINSIM_FUSED_IPT=8, SPINSIM_SCAN_PATH=path)
     run(one_lt, precision="fp32", SPINSIM_FUSED_IPT=8)
     run(one_an, precision="fp32", SPINSIM_FUSED_IPT=8)

@@ -16,7 +16,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2204_05586_b200 as ss  # noqa: E402
 
 HBM = 6534.8e9
-PATHS = ["coop", "chain", "scan2", "scan3", "scan4"]
+PATHS = ["coop", "chain", "scan2", "scan3", "twopass"]
 
 
 def random_ops(B, K, d, compact, gen):
