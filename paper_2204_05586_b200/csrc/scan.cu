@@ -1,22 +1,22 @@
 // scan.cu — state propagation and the small kernels around it.
 //
 // ψ_{k+1} = U_k ψ_k (Eq. integration_compilation) is a linear recurrence; the paper runs it sequentially
-// on the CPU.  Here it is an associative matrix-product scan (combine = later·earlier) over tiles of
-// kTile consecutive intervals of one sweep, with decoupled look-back between tiles:
-//   1. a block takes the next tile ticket (atomic; tiles of a sweep get increasing tickets, so every tile a block
-//      waits on is already resident → forward progress), stages the tile's U_k in shared memory (coalesced),
-//   2. each thread multiplies its kItems consecutive operators (thread aggregate), a warp Kogge–Stone scan with
-//      shuffles and a block combine through shared memory give every thread its exclusive prefix and the block its
-//      tile aggregate,
-//   3. the tile publishes its aggregate (flag AGG), looks back over predecessors (M ← M·A_j′ over AGG tiles until a
-//      PREFIX tile gives ψ_end(j′)), publishes its inclusive end state ψ_end = A·ψ_in (flag PREFIX),
-//   4. each thread applies its exclusive prefix to ψ_in and then its own operators in order, writing states through
-//      shared memory (coalesced).
+// on the CPU.  Here it is an associative matrix-product scan (combine = later·earlier), with one kernel per
+// problem shape (run_state_scan picks; DESIGN.md §5 "State propagation"):
+//   * chain_kernel — batch ≥ 4096: one thread per sweep chains its states, operators TMA-streamed (bulk copies);
+//   * scan_coop_kernel — problems whose operators fit in L2: one cooperative wave, thread products, block
+//     Kogge–Stone, one grid barrier, predecessor aggregates, states;
+//   * run_chain_kernel — the fused path's states pass (the interval kernel wrote run products) and, in AGG mode, the
+//     first pass of the standalone two-pass scan of compact operators: one lane per run of 4–32 operators, a warp's
+//     32 runs staged by coalesced cp.async, states out with coalesced stores;
+//   * scan3_kernel — dense long sweeps at moderate batch: persistent CTAs over tensor-TMA-staged tiles with
+//     decoupled look-back (aggregate published, predecessors' aggregates multiplied until an inclusive prefix);
+//   * scan2_kernel — the rest: double-buffered tiles, warp Kogge–Stone, block combine, warp-parallel look-back.
 // HBM traffic per interval: read U_k + write ψ_{k+1} (2·dim doubles).  U_k travels either as the dense dim×dim complex
 // matrix (the public layout: 144 / 64 B) or, for the SU(2)-form interval kernels (spin-half, analytic spin-one) when
 // U_k is not an output, as the SU(2) element (a, b) (32 B) the kernel accumulates: 192 / 96 B per interval dense,
 // 80 / 64 B compact.  Every scan is HBM bound.  The kernels are templated on the operator type M
-// (CM<D> dense, SU<D> compact acting on dim-D states), so each path exists for both formats.
+// (CM<D> dense, SU<D> compact acting on dim-D states, ops.cuh), so each path exists for both formats.
 #include <cooperative_groups.h>
 #include <cuda/atomic>
 
