@@ -497,7 +497,9 @@ def run_ours(args, rank, world, local):
     elapsed_ms, evs, launches, clocks = timed_loop(step, args.steps, stream, local, barrier)
     t_interval = float(np.mean([e[0].elapsed_time(e[1]) for e in evs]))
     t_scan = float(np.mean([e[1].elapsed_time(e[2]) for e in evs]))
-    elapsed_ms, t_interval, t_scan = reduce_max([elapsed_ms, t_interval, t_scan], dev, world)
+    per_step = [e[0].elapsed_time(e[2]) for e in evs]          # best and median step beside the mean
+    best, med = float(np.min(per_step)), float(np.median(per_step))
+    elapsed_ms, t_interval, t_scan, best, med = reduce_max([elapsed_ms, t_interval, t_scan, best, med], dev, world)
     steps_per_rank = w.fine_steps
     emulated = world == 1 and args.emulate_ranks > 1
     total_steps = steps_per_rank * world if (args.scaling == "weak" or emulated) else full.fine_steps
@@ -575,6 +577,9 @@ def run_ours(args, rank, world, local):
                      "operators": "SU(2) elements, 32 B" if su2_form(w) else f"dense {D}x{D} complex128"},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
             "fine_steps_per_step": total_steps,
+            "step_ms": {"mean": elapsed_ms / args.steps, "best": best, "median": med,
+                        "note": "best/median of the per-step events (interval kernel start to state pass end); "
+                                "mean = the bracketed region / K"},
         }
         if world == 1 and args.workload == "C3" and not emulated and not args.no_secondary:
             line["paper_benchmark"] = paper_benchmark(args, dev)
