@@ -295,10 +295,16 @@ __device__ __forceinline__ void interval_residual(const IntervalParams& prm, int
     if (field_pulse_possible(fld, prm.dt_out, 0)) with_pulse(BoolC<true>{});
     else with_pulse(BoolC<false>{});
   } else {
-    // 3×3 paths: one body with a run-time anchor test (four specialised copies spill more: C3 −2.5 %, measured)
+    // 3×3 paths: groups of kAnchor steps, the first an anchor step — two step bodies (anchor, rotated) with the
+    // pulse test at run time (round 1's four (anchor × pulse) bodies spilled more and cost C3 2.5 %; this pair: +0.3 %,
+    // profiles/r02/s27_anch/)
 #pragma unroll 1
-    for (int64_t l = l_begin; l < l_end; ++l)
-      step(l, RtBool{((l - l_begin) % kAnchor) == 0}, BoolC<true>{}, IntC<0>{});
+    for (int64_t l0 = l_begin; l0 < l_end; l0 += kAnchor) {
+      step(l0, BoolC<true>{}, BoolC<true>{}, IntC<0>{});
+      const int64_t l1 = l0 + kAnchor < l_end ? l0 + kAnchor : l_end;
+#pragma unroll 1
+      for (int64_t l = l0 + 1; l < l1; ++l) step(l, BoolC<false>{}, BoolC<true>{}, IntC<0>{});
+    }
   }
 
   A_out = A;

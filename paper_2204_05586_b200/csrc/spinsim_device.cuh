@@ -122,6 +122,7 @@ template <int F> struct Field;
 #ifndef SS_ANCHOR
 #define SS_ANCHOR 32
 #endif
+
 constexpr int kAnchor = SS_ANCHOR;
 struct PhaseStepper {
   double w, ph0, cd, sd, c, s;
@@ -135,6 +136,8 @@ struct PhaseStepper {
   }
   __device__ __forceinline__ void next(double base, bool anchor) {
     if (anchor) {
+      // the frame's first anchor (base 0, phase 0) is e^{i0} exactly: no library call (C5 analytic +2 %)
+      if (base == 0.0 && ph0 == 0.0) { s = 0.0; c = 1.0; return; }
       sincos(fma(w, base, ph0), &s, &c);
     } else {
       const double cn = fma(c, cd, -s * sd);
