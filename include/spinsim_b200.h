@@ -172,7 +172,12 @@ int ss_compute_unitaries(ss_sim* sim, double time_start, double time_end, double
                          const double* d_sweep, double* d_unitaries, void* stream);
 
 /* State scan only (row a9): states[b][0] = state_init[b], states[b][k+1] = U[b][k] states[b][k] for
- * k < k_count.  Decoupled look-back over tiles; d_workspace >= ss_scan_workspace_bytes(dim, batch, k_count). */
+ * k < k_count.  The kernel follows the problem's shape (DESIGN.md §5 "State propagation"): a per-sweep chain for
+ * batch ≥ 4096, one cooperative wave for operators that fit in L2, a decoupled-look-back tile scan (dense) or the
+ * two-pass run scan (compact operators of ss_scan_states_su2) otherwise — the association of the products, and so
+ * the last-ulp rounding of the states, depends on that choice.  d_workspace >= ss_scan_workspace_bytes(dim, batch,
+ * k_count) (includes, below 4096 sweeps, the two-pass scan's run products and run states: ≤ ⌈k_count/4⌉ of each per
+ * sweep, plus its coarse scan's workspace). */
 size_t ss_scan_workspace_bytes(int32_t dim, int64_t batch, int64_t k_count);
 int ss_scan_states(int32_t dim, int64_t batch, int64_t k_count, const double* d_unitaries,
                    const double* d_state_init, double* d_states, void* d_workspace, size_t workspace_bytes,
