@@ -53,6 +53,17 @@ def main():
     run(one_lt, precision="fp32", SPINSIM_FUSED_IPT=8)
     run(one_an, precision="fp32", SPINSIM_FUSED_IPT=8)
     run(one_lt, field="user", SPINSIM_FUSED_IPT=8)
+    # the standalone two-pass scan of compact operators (run products, coarse scan, run chain), K = 4·odd, 32·m
+    for d in (2, 3):
+        for B, K in ((3, 36 * 7), (2, 32 * 9)):
+            q = np.random.default_rng(K).standard_normal((B, K, 4))
+            q /= np.linalg.norm(q, axis=-1, keepdims=True)
+            ops = np.stack([q[..., 0] + 1j * q[..., 1], q[..., 2] + 1j * q[..., 3]], -1)
+            os.environ["SPINSIM_SCAN_PATH"] = "twopass"
+            ss.scan_states_su2(torch.from_numpy(ops).cuda(), torch.from_numpy(W.random_states(B, d, 6)).cuda(), d,
+                               want_spin=True)
+            torch.cuda.synchronize()
+            del os.environ["SPINSIM_SCAN_PATH"]
     # a partial last warp (K·batch not a multiple of 32) and sweeps straddling warps: warp_trig's fallback
     run(W.c5_matrix("lie_trotter", batch=3).with_(t1=37e-6, psi0=W.random_states(3, 3, 5)))
     print("ok")
