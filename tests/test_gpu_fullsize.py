@@ -77,12 +77,20 @@ def test_c5_full_fp64_and_fp32(ss, orc, expo):
     assert np.abs(r32.state.cpu().numpy() - st_o).max() <= 1e-4
 
 
-def test_c5_throughput_batch_sampled(ss, orc):
-    w = W.c5_matrix("lie_trotter", batch=100)
-    _, res = run_gpu(ss, w)
+@pytest.mark.parametrize("expo,precision,want_unitaries", [("lie_trotter", "fp64", True),
+                                                           ("analytic", "fp64", False),
+                                                           ("analytic", "fp32", False),
+                                                           ("lie_trotter", "fp32", False)])
+def test_c5_throughput_batch_sampled(ss, orc, expo, precision, want_unitaries):
+    """C5's throughput workload (100 sweeps × 1e5 intervals) in the launch configuration bench.py times — the fused
+    path (run products in the interval kernel, coarse scan, run chain), compact operators when U is not requested —
+    sampled sweeps against the oracle at the precision's bar."""
+    w = W.c5_matrix(expo, batch=100)
+    _, res = run_gpu(ss, w, precision=precision, want_unitaries=want_unitaries)
     idx = np.array([0, 49, 99])
-    st_o, U_o = oracle_sweeps(orc, w, idx)
-    assert np.abs(res.state[torch.from_numpy(idx).cuda()].cpu().numpy() - st_o).max() <= 1e-10
+    st_o, U_o = oracle_sweeps(orc, w, idx, want_unitaries=want_unitaries)
+    tol = 1e-10 if precision == "fp64" else 1e-4
+    assert np.abs(res.state[torch.from_numpy(idx).cuda()].cpu().numpy() - st_o).max() <= tol
 
 
 def test_c4_full_1s_at_1ns(ss, orc):
