@@ -207,3 +207,27 @@ def test_wrappers_reject_bad_shapes_before_the_library(lib):
                           out_states=np.zeros((2, 2, 11), np.complex128).transpose(0, 2, 1))
     with pytest.raises((TypeError, ValueError)):
         sim.evaluate(torch.zeros(2, 2, dtype=torch.float64), 0.0, 1e-5, 1e-7, 1e-6, torch.zeros(2, 2))
+
+
+def test_workspace_sizes_cover_every_path(lib):
+    """Host-only sizing (no GPU): ss_scan_workspace_bytes is non-decreasing in K below the chain kernel's batch size
+    (the fused path's coarse scan over K/ipt runs and the two-pass scan's own coarse scan over ⌈K/4⌉ run the workspace
+    sized for K), covers the two-pass scan's run products and run states (≥ ⌈K/4⌉ of each per sweep), and
+    ss_workspace_bytes adds the fused region (≥ ⌈K/4⌉ run products and run states per sweep) below 4096 sweeps only."""
+    from paper_2204_05586_b200 import Simulator
+    rng = np.random.default_rng(3)
+    for dim in (2, 3):
+        for batch in (1, 7, 100, 4095):
+            Ks = np.unique(np.concatenate([np.arange(1, 300), rng.integers(1, 3_000_000, 200)]))
+            sizes = [int(lib.ss_scan_workspace_bytes(dim, batch, int(K))) for K in Ks]
+            assert all(b >= a for a, b in zip(sizes, sizes[1:])), (dim, batch)
+            for K, size in zip(Ks[::17], sizes[::17]):
+                if K >= 8:
+                    runs = -(-int(K) // 4)
+                    assert size >= batch * runs * 16 * (2 + dim)
+    sim = Simulator("one", "cf4", "analytic", 24, True, "fp64", "neural")
+    for batch, K in ((100, 100_000), (1, 100_000_000 // 32)):
+        with_f = sim.workspace_bytes(batch, K, True)
+        runs = -(-K // 4)
+        assert with_f >= batch * K * 16 * 9 + batch * runs * 16 * (9 + 3)      # U, run products (dense), run states
+    assert sim.workspace_bytes(8192, 10_000, True) < 8192 * 10_000 * 16 * 9 * 1.02   # no fused region at 8192
