@@ -288,6 +288,10 @@ int64_t fused_ipt(const ss_sim* s, int64_t batch, int64_t K, int S, int op_forma
     const int64_t v = std::atoll(fi);
     return (v >= kFusedMinIpt && v <= max_ipt && (v & (v - 1)) == 0 && K % v == 0 && K >= 2 * v) ? v : 0;
   }
+  // Dense 3×3 operators (Lie–Trotter, su(3), analytic spin-one with U requested): the run products cost the interval
+  // kernel more than the streamed states pass saves (measured: C3's 1024-sweep shard −0.8 %, C5 Lie–Trotter −0.2 %,
+  // G1 shard −3 %, profiles/r02/s32_dense/), so only SPINSIM_FUSED_IPT takes them fused.
+  if (s->dim == 3 && op_format != ssb::OP_SU2) return 0;
   const double R = resident_threads(s);
   for (int64_t ipt = max_ipt; ipt >= kFusedMinIpt; ipt /= 2)
     if (K % ipt == 0 && (double)batch * (double)(K / ipt) >= kFusedMinWaves * R) return ipt;
