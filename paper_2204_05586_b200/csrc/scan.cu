@@ -3,7 +3,8 @@
 // ψ_{k+1} = U_k ψ_k (Eq. integration_compilation) is a linear recurrence; the paper runs it sequentially
 // on the CPU.  Here it is an associative matrix-product scan (combine = later·earlier), with one kernel per
 // problem shape (run_state_scan picks; DESIGN.md §5 "State propagation"):
-//   * chain_kernel — batch ≥ 4096: one thread per sweep chains its states, operators TMA-streamed (bulk copies);
+//   * chain_kernel — batch ≥ 4096 (dense spin-one: 1536): one thread per sweep chains its states, operators
+//     TMA-streamed through a per-sweep ring of bulk copies as deep as the shared memory allows;
 //   * scan_coop_kernel — problems whose operators fit in L2: one cooperative wave, thread products, block
 //     Kogge–Stone, one grid barrier, predecessor aggregates, states;
 //   * run_chain_kernel — the fused path's states pass (the interval kernel wrote run products) and, in AGG mode, the
@@ -966,27 +967,47 @@ __global__ void __launch_bounds__(128) scan_coop_kernel(const CoopArgs a) {
 
 // ---- state chain for large batches: one thread per sweep, TMA-streamed ------------------------------------------
 //
-// With batch ≥ kChainMinBatch the sweeps alone give enough parallelism to saturate HBM, so each thread runs its own
-// sweep's recurrence ψ_{k+1} = U_k ψ_k sequentially (36 FP64 ops per interval, no matrix products, no look-back):
-// lane ℓ bulk-copies (cp.async.bulk → UBLKCP) its next CH operators into its own shared-memory slot while it applies
-// the current CH, so every SM keeps ≥ 64 × CH × 16·dim² bytes of HBM reads in flight.
-#ifndef SS_CHAIN_THREADS
-#define SS_CHAIN_THREADS 64
-#endif
-constexpr int kChainThreads = SS_CHAIN_THREADS;
+// With enough sweeps the sweeps alone give the parallelism to saturate HBM, so each thread runs its own sweep's
+// recurrence ψ_{k+1} = U_k ψ_k sequentially (36 FP64 ops per interval, no matrix products, no look-back): the thread
+// streams its sweep's operators through its own NST-stage ring of shared-memory slots, CH operators per bulk copy
+// (cp.async.bulk → UBLKCP, one mbarrier per warp and stage), so NST − 1 copies per sweep are in flight while it
+// applies the current CH.  One CTA per SM holds spc = ⌈batch / #SMs⌉ sweeps, dealt round-robin over its four warps
+// (one per SM sub-partition: the recurrence is latency-bound per sweep, ≈ 300 cycles per interval, so four short
+// warps beat one full one); the ring depth is what the shared memory gives spc slots (8192 sweeps: 56 slots × 2
+// stages; 4096 sweeps, one GPU's shard of C3 at 2 GPUs: 28 × 4), so every SM keeps ≈ 100 KB of operator reads in
+// flight.
+constexpr int kChainThreads = 128;   // four warps
+constexpr int kChainMaxSpc = 64;     // sweeps per CTA
 #ifndef SS_COOP_MAXCPS
 #define SS_COOP_MAXCPS 128     // CTAs per sweep of the cooperative scan (one predecessor round)
 #endif
 constexpr int64_t kChainMinBatch = 4096;
+// Dense spin-one operators take the chain from 1536 sweeps: one sweep's serial recurrence costs ≈ 250 cycles per
+// interval whatever the batch below ~3000 sweeps, against scan3's ≈ 0.34 of HBM (B200, 1e4 intervals: 2048 sweeps
+// 1.32 vs 1.75 ms, 1024 sweeps 1.21 vs 0.90 ms; profiles/r02/s34_chain/scan_paths.txt), so the crossover is
+// K·250 cycles = B·K·192 B / (0.34·HBM), B ≈ 1500.  Other operators keep 4096 (compact ones prefer the two-pass scan).
+template <class M> constexpr int64_t chain_min_batch_of() { return M::W == 9 ? 1536 : kChainMinBatch; }
 #ifndef SS_CHAIN_CH
-#define SS_CHAIN_CH 12   // operators per bulk copy: 4 / 8 / 12 → 2.9 / 5.2 / 5.4 TB/s on C3 (14 exceeds shared memory)
+#define SS_CHAIN_CH 12   // operators per bulk copy: 4 / 8 / 12 → 2.9 / 5.2 / 5.4 TB/s on C3 (two stages)
 #endif
+#ifndef SS_CHAIN_MAX_STAGES
+#define SS_CHAIN_MAX_STAGES 16
+#endif
+constexpr int kChainMaxStages = SS_CHAIN_MAX_STAGES;
+constexpr int kChainSmemBudget = 220 * 1024;   // dynamic shared memory of the ring (one CTA per SM)
 // compact SU(2) operators (32 B) are copied 48 at a time: ≈ 1.5 KB per copy like 12 dense spin-one operators
 template <class M> struct ChainCfg { static constexpr int CH = M::W == 2 ? 4 * SS_CHAIN_CH : SS_CHAIN_CH; };
-// Per-lane slot: 2 stages of CH operators, stride padded to an odd number of 16-byte words so the 32 lanes' LDS.128
-// at the same offset hit distinct banks (an unpadded stride is a multiple of 128 B: a 32-way conflict).
-template <class M> __host__ __device__ constexpr int chain_slot_stride() { return (2 * ChainCfg<M>::CH * M::W) | 1; }
-template <class M> constexpr size_t chain_smem() { return sizeof(double2) * (size_t)kChainThreads * chain_slot_stride<M>(); }
+// Ring depth for spc lanes: the most stages (≤ kChainMaxStages) whose per-lane slots fit the budget, at least 2.
+template <class M> __host__ __device__ constexpr int chain_slot_stride(int nst) {
+  // stride padded to an odd number of 16-byte words so the lanes' LDS.128 at the same offset hit distinct banks (an
+  // unpadded stride is a multiple of 128 B: a 32-way conflict)
+  return (nst * ChainCfg<M>::CH * M::W) | 1;
+}
+template <class M> static int chain_stages(int spc) {
+  int nst = kChainMaxStages;
+  while (nst > 2 && (size_t)spc * chain_slot_stride<M>(nst) * sizeof(double2) > (size_t)kChainSmemBudget) --nst;
+  return nst;
+}
 
 struct ChainArgs {
   int64_t batch, k_count;
@@ -994,7 +1015,8 @@ struct ChainArgs {
   const double2* psi0;
   double2* states;   // [batch][K+1][D] or NULL
   double* spin;      // [batch][K+1][3] or NULL (⟨J⟩ fused into the write-out)
-  int spc;           // sweeps per CTA (≤ kChainThreads): spreads the batch over every SM
+  int spc;           // sweeps per CTA (≤ kChainMaxSpc): spreads the batch over every SM
+  int nst;           // ring stages per lane (2 … kChainMaxStages)
 };
 
 template <class M>
@@ -1002,14 +1024,19 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(const ChainArgs a)
   constexpr int D = M::SD, W = M::W;
   constexpr int CH = ChainCfg<M>::CH;
   extern __shared__ __align__(128) double2 smem3[];
-  __shared__ __align__(8) uint64_t sBar[kChainThreads / 32][2];
+  __shared__ __align__(8) uint64_t sBar[kChainThreads / 32][kChainMaxStages];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t b = (int64_t)blockIdx.x * a.spc + tid;
-  const bool valid = tid < a.spc && b < a.batch;
-  double2* slot[2] = {smem3 + (size_t)tid * chain_slot_stride<M>(), smem3 + (size_t)tid * chain_slot_stride<M>() + CH * W};
+  const int NST = a.nst;
+  // this thread's sweep slot: the spc slots split into four contiguous runs, one per warp (adjacent lanes, adjacent
+  // slots: the odd slot stride keeps their LDS.128 conflict-free)
+  const int per_warp = (a.spc + 3) / 4;
+  const int j = warp * per_warp + lane;
+  const int64_t b = (int64_t)blockIdx.x * a.spc + j;
+  const bool valid = lane < per_warp && j < a.spc && b < a.batch;
+  // threads past spc own no slot (the CTA's shared memory holds spc slots) and only arrive on their warp's barriers
+  double2* slot = smem3 + (size_t)(valid ? j : 0) * chain_slot_stride<M>(NST);
   if (lane == 0) {
-    mbar_init(&sBar[warp][0], 32);
-    mbar_init(&sBar[warp][1], 32);
+    for (int st = 0; st < NST; ++st) mbar_init(&sBar[warp][st], 32);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
@@ -1021,12 +1048,12 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(const ChainArgs a)
     const unsigned bytes = (unsigned)(n * W * sizeof(double2));
     if (bytes) {
       mbar_expect_tx(&sBar[warp][st], bytes);
-      tma_load_1d(slot[st], gU + (size_t)k0 * W, bytes, &sBar[warp][st]);
+      tma_load_1d(slot + st * (CH * W), gU + (size_t)k0 * W, bytes, &sBar[warp][st]);
     } else {
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&sBar[warp][st])) : "memory");
     }
   };
-  issue(0, 0);
+  for (int st = 0; st < NST && st < nchunks; ++st) issue(st, st);   // fill the ring
   double pr[D], pi[D];
   double2* gS = a.states ? a.states + (size_t)(valid ? b : 0) * (a.k_count + 1) * D : nullptr;
   double* gJ = a.spin ? a.spin + (size_t)(valid ? b : 0) * (a.k_count + 1) * 3 : nullptr;
@@ -1041,21 +1068,15 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(const ChainArgs a)
     spin_of<D>(pr, pi, j);
     for (int q = 0; q < 3; ++q) __stcs(gJ + q, j[q]);
   }
-  unsigned phase[2] = {0u, 0u};
+  int st = 0;
+  unsigned parity = 0u;   // phase parity of stage st's current use: flips each time the ring wraps
   for (int64_t c = 0; c < nchunks; ++c) {
-    const int st = (int)(c & 1);
-    if (c + 1 < nchunks) {
-      __syncwarp();
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue(c + 1, st ^ 1);
-    }
-    mbar_wait(&sBar[warp][st], phase[st]);
-    phase[st] ^= 1u;
+    mbar_wait(&sBar[warp][st], parity);
     if (valid) {
       const int n = (int)min((int64_t)CH, a.k_count - c * CH);
-      const double2* u = slot[st];
+      const double2* u = slot + st * (CH * W);
       const size_t kout = (size_t)(c * CH + 1);
-      for (int i = 0; i < n; ++i) {
+      auto one = [&](int i) {
         double yr[D], yi[D];
         M m;
         cm_load(u + i * W, m);
@@ -1066,35 +1087,48 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(const ChainArgs a)
 #pragma unroll
           for (int d = 0; d < D; ++d) __stcs(gS + (kout + i) * D + d, make_double2(yr[d], yi[d]));
         if (gJ) {
-          double j[3];
-          spin_of<D>(pr, pi, j);
-          for (int q = 0; q < 3; ++q) __stcs(gJ + (kout + i) * 3 + q, j[q]);
+          double jj[3];
+          spin_of<D>(pr, pi, jj);
+          for (int q = 0; q < 3; ++q) __stcs(gJ + (kout + i) * 3 + q, jj[q]);
         }
+      };
+      if (n == CH) {   // full chunk unrolled: the operator loads are independent of ψ and issue ahead of the chain
+#pragma unroll
+        for (int i = 0; i < CH; ++i) one(i);
+      } else {
+        for (int i = 0; i < n; ++i) one(i);
       }
     }
+    if (c + NST < nchunks) {   // refill the stage just consumed (generic reads before the async-proxy write)
+      __syncwarp();
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(c + NST, st);
+    }
+    if (++st == NST) { st = 0; parity ^= 1u; }
   }
 }
 
 template <class M>
 static cudaError_t run_chain(int64_t batch, int64_t k_count, const double* U, const double* psi0, double* states,
                              double* spin, cudaStream_t s, int* launches) {
-  constexpr size_t smem = chain_smem<M>();
   static DeviceCache attr;   // per device: the shared-memory opt-in applies to the current device's context
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   if (!attr.get(dev)) {
-    e = cudaFuncSetAttribute(chain_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = cudaFuncSetAttribute(chain_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, kChainSmemBudget);
     if (e != cudaSuccess) return e;
     attr.set(dev, 1);
   }
-  // Sweeps per CTA: at most kChainThreads, and few enough that the CTAs cover every SM (8192 sweeps: 56 per CTA on
+  // Sweeps per CTA: at most kChainMaxSpc, and few enough that the CTAs cover every SM (8192 sweeps: 56 per CTA on
   // 147 CTAs instead of 64 on 128 — the per-SM TMA/L1 path, not HBM, limited the 128-CTA launch).
   const int sms = device_sms(dev);
-  int spc = (int)std::min<int64_t>(kChainThreads, (batch + sms - 1) / sms);
+  int spc = (int)std::min<int64_t>(kChainMaxSpc, (batch + sms - 1) / sms);
   if (spc < 1) spc = 1;
+  const int nst = chain_stages<M>(spc);
+  const size_t smem = (size_t)spc * chain_slot_stride<M>(nst) * sizeof(double2);
   ChainArgs a{batch, k_count, reinterpret_cast<const double2*>(U), reinterpret_cast<const double2*>(psi0),
-              reinterpret_cast<double2*>(states), spin, spc};
+              reinterpret_cast<double2*>(states), spin, spc, nst};
   chain_kernel<M><<<(unsigned)((batch + spc - 1) / spc), kChainThreads, smem, s>>>(a);
   ++*launches;
   return cudaGetLastError();
@@ -1645,7 +1679,7 @@ static int forced_scan_path() {
   return 0;
 }
 
-// Path choice: the cooperative single-wave scan for L2-sized problems; the per-sweep chain for ≥ kChainMinBatch
+// Path choice: the cooperative single-wave scan for L2-sized problems; the per-sweep chain for ≥ chain_min_batch_of
 // sweeps; otherwise compact SU(2) operators take the two-pass scan where a run length divides K, dense ones scan3
 // where its tiles get ≥ 4 stages (long sweeps, moderate batch) and scan2 for the rest.
 template <class M>
@@ -1669,7 +1703,7 @@ static cudaError_t run_state_scan(int64_t batch, int64_t k_count, const double* 
   }
   const cudaError_t e = run_scan_coop<M>(batch, k_count, U, psi0, states, spin, ws, s, launches);
   if (e != cudaErrorNotSupported) return e;
-  if (batch >= kChainMinBatch) return run_chain<M>(batch, k_count, U, psi0, states, spin, s, launches);
+  if (batch >= chain_min_batch_of<M>()) return run_chain<M>(batch, k_count, U, psi0, states, spin, s, launches);
   if constexpr (M::W == 2) {
     const cudaError_t e2 = run_two_pass<M>(batch, k_count, U, psi0, states, spin, ws, s, launches);
     if (e2 != cudaErrorNotSupported) return e2;

@@ -3,7 +3,7 @@
     python tools/scan_paths.py > profiles/r02/<tag>/scan_paths.txt
 
 Shapes (B sweeps × K intervals): C5 (100 × 1e5), the scan-stress sweep (1 × 1e8), one rank's shard of C3 at 8 GPUs
-(1024 × 1e4) and at 2 GPUs (4096 × 1e4), C2 (1 × 1e5), C3 (8192 × 1e4).  Operators are random (unit quaternions →
+(1024 × 1e4), at 4 GPUs (2048 × 1e4) and at 2 GPUs (4096 × 1e4), C2 (1 × 1e5), C3 (8192 × 1e4).  Operators are random (unit quaternions →
 SU(2) elements; dense = the same matrices written out, D¹ for dim 3) generated on the device; each kernel is timed
 with CUDA events over 3 repetitions after a warm-up, and reported as algorithmic HBM bytes / time against 6534.8 GB/s.
 """
@@ -58,7 +58,7 @@ def main():
     gen = torch.Generator(device="cuda")
     gen.manual_seed(7)
     shapes = [("C5", 100, 100000, 3), ("scan-stress", 1, 100000000, 2), ("C3 shard/8", 1024, 10000, 3),
-              ("C3 shard/2", 4096, 10000, 3), ("C2", 1, 100000, 3), ("C3", 8192, 10000, 3)]
+              ("C3 shard/4", 2048, 10000, 3), ("C3 shard/2", 4096, 10000, 3), ("C2", 1, 100000, 3), ("C3", 8192, 10000, 3)]
     print(f"{'shape':12s} {'B':>5s} {'K':>10s} {'d':>2s} {'ops':7s} " + " ".join(f"{p:>17s}" for p in PATHS))
     for name, B, K, d in shapes:
         for compact in (True, False):
