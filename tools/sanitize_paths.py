@@ -1,7 +1,7 @@
 """Small end-to-end calls through every round-2 kernel path, for compute-sanitizer (memcheck / racecheck / synccheck /
 initcheck): the fused interval kernel (compact and dense operators, both spins, every exponentiator, FP32), the coarse
 scans, the warp-cooperative run chain (cp.async staging, in-place states), warp-shared trigonometry (full and partial
-warps), and the NVRTC user-field kernel in fused mode.
+warps), the NVRTC user-field kernel in fused mode, and the chain kernel's per-sweep ring (several warps, ring wrap).
 
     compute-sanitizer --tool memcheck python tools/sanitize_paths.py
 """
@@ -64,6 +64,17 @@ def main():
                                want_spin=True)
             torch.cuda.synchronize()
             del os.environ["SPINSIM_SCAN_PATH"]
+    # the chain kernel's per-sweep ring with several warps per CTA, a partial last CTA and the ring wrapping (dense
+    # spin-one and spin-half operators, states and ⟨J⟩)
+    for d in (2, 3):
+        B, K = 601, 12 * 16 + 37
+        z = np.random.default_rng(d).standard_normal((B, K, d, d, 2))
+        U = np.linalg.qr(z[..., 0] + 1j * z[..., 1])[0]
+        os.environ["SPINSIM_SCAN_PATH"] = "chain"
+        ss.scan_states_spin(torch.from_numpy(U).cuda(), torch.from_numpy(W.random_states(B, d, 7)).cuda(),
+                            want_states=True)
+        torch.cuda.synchronize()
+        del os.environ["SPINSIM_SCAN_PATH"]
     # a partial last warp (K·batch not a multiple of 32) and sweeps straddling warps: warp_trig's fallback
     run(W.c5_matrix("lie_trotter", batch=3).with_(t1=37e-6, psi0=W.random_states(3, 3, 5)))
     print("ok")
