@@ -173,7 +173,7 @@ int ss_compute_unitaries(ss_sim* sim, double time_start, double time_end, double
 
 /* State scan only (row a9): states[b][0] = state_init[b], states[b][k+1] = U[b][k] states[b][k] for
  * k < k_count.  The kernel follows the problem's shape (DESIGN.md §5 "State propagation"): a per-sweep chain for
- * batch ≥ 4096 (dense spin-one operators: ≥ 1536), one cooperative wave for operators that fit in L2, a decoupled-look-back tile scan (dense) or the
+ * batch ≥ 4096 (dense spin-one operators: ≥ 2304), one cooperative wave for operators that fit in L2, a decoupled-look-back tile scan (dense) or the
  * two-pass run scan (compact operators of ss_scan_states_su2) otherwise — the association of the products, and so
  * the last-ulp rounding of the states, depends on that choice.  d_workspace >= ss_scan_workspace_bytes(dim, batch,
  * k_count) (includes, below 4096 sweeps, the two-pass scan's run products and run states: ≤ ⌈k_count/4⌉ of each per

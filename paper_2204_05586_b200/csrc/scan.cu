@@ -3,7 +3,7 @@
 // ψ_{k+1} = U_k ψ_k (Eq. integration_compilation) is a linear recurrence; the paper runs it sequentially
 // on the CPU.  Here it is an associative matrix-product scan (combine = later·earlier), with one kernel per
 // problem shape (run_state_scan picks; DESIGN.md §5 "State propagation"):
-//   * chain_kernel — batch ≥ 4096 (dense spin-one: 1536): one thread per sweep chains its states, operators
+//   * chain_kernel — batch ≥ 4096 (dense spin-one: 2304): one thread per sweep chains its states, operators
 //     TMA-streamed through a per-sweep ring of bulk copies as deep as the shared memory allows;
 //   * scan_coop_kernel — problems whose operators fit in L2: one cooperative wave, thread products, block
 //     Kogge–Stone, one grid barrier, predecessor aggregates, states;
@@ -573,14 +573,18 @@ __global__ void __launch_bounds__(Scan3Cfg<M>::NT, 1)
       } else {
         mbar_arrive(&sFull[x]);
       }
-    } else {                                                 // last tile of a sweep: per-thread bulk copies
+    } else {
+      // last tile of a sweep (K not a multiple of the tile): every thread copies its own ≤ C operators with 16-byte
+      // cp.async, all threads at once, and the mbarrier counts its arrival when they land (arrive.noinc).  (Per-thread
+      // bulk copies serialised their 128 issues through an elect loop: 1/3 of the tiles at K = 1e4.)
       const long long k0 = j * TILE + (long long)tid * IPT + (long long)s * C;
       const int nit = (int)max(0LL, min((long long)C, a.k_count - k0));
       if (nit > 0) {
-        const unsigned bytes = (unsigned)(nit * W * sizeof(double2));
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(&sFull[x], bytes);
-        tma_load_1d(smem5 + (x * NT + tid) * SU, a.U + ((size_t)b * a.k_count + k0) * W, bytes, &sFull[x]);
+        const double2* src = a.U + ((size_t)b * a.k_count + k0) * W;
+        double2* dst = smem5 + (x * NT + tid) * SU;
+        for (int q = 0; q < nit * W; ++q)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst + q)), "l"(src + q) : "memory");
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&sFull[x])) : "memory");
       } else {
         mbar_arrive(&sFull[x]);
       }
@@ -784,9 +788,9 @@ __global__ void __launch_bounds__(Scan3Cfg<M>::NT, 1)
                          pol_stream);
             bulk_commit();
           }
-        } else if (nit > 0) {
-          bulk_store(a.states + ((size_t)b * (a.k_count + 1) + k0 + 1) * D, st, (unsigned)(nit * D * sizeof(double2)));
-          bulk_commit();
+        } else if (nit > 0) {                                // last tile: plain per-thread stores (no elect loop)
+          double2* dstS = a.states + ((size_t)b * (a.k_count + 1) + k0 + 1) * D;
+          for (int q = 0; q < nit * D; ++q) __stcs(dstS + q, st[q]);
         }
       }
       top_up();
@@ -982,11 +986,11 @@ constexpr int kChainMaxSpc = 64;     // sweeps per CTA
 #define SS_COOP_MAXCPS 128     // CTAs per sweep of the cooperative scan (one predecessor round)
 #endif
 constexpr int64_t kChainMinBatch = 4096;
-// Dense spin-one operators take the chain from 1536 sweeps: one sweep's serial recurrence costs ≈ 250 cycles per
-// interval whatever the batch below ~3000 sweeps, against scan3's ≈ 0.34 of HBM (B200, 1e4 intervals: 2048 sweeps
-// 1.32 vs 1.75 ms, 1024 sweeps 1.21 vs 0.90 ms; profiles/r02/s34_chain/scan_paths.txt), so the crossover is
-// K·250 cycles = B·K·192 B / (0.34·HBM), B ≈ 1500.  Other operators keep 4096 (compact ones prefer the two-pass scan).
-template <class M> constexpr int64_t chain_min_batch_of() { return M::W == 9 ? 1536 : kChainMinBatch; }
+// Dense spin-one operators take the chain from 2304 sweeps: one sweep's serial recurrence costs ≈ 250 cycles per
+// interval whatever the batch below ~3000 sweeps (1e4 intervals: 1.21 / 1.32 ms at 1024 / 2048 sweeps), while scan3
+// runs at ≈ 0.46 of HBM, i.e. in time ∝ B (0.67 / 1.28 ms; profiles/r02/s42_scan3/scan_paths.txt): the crossover is
+// near 2100 sweeps.  Other operators keep 4096 (compact ones prefer the two-pass scan).
+template <class M> constexpr int64_t chain_min_batch_of() { return M::W == 9 ? 2304 : kChainMinBatch; }
 #ifndef SS_CHAIN_CH
 #define SS_CHAIN_CH 12   // operators per bulk copy: 4 / 8 / 12 → 2.9 / 5.2 / 5.4 TB/s on C3 (two stages)
 #endif

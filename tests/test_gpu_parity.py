@@ -191,8 +191,8 @@ def _random_unitaries(B, K, d, seed):
 @pytest.mark.parametrize("d", [2, 3])
 @pytest.mark.parametrize("B,K", [(1, 1), (3, 255), (2, 256), (5, 1031), (1, 20000), (300, 7),
                                  (4096, 1), (4100, 37), (4097, 8), (5000, 9),    # B >= 4096: per-sweep chain kernel
-                                 (1536, 269), (1600, 37), (1535, 40)])   # dense spin-one: chain from 1536 sweeps,
-                                                                         # a ring of 11 stages wrapped twice at K = 269
+                                 (2304, 269), (2400, 37), (2303, 40)])   # dense spin-one: chain from 2304 sweeps,
+                                                                         # rings of 7–8 stages wrapped ≥ 2× at K = 269
 def test_scan_vs_sequential_chain(ss, orc, d, B, K):
     U = _random_unitaries(B, K, d, seed=B * 1000 + K)
     psi0 = W.random_states(B, d, seed=27)
