@@ -446,10 +446,16 @@ __global__ void __launch_bounds__(Scan2Cfg<M>::NT) scan2_kernel(const Scan2Args 
 #endif
 // C intervals per thread and stage: ≈ 256 B of operators per row (dense: 4 × 64 B, 2 × 144 B); compact SU(2)
 // operators (32 B) take C = 4 and a deeper ring (8 stages) so that as many bytes are in flight.
+#ifndef SS_SCAN3_NT9
+#define SS_SCAN3_NT9 128     // threads per CTA for dense spin-one operators (tuning knob)
+#endif
+#ifndef SS_SCAN3_NSTAGE9
+#define SS_SCAN3_NSTAGE9 SS_SCAN3_NSTAGE
+#endif
 template <class M> struct Scan3Cfg {
   static constexpr int D = M::SD, W = M::W;
-  static constexpr int NT = 128, NW = NT / 32, C = (W == 9) ? 2 : 4;
-  static constexpr int NSTAGE = (W == 2) ? 8 : SS_SCAN3_NSTAGE, MAXST = SS_SCAN3_MAXST;
+  static constexpr int NT = (W == 9) ? SS_SCAN3_NT9 : 128, NW = NT / 32, C = (W == 9) ? 256 / NT : 4;
+  static constexpr int NSTAGE = (W == 2) ? 8 : (W == 9 ? SS_SCAN3_NSTAGE9 : SS_SCAN3_NSTAGE), MAXST = SS_SCAN3_MAXST;
   static constexpr int SU = C * W + 1;       // slot pitch in double2: odd → conflict-free per-thread reads
   static constexpr int SS = C * D + 1;       // state staging pitch in double2
 };
