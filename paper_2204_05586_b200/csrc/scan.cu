@@ -452,9 +452,13 @@ __global__ void __launch_bounds__(Scan2Cfg<M>::NT) scan2_kernel(const Scan2Args 
 #ifndef SS_SCAN3_NSTAGE9
 #define SS_SCAN3_NSTAGE9 SS_SCAN3_NSTAGE
 #endif
+#ifndef SS_SCAN3_C9
+#define SS_SCAN3_C9 0        // intervals per row and stage for dense spin-one operators (0: 256 / NT)
+#endif
 template <class M> struct Scan3Cfg {
   static constexpr int D = M::SD, W = M::W;
-  static constexpr int NT = (W == 9) ? SS_SCAN3_NT9 : 128, NW = NT / 32, C = (W == 9) ? 256 / NT : 4;
+  static constexpr int NT = (W == 9) ? SS_SCAN3_NT9 : 128, NW = NT / 32;
+  static constexpr int C = (W == 9) ? (SS_SCAN3_C9 > 0 ? SS_SCAN3_C9 : 256 / NT) : 4;
   static constexpr int NSTAGE = (W == 2) ? 8 : (W == 9 ? SS_SCAN3_NSTAGE9 : SS_SCAN3_NSTAGE), MAXST = SS_SCAN3_MAXST;
   static constexpr int SU = C * W + 1;       // slot pitch in double2: odd → conflict-free per-thread reads
   static constexpr int SS = C * D + 1;       // state staging pitch in double2
