@@ -638,6 +638,62 @@ template <typename T> __device__ __forceinline__ void sym_square_s(Sym3<T>& a) {
 // The Sym3 between trotter_init and trotter_expand holds the scaled pair (x̃, ỹ) = (2x, −2y).
 template <typename T> __device__ __forceinline__ void lt_square(Sym3<T>& a) { sym_square_s<T>(a); }
 
+// Shifted-diagonal form of the τ-squaring loop (DESIGN.md §5 item 19).  The doubling reads x̃'s diagonal only as
+// d_i = x̃_ii + 2, so between squarings the Sym3 may carry w_ii = x̃_ii + 2 on its diagonal instead: the next
+// diagonal is then w'_ii = 2 − (ỹ²)_ii, three FMAs with the constant as the innermost addend, where x̃'_ii = −(ỹ²)_ii
+// took two FMAs and a DMUL and d_i one DADD more — 36 FP64 instructions per squaring instead of 39.  Same squarings
+// (P:456-462); only d_i's rounding moves (three roundings at the magnitude of 2 instead of one).  The last squaring
+// writes x̃'s diagonal again (−(ỹ²)_ii with full relative precision), so T₀^n − I keeps its residual accuracy.
+#ifndef SS_SQ_WFORM
+#define SS_SQ_WFORM 1
+#endif
+template <typename T, bool W_OUT> __device__ __forceinline__ void sym_square_w(Sym3<T>& a) {
+  const T two = splat<T>(2.0);
+  const T d0 = a.r00, d1 = a.r11, d2 = a.r22;         // w_ii = x̃_ii + 2
+  const T x01 = a.r01, x02 = a.r02, x12 = a.r12;
+  const T y00 = a.i00, y01 = a.i01, y02 = a.i02, y11 = a.i11, y12 = a.i12, y22 = a.i22;
+  if constexpr (W_OUT) {                               // w' = 2I − ỹ² on the diagonal
+    a.r00 = fmaT(-y00, y00, fmaT(-y01, y01, fmaT(-y02, y02, two)));
+    a.r11 = fmaT(-y01, y01, fmaT(-y11, y11, fmaT(-y12, y12, two)));
+    a.r22 = fmaT(-y02, y02, fmaT(-y12, y12, fmaT(-y22, y22, two)));
+  } else {                                             // x̃' = −ỹ² on the diagonal (the last squaring)
+    a.r00 = fmaT(-y00, y00, fmaT(-y01, y01, -(y02 * y02)));
+    a.r11 = fmaT(-y01, y01, fmaT(-y11, y11, -(y12 * y12)));
+    a.r22 = fmaT(-y02, y02, fmaT(-y12, y12, -(y22 * y22)));
+  }
+  a.r01 = fmaT(-y00, y01, fmaT(-y01, y11, -(y02 * y12)));
+  a.r02 = fmaT(-y00, y02, fmaT(-y01, y12, -(y02 * y22)));
+  a.r12 = fmaT(-y01, y02, fmaT(-y11, y12, -(y12 * y22)));
+  // ỹ' = (x̃ + 2I)·ỹ
+  a.i00 = fmaT(d0, y00, fmaT(x01, y01, x02 * y02));
+  a.i01 = fmaT(d0, y01, fmaT(x01, y11, x02 * y12));
+  a.i02 = fmaT(d0, y02, fmaT(x01, y12, x02 * y22));
+  a.i11 = fmaT(x01, y01, fmaT(d1, y11, x12 * y12));
+  a.i12 = fmaT(x01, y02, fmaT(d1, y12, x12 * y22));
+  a.i22 = fmaT(x02, y02, fmaT(x12, y12, d2 * y22));
+}
+
+#ifndef SS_SQ_UNROLL
+#define SS_SQ_UNROLL 2      // unroll of the τ-squaring loop (tuning knob, DESIGN.md §5)
+#endif
+#define SS_PRAGMA(x) _Pragma(#x)
+#define SS_UNROLL(n) SS_PRAGMA(unroll n)
+
+// The τ residual squarings of the scaled pair: shifted-diagonal form when SS_SQ_WFORM.
+template <typename T> __device__ __forceinline__ void lt_square_tau(Sym3<T>& m, int tau) {
+  if constexpr (SS_SQ_WFORM) {
+    if (tau <= 0) return;
+    const T two = splat<T>(2.0);
+    m.r00 = m.r00 + two; m.r11 = m.r11 + two; m.r22 = m.r22 + two;
+    SS_UNROLL(SS_SQ_UNROLL)
+    for (int it = 1; it < tau; ++it) sym_square_w<T, true>(m);
+    sym_square_w<T, false>(m);
+  } else {
+    SS_UNROLL(SS_SQ_UNROLL)
+    for (int it = 0; it < tau; ++it) lt_square<T>(m);
+  }
+}
+
 // Two FP32 symmetric residuals packed one per float2 lane (FP32 mode squares both exponentials of a CF4 step in
 // lockstep with packed FFMA2).
 __device__ __forceinline__ Sym3<float2> sym_pack(const Sym3<float>& a, const Sym3<float>& b) {
@@ -760,18 +816,11 @@ __device__ __forceinline__ void trotter_expand(const Sym3<T>& m0, T cphi, T sphi
   e.re[6] = m.r02 * c2phi - m.i02 * s2phi; e.im[6] = m.i02 * c2phi + m.r02 * s2phi;
 }
 
-#ifndef SS_SQ_UNROLL
-#define SS_SQ_UNROLL 2      // unroll of the τ-squaring loop (tuning knob, DESIGN.md §5)
-#endif
-#define SS_PRAGMA(x) _Pragma(#x)
-#define SS_UNROLL(n) SS_PRAGMA(unroll n)
-
 template <typename T> __device__ __forceinline__ void trotter_residual(const T a[4], int tau, Res<3, T>& e) {
   Sym3<T> m;
   T cphi, sphi;
   trotter_init<T>(a, tau, m, cphi, sphi);
-  SS_UNROLL(SS_SQ_UNROLL)
-  for (int it = 0; it < tau; ++it) lt_square<T>(m);
+  lt_square_tau<T>(m, tau);
   trotter_expand<T>(m, cphi, sphi, e);
 }
 
@@ -1016,8 +1065,7 @@ template <typename T> __device__ __forceinline__ void trotter_residual_su3(const
   Sym3<T> m;
   Su3W<T> w;
   su3_init<T>(a, tau, m, w);
-  SS_UNROLL(SS_SQ_UNROLL)
-  for (int it = 0; it < tau; ++it) lt_square<T>(m);
+  lt_square_tau<T>(m, tau);
   su3_expand<T>(m, w, e);
 }
 
