@@ -613,7 +613,8 @@ template <> __device__ __forceinline__ float taylor_bound<float>() { return 2.44
 // Scaled double-angle form: carrying x̃ = 2x and ỹ = −2y (exact rescalings by powers of two) the doubling becomes
 //   x̃' = −ỹ²,  ỹ' = (x̃ + 2I)·ỹ
 // (x̃' = 2x' = −4y² = −ỹ²;  ỹ' = −2y' = −4y − 4xy = (2x + 2I)(−2y)) — two symmetric products and a diagonal shift:
-// 3 DADD + 12 DMUL + 24 DFMA = 39 FP64 instructions.  trotter_init produces and trotter_expand consumes this form.
+// 3 DADD + 12 DMUL + 24 DFMA = 39 FP64 instructions (36 in the shifted-diagonal form below).  trotter_init produces
+// and trotter_expand consumes this form.
 template <typename T> __device__ __forceinline__ void sym_square_s(Sym3<T>& a) {
   const T two = splat<T>(2.0);
   const T d0 = a.r00 + two, d1 = a.r11 + two, d2 = a.r22 + two;
@@ -679,9 +680,11 @@ template <typename T, bool W_OUT> __device__ __forceinline__ void sym_square_w(S
 #define SS_PRAGMA(x) _Pragma(#x)
 #define SS_UNROLL(n) SS_PRAGMA(unroll n)
 
-// The τ residual squarings of the scaled pair: shifted-diagonal form when SS_SQ_WFORM.
+// The τ residual squarings of the scaled pair: shifted-diagonal form in FP64 when SS_SQ_WFORM.  FP32
+// keeps the unshifted form: at its precision the diagonal's three roundings at the magnitude of 2 doubled C5's
+// error against the oracle (1.72e-5 → 3.26e-5, bar 1e-4) for a 0.9 % faster step (profiles/r02/s54_wform_fp32/).
 template <typename T> __device__ __forceinline__ void lt_square_tau(Sym3<T>& m, int tau) {
-  if constexpr (SS_SQ_WFORM) {
+  if constexpr (SS_SQ_WFORM && sizeof(T) == 8) {
     if (tau <= 0) return;
     const T two = splat<T>(2.0);
     m.r00 = m.r00 + two; m.r11 = m.r11 + two; m.r22 = m.r22 + two;
@@ -856,7 +859,7 @@ template <typename T> __device__ __forceinline__ void su2_to_spin1(const Res<2, 
 // real symmetric tridiagonal form S = W†HW by W = diag(1, g), g = G·diag(1, e^{iψ}) with
 // G = [[H01*, −H02], [H02*, H01]]/r, r = √(|H01|² + |H02|²), and e^{iψ} = B12*/|B12| for B = G†H_blk G (reading R20);
 // the factor is T = W T₀ W†, T₀ = e^{−iD/2} e^{−iX} e^{−iD/2} on S/n (the paper's Eq. lie_trotter_4 shape).  T₀ is
-// complex symmetric and unitary, so its τ squarings take the scaled double-angle form (39 instructions, §5 item 13)
+// complex symmetric and unitary, so its τ squarings take the scaled double-angle form (36 instructions, §5 items 13, 19)
 // and W is applied once at the end: (W T₀ W†)^n − I = W (T₀^n − I) W† (DESIGN.md §5 item 14).
 
 // sin r / r and (cos r − 1)/r² from r² (both even): series for r ≤ 2^-4 (truncation < 1e-19 relative), else library.

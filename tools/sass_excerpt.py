@@ -2,7 +2,7 @@
   * a mnemonic census of the hot kernels (FP64 DFMA/DMUL/DADD, packed FP32 FFMA2/FMUL2/FADD2, the bulk/tensor copies
     UBLKCP/UTMALDG/UTMASTG and LDGSTS that move the scan's operators),
   * the innermost backward-branch loops of the C3/C2 interval kernel with their FP64 mix — the τ residual squaring
-    (39 FP64 instructions per squaring, DESIGN.md §5 item 13) and of the FP32 kernel (packed float2 squarings).
+    (36 FP64 instructions per squaring, DESIGN.md §5 items 13 and 19) and of the FP32 kernel (packed float2 squarings).
 
     python tools/sass_excerpt.py > profiles/r02/<tag>/sass_excerpt.txt
 """
@@ -16,14 +16,14 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = os.path.join(ROOT, "paper_2204_05586_b200", "libspinsim_b200.so")
 KEYS = ["DFMA", "DMUL", "DADD", "FFMA2", "FMUL2", "FADD2", "UBLKCP", "UTMALDG", "UTMASTG", "LDGSTS", "SHFL"]
 HOT = {
-    "_ZN3ssb15interval_kernelILi2ELi1ELi0ELi3EdLb0EEEvNS_14IntervalParamsE": "interval kernel, spin-one LT, CF4, neural, FP64 (C3, C2)",
-    "_ZN3ssb15interval_kernelILi2ELi1ELi0ELi3EdLb1EEEvNS_14IntervalParamsE": "  same, FUSED instance (run aggregates)",
-    "_ZN3ssb15interval_kernelILi2ELi1ELi0ELi3EfLb0EEEvNS_14IntervalParamsE": "interval kernel, spin-one LT, FP32 mode (C5 FP32)",
-    "_ZN3ssb15interval_kernelILi1ELi0ELi0ELi3EdLb0EEEvNS_14IntervalParamsE": "interval kernel, spin-half, FP64 (C4)",
-    "_ZN3ssb15interval_kernelILi2ELi2ELi0ELi7EdLb0EEEvNS_14IntervalParamsE": "interval kernel, general spin-one su(3) (G1)",
+    "_ZN3ssb15interval_kernelILi2ELi1ELi0ELi3EdLi0EEEvNS_14IntervalParamsE": "interval kernel, spin-one LT, CF4, neural, FP64 (C3, C2)",
+    "_ZN3ssb15interval_kernelILi2ELi1ELi0ELi3EdLi1EEEvNS_14IntervalParamsE": "  same, FUSED instance (run aggregates)",
+    "_ZN3ssb15interval_kernelILi2ELi1ELi0ELi3EfLi0EEEvNS_14IntervalParamsE": "interval kernel, spin-one LT, FP32 mode (C5 FP32)",
+    "_ZN3ssb15interval_kernelILi1ELi0ELi0ELi3EdLi0EEEvNS_14IntervalParamsE": "interval kernel, spin-half, FP64 (C4)",
+    "_ZN3ssb15interval_kernelILi2ELi2ELi0ELi7EdLi0EEEvNS_14IntervalParamsE": "interval kernel, general spin-one su(3) (G1)",
     "_ZN3ssb12chain_kernelINS_2CMILi3EEEEEvNS_9ChainArgsE": "chain kernel (C3 states)",
-    "_ZN3ssb16run_chain_kernelINS_2SUILi2EEELi32EEEvNS_12RunChainArgsE": "run chain, SU(2) ops, 32-interval runs (scan-stress)",
-    "_ZN3ssb16run_chain_kernelINS_2SUILi3EEELi4EEEvNS_12RunChainArgsE": "run chain, D1(SU(2)) ops, 4-interval runs (C5 analytic)",
+    "_ZN3ssb16run_chain_kernelINS_2SUILi2EEELi32ELb0EEEvNS_12RunChainArgsE": "run chain, SU(2) ops, 32-interval runs (scan-stress)",
+    "_ZN3ssb16run_chain_kernelINS_2SUILi3EEELi4ELb0EEEvNS_12RunChainArgsE": "run chain, D1(SU(2)) ops, 4-interval runs (C5 analytic)",
     "_ZN3ssb12scan3_kernelINS_2CMILi3EEEEEvNS_9Scan3ArgsE14CUtensorMap_stS4_": "scan3 (tensor-TMA look-back scan)",
 }
 INS = re.compile(r"/\*([0-9a-f]{4,})\*/\s+(@!?U?P\w+\s+)?([A-Z][A-Z0-9_]*)(\.[A-Z0-9_.]+)?([^;]*);")
@@ -58,8 +58,8 @@ def main():
             continue
         c = collections.Counter(op for _, op, _ in ins)
         print(f"{what}: {len(ins)} instructions; " + ", ".join(f"{k} {c[k]}" for k in KEYS if c[k]))
-    for name in ("_ZN3ssb15interval_kernelILi2ELi1ELi0ELi3EdLb0EEEvNS_14IntervalParamsE",
-                 "_ZN3ssb15interval_kernelILi2ELi1ELi0ELi3EfLb0EEEvNS_14IntervalParamsE"):
+    for name in ("_ZN3ssb15interval_kernelILi2ELi1ELi0ELi3EdLi0EEEvNS_14IntervalParamsE",
+                 "_ZN3ssb15interval_kernelILi2ELi1ELi0ELi3EfLi0EEEvNS_14IntervalParamsE"):
         ins = funcs[name]
         print(f"\n## innermost loops of {HOT[name]}\n")
         def arith(r):   # FP64 / packed-FP32 arithmetic fraction of a loop body
